@@ -1,0 +1,160 @@
+/*
+ * vtrain_b200.h -- C ABI of the B200 (sm_100a) hot path of the vtrain
+ * verifiable-training scheme (arXiv 2403.09603).
+ *
+ * Every entry point is stateless and stream-ordered: the caller owns all
+ * device buffers (plain device pointers + sizes), passes a cudaStream_t as
+ * an opaque pointer, and reads results (counters, error bits) back when it
+ * synchronises.  No torch types appear here.  Status return values describe
+ * argument / launch problems only; data-dependent failures (non-finite
+ * input, range, bad code, corrupt log) are reported as VT_ERR_* bits OR-ed
+ * into the caller's device int32 `err`, which the host wrapper turns into
+ * the reference's exact exception text, in the reference's check order.
+ *
+ * Reference interfaces replaced (paths relative to the reference root
+ * /root/reference, vtrain 0.1.0):
+ *   vt_round_log      <- protocol._TrainerChannel.process   pkg/src/vtrain/protocol.py:198-202
+ *                        (= fpround.direction_array :164-177 + rnd_array :127-135
+ *                           + roundlog.LogWriter.write_array pkg/src/vtrain/roundlog.py:119-137),
+ *                        fpround.rnd_array (no log outputs), direction_array (codes only),
+ *                        protocol._PlainChannel.process      protocol.py:225-226
+ *   vt_replay         <- protocol._AuditorChannel.process    protocol.py:212-216
+ *                        (= roundlog.LogReader.read_array :195-201 + fpround.rev_array :227-247)
+ *   vt_grid_neighbors <- fpround.grid_neighbors_array        fpround.py:185-218
+ *   vt_exponent_scale <- fpround.exponent_scale_array        fpround.py:149-156
+ *   vt_is_on_grid     <- fpround.is_on_grid                  fpround.py:255-264
+ *   vt_norm_distance  <- the |x-rnd(x)|/max(scale,2^-126) term of direction_array :171-173
+ *   vt_pack5          <- roundlog._pack_block                roundlog.py:67-70
+ *   vt_unpack5        <- roundlog._unpack_block              roundlog.py:73-82
+ *   vt_log_validate   <- the byte check of _unpack_block     roundlog.py:75-76
+ *   vt_log_histogram  <- roundlog.LogReader.histogram        roundlog.py:203-206
+ *   vt_tau_kth_key    <- protocol.search_tau predicate       protocol.py:494-506 (budget form,
+ *                        SURVEY.md Appendix A.4)
+ *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
+ *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
+ *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
+ *   vt_merkle_build   <- merkle.build over chunked leaves    merkle.py:55-72
+ */
+#ifndef VTRAIN_B200_H
+#define VTRAIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *vt_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+/* status codes */
+#define VT_OK 0
+#define VT_EINVAL (-1) /* bad argument (size, b_r, alignment, workspace) */
+#define VT_ECUDA (-2)  /* CUDA runtime / launch failure, see vt_last_error() */
+
+/* device error bits */
+#define VT_ERR_NONFINITE 1      /* "non-finite value" */
+#define VT_ERR_RANGE 2          /* rnd(x) > grid_max: "out of representable range" */
+#define VT_ERR_RANGE_NEIGHBOR 4 /* |x| > grid_max (neighbour / rev semantics), same text */
+#define VT_ERR_BAD_CODE 8       /* code not in {0,1,2}: "invalid direction code" */
+#define VT_ERR_BAD_LOG_BYTE 16  /* packed byte > 242: "corrupt log byte" */
+#define VT_ERR_BAD_SPARSE 32    /* sparse log not strictly ascending / out of range */
+
+/* output kinds for the rounded tensor */
+#define VT_OUT_NONE 0
+#define VT_OUT_F32 1
+#define VT_OUT_F64 2
+
+/* log kinds consumed by vt_replay */
+#define VT_LOG_SPARSE 0 /* uint64 words (global_index << 1) | up, strictly ascending */
+#define VT_LOG_CODES 1  /* uint8 ternary code per element (0 down, 1 ignore, 2 up) */
+#define VT_LOG_PACKED 2 /* .vtrl payload bytes, 5 base-3 digits per byte */
+
+const char *vt_version(void);
+const char *vt_last_error(void);
+int vt_tile_elems(void); /* elements per CTA tile (shard boundaries align to it) */
+
+/* ---- fused round-and-log (trainer) ------------------------------------ */
+size_t vt_round_log_workspace(int64_t n);
+/*
+ * x[n] FP64 (16-byte aligned) -> out (FP32/FP64, or none) plus any of:
+ *   sparse:  entries (global_base + i) << 1 | (code == UP) for every code != 1,
+ *            ascending; written at *cursor_in (0 if NULL) + rank, at most
+ *            sparse_cap words; *cursor_out (if not NULL) = cursor + count.
+ *   codes:   uint8 ternary code per element.
+ *   packed:  .vtrl bytes for the element stream starting at log position
+ *            log_pos: full 5-digit groups only, byte g covers elements
+ *            [head + 5g, head + 5g + 5) with head = (5 - log_pos % 5) % 5
+ *            (clipped to n); edge_codes[0..7] receives the head codes then
+ *            the tail codes (elements after the last full group).
+ * counters[0] = number of codes != 1 (directed count / sparse entry count).
+ */
+int vt_round_log(const double *x, int64_t n, int b_r, double tau, int out_kind, void *out,
+                 uint64_t *sparse, int64_t sparse_cap, int64_t global_base,
+                 const int64_t *cursor_in, int64_t *cursor_out, uint8_t *codes, uint8_t *packed,
+                 int64_t log_pos, uint8_t *edge_codes, int64_t *counters, int32_t *err, void *ws,
+                 size_t ws_bytes, vt_stream_t stream);
+
+/* ---- fused replay (auditor) ------------------------------------------- */
+size_t vt_replay_workspace(int64_t n);
+/*
+ * log_kind SPARSE: log = uint64 words, log_len = word count, log_base = global
+ *   index of x[0]; counters[1] / counters[2] = first / one-past-last word consumed.
+ * log_kind CODES:  log = uint8[n].
+ * log_kind PACKED: log = payload bytes, log_base = stream position of x[0],
+ *   log_len = payload byte count (bounds).
+ * counters[0] = corrections (elements whose output differs from rnd(x)).
+ */
+int vt_replay(const double *x, int64_t n, int b_r, int log_kind, const void *log,
+              int64_t log_len, int64_t log_base, int out_kind, void *out, int64_t *counters,
+              int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+
+/* ---- elementwise grid helpers ----------------------------------------- */
+int vt_grid_neighbors(const double *x, int64_t n, int b_r, double *below, double *above,
+                      int32_t *err, vt_stream_t stream);
+int vt_exponent_scale(const double *x, int64_t n, double *out, int32_t *err, vt_stream_t stream);
+int vt_is_on_grid(const double *x, int64_t n, int b_r, uint8_t *out, vt_stream_t stream);
+int vt_norm_distance(const double *x, int64_t n, int b_r, double *out, int32_t *err,
+                     vt_stream_t stream);
+
+/* ---- .vtrl codec -------------------------------------------------------- */
+int vt_pack5(const uint8_t *codes, int64_t n_groups, uint8_t *out, int32_t *err,
+             vt_stream_t stream);
+/* entries [pos, pos + n) of the payload stream -> codes[n] */
+int vt_unpack5(const uint8_t *payload, int64_t pos, int64_t n, uint8_t *codes, int32_t *err,
+               vt_stream_t stream);
+int vt_log_validate(const uint8_t *payload, int64_t nbytes, int32_t *err, vt_stream_t stream);
+/* counts3[0..2] += histogram of the first n_entries digits */
+int vt_log_histogram(const uint8_t *payload, int64_t n_entries, int64_t *counts3, int32_t *err,
+                     vt_stream_t stream);
+
+/* ---- adaptive threshold ------------------------------------------------- */
+size_t vt_tau_workspace(int64_t n);
+/*
+ * *key_out = FP64 bit pattern of the (rank+1)-th largest normalized distance
+ * p = |x - rnd(x)| / max(scale(x), 2^-126) (radix select; 0 if rank >= n).
+ */
+int vt_tau_kth_key(const double *x, int64_t n, int b_r, int64_t rank, uint64_t *key_out,
+                   int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+/* out[0] = min over s[n] ignoring NaN (+inf if none), *nan_flag |= 1 if any NaN */
+int vt_min_f64(const double *s, int64_t n, double *out, int32_t *nan_flag, vt_stream_t stream);
+
+/* ---- SHA-256 Merkle ---------------------------------------------------- */
+/* digests[ceil(nbytes / leaf_bytes)][32] = SHA-256 of each leaf_bytes chunk */
+int vt_sha256_leaves(const uint8_t *data, int64_t nbytes, int64_t leaf_bytes, uint8_t *digests,
+                     vt_stream_t stream);
+/* out[ceil(n_in/2)][32]: SHA-256(in[2i] || in[2i+1]); an unpaired last node is copied */
+int vt_merkle_level(const uint8_t *in, int64_t n_in, uint8_t *out, vt_stream_t stream);
+/* number of nodes of all levels (leaves included) for n_leaves >= 1 */
+int64_t vt_merkle_node_count(int64_t n_leaves);
+/*
+ * Whole tree over chunked leaves: nodes = level 0 (leaves), then level 1, ...
+ * concatenated, nodes_cap >= vt_merkle_node_count(ceil(nbytes / leaf_bytes)).
+ */
+int vt_merkle_build(const uint8_t *data, int64_t nbytes, int64_t leaf_bytes, uint8_t *nodes,
+                    int64_t nodes_cap, vt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VTRAIN_B200_H */

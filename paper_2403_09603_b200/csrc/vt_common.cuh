@@ -1,0 +1,221 @@
+// Shared device code: grid parameters, bit-exact rounding / direction /
+// replay primitives, streaming load/store wrappers, error plumbing.
+//
+// Semantics follow the reference (vtrain 0.1.0, pkg/src/vtrain/fpround.py):
+//   rnd        fpround.py:99-135   RNE on the kept mantissa bits, absolute grid below 2^-126
+//   direction  fpround.py:164-177  strict |x - rnd(x)| > max(scale(x), 2^-126) * tau
+//   neighbours fpround.py:185-218  truncate + one step in magnitude space
+//   rev        fpround.py:227-247  neighbour on the coded side when rnd disagrees
+// The integer forms used here are derived in SURVEY.md Appendix B and are
+// checked bit for bit against the oracle by tests/test_gpu_*.py.
+//
+// Build flags never include --use_fast_math / -ftz: FP32/FP64 subnormals must
+// survive, and FP64 arithmetic below uses explicit _rn intrinsics so nothing
+// is contracted into an FMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vtrain_b200.h"
+
+namespace vt {
+
+constexpr uint64_t kSign = 0x8000000000000000ull;
+constexpr uint64_t kMag = 0x7fffffffffffffffull;
+constexpr uint64_t kNormalMin = 0x3810000000000000ull;  // bits of 2^-126
+constexpr uint64_t kExpAllOnes = 0x7ff0000000000000ull;  // inf / nan threshold
+
+// Tile geometry shared by every streaming kernel: 8 warps x 5 slots x
+// 32 lanes x 4 consecutive FP64 (one 256-bit load per lane per slot).
+// 640 = lcm(5, 128) elements per warp keeps .vtrl byte groups and 128-bit
+// vectors aligned to warp boundaries.
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kVec = 4;
+constexpr int kSlots = 5;
+constexpr int kWarpElems = 32 * kVec * kSlots;  // 640
+constexpr int kTile = kWarps * kWarpElems;      // 5120
+
+struct Grid {
+  int drop;             // 52 - (b_r - 9) mantissa bits dropped
+  int _pad;
+  uint64_t low_mask;    // (1 << drop) - 1
+  uint64_t half;        // 1 << (drop - 1)
+  uint64_t one;         // 1 << drop
+  uint64_t gmax_bits;   // bit pattern of grid_max(b_r)
+  double sub_up;        // 2^-q, q = (32 - b_r) - 149
+  double sub_dn;        // 2^q
+  int64_t thr;          // integer threshold on d (units of ulp(x) in FP64)
+  double thr_sub;       // 2^-126 * tau, the FP64 threshold below 2^-126
+};
+
+// Host-side construction (also used by the C ABI wrappers).
+inline Grid make_grid(int b_r, double tau) {
+  Grid g;
+  g.drop = 52 - (b_r - 9);
+  g._pad = 0;
+  g.one = 1ull << g.drop;
+  g.low_mask = g.one - 1;
+  g.half = 1ull << (g.drop - 1);
+  // grid_max = (2 - 2^-(b_r-9)) * 2^127: FP64 biased exponent 1023 + 127,
+  // the kept mantissa bits all ones
+  g.gmax_bits = (1150ull << 52) | (((1ull << (b_r - 9)) - 1) << g.drop);
+  int q = (32 - b_r) - 149;
+  g.sub_up = ldexp(1.0, -q);
+  g.sub_dn = ldexp(1.0, q);
+  // Normal range: |x - r| = d * 2^(E-52) exactly and scale*tau = 2^E * tau,
+  // so (strict) |x - r| > scale * tau  <=>  d > tau * 2^52  <=>  d > floor(tau * 2^52).
+  // Degenerate taus are mapped so the comparison keeps the FP64 outcome.
+  if (tau != tau) {
+    g.thr = INT64_MAX;  // NaN: comparison always false
+  } else if (tau < 0.0) {
+    g.thr = -1;  // every d >= 0 passes; d == 0 still yields IGNORE
+  } else if (tau < 0x1p-800) {
+    g.thr = 0;  // tau * 2^E may underflow, but any d >= 1 exceeds it
+  } else {
+    double t = floor(ldexp(tau, 52));
+    g.thr = (t >= 0x1p62) ? INT64_MAX : (int64_t)t;
+  }
+  g.thr_sub = 0x1p-126 * tau;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// element primitives
+// ---------------------------------------------------------------------------
+
+// Round x onto the grid and classify it.  Returns the rounded FP64 bits;
+// `code` gets 0 (DOWN: x > r), 1 (IGNORE), 2 (UP: x < r); `err` collects
+// VT_ERR_NONFINITE / VT_ERR_RANGE.
+__device__ __forceinline__ uint64_t round_dir(double x, const Grid& g, uint32_t& code,
+                                              uint32_t& err) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const uint64_t mag = bits & kMag;
+  const uint64_t sgn = bits & kSign;
+  if (mag >= kNormalMin) {
+    const uint64_t low = mag & g.low_mask;
+    const uint64_t base = mag >> g.drop;
+    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
+    const uint64_t rmag = (base + (up ? 1ull : 0ull)) << g.drop;
+    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
+    const int64_t d = (int64_t)(up ? (g.one - low) : low);
+    const bool logged = (d > g.thr) && (low != 0);
+    const bool r_above = up != (sgn != 0);  // x < r
+    code = logged ? (r_above ? 2u : 0u) : 1u;
+    return sgn | rmag;
+  }
+  const double s = __dmul_rn(x, g.sub_up);
+  const double r = __dmul_rn(rint(s), g.sub_dn);
+  const double dist = fabs(__dsub_rn(x, r));
+  const bool logged = dist > g.thr_sub;
+  code = logged ? ((x < r) ? 2u : ((x > r) ? 0u : 1u)) : 1u;
+  return (uint64_t)__double_as_longlong(r);
+}
+
+// Plain rounding (no classification).
+__device__ __forceinline__ uint64_t round_only(double x, const Grid& g, uint32_t& err) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const uint64_t mag = bits & kMag;
+  if (mag >= kNormalMin) {
+    const uint64_t low = mag & g.low_mask;
+    const uint64_t base = mag >> g.drop;
+    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
+    const uint64_t rmag = (base + (up ? 1ull : 0ull)) << g.drop;
+    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
+    return (bits & kSign) | rmag;
+  }
+  const double r = __dmul_rn(rint(__dmul_rn(x, g.sub_up)), g.sub_dn);
+  return (uint64_t)__double_as_longlong(r);
+}
+
+// Replay: rnd(x) unless the recorded code points at the other neighbour.
+// `flip` is set when the output differs from rnd(x) (an auditor correction).
+__device__ __forceinline__ uint64_t replay_one(double x, uint32_t c, const Grid& g,
+                                               uint32_t& err, uint32_t& flip) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const uint64_t mag = bits & kMag;
+  const uint64_t sgn = bits & kSign;
+  err |= (c > 2u) ? (uint32_t)VT_ERR_BAD_CODE : 0u;
+  if (mag >= kNormalMin) {
+    const uint64_t low = mag & g.low_mask;
+    const uint64_t base = mag >> g.drop;
+    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
+    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                : ((mag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE_NEIGHBOR : 0u);
+    const bool off = low != 0;
+    const bool r_above = up != (sgn != 0);  // x < r when off grid
+    const bool f = off && ((c == 0u && r_above) || (c == 2u && !r_above));
+    flip = f ? 1u : 0u;
+    return sgn | ((base + ((up != f) ? 1ull : 0ull)) << g.drop);
+  }
+  const double s = __dmul_rn(x, g.sub_up);
+  const double r = __dmul_rn(rint(s), g.sub_dn);
+  if (c == 0u && x < r) {
+    flip = 1u;
+    return (uint64_t)__double_as_longlong(__dmul_rn(floor(s), g.sub_dn));
+  }
+  if (c == 2u && x > r) {
+    flip = 1u;
+    return (uint64_t)__double_as_longlong(__dmul_rn(ceil(s), g.sub_dn));
+  }
+  flip = 0u;
+  return (uint64_t)__double_as_longlong(r);
+}
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+
+struct D4 {
+  double v[4];
+};
+
+// 256-bit streaming load (LDG.E.NA...256 on sm_100a), read-once data.
+__device__ __forceinline__ D4 ldg_stream4(const double* p) {
+  D4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void stg_stream4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b),
+               "d"(c), "d"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void stg_stream4f(float* p, float a, float b, float c, float d) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ void report_err(int32_t* err, uint32_t e) {
+  if (e) atomicOr(reinterpret_cast<int*>(err), (int)e);
+}
+
+}  // namespace vt
+
+// host-side error bookkeeping shared by the ABI translation units
+void vt_set_error(const char* what);
+int vt_check_launch(const char* what);

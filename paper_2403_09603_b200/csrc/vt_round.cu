@@ -1,0 +1,691 @@
+// Fused round-and-log (trainer) and replay (auditor) streaming kernels.
+//
+// round_log_kernel replaces protocol._TrainerChannel.process
+// (pkg/src/vtrain/protocol.py:198-202): direction_array + LogWriter.write_array
+// + rnd_array in ONE pass over the FP64 input.  replay_kernel replaces
+// protocol._AuditorChannel.process (protocol.py:212-216): LogReader.read_array
+// + rev_array + the correction count in ONE pass.
+//
+// HBM layout per call (element i of a contiguous FP64 tensor):
+//   x[i]        FP64, read once with 256-bit L1::no_allocate loads
+//   out[i]      FP32 (north-star form) or FP64 (drop-in form), 128/256-bit stores
+//   sparse log  uint64 words (global_index << 1) | up, ascending, 8 B per logged element
+//   codes[i]    optional uint8 ternary code
+//   packed      optional .vtrl payload, 5 codes per byte
+//
+// The sparse log is emitted in index order by a single-pass decoupled
+// look-back scan: CTAs take tile ids from an atomic ticket (so every
+// predecessor of a running tile is itself running or done), publish their
+// aggregate count, and warp 0 walks back over predecessors 32 at a time.
+// Flag and value share one 64-bit word, so relaxed loads/stores suffice.
+#include <algorithm>
+
+#include "vt_common.cuh"
+
+namespace vt {
+
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+struct RoundLogArgs {
+  const double* x;
+  int64_t n;
+  Grid g;
+  void* out;
+  uint64_t* sparse;
+  int64_t sparse_cap;
+  int64_t global_base;
+  const int64_t* cursor_in;
+  int64_t* cursor_out;
+  uint8_t* codes;
+  uint8_t* packed;
+  int64_t head;   // elements before the first full .vtrl group
+  int64_t nfull;  // full groups emitted by this call
+  uint8_t* edge;  // head codes then tail codes (<= 8)
+  int64_t* counters;
+  int32_t* err;
+  uint64_t* status;
+  uint32_t* ticket;
+  int64_t num_tiles;
+};
+
+__device__ __forceinline__ void load_slots(const double* __restrict__ x, int64_t n, int64_t wbase,
+                                           int lane, D4 (&xv)[kSlots]) {
+#pragma unroll
+  for (int j = 0; j < kSlots; ++j) {
+    const int64_t i0 = wbase + j * 128 + lane * 4;
+    if (i0 + 3 < n) {
+      xv[j] = ldg_stream4(x + i0);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xv[j].v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
+    }
+  }
+}
+
+template <int OUT>
+__device__ __forceinline__ void store_out(void* out, int64_t i0, int64_t n, const uint64_t (&rb)[4]) {
+  if (OUT == VT_OUT_F32) {
+    float* o = static_cast<float*>(out);
+    float f[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) f[v] = __double2float_rn(__longlong_as_double((long long)rb[v]));
+    if (i0 + 3 < n) {
+      stg_stream4f(o + i0, f[0], f[1], f[2], f[3]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (i0 + v < n) o[i0 + v] = f[v];
+    }
+  } else if (OUT == VT_OUT_F64) {
+    double* o = static_cast<double*>(out);
+    double d[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) d[v] = __longlong_as_double((long long)rb[v]);
+    if (i0 + 3 < n) {
+      stg_stream4(o + i0, d[0], d[1], d[2], d[3]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (i0 + v < n) o[i0 + v] = d[v];
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Decoupled look-back by one warp.  Returns the exclusive prefix of `tile`.
+__device__ __forceinline__ int64_t lookback(uint64_t* status, int64_t tile, uint64_t agg, int lane) {
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_u64(status, kFlagInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | agg);
+  int64_t excl = 0;
+  int64_t pred = tile - 1;
+  while (true) {
+    const int64_t idx = pred - lane;
+    const uint64_t s = (idx >= 0) ? ld_relaxed_u64(status + idx) : kFlagInc;
+    const uint64_t flag = s >> 62;
+    const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
+    const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
+    const int first = inc ? (__ffs(inc) - 1) : 31;
+    const uint32_t upto = (2u << first) - 1u;  // lanes 0..first (all lanes if first == 31)
+    if (inv & upto) {
+      __nanosleep(20);
+      continue;
+    }
+    uint64_t v = (lane <= first) ? (s & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += (int64_t)v;
+    if (inc) break;
+    pred -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | ((uint64_t)excl + agg));
+  return excl;
+}
+
+template <int OUT, bool SPARSE, bool CODES, bool PACKED>
+__global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[kWarps];
+  __shared__ int64_t s_base;
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int64_t tile;
+  if (SPARSE) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    tile = s_tile;
+  } else {
+    tile = blockIdx.x;
+  }
+  const int64_t tile_base = tile * kTile;
+  const int64_t wbase = tile_base + warp * kWarpElems;
+
+  D4 xv[kSlots];
+  load_slots(a.x, a.n, wbase, lane, xv);
+
+  uint64_t* stage = reinterpret_cast<uint64_t*>(smem) + warp * kWarpElems;  // SPARSE
+  uint8_t* cs = smem + (SPARSE ? kTile * sizeof(uint64_t) : 0);              // PACKED
+  uint32_t err = 0;
+  uint32_t cnt = 0;  // SPARSE: warp-uniform running count; else per-thread count
+  const uint32_t lt = lanemask_lt();
+
+#pragma unroll
+  for (int j = 0; j < kSlots; ++j) {
+    const int64_t i0 = wbase + j * 128 + lane * 4;
+    uint32_t code[4];
+    uint64_t rb[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) rb[v] = round_dir(xv[j].v[v], a.g, code[v], err);
+    store_out<OUT>(a.out, i0, a.n, rb);
+    if (CODES) {
+      if (i0 + 3 < a.n) {
+        *reinterpret_cast<uint32_t*>(a.codes + i0) = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (i0 + v < a.n) a.codes[i0 + v] = (uint8_t)code[v];
+      }
+    }
+    if (PACKED) {
+      const int e0 = warp * kWarpElems + j * 128 + lane * 4;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        cs[e0 + v] = (uint8_t)code[v];
+        const int64_t i = i0 + v;
+        if (i < a.n && (i < a.head || i >= a.head + 5 * a.nfull))
+          a.edge[i < a.head ? i : i - 5 * a.nfull] = (uint8_t)code[v];
+      }
+    }
+    if (SPARSE) {
+      const uint32_t b0 = __ballot_sync(0xffffffffu, code[0] != 1u);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, code[1] != 1u);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, code[2] != 1u);
+      const uint32_t b3 = __ballot_sync(0xffffffffu, code[3] != 1u);
+      uint32_t r = cnt + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        if (code[v] != 1u) {
+          stage[r] = ((uint64_t)(a.global_base + i0 + v) << 1) | (code[v] == 2u ? 1ull : 0ull);
+          ++r;
+        }
+      }
+      cnt += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cnt += (code[v] != 1u) ? 1u : 0u;
+    }
+  }
+  report_err(a.err, err);
+
+  if (SPARSE) {
+    if (lane == 0) s_warp[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t c = (lane < kWarps) ? s_warp[lane] : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, kWarps - 1);
+      __syncwarp();
+      if (lane < kWarps) s_warp[lane] = incl - c;
+      const int64_t excl = lookback(a.status, tile, total, lane);
+      if (lane == 0) {
+        const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
+        s_base = cur + excl;
+        if (tile == a.num_tiles - 1) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)total));
+          if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)total;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t base = s_base + s_warp[warp];
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const int64_t pos = base + i;
+      if (pos < a.sparse_cap) a.sparse[pos] = stage[i];
+    }
+  } else {
+    const uint32_t w = warp_sum_u32(cnt);
+    if (lane == 0) s_warp[warp] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int k = 0; k < kWarps; ++k) t += s_warp[k];
+      if (t) atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)t);
+    }
+  }
+
+  if (PACKED) {
+    // A .vtrl group is owned by the tile holding its first element; groups
+    // straddling the tile end need up to 4 codes from the next tile.
+    if (threadIdx.x < 4) {
+      const int64_t i = tile_base + kTile + threadIdx.x;
+      uint32_t c = 1u, e2 = 0u;
+      if (i < a.n) (void)round_dir(a.x[i], a.g, c, e2);
+      cs[kTile + threadIdx.x] = (uint8_t)c;
+    }
+    __syncthreads();
+    const int64_t g_lo = (tile_base <= a.head) ? 0 : (tile_base - a.head + 4) / 5;
+    const int64_t g_hi = std::min<int64_t>(a.nfull, (tile_base + kTile - a.head + 4) / 5);
+    for (int64_t gi = g_lo + threadIdx.x; gi < g_hi; gi += kThreads) {
+      const int st = (int)(a.head + 5 * gi - tile_base);
+      const uint32_t b = cs[st] + 3u * cs[st + 1] + 9u * cs[st + 2] + 27u * cs[st + 3] + 81u * cs[st + 4];
+      a.packed[gi] = (uint8_t)b;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// replay
+// ---------------------------------------------------------------------------
+
+struct ReplayArgs {
+  const double* x;
+  int64_t n;
+  Grid g;
+  const void* log;
+  int64_t log_len;
+  int64_t log_base;
+  void* out;
+  const int64_t* offs;  // SPARSE: per-tile [lo, hi) word ranges
+  int64_t* counters;
+  int32_t* err;
+};
+
+__global__ void log_tile_offsets_kernel(const uint64_t* __restrict__ w, int64_t n_words,
+                                        int64_t base, int64_t n, int64_t num_tiles,
+                                        int64_t* __restrict__ offs, int64_t* counters) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > num_tiles) return;
+  const int64_t key = base + std::min<int64_t>(t * kTile, n);
+  int64_t lo = 0, hi = n_words;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)(w[mid] >> 1) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  offs[t] = lo;
+  if (t == 0) counters[1] = lo;
+  if (t == num_tiles) counters[2] = lo;
+}
+
+template <int OUT, int LOGK>
+__global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
+  __shared__ __align__(16) uint8_t cs[kTile];
+  __shared__ uint32_t s_warp[kWarps];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t tile_base = tile * kTile;
+  const int64_t wbase = tile_base + warp * kWarpElems;
+
+  D4 xv[kSlots];
+  load_slots(a.x, a.n, wbase, lane, xv);
+  uint32_t err = 0;
+
+  if (LOGK == VT_LOG_SPARSE) {
+    uint4* c4 = reinterpret_cast<uint4*>(cs);
+    for (int k = threadIdx.x; k < kTile / 16; k += kThreads) c4[k] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    __syncthreads();
+    const uint64_t* w = static_cast<const uint64_t*>(a.log);
+    const int64_t lo = a.offs[tile], hi = a.offs[tile + 1];
+    const int64_t t0 = a.log_base + tile_base;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+      const uint64_t word = w[i];
+      const int64_t idx = (int64_t)(word >> 1) - t0;
+      const bool ordered = (i == 0) || ((w[i - 1] >> 1) < (word >> 1));
+      if (idx >= 0 && idx < kTile && ordered) cs[idx] = (word & 1ull) ? 2 : 0;
+      else err |= VT_ERR_BAD_SPARSE;
+    }
+    __syncthreads();
+  } else if (LOGK == VT_LOG_PACKED) {
+    const uint8_t* p = static_cast<const uint8_t*>(a.log);
+    const int64_t pos0 = a.log_base + tile_base;
+    const int64_t b0 = pos0 / 5;
+    const int r0 = (int)(pos0 - 5 * b0);
+    const int lim = (int)std::min<int64_t>(kTile, a.n - tile_base);
+    for (int e = threadIdx.x; e < lim; e += kThreads) {
+      const int q = (r0 + e) / 5;
+      const int dpos = r0 + e - 5 * q;
+      const int64_t bi = b0 + q;
+      const uint32_t b = (bi < a.log_len) ? (uint32_t)__ldg(p + bi) : 255u;
+      if (b > 242u) err |= VT_ERR_BAD_LOG_BYTE;
+      const uint32_t p3 = dpos == 0 ? 1u : dpos == 1 ? 3u : dpos == 2 ? 9u : dpos == 3 ? 27u : 81u;
+      cs[e] = (uint8_t)((b / p3) % 3u);
+    }
+    __syncthreads();
+  }
+
+  uint32_t flips = 0;
+#pragma unroll
+  for (int j = 0; j < kSlots; ++j) {
+    const int64_t i0 = wbase + j * 128 + lane * 4;
+    uint32_t code[4];
+    if (LOGK == VT_LOG_CODES) {
+      const uint8_t* cg = static_cast<const uint8_t*>(a.log);
+      if (i0 + 3 < a.n) {
+        const uint32_t c4 = *reinterpret_cast<const uint32_t*>(cg + i0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) code[v] = (c4 >> (8 * v)) & 0xffu;
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) code[v] = (i0 + v < a.n) ? cg[i0 + v] : 1u;
+      }
+    } else {
+      const int e0 = warp * kWarpElems + j * 128 + lane * 4;
+      const uint32_t c4 = *reinterpret_cast<const uint32_t*>(cs + e0);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) code[v] = (c4 >> (8 * v)) & 0xffu;
+    }
+    uint64_t rb[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      uint32_t f;
+      rb[v] = replay_one(xv[j].v[v], code[v], a.g, err, f);
+      flips += (i0 + v < a.n) ? f : 0u;
+    }
+    store_out<OUT>(a.out, i0, a.n, rb);
+  }
+  report_err(a.err, err);
+  const uint32_t w = warp_sum_u32(flips);
+  if (lane == 0) s_warp[warp] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) t += s_warp[k];
+    if (t) atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers (not on the bandwidth-critical path)
+// ---------------------------------------------------------------------------
+
+__global__ void neighbors_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                 double* __restrict__ below, double* __restrict__ above,
+                                 int32_t* errp) {
+  uint32_t err = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x[i];
+    const uint64_t bits = (uint64_t)__double_as_longlong(xi);
+    const uint64_t mag = bits & kMag, sgn = bits & kSign;
+    double lo, hi;
+    if (mag >= kNormalMin) {
+      err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                  : ((mag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE_NEIGHBOR : 0u);
+      const uint64_t trunc = mag & ~g.low_mask;
+      const uint64_t away = trunc + (((mag & g.low_mask) != 0) ? g.one : 0ull);
+      const double tv = __longlong_as_double((long long)(sgn | trunc));
+      const double av = __longlong_as_double((long long)(sgn | away));
+      const bool nonneg = !(xi < 0.0);
+      lo = nonneg ? tv : av;
+      hi = nonneg ? av : tv;
+    } else {
+      const double s = __dmul_rn(xi, g.sub_up);
+      lo = __dmul_rn(floor(s), g.sub_dn);
+      hi = __dmul_rn(ceil(s), g.sub_dn);
+    }
+    below[i] = lo;
+    above[i] = hi;
+  }
+  report_err(errp, err);
+}
+
+__global__ void exponent_scale_kernel(const double* __restrict__ x, int64_t n,
+                                      double* __restrict__ out, int32_t* errp) {
+  uint32_t err = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x[i];
+    if (!isfinite(xi)) err |= VT_ERR_NONFINITE;
+    int e = 0;
+    (void)frexp(xi, &e);
+    out[i] = (xi == 0.0) ? 0x1p-126 : ldexp(1.0, e - 1);
+  }
+  report_err(errp, err);
+}
+
+__global__ void on_grid_kernel(const double* __restrict__ x, int64_t n, uint32_t mask,
+                               uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x[i];
+    const float f = __double2float_rn(xi);
+    const bool exact = isfinite(f) && ((double)f == xi);
+    out[i] = (exact && ((__float_as_uint(f) & mask) == 0u)) ? 1 : 0;
+  }
+}
+
+__global__ void norm_distance_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                     double* __restrict__ out, int32_t* errp) {
+  uint32_t err = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x[i];
+    const double r = __longlong_as_double((long long)round_only(xi, g, err));
+    int e = 0;
+    (void)frexp(xi, &e);
+    double scale = (xi == 0.0) ? 0x1p-126 : ldexp(1.0, e - 1);
+    scale = scale < 0x1p-126 ? 0x1p-126 : scale;
+    out[i] = __ddiv_rn(fabs(__dsub_rn(xi, r)), scale);
+  }
+  report_err(errp, err);
+}
+
+}  // namespace vt
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+using namespace vt;
+
+namespace {
+
+bool valid_b(int b_r) { return b_r >= 10 && b_r <= 32; }
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+int64_t num_tiles_for(int64_t n) { return (n + kTile - 1) / kTile; }
+
+template <int OUT, bool S, bool C, bool P>
+void launch_rl(const RoundLogArgs& a, int64_t tiles, cudaStream_t st) {
+  size_t smem = (S ? (size_t)kTile * sizeof(uint64_t) : 0) + (P ? (size_t)kTile + 8 : 0);
+  auto k = round_log_kernel<OUT, S, C, P>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<(unsigned)tiles, kThreads, smem, st>>>(a);
+}
+
+typedef void (*rl_fn)(const RoundLogArgs&, int64_t, cudaStream_t);
+
+template <int OUT>
+rl_fn pick_rl(bool s, bool c, bool p) {
+  const int key = (s ? 4 : 0) | (c ? 2 : 0) | (p ? 1 : 0);
+  switch (key) {
+    case 0: return launch_rl<OUT, false, false, false>;
+    case 1: return launch_rl<OUT, false, false, true>;
+    case 2: return launch_rl<OUT, false, true, false>;
+    case 3: return launch_rl<OUT, false, true, true>;
+    case 4: return launch_rl<OUT, true, false, false>;
+    case 5: return launch_rl<OUT, true, false, true>;
+    case 6: return launch_rl<OUT, true, true, false>;
+    default: return launch_rl<OUT, true, true, true>;
+  }
+}
+
+}  // namespace
+
+extern "C" int vt_tile_elems(void) { return kTile; }
+
+extern "C" size_t vt_round_log_workspace(int64_t n) {
+  return (size_t)(num_tiles_for(n) * 8 + 256);
+}
+
+extern "C" int vt_round_log(const double* x, int64_t n, int b_r, double tau, int out_kind, void* out,
+                            uint64_t* sparse, int64_t sparse_cap, int64_t global_base,
+                            const int64_t* cursor_in, int64_t* cursor_out, uint8_t* codes,
+                            uint8_t* packed, int64_t log_pos, uint8_t* edge_codes,
+                            int64_t* counters, int32_t* err, void* ws, size_t ws_bytes,
+                            vt_stream_t stream) {
+  if (n < 0 || !valid_b(b_r) || out_kind < 0 || out_kind > 2 || !counters || !err) {
+    vt_set_error("vt_round_log: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  if (!x || !aligned(x, 32) || (out_kind == VT_OUT_F32 && !aligned(out, 16)) ||
+      (out_kind == VT_OUT_F64 && !aligned(out, 32)) || (codes && !aligned(codes, 4)) ||
+      (packed && !edge_codes) || log_pos < 0) {
+    vt_set_error("vt_round_log: null or misaligned buffer (x needs 32 B, f32 out 16 B, f64 out 32 B, codes 4 B)");
+    return VT_EINVAL;
+  }
+  const int64_t tiles = num_tiles_for(n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RoundLogArgs a;
+  a.x = x;
+  a.n = n;
+  a.g = make_grid(b_r, tau);
+  a.out = out;
+  a.sparse = sparse;
+  a.sparse_cap = sparse_cap;
+  a.global_base = global_base;
+  a.cursor_in = cursor_in;
+  a.cursor_out = cursor_out;
+  a.codes = codes;
+  a.packed = packed;
+  const int64_t head = std::min<int64_t>((5 - log_pos % 5) % 5, n);
+  a.head = head;
+  a.nfull = (n - head) / 5;
+  a.edge = edge_codes;
+  a.counters = counters;
+  a.err = err;
+  a.num_tiles = tiles;
+  a.status = nullptr;
+  a.ticket = nullptr;
+  if (sparse) {
+    if (!ws || ws_bytes < vt_round_log_workspace(n)) {
+      vt_set_error("vt_round_log: workspace too small");
+      return VT_EINVAL;
+    }
+    a.status = static_cast<uint64_t*>(ws);
+    a.ticket = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + tiles * 8);
+    if (cudaMemsetAsync(ws, 0, (size_t)tiles * 8 + 4, st) != cudaSuccess) return vt_check_launch("memset");
+  }
+  rl_fn f = out_kind == VT_OUT_F32 ? pick_rl<VT_OUT_F32>(sparse != nullptr, codes != nullptr, packed != nullptr)
+          : out_kind == VT_OUT_F64 ? pick_rl<VT_OUT_F64>(sparse != nullptr, codes != nullptr, packed != nullptr)
+                                   : pick_rl<VT_OUT_NONE>(sparse != nullptr, codes != nullptr, packed != nullptr);
+  f(a, tiles, st);
+  return vt_check_launch("round_log_kernel");
+}
+
+namespace {
+template <int OUT, int L>
+void launch_rp(const ReplayArgs& a, int64_t tiles, cudaStream_t st) {
+  replay_kernel<OUT, L><<<(unsigned)tiles, kThreads, 0, st>>>(a);
+}
+typedef void (*rp_fn)(const ReplayArgs&, int64_t, cudaStream_t);
+template <int OUT>
+rp_fn pick_rp(int lk) {
+  return lk == VT_LOG_SPARSE ? launch_rp<OUT, VT_LOG_SPARSE>
+       : lk == VT_LOG_CODES  ? launch_rp<OUT, VT_LOG_CODES>
+                             : launch_rp<OUT, VT_LOG_PACKED>;
+}
+}  // namespace
+
+extern "C" size_t vt_replay_workspace(int64_t n) { return (size_t)((num_tiles_for(n) + 1) * 8 + 256); }
+
+extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, const void* log,
+                         int64_t log_len, int64_t log_base, int out_kind, void* out,
+                         int64_t* counters, int32_t* err, void* ws, size_t ws_bytes,
+                         vt_stream_t stream) {
+  if (n < 0 || !valid_b(b_r) || out_kind < 0 || out_kind > 2 || log_kind < 0 || log_kind > 2 ||
+      !counters || !err || log_len < 0 || log_base < 0) {
+    vt_set_error("vt_replay: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = num_tiles_for(n);
+  if (n == 0) return VT_OK;
+  if (!x || !aligned(x, 32) || (out_kind == VT_OUT_F32 && !aligned(out, 16)) ||
+      (out_kind == VT_OUT_F64 && !aligned(out, 32)) || (!log && (log_len > 0 || log_kind == VT_LOG_CODES)) ||
+      (log_kind == VT_LOG_CODES && !aligned(log, 4))) {
+    vt_set_error("vt_replay: null or misaligned buffer");
+    return VT_EINVAL;
+  }
+  ReplayArgs a;
+  a.x = x;
+  a.n = n;
+  a.g = make_grid(b_r, 0.0);
+  a.log = log;
+  a.log_len = log_len;
+  a.log_base = log_base;
+  a.out = out;
+  a.counters = counters;
+  a.err = err;
+  a.offs = nullptr;
+  if (log_kind == VT_LOG_SPARSE) {
+    if (!ws || ws_bytes < vt_replay_workspace(n)) {
+      vt_set_error("vt_replay: workspace too small");
+      return VT_EINVAL;
+    }
+    int64_t* offs = static_cast<int64_t*>(ws);
+    const int64_t threads = tiles + 1;
+    log_tile_offsets_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint64_t*>(log), log_len, log_base, n, tiles, offs, counters);
+    int rc = vt_check_launch("log_tile_offsets_kernel");
+    if (rc) return rc;
+    a.offs = offs;
+  }
+  rp_fn f = out_kind == VT_OUT_F32 ? pick_rp<VT_OUT_F32>(log_kind)
+          : out_kind == VT_OUT_F64 ? pick_rp<VT_OUT_F64>(log_kind)
+                                   : pick_rp<VT_OUT_NONE>(log_kind);
+  f(a, tiles, st);
+  return vt_check_launch("replay_kernel");
+}
+
+namespace {
+unsigned ew_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+}  // namespace
+
+extern "C" int vt_grid_neighbors(const double* x, int64_t n, int b_r, double* below, double* above,
+                                 int32_t* err, vt_stream_t stream) {
+  if (n < 0 || !valid_b(b_r) || !err) {
+    vt_set_error("vt_grid_neighbors: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  neighbors_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, n, make_grid(b_r, 0.0), below, above, err);
+  return vt_check_launch("neighbors_kernel");
+}
+
+extern "C" int vt_exponent_scale(const double* x, int64_t n, double* out, int32_t* err,
+                                 vt_stream_t stream) {
+  if (n < 0 || !err) {
+    vt_set_error("vt_exponent_scale: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  exponent_scale_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, n, out, err);
+  return vt_check_launch("exponent_scale_kernel");
+}
+
+extern "C" int vt_is_on_grid(const double* x, int64_t n, int b_r, uint8_t* out, vt_stream_t stream) {
+  if (n < 0 || !valid_b(b_r)) {
+    vt_set_error("vt_is_on_grid: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  const uint32_t mask = (b_r < 32) ? ((1u << (32 - b_r)) - 1u) : 0u;
+  on_grid_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, n, mask, out);
+  return vt_check_launch("on_grid_kernel");
+}
+
+extern "C" int vt_norm_distance(const double* x, int64_t n, int b_r, double* out, int32_t* err,
+                                vt_stream_t stream) {
+  if (n < 0 || !valid_b(b_r) || !err) {
+    vt_set_error("vt_norm_distance: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  norm_distance_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, n, make_grid(b_r, 0.0), out, err);
+  return vt_check_launch("norm_distance_kernel");
+}

@@ -1,0 +1,300 @@
+// SHA-256 Merkle hashing of checkpoint bytes (FIPS 180-4 compression).
+//
+// Leaves: SHA-256 of each `leaf_bytes` chunk of the FP32 little-endian
+// weight serialization (north-star chunked leaf, SURVEY.md Appendix A.5;
+// the per-leaf hash is merkle._sha256, pkg/src/vtrain/merkle.py:24-25).
+// Internal nodes: SHA-256(left || right), an unpaired last node promoted
+// unchanged, every level kept (merkle.build, merkle.py:55-72).
+//
+// One message per thread with a register-resident 16-word rolling schedule;
+// rotations are funnel shifts (SHF), Ch/Maj/Sigma fold into LOP3, byte swaps
+// are PRMT.  A message whose length is a multiple of 64 ends in a padding
+// block of constant content, so its schedule W[t] + K[t] is precomputed on
+// the host once per length and passed in the kernel parameters.
+#include <algorithm>
+#include <vector>
+
+#include "vt_common.cuh"
+
+namespace vt {
+
+__constant__ uint32_t kK[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
+    0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
+    0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+    0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
+    0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
+    0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+    0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+
+static const uint32_t kKHost[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
+    0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
+    0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+    0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
+    0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
+    0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+    0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+
+__constant__ uint32_t kIV[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                             0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+
+struct PadWK {
+  uint32_t wk[64];  // W[t] + K[t] of a constant padding block
+};
+
+__device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+__device__ __forceinline__ uint32_t bswap(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+#define VT_ROUND(a, b, c, d, e, f, g, h, wk)                                             \
+  {                                                                                     \
+    const uint32_t t1 = h + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + (wk); \
+    const uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));  \
+    d += t1;                                                                            \
+    h = t1 + t2;                                                                        \
+  }
+
+// One compression of a data block held in w[16] (consumed).
+__device__ __forceinline__ void compress(uint32_t (&s)[8], uint32_t (&w)[16]) {
+  uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+  for (int t = 0; t < 64; t += 8) {
+    if (t >= 16) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = (t + k) & 15;
+        const uint32_t w15 = w[(j + 1) & 15], w2 = w[(j + 14) & 15];
+        w[j] += (rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10)) + w[(j + 9) & 15] +
+                (rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3));
+      }
+    }
+    VT_ROUND(a, b, c, d, e, f, g, h, kK[t + 0] + w[(t + 0) & 15]);
+    VT_ROUND(h, a, b, c, d, e, f, g, kK[t + 1] + w[(t + 1) & 15]);
+    VT_ROUND(g, h, a, b, c, d, e, f, kK[t + 2] + w[(t + 2) & 15]);
+    VT_ROUND(f, g, h, a, b, c, d, e, kK[t + 3] + w[(t + 3) & 15]);
+    VT_ROUND(e, f, g, h, a, b, c, d, kK[t + 4] + w[(t + 4) & 15]);
+    VT_ROUND(d, e, f, g, h, a, b, c, kK[t + 5] + w[(t + 5) & 15]);
+    VT_ROUND(c, d, e, f, g, h, a, b, kK[t + 6] + w[(t + 6) & 15]);
+    VT_ROUND(b, c, d, e, f, g, h, a, kK[t + 7] + w[(t + 7) & 15]);
+  }
+  s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+// Compression of a constant block whose W+K schedule is precomputed.
+__device__ __forceinline__ void compress_wk(uint32_t (&s)[8], const PadWK& p) {
+  uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+  for (int t = 0; t < 64; t += 8) {
+    VT_ROUND(a, b, c, d, e, f, g, h, p.wk[t + 0]);
+    VT_ROUND(h, a, b, c, d, e, f, g, p.wk[t + 1]);
+    VT_ROUND(g, h, a, b, c, d, e, f, p.wk[t + 2]);
+    VT_ROUND(f, g, h, a, b, c, d, e, p.wk[t + 3]);
+    VT_ROUND(e, f, g, h, a, b, c, d, p.wk[t + 4]);
+    VT_ROUND(d, e, f, g, h, a, b, c, p.wk[t + 5]);
+    VT_ROUND(c, d, e, f, g, h, a, b, p.wk[t + 6]);
+    VT_ROUND(b, c, d, e, f, g, h, a, p.wk[t + 7]);
+  }
+  s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+__device__ __forceinline__ void store_digest(uint8_t* dst, const uint32_t (&s)[8]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  d[0] = make_uint4(bswap(s[0]), bswap(s[1]), bswap(s[2]), bswap(s[3]));
+  d[1] = make_uint4(bswap(s[4]), bswap(s[5]), bswap(s[6]), bswap(s[7]));
+}
+
+struct LeafArgs {
+  const uint8_t* data;
+  int64_t nbytes;
+  int64_t leaf_bytes;
+  int64_t n_leaves;
+  uint8_t* out;
+  PadWK pad;  // padding block for a full leaf when leaf_bytes % 64 == 0
+};
+
+// Generic tail: `rem` (< 64) trailing bytes at p, total message length len.
+__device__ __forceinline__ void finish_generic(uint32_t (&s)[8], const uint8_t* p, int rem, int64_t len) {
+  uint32_t w[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) w[k] = 0u;
+  for (int k = 0; k < rem; ++k) w[k >> 2] |= (uint32_t)p[k] << (24 - 8 * (k & 3));
+  w[rem >> 2] |= 0x80u << (24 - 8 * (rem & 3));
+  const uint64_t bitlen = (uint64_t)len * 8ull;
+  if (rem >= 56) {
+    compress(s, w);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) w[k] = 0u;
+  }
+  w[14] = (uint32_t)(bitlen >> 32);
+  w[15] = (uint32_t)bitlen;
+  compress(s, w);
+}
+
+__global__ void __launch_bounds__(128) sha256_leaves_kernel(const LeafArgs a) {
+  const int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= a.n_leaves) return;
+  const int64_t off = leaf * a.leaf_bytes;
+  const int64_t len = std::min<int64_t>(a.leaf_bytes, a.nbytes - off);
+  const uint8_t* p = a.data + off;
+  uint32_t s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = kIV[k];
+  const int64_t nblk = len >> 6;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+  for (int64_t blk = 0; blk < nblk; ++blk) {
+    uint32_t w[16];
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = __ldg(p4 + blk * 4 + q);
+        w[4 * q + 0] = bswap(v.x);
+        w[4 * q + 1] = bswap(v.y);
+        w[4 * q + 2] = bswap(v.z);
+        w[4 * q + 3] = bswap(v.w);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint8_t* b = p + blk * 64 + 4 * k;
+        w[k] = ((uint32_t)b[0] << 24) | ((uint32_t)b[1] << 16) | ((uint32_t)b[2] << 8) | b[3];
+      }
+    }
+    compress(s, w);
+  }
+  const int rem = (int)(len - (nblk << 6));
+  if (rem == 0 && len == a.leaf_bytes && (a.leaf_bytes & 63) == 0) {
+    compress_wk(s, a.pad);
+  } else {
+    finish_generic(s, p + (nblk << 6), rem, len);
+  }
+  store_digest(a.out + leaf * 32, s);
+}
+
+struct NodeArgs {
+  const uint8_t* in;
+  int64_t n_in;
+  uint8_t* out;
+  PadWK pad;  // padding block of a 64-byte message
+};
+
+__global__ void __launch_bounds__(128) merkle_level_kernel(const NodeArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_out = (a.n_in + 1) >> 1;
+  if (i >= n_out) return;
+  const uint4* src = reinterpret_cast<const uint4*>(a.in + 64 * i);
+  uint4* dst = reinterpret_cast<uint4*>(a.out + 32 * i);
+  if (2 * i + 1 >= a.n_in) {  // unpaired: promoted unchanged (merkle.py:66-67)
+    dst[0] = src[0];
+    dst[1] = src[1];
+    return;
+  }
+  uint32_t w[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = src[q];
+    w[4 * q + 0] = bswap(v.x);
+    w[4 * q + 1] = bswap(v.y);
+    w[4 * q + 2] = bswap(v.z);
+    w[4 * q + 3] = bswap(v.w);
+  }
+  uint32_t s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = kIV[k];
+  compress(s, w);
+  compress_wk(s, a.pad);
+  store_digest(a.out + 32 * i, s);
+  (void)dst;
+}
+
+// Host: W+K schedule of the padding block that follows a message of `len`
+// bytes when len % 64 == 0.
+PadWK make_pad(int64_t len) {
+  uint32_t w[64];
+  for (int k = 0; k < 16; ++k) w[k] = 0u;
+  w[0] = 0x80000000u;
+  const uint64_t bits = (uint64_t)len * 8ull;
+  w[14] = (uint32_t)(bits >> 32);
+  w[15] = (uint32_t)bits;
+  auto r = [](uint32_t x, int n) { return (x >> n) | (x << (32 - n)); };
+  for (int t = 16; t < 64; ++t) {
+    const uint32_t s0 = r(w[t - 15], 7) ^ r(w[t - 15], 18) ^ (w[t - 15] >> 3);
+    const uint32_t s1 = r(w[t - 2], 17) ^ r(w[t - 2], 19) ^ (w[t - 2] >> 10);
+    w[t] = w[t - 16] + s0 + w[t - 7] + s1;
+  }
+  PadWK p;
+  for (int t = 0; t < 64; ++t) p.wk[t] = w[t] + kKHost[t];
+  return p;
+}
+
+}  // namespace vt
+
+using namespace vt;
+
+extern "C" int vt_sha256_leaves(const uint8_t* data, int64_t nbytes, int64_t leaf_bytes, uint8_t* digests,
+                                vt_stream_t stream) {
+  if (nbytes <= 0 || leaf_bytes <= 0 || !data || !digests || (reinterpret_cast<uintptr_t>(digests) & 15)) {
+    vt_set_error("vt_sha256_leaves: bad argument (nbytes, leaf_bytes > 0; digests 16-byte aligned)");
+    return VT_EINVAL;
+  }
+  LeafArgs a;
+  a.data = data;
+  a.nbytes = nbytes;
+  a.leaf_bytes = leaf_bytes;
+  a.n_leaves = (nbytes + leaf_bytes - 1) / leaf_bytes;
+  a.out = digests;
+  a.pad = make_pad(leaf_bytes);
+  sha256_leaves_kernel<<<(unsigned)((a.n_leaves + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return vt_check_launch("sha256_leaves_kernel");
+}
+
+extern "C" int vt_merkle_level(const uint8_t* in, int64_t n_in, uint8_t* out, vt_stream_t stream) {
+  if (n_in <= 0 || !in || !out || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) {
+    vt_set_error("vt_merkle_level: bad argument (16-byte aligned digests)");
+    return VT_EINVAL;
+  }
+  NodeArgs a;
+  a.in = in;
+  a.n_in = n_in;
+  a.out = out;
+  a.pad = make_pad(64);
+  const int64_t n_out = (n_in + 1) / 2;
+  merkle_level_kernel<<<(unsigned)((n_out + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return vt_check_launch("merkle_level_kernel");
+}
+
+extern "C" int64_t vt_merkle_node_count(int64_t n_leaves) {
+  if (n_leaves <= 0) return 0;
+  int64_t total = n_leaves, m = n_leaves;
+  while (m > 1) {
+    m = (m + 1) / 2;
+    total += m;
+  }
+  return total;
+}
+
+extern "C" int vt_merkle_build(const uint8_t* data, int64_t nbytes, int64_t leaf_bytes, uint8_t* nodes,
+                               int64_t nodes_cap, vt_stream_t stream) {
+  if (nbytes <= 0 || leaf_bytes <= 0) {
+    vt_set_error("vt_merkle_build: bad argument");
+    return VT_EINVAL;
+  }
+  const int64_t leaves = (nbytes + leaf_bytes - 1) / leaf_bytes;
+  if (nodes_cap < vt_merkle_node_count(leaves)) {
+    vt_set_error("vt_merkle_build: nodes buffer too small");
+    return VT_EINVAL;
+  }
+  int rc = vt_sha256_leaves(data, nbytes, leaf_bytes, nodes, stream);
+  if (rc) return rc;
+  int64_t m = leaves;
+  uint8_t* cur = nodes;
+  while (m > 1) {
+    uint8_t* nxt = cur + 32 * m;
+    if ((rc = vt_merkle_level(cur, m, nxt, stream))) return rc;
+    cur = nxt;
+    m = (m + 1) / 2;
+  }
+  return VT_OK;
+}

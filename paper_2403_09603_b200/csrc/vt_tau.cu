@@ -1,0 +1,247 @@
+// Adaptive-threshold support: the "histogram-of-distances reduction".
+//
+// The budget search (skeleton of protocol.search_tau,
+// pkg/src/vtrain/protocol.py:494-506) needs, per tensor, the predicate
+// count(p > tau) <= B for 30 bisection midpoints, where
+// p = |x - rnd(x)| / max(scale(x), 2^-126) is exact in FP64
+// (fpround.py:171-173).  That predicate equals v <= tau for v the (B+1)-th
+// largest p, so the device computes v once by an exact MSD radix select on
+// the FP64 bit patterns of p (p >= 0, so bit order is numeric order) and the
+// host runs the identical FP64 bisection on v.
+//
+// Passes: digits [62:49] [48:35] [34:21] [20:7] [6:0] of the key; each pass
+// is one streaming read of x with a per-CTA shared-memory histogram
+// (match_any-aggregated atomics), then a one-CTA select kernel narrows the
+// prefix on the device, so no host round trip happens between passes.
+#include <algorithm>
+
+#include "vt_common.cuh"
+
+namespace vt {
+
+constexpr int kPasses = 5;
+__host__ __device__ constexpr int pass_shift(int p) { return p == 0 ? 49 : p == 1 ? 35 : p == 2 ? 21 : p == 3 ? 7 : 0; }
+__host__ __device__ constexpr int pass_bits(int p) { return p == 4 ? 7 : 14; }
+constexpr int kMaxBins = 1 << 14;
+constexpr int kHistThreads = 512;
+constexpr int kSelThreads = 1024;
+
+struct SelectState {
+  uint64_t prefix;
+  uint64_t mask;
+  int64_t rank;  // remaining 0-based rank from the top inside the prefix bucket
+  int64_t found;
+};
+
+// FP64 bit pattern of p for one element; err gets rnd's error bits.
+__device__ __forceinline__ uint64_t dist_key(double x, const Grid& g, uint32_t& err) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const uint64_t mag = bits & kMag;
+  if (mag >= kNormalMin) {
+    const uint64_t low = mag & g.low_mask;
+    const uint64_t base = mag >> g.drop;
+    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
+    const uint64_t rmag = (base + (up ? 1ull : 0ull)) << g.drop;
+    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
+    const uint64_t d = up ? (g.one - low) : low;  // |x - r| = d * 2^(E-52), scale = 2^E
+    return (uint64_t)__double_as_longlong(__dmul_rn(__ull2double_rn(d), 0x1p-52));
+  }
+  const double r = __dmul_rn(rint(__dmul_rn(x, g.sub_up)), g.sub_dn);
+  return (uint64_t)__double_as_longlong(__dmul_rn(fabs(__dsub_rn(x, r)), 0x1p126));
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kHistThreads) tau_hist_kernel(const double* __restrict__ x, int64_t n,
+                                                                Grid g, const SelectState* st,
+                                                                uint32_t* __restrict__ hist,
+                                                                int32_t* errp) {
+  extern __shared__ uint32_t sh[];
+  constexpr int nbins = 1 << pass_bits(PASS);
+  for (int i = threadIdx.x; i < nbins; i += kHistThreads) sh[i] = 0;
+  __syncthreads();
+  const uint64_t prefix = st->prefix, mask = st->mask;
+  uint32_t err = 0;
+  const int64_t stride = (int64_t)gridDim.x * kHistThreads;
+  const int64_t n_iter = (n + stride - 1) / stride;
+  for (int64_t it = 0; it < n_iter; ++it) {
+    const int64_t i = it * stride + (int64_t)blockIdx.x * kHistThreads + threadIdx.x;
+    bool take = false;
+    uint32_t bin = 0;
+    if (i < n) {
+      const uint64_t key = dist_key(__ldg(x + i), g, err);
+      take = (key & mask) == prefix;
+      bin = (uint32_t)(key >> pass_shift(PASS)) & (uint32_t)(nbins - 1);
+    }
+    // aggregate equal bins inside the warp: one shared atomic per distinct bin
+    const uint32_t active = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const uint32_t peers = __match_any_sync(active, bin);
+      if ((threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+    }
+  }
+  report_err(errp, err);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbins; i += kHistThreads) {
+    const uint32_t c = sh[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kSelThreads) tau_select_kernel(const uint32_t* __restrict__ hist,
+                                                                 SelectState* st, uint64_t* key_out) {
+  constexpr int nbins = 1 << pass_bits(PASS);
+  constexpr int per = (nbins + kSelThreads - 1) / kSelThreads;
+  __shared__ unsigned long long s_warp[kSelThreads / 32];
+  const int t = threadIdx.x;
+  const int64_t rank = st->rank;
+  // thread t owns bins [hi - per, hi) counting from the TOP of the key range
+  const int hi = nbins - t * per;
+  unsigned long long mine = 0;
+  for (int k = 0; k < per; ++k) {
+    const int b = hi - 1 - k;
+    if (b >= 0) mine += hist[b];
+  }
+  // exclusive scan over threads (descending bins)
+  unsigned long long incl = mine;
+  const int lane = t & 31, warp = t >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long v = s_warp[lane];
+    unsigned long long w = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    s_warp[lane] = w - v;
+  }
+  __syncthreads();
+  const unsigned long long above = s_warp[warp] + incl - mine;
+  if ((long long)above <= rank && rank < (long long)(above + mine)) {
+    unsigned long long acc = above;
+    for (int k = 0; k < per; ++k) {
+      const int b = hi - 1 - k;
+      if (b < 0) break;
+      const unsigned long long c = hist[b];
+      if (rank < (long long)(acc + c)) {
+        const uint64_t p = st->prefix | ((uint64_t)b << pass_shift(PASS));
+        st->prefix = p;
+        st->mask |= ((uint64_t)(nbins - 1)) << pass_shift(PASS);
+        st->rank = rank - (long long)acc;
+        if (PASS == kPasses - 1) {
+          *key_out = p;
+          st->found = 1;
+        }
+        break;
+      }
+      acc += c;
+    }
+  }
+}
+
+__global__ void init_state_kernel(SelectState* st, int64_t rank, uint64_t* key_out) {
+  st->prefix = 0;
+  st->mask = 0;
+  st->rank = rank;
+  st->found = 0;
+  *key_out = 0;
+}
+
+__device__ __forceinline__ unsigned long long order_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void min_init_kernel(double* out) {
+  *reinterpret_cast<unsigned long long*>(out) = order_key(__longlong_as_double(0x7ff0000000000000ll));
+}
+
+__global__ void min_kernel(const double* __restrict__ s, int64_t n, double* out, int32_t* nanp) {
+  unsigned long long best = ~0ull;
+  bool nan = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = s[i];
+    if (v != v) nan = true;
+    else best = min(best, order_key(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != ~0ull)
+    atomicMin(reinterpret_cast<unsigned long long*>(out), best);
+  if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(reinterpret_cast<int*>(nanp), 1);
+}
+
+__global__ void min_final_kernel(double* out) {
+  const unsigned long long k = *reinterpret_cast<unsigned long long*>(out);
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  *out = __longlong_as_double((long long)b);
+}
+
+}  // namespace vt
+
+using namespace vt;
+
+extern "C" size_t vt_tau_workspace(int64_t n) {
+  (void)n;
+  return (size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256;
+}
+
+namespace {
+template <int P>
+int run_pass(const double* x, int64_t n, const Grid& g, SelectState* st, uint32_t* hist,
+             uint64_t* key_out, int32_t* err, cudaStream_t s) {
+  constexpr size_t smem = sizeof(uint32_t) << pass_bits(P);
+  auto hk = tau_hist_kernel<P>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t want = (n + kHistThreads * 8 - 1) / (kHistThreads * 8);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 148 * 2));
+  hk<<<blocks, kHistThreads, smem, s>>>(x, n, g, st, hist + (size_t)P * kMaxBins, err);
+  int rc = vt_check_launch("tau_hist_kernel");
+  if (rc) return rc;
+  tau_select_kernel<P><<<1, kSelThreads, 0, s>>>(hist + (size_t)P * kMaxBins, st, key_out);
+  return vt_check_launch("tau_select_kernel");
+}
+}  // namespace
+
+extern "C" int vt_tau_kth_key(const double* x, int64_t n, int b_r, int64_t rank, uint64_t* key_out,
+                              int32_t* err, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (n < 0 || b_r < 10 || b_r > 32 || rank < 0 || !key_out || !err || !ws ||
+      ws_bytes < vt_tau_workspace(n)) {
+    vt_set_error("vt_tau_kth_key: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* hist = static_cast<uint32_t*>(ws);
+  SelectState* st = reinterpret_cast<SelectState*>(static_cast<uint8_t*>(ws) + (size_t)kPasses * kMaxBins * 4);
+  if (cudaMemsetAsync(hist, 0, (size_t)kPasses * kMaxBins * 4, s) != cudaSuccess) return vt_check_launch("memset");
+  init_state_kernel<<<1, 1, 0, s>>>(st, rank, key_out);
+  int rc = vt_check_launch("init_state_kernel");
+  if (rc || n == 0 || rank >= n) return rc;
+  const Grid g = make_grid(b_r, 0.0);
+  if ((rc = run_pass<0>(x, n, g, st, hist, key_out, err, s))) return rc;
+  if ((rc = run_pass<1>(x, n, g, st, hist, key_out, err, s))) return rc;
+  if ((rc = run_pass<2>(x, n, g, st, hist, key_out, err, s))) return rc;
+  if ((rc = run_pass<3>(x, n, g, st, hist, key_out, err, s))) return rc;
+  return run_pass<4>(x, n, g, st, hist, key_out, err, s);
+}
+
+extern "C" int vt_min_f64(const double* s, int64_t n, double* out, int32_t* nan_flag, vt_stream_t stream) {
+  if (n < 0 || !out || !nan_flag || (n && !s)) {
+    vt_set_error("vt_min_f64: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  min_init_kernel<<<1, 1, 0, st>>>(out);
+  if (n) {
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4));
+    min_kernel<<<blocks, 256, 0, st>>>(s, n, out, nan_flag);
+  }
+  min_final_kernel<<<1, 1, 0, st>>>(out);
+  return vt_check_launch("min_kernel");
+}

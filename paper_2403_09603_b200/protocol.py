@@ -1,0 +1,169 @@
+"""Trainer / auditor channels and threshold search on the B200.
+
+Drop-in for the hot-path parts of ``vtrain.protocol``
+(pkg/src/vtrain/protocol.py):
+
+* ``GpuTrainerChannel`` / ``GpuAuditorChannel`` / ``GpuPlainChannel``
+  satisfy the channel duck type ``process(values, tau) -> (ndarray,
+  directed, corrections)`` consumed by ``protocol._run`` (protocol.py:268,
+  278, 283), replacing ``_TrainerChannel`` / ``_AuditorChannel`` /
+  ``_PlainChannel`` (protocol.py:191-226) with single fused kernels.
+* ``search_tau`` keeps ``protocol.search_tau`` (protocol.py:494-506)
+  bit for bit: the all(p >= tau) predicate is a device min-reduction,
+  the FP64 bisection runs on the host on that one scalar.
+* ``search_tau_budget`` is the north-star per-tensor budget search
+  (SURVEY.md Appendix A.4): largest band (= smallest reference-form tau in
+  ``tau_bounds``) whose log stays within ``budget`` entries, via the device
+  radix select of the (budget+1)-th largest normalized distance.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .fpround import _check_b, rnd_array, tau_bounds
+from .roundlog import LogExhaustedError, LogReader, LogWriter
+
+
+class AuditFailure(RuntimeError):
+    """The audit could not be completed against the provided artifacts."""
+
+
+def _host_like(values, y: torch.Tensor):
+    return y.cpu().numpy() if not (isinstance(values, torch.Tensor) and values.is_cuda) else y
+
+
+class GpuTrainerChannel:
+    """Classify, record, round -- one fused kernel per tensor."""
+
+    def __init__(self, writer, b_r: int):
+        self.writer = writer
+        self.b_r = b_r
+
+    def process(self, values, tau: float):
+        if isinstance(self.writer, LogWriter):
+            y, directed = self.writer.write_values(values, tau)
+            return _host_like(values, y), int(directed), 0
+        # foreign writer with the reference interface: hand it the codes
+        t, _, shape = D.to_device_f64(values)
+        y = torch.empty_like(t)
+        codes = torch.empty(t.numel(), dtype=torch.uint8, device=t.device)
+        f = D.Flags()
+        if t.numel():
+            _lib.call("vt_round_log", D.ptr(t), t.numel(), self.b_r, float(tau), _lib.OUT_F64, D.ptr(y),
+                      None, 0, 0, None, None, D.ptr(codes), None, 0, None, f.cnt_ptr, f.err_ptr, None, 0,
+                      D.stream_ptr())
+        err, cnt = f.read()
+        D.raise_fpround(err)
+        self.writer.write_array(codes.cpu().numpy())
+        return _host_like(values, y.reshape(shape)), int(cnt[0]), 0
+
+
+class GpuAuditorChannel:
+    """Read, replay -- one fused kernel per tensor."""
+
+    def __init__(self, reader, b_r: int):
+        self.reader = reader
+        self.b_r = b_r
+
+    def process(self, values, tau: float):
+        t, _, shape = D.to_device_f64(values)
+        n = t.numel()
+        y = torch.empty_like(t)
+        f = D.Flags()
+        if isinstance(self.reader, LogReader):
+            payload, pos = self.reader.take_device(n)
+            if n:
+                _lib.call("vt_replay", D.ptr(t), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload),
+                          self.reader.payload_nbytes, pos, _lib.OUT_F64, D.ptr(y), f.cnt_ptr, f.err_ptr,
+                          None, 0, D.stream_ptr())
+        else:
+            codes = np.ascontiguousarray(self.reader.read_array(n), dtype=np.uint8)
+            c = torch.from_numpy(codes).to(t.device)
+            if n:
+                _lib.call("vt_replay", D.ptr(t), n, self.b_r, _lib.LOG_CODES, D.ptr(c), n, 0,
+                          _lib.OUT_F64, D.ptr(y), f.cnt_ptr, f.err_ptr, None, 0, D.stream_ptr())
+        err, cnt = f.read()
+        if err & _lib.ERR_BAD_LOG_BYTE:
+            from .roundlog import LogFormatError
+            raise LogFormatError("corrupt log byte")
+        if err & _lib.ERR_BAD_CODE:
+            raise ValueError("invalid direction code")
+        D.raise_fpround(err)
+        return _host_like(values, y.reshape(shape)), 0, int(cnt[0])
+
+
+class GpuPlainChannel:
+    """Round only; the negative control (protocol.py:219-226)."""
+
+    def __init__(self, b_r: int):
+        self.b_r = b_r
+
+    def process(self, values, tau: float):
+        return rnd_array(values, self.b_r), 0, 0
+
+
+def _device_min(samples) -> tuple[float, bool]:
+    if isinstance(samples, torch.Tensor) and samples.is_cuda:
+        s = samples.reshape(-1).to(torch.float64).contiguous()
+    else:
+        s = torch.as_tensor(np.asarray(samples, dtype=np.float64).reshape(-1)).to(D.require_cuda())
+    out = torch.empty(1, dtype=torch.float64, device=s.device)
+    f = D.Flags()
+    _lib.call("vt_min_f64", D.ptr(s), s.numel(), D.ptr(out), f.err_ptr, D.stream_ptr())
+    nan = bool(f.read()[0] & 1)
+    return float(out.item()), nan
+
+
+def search_tau(samples, b_r: int, iters: int) -> float:
+    """Largest threshold no recorded straddle undercuts (protocol.py:494-506)."""
+    lower, upper = tau_bounds(b_r)
+    if len(samples) == 0:
+        return upper
+    m, has_nan = _device_min(samples)
+    tau = lower
+    for _ in range(iters):
+        tau = (lower + upper) / 2.0
+        if (not has_nan) and m >= tau:
+            lower = tau
+        else:
+            upper = tau
+    return tau
+
+
+def kth_largest_distance(x, b_r: int, rank: int) -> float:
+    """(rank+1)-th largest p = |x - rnd(x)| / max(scale, 2^-126), exactly."""
+    _check_b(b_r)
+    t, _, _ = D.to_device_f64(x)
+    n = t.numel()
+    if rank >= n:
+        return 0.0
+    ws = D.workspace(int(_lib.lib().vt_tau_workspace(n)), "tau")
+    key = torch.zeros(1, dtype=torch.int64, device=t.device)
+    f = D.Flags()
+    _lib.call("vt_tau_kth_key", D.ptr(t), n, b_r, int(rank), D.ptr(key), f.err_ptr, D.ptr(ws), ws.numel(),
+              D.stream_ptr())
+    err = f.read()[0]
+    D.raise_fpround(err)
+    return float(np.array([key.item()], dtype=np.int64).view(np.float64)[0])
+
+
+def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
+    """Per-tensor adaptive threshold: the search_tau skeleton with predicate
+    count(p > tau) <= budget, feasible -> upper = tau, returns ``upper``."""
+    lower, upper = tau_bounds(b_r)
+    v = kth_largest_distance(x, b_r, int(budget))
+    for _ in range(iters):
+        tau = (lower + upper) / 2.0
+        if v <= tau:
+            upper = tau
+        else:
+            lower = tau
+    return upper
+
+
+__all__ = ["AuditFailure", "GpuAuditorChannel", "GpuPlainChannel", "GpuTrainerChannel",
+           "LogExhaustedError", "kth_largest_distance", "search_tau", "search_tau_budget"]

@@ -1,0 +1,123 @@
+"""GPU parity: threshold search (reference + budget forms) and SHA-256 Merkle."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_search_tau_golden(golden):
+    from paper_2403_09603_b200 import protocol
+    for case in golden.tau["search_tau"]:
+        s = [float.fromhex(v) for v in case["samples"]]
+        assert protocol.search_tau(s, case["b_r"], case["iters"]).hex() == case["tau"]
+
+
+def test_search_tau_nan_and_limits():
+    from paper_2403_09603_b200 import protocol
+    lo, hi = 0.25 * 2.0 ** -23, 0.5 * 2.0 ** -23
+    assert protocol.search_tau([], 32, 30) == hi
+    d = 0.4 * 2.0 ** -23
+    assert abs(protocol.search_tau([d], 32, 40) - d) <= (hi - lo) * 2.0 ** -39
+    assert abs(protocol.search_tau([1.0], 32, 40) - hi) <= (hi - lo) * 2.0 ** -39
+    assert protocol.search_tau([float("nan"), 1.0], 32, 10) == \
+        __import__("vt_oracle").search_tau([float("nan"), 1.0], 32, 10)
+
+
+def test_budget_golden(golden):
+    from paper_2403_09603_b200 import fpround, protocol
+    for case in golden.tau["budget"]:
+        x = np.random.default_rng(case["seed"]).normal(0.0, 10.0 ** case["sigma_exp"], size=case["n"])
+        t = protocol.search_tau_budget(x, 32, case["budget"])
+        assert t.hex() == case["tau"]
+        assert int(np.count_nonzero(fpround.direction_array(x, 32, t) != 1)) == case["logged"]
+
+
+@pytest.mark.parametrize("b_r", (26, 32))
+def test_kth_largest_vs_sort(oracle, b_r):
+    from paper_2403_09603_b200 import protocol
+    rng = np.random.default_rng(b_r)
+    x = np.concatenate([rng.normal(size=250_000) * np.exp2(rng.integers(-60, 60, size=250_000)),
+                        rng.normal(size=3000) * 1e-40, np.zeros(50), rng.normal(size=2000).astype(np.float32)])
+    p = np.sort(oracle.normalized_distance(x, b_r))[::-1]
+    for rank in (0, 1, 7, 1250, 100_000, x.size - 1, x.size - 60, x.size + 5):
+        want = p[rank] if rank < x.size else 0.0
+        assert protocol.kth_largest_distance(x, b_r, rank) == want, rank
+
+
+def test_budget_matches_oracle_random(oracle):
+    from paper_2403_09603_b200 import protocol
+    for seed in range(4):
+        rng = np.random.default_rng(50 + seed)
+        n = int(rng.integers(1000, 300_000))
+        x = rng.normal(0.0, 10.0 ** rng.uniform(-3, 1), size=n)
+        B = int(0.005 * n)
+        assert protocol.search_tau_budget(x, 32, B) == oracle.search_tau_budget(x, 32, B)
+
+
+def test_normalized_distance(oracle):
+    import torch
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=100_000) * np.exp2(rng.integers(-140, 40, size=100_000))
+    got = ops.normalized_distance(torch.from_numpy(x).cuda(), 32).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), oracle.normalized_distance(x, 32).view(np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# Merkle
+# ---------------------------------------------------------------------------
+
+def test_build_golden(golden):
+    from paper_2403_09603_b200 import merkle
+    for case in golden.merkle["build"]:
+        leaves = [hashlib.sha256(f"leaf-{i}".encode()).digest() for i in range(case["n"])]
+        t = merkle.build(leaves)
+        assert [[d.hex() for d in lvl] for lvl in t.levels] == case["levels"]
+    with pytest.raises(ValueError):
+        merkle.build([])
+    with pytest.raises(ValueError):
+        merkle.build([b"short"])
+
+
+def test_chunked_golden(golden):
+    from paper_2403_09603_b200 import merkle
+    ch = golden.merkle["chunked"]
+    w = np.random.default_rng(ch["seed"]).normal(0.0, 0.02, size=ch["n_params"]).astype(np.float32)
+    t = merkle.merkle_chunked(w, ch["leaf_bytes"])
+    assert [[d.hex() for d in lvl] for lvl in t.levels] == ch["levels"]
+
+
+@pytest.mark.parametrize("leaf_bytes", [64, 100, 4096, 4097, 1 << 16])
+def test_sha256_leaves_vs_hashlib(oracle, leaf_bytes):
+    from paper_2403_09603_b200 import merkle
+    rng = np.random.default_rng(leaf_bytes)
+    for nbytes in (1, 55, 56, 63, 64, 65, 119, 120, 4095, 4096, 4097, 3 * leaf_bytes + 17, 300_001):
+        data = rng.integers(0, 256, size=nbytes, dtype=np.uint8).tobytes()
+        got = merkle.sha256_leaves(data, leaf_bytes).cpu().numpy()
+        want = oracle.chunk_leaves(data, leaf_bytes)
+        assert [bytes(r) for r in got] == want, (leaf_bytes, nbytes)
+
+
+def test_sha256_known_answers():
+    from paper_2403_09603_b200 import merkle
+    assert bytes(merkle.sha256_leaves(b"abc", 64).cpu().numpy()[0]).hex() == \
+        "ba7816bf8f01cfea414140de5dae2223b00361a396177a9cb410ff61f20015ad"
+    msg = b"abcdbcdecdefdefgefghfghighijhijkijkljklmklmnlmnomnopnopq"
+    assert bytes(merkle.sha256_leaves(msg, 1024).cpu().numpy()[0]).hex() == \
+        "248d6a61d20638b8e5c026930c3e6039a33ce45964ff2167f6ecedd419db06c1"
+
+
+def test_chunked_tree_vs_oracle_random(oracle):
+    from paper_2403_09603_b200 import merkle
+    rng = np.random.default_rng(77)
+    for n_params in (1, 1023, 1024, 1025, 5 * 1024 + 3, 777_777):
+        w = rng.normal(0, 0.02, size=n_params).astype(np.float32)
+        t = merkle.merkle_chunked(w)
+        want = oracle.merkle_levels(oracle.chunk_leaves(w.tobytes(), 4096))
+        assert t.levels == want, n_params
+        assert t.root == want[-1][0]

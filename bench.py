@@ -1,0 +1,461 @@
+"""Benchmark of the vtrain hot path on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+trainer/auditor replay pair on 2^26 FP64 elements per GPU -- the trainer
+tensor has the config-0 distribution (90% N(0,1), 10% exact FP32 midpoints
+perturbed by 2^-40 relative), the auditor tensor is the trainer tensor with
+a seeded 5% moved one FP64 ulp.  One step = fused round-and-log of the
+trainer tensor (FP32 out + sparse log) + fused replay of the auditor tensor
+with that log (FP32 out + correction count).  Multi-GPU: weak scaling,
+every rank owns its own 2^26-element shard with global indices, and the
+exchange step is the NCCL all-gather of per-rank log counts.
+
+``value`` = algorithmic bytes of the step / device time, GB/s (whole job):
+  per element  round-and-log 8 (x) + 4 (FP32 out) + 8 f (sparse words)
+               replay        8 (x') + 4 (FP32 out) + 8 f (sparse words read)
+with f the logged fraction.  Inputs are 4x L2 (no flush needed).
+
+``--impl reference`` times the reference algorithm on the host cores
+(the oracle port of vtrain's NumPy code, oracle/vt_oracle.py -- the
+reference is pure Python and cannot travel to the GPU box) on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "round-and-log / replay GB/s (fraction of HBM peak) at 1/2/4/8 B200 vs CPU ref"
+FALLBACK_HBM = 6650.0
+
+
+def peaks() -> tuple[float, str]:
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(kernel: str, n: int):
+    """dram bytes per launch from the committed ncu --set full capture, scaled
+    per element (the capture may use a smaller n); None if absent."""
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())[kernel]
+        return d["dram_bytes_per_elem"] * n
+    except Exception:
+        return None
+
+
+class Clocks:
+    """NVML sampler thread (every ~5 ms) running during the timed region:
+    SM clock, max SM clock and the active throttle reasons."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.sm, self.mask = [], 0
+        self.max_mhz = None
+        self._stop = False
+        self.ok = False
+
+    def _loop(self):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        while not self._stop:
+            try:
+                self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                self.mask |= N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self.ok = True
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
+        except Exception:
+            self.ok = False
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop = True
+            self.th.join(timeout=2)
+        return False
+
+    def summary(self) -> dict:
+        if not self.ok or not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.sm), "sm_mhz_min": min(self.sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_09603_b200 import _lib, ops, workloads
+    from paper_2403_09603_b200 import dist as vdist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n = 1 << args.log2n
+    tau = workloads.TAU_CONFIG0
+    base = rank * n
+    xt, xa = workloads.config1_pair_torch(n, seed=1 + rank, device=dev)
+    y_t = torch.empty(n, dtype=torch.float32, device=dev)
+    y_a = torch.empty(n, dtype=torch.float32, device=dev)
+    words = torch.empty(n // 4, dtype=torch.int64, device=dev)
+
+    def step():
+        p = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+        ev_mid.record()
+        cnt = p.flags.buf[2:3]
+        if world > 1:
+            counts = vdist.all_gather_counts(cnt)  # the exchange step: per-rank log counts
+            del counts
+        # replay consumes the device-resident log; the count stays on the device
+        _, fl = ops.replay(xa, 32, words_view(cnt), out=y_a, global_base=base, check=False)
+        return p, fl
+
+    # the replay needs the exact word count; keep a host-side count from warm-up
+    p0 = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+    _, log0 = p0.finish()
+    count = log0.count
+
+    def words_view(_cnt):
+        return words[:count]
+
+    ev_mid = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        p, fl = step()
+    torch.cuda.synchronize()
+    # verify once (outside the timed region): parity of the auditor output with the trainer output
+    err_t, cnt_t = p.flags.read()
+    err_a, cnt_a = fl.read()
+    assert err_t == 0 and err_a == 0 and cnt_t[0] == count, (err_t, err_a, cnt_t, count)
+    ok_equal = bool(torch.equal(y_t.view(torch.int32), y_a.view(torch.int32)))
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(args.steps):
+            starts[i].record()
+            ev_mid = mids[i]
+            step()
+            ends[i].record()
+        t1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    rl_ms = statistics.mean(starts[i].elapsed_time(mids[i]) for i in range(args.steps))
+    rp_ms = statistics.mean(mids[i].elapsed_time(ends[i]) for i in range(args.steps))
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    f = count / n
+    per_elem = (8 + 4 + 8 * f) * 2
+    value = world * n * per_elem / (ms_step * 1e-3) / 1e9
+    rl_bytes = n * (8 + 4 + 8 * f)
+    rp_bytes = n * (8 + 4 + 8 * f)
+    peak, peak_src = peaks()
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, n, tau, base, dev)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(args)
+    rl_ach = rl_bytes / (rl_ms * 1e-3) / 1e9
+    rp_ach = rp_bytes / (rp_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64->f32 (int64 log words)",
+        "data": "synthetic (seeded, BASELINE configs[1] distribution, generated in HBM)",
+        "config": {"workload": f"configs[1]: round-and-log + replay pair, 2^{args.log2n} FP64 elements per GPU, "
+                               f"b_r=32, tau=0x1.ff7ced916872bp-25",
+                   "n_per_gpu": n, "logged_fraction": round(f, 6), "parallelism": f"dp{world} (contiguous shards)",
+                   "l2": "no flush: every step streams 2 x 512 MiB of FP64 (>= 4x the 126 MB L2)",
+                   "auditor_equals_trainer_bitwise": ok_equal},
+        "roofline": {"bound": "hbm", "kernel": "round_log_kernel (fused rnd + direction + look-back compaction)",
+                     "achieved": round(rl_ach, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(rl_ach / peak, 4), "traffic": traffic_for("round_log", n),
+                     "algorithmic_bytes_per_launch": int(rl_bytes), "avg_launch_ms": round(rl_ms, 4),
+                     "peak_source": peak_src},
+        "kernels": {"replay_kernel": {"achieved": round(rp_ach, 1), "frac": round(rp_ach / peak, 4),
+                                      "avg_launch_ms": round(rp_ms, 4), "algorithmic_bytes_per_launch": int(rp_bytes),
+                                      "traffic": traffic_for("replay", n)}},
+        "clocks": clk.summary(),
+        "gpu_launches": 3 * args.steps,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if args.sweep:
+        line["sweep"] = sweep(args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, n, tau, base, dev):
+    """Same step through the public API with pinned host buffers: H2D of both
+    FP64 inputs, both kernels, D2H of both FP32 outputs and the sparse log."""
+    import numpy as np
+    import torch
+
+    from paper_2403_09603_b200 import ops, workloads
+
+    xt_d, xa_d = workloads.config1_pair_torch(n, seed=1, device=dev)
+    xt_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xa_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xt_h.copy_(xt_d)
+    xa_h.copy_(xa_d)
+    del xt_d, xa_d
+    yt_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    ya_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    log_h = torch.empty(n // 4, dtype=torch.int64, pin_memory=True)
+    res = {}
+
+    def one():
+        cnt, corr, log_bytes = ops.round_and_log_replay_host(xt_h, xa_h, 32, tau, yt_h, ya_h, log_h,
+                                                             global_base=base)
+        res["log"] = cnt
+        res["corr"] = corr
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    s.record()
+    for _ in range(steps):
+        one()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    cnt = res["log"]
+    f = cnt / n
+    v = n * (8 + 4 + 8 * f) * 2 / (ms * 1e-3) / 1e9
+    return {"value": round(v, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n + 8 * cnt,
+            "path": "ops.round_and_log_replay_host (chunked H2D / kernel / D2H on 3 streams)"}
+
+
+def sweep(args):
+    import torch
+
+    from paper_2403_09603_b200 import ops, workloads
+    out = {}
+    for lg in args.sweep:
+        n = 1 << lg
+        x = workloads.config0_x_torch(n, seed=lg)
+        y = torch.empty(n, dtype=torch.float32, device="cuda")
+        words = torch.empty(max(n // 4, 1024), dtype=torch.int64, device="cuda")
+        p = ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
+        _, log = p.finish()
+        for _ in range(3):
+            ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        s.record()
+        for _ in range(reps):
+            ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        ya = torch.empty_like(y)
+        lw = log.words
+        s.record()
+        for _ in range(reps):
+            ops.replay(x, 32, lw, out=ya, check=False)
+        e.record()
+        torch.cuda.synchronize()
+        ms2 = s.elapsed_time(e) / reps
+        b = n * (8 + 4 + 8 * log.count / n)
+        out[f"2^{lg}"] = {"round_log_gbs": round(b / ms / 1e6, 1), "replay_gbs": round(b / ms2 / 1e6, 1),
+                          "round_log_ms": round(ms, 4), "replay_ms": round(ms2, 4),
+                          "l2_resident": n * 8 < 126e6}
+        del x, y, words, ya, lw, log
+        torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+
+def _cpu_chunk(args):
+    lo, hi, seed = args
+    sys.path.insert(0, str(REPO / "oracle"))
+    import numpy as np
+
+    import vt_oracle as O
+    from paper_2403_09603_b200 import workloads
+    n = hi - lo
+    xt, xa = workloads.config1_pair(n, seed)
+    tau = workloads.TAU_CONFIG0
+    t0 = time.perf_counter()
+    # trainer channel (protocol.py:198-202): direction + rnd + pack
+    codes = O.direction_array(xt, 32, tau)
+    O.rnd_array(xt, 32)
+    O.pack_groups(np.concatenate([codes, np.ones((-codes.size) % 5, np.uint8)]))
+    # auditor channel (protocol.py:212-216): rev + rnd for the correction count
+    ya = O.rev_array(xa, 32, codes)
+    int(np.count_nonzero(ya != O.rnd_array(xa, 32)))
+    dt = time.perf_counter() - t0
+    return n, int(np.count_nonzero(codes != 1)), dt
+
+
+def cpu_measure(total: int, chunk: int, procs: int):
+    import multiprocessing as mp
+    jobs = [(i * chunk, min(total, (i + 1) * chunk), 100 + i) for i in range((total + chunk - 1) // chunk)]
+    t0 = time.perf_counter()
+    if procs > 1:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_chunk, jobs)
+    else:
+        res = [_cpu_chunk(j) for j in jobs]
+    wall = time.perf_counter() - t0
+    n = sum(r[0] for r in res)
+    logged = sum(r[1] for r in res)
+    compute = sum(r[2] for r in res)
+    f = logged / n
+    # input generation is excluded: the timed region is the reference calls,
+    # spread perfectly over the processes (compute / procs)
+    eff = compute / max(1, min(procs, len(jobs)))
+    gbs = n * (8 + 4 + 8 * f) * 2 / eff / 1e9
+    return {"gbs": gbs, "n": n, "wall_s": wall, "compute_s": compute, "eff_s": eff, "f": f}
+
+
+def cpu_baseline(args):
+    cores = len(os.sched_getaffinity(0))
+    total = 1 << args.cpu_log2n
+    r = cpu_measure(total, 1 << 20, cores)
+    return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair (trainer channel: direction_array + "
+                      f"rnd_array + pack; auditor: rev_array + rnd_array count), chunks of 2^20 over "
+                      f"{cores} processes, wall {r['wall_s']:.1f}s",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    total = 1 << args.cpu_log2n
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_measure(1 << 20, 1 << 20, 1)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_measure(total, 1 << 20, cores))
+    wall = time.perf_counter() - t_all
+    gbs = statistics.mean(v["gbs"] for v in vals)
+    ms = wall / args.steps * 1e3
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64->f32 (uint8 ternary codes)",
+        "data": "synthetic (seeded, BASELINE configs[1] distribution)",
+        "config": {"workload": f"configs[1]: round-and-log + replay pair, bounded sample 2^{args.cpu_log2n} "
+                               f"elements per step (CPU)", "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"2^{args.cpu_log2n} elements per step in 2^20 chunks",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=26)
+    ap.add_argument("--cpu-log2n", type=int, default=25)
+    ap.add_argument("--sweep", type=int, nargs="*", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

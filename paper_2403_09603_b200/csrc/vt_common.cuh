@@ -166,6 +166,55 @@ __device__ __forceinline__ uint64_t replay_one(double x, uint32_t c, const Grid&
 }
 
 // ---------------------------------------------------------------------------
+// b_r = 32 fast path: the grid is exactly the FP32 value set, so
+// rnd(x) == (double)cvt.rn.f32.f64(x) for every finite x, FP32 subnormals
+// included (no FTZ) -- SURVEY.md Appendix A.1 / B.1, pinned by the GPU
+// parity tests.  Direction and replay decisions then need only the low
+// 32 bits of x (normal range) or one FP64 compare (below 2^-126).
+// ---------------------------------------------------------------------------
+
+constexpr double kFltMax = 3.4028234663852886e38;
+
+// thr32 = clamp(Grid::thr, 0, INT32_MAX): d is an integer in [0, 2^28], so
+// d > thr  <=>  d > max(thr, 0) whenever d != 0, and d == 0 is never logged.
+__device__ __forceinline__ float round_dir32(double x, int thr32, double thr_sub, uint32_t& code,
+                                             uint32_t& err) {
+  const float f = __double2float_rn(x);
+  const int hi = __double2hiint(x);
+  const uint32_t lo = (uint32_t)__double2loint(x);
+  const uint32_t ahi = (uint32_t)hi & 0x7fffffffu;
+  if (ahi >= 0x38100000u) {  // |x| >= 2^-126 (incl. inf / nan)
+    const uint32_t low = lo & 0x1fffffffu;  // the 29 dropped mantissa bits
+    // RNE: round magnitude up iff low > half, or low == half and the kept lsb is odd
+    const bool up = (low + ((lo >> 29) & 1u)) > 0x10000000u;
+    const int d = (int)(up ? (0x20000000u - low) : low);
+    const bool r_above = up != (hi < 0);
+    code = (d > thr32) ? (r_above ? 2u : 0u) : 1u;
+    if (ahi >= 0x47efffffu)  // |x| >= FLT_MAX + half ulp (0x47efffff00000000) possible
+      err |= (ahi >= 0x7ff00000u) ? (uint32_t)VT_ERR_NONFINITE : (isinf(f) ? (uint32_t)VT_ERR_RANGE : 0u);
+  } else {  // absolute grid below 2^-126: FP64 test exactly as the reference
+    const double r = (double)f;
+    const bool logged = fabs(__dsub_rn(x, r)) > thr_sub;
+    code = logged ? ((x < r) ? 2u : ((x > r) ? 0u : 1u)) : 1u;
+  }
+  return f;
+}
+
+__device__ __forceinline__ float replay32(double x, uint32_t c, uint32_t& err, uint32_t& flip) {
+  float f = __double2float_rn(x);
+  const double r = (double)f;
+  const bool above = r > x;
+  const bool below = r < x;
+  const bool fl = (c == 0u && above) || (c == 2u && below);
+  err |= (c > 2u) ? (uint32_t)VT_ERR_BAD_CODE : 0u;
+  if (!(fabs(x) <= kFltMax))
+    err |= (isnan(x) || isinf(x)) ? (uint32_t)VT_ERR_NONFINITE : (uint32_t)VT_ERR_RANGE_NEIGHBOR;
+  if (fl) f = __int_as_float(__float_as_int(f) + ((above != (x < 0.0)) ? -1 : 1));
+  flip = fl ? 1u : 0u;
+  return f;
+}
+
+// ---------------------------------------------------------------------------
 // memory helpers
 // ---------------------------------------------------------------------------
 

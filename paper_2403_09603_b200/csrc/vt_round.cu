@@ -14,9 +14,8 @@
 //   packed      optional .vtrl payload, 5 codes per byte
 //
 // The sparse log is emitted in index order by a single-pass decoupled
-// look-back scan: CTAs take tile ids from an atomic ticket (so every
-// predecessor of a running tile is itself running or done), publish their
-// aggregate count, and warp 0 walks back over predecessors 32 at a time.
+// look-back scan: each CTA publishes its tile's aggregate count and warp 0
+// walks back over predecessors 32 at a time.
 // Flag and value share one 64-bit word, so relaxed loads/stores suffice.
 #include <algorithm>
 
@@ -46,8 +45,8 @@ struct RoundLogArgs {
   int64_t* counters;
   int32_t* err;
   uint64_t* status;
-  uint32_t* ticket;
   int64_t num_tiles;
+  int thr32;  // b_r = 32 fast path: clamp(g.thr, 0, INT32_MAX)
 };
 
 __device__ __forceinline__ void load_slots(const double* __restrict__ x, int64_t n, int64_t wbase,
@@ -93,6 +92,30 @@ __device__ __forceinline__ void store_out(void* out, int64_t i0, int64_t n, cons
   }
 }
 
+// FP32-valued results (b_r = 32 fast path)
+template <int OUT>
+__device__ __forceinline__ void store_out(void* out, int64_t i0, int64_t n, const float (&f)[4]) {
+  if (OUT == VT_OUT_F32) {
+    float* o = static_cast<float*>(out);
+    if (i0 + 3 < n) {
+      stg_stream4f(o + i0, f[0], f[1], f[2], f[3]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (i0 + v < n) o[i0 + v] = f[v];
+    }
+  } else if (OUT == VT_OUT_F64) {
+    double* o = static_cast<double*>(out);
+    if (i0 + 3 < n) {
+      stg_stream4(o + i0, (double)f[0], (double)f[1], (double)f[2], (double)f[3]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (i0 + v < n) o[i0 + v] = (double)f[v];
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -131,23 +154,17 @@ __device__ __forceinline__ int64_t lookback(uint64_t* status, int64_t tile, uint
   return excl;
 }
 
-template <int OUT, bool SPARSE, bool CODES, bool PACKED>
+template <int OUT, bool SPARSE, bool CODES, bool PACKED, bool FAST>
 __global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[kWarps];
   __shared__ int64_t s_base;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  int64_t tile;
-  if (SPARSE) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    tile = s_tile;
-  } else {
-    tile = blockIdx.x;
-  }
+  // Tile = blockIdx.x: 1-D grids are dispatched in increasing block order,
+  // so every predecessor a tile waits on in the look-back is resident or done.
+  const int64_t tile = blockIdx.x;
   const int64_t tile_base = tile * kTile;
   const int64_t wbase = tile_base + warp * kWarpElems;
 
@@ -164,10 +181,17 @@ __global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs 
   for (int j = 0; j < kSlots; ++j) {
     const int64_t i0 = wbase + j * 128 + lane * 4;
     uint32_t code[4];
-    uint64_t rb[4];
+    if (FAST) {
+      float f[4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) rb[v] = round_dir(xv[j].v[v], a.g, code[v], err);
-    store_out<OUT>(a.out, i0, a.n, rb);
+      for (int v = 0; v < 4; ++v) f[v] = round_dir32(xv[j].v[v], a.thr32, a.g.thr_sub, code[v], err);
+      store_out<OUT>(a.out, i0, a.n, f);
+    } else {
+      uint64_t rb[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) rb[v] = round_dir(xv[j].v[v], a.g, code[v], err);
+      store_out<OUT>(a.out, i0, a.n, rb);
+    }
     if (CODES) {
       if (i0 + 3 < a.n) {
         *reinterpret_cast<uint32_t*>(a.codes + i0) = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
@@ -188,19 +212,24 @@ __global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs 
       }
     }
     if (SPARSE) {
-      const uint32_t b0 = __ballot_sync(0xffffffffu, code[0] != 1u);
-      const uint32_t b1 = __ballot_sync(0xffffffffu, code[1] != 1u);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, code[2] != 1u);
-      const uint32_t b3 = __ballot_sync(0xffffffffu, code[3] != 1u);
-      uint32_t r = cnt + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+      // warp-exclusive rank of this lane's logged elements: the lane's count
+      // (0..4) is spread over three ballots, one per binary digit
+      const uint32_t c = (code[0] != 1u) + (code[1] != 1u) + (code[2] != 1u) + (code[3] != 1u);
+      const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, c & 2u);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, c & 4u);
+      uint32_t r = cnt + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+      if (c) {
+        const uint64_t w0 = (uint64_t)(a.global_base + i0) << 1;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        if (code[v] != 1u) {
-          stage[r] = ((uint64_t)(a.global_base + i0 + v) << 1) | (code[v] == 2u ? 1ull : 0ull);
-          ++r;
+        for (int v = 0; v < 4; ++v) {
+          if (code[v] != 1u) {
+            stage[r] = w0 + ((uint64_t)v << 1) + (code[v] == 2u ? 1ull : 0ull);
+            ++r;
+          }
         }
       }
-      cnt += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+      cnt += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
     } else {
 #pragma unroll
       for (int v = 0; v < 4; ++v) cnt += (code[v] != 1u) ? 1u : 0u;
@@ -304,7 +333,7 @@ __global__ void log_tile_offsets_kernel(const uint64_t* __restrict__ w, int64_t 
   if (t == num_tiles) counters[2] = lo;
 }
 
-template <int OUT, int LOGK>
+template <int OUT, int LOGK, bool FAST>
 __global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
   __shared__ __align__(16) uint8_t cs[kTile];
   __shared__ uint32_t s_warp[kWarps];
@@ -339,6 +368,7 @@ __global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
     const int64_t b0 = pos0 / 5;
     const int r0 = (int)(pos0 - 5 * b0);
     const int lim = (int)std::min<int64_t>(kTile, a.n - tile_base);
+    for (int e = lim + threadIdx.x; e < kTile; e += kThreads) cs[e] = 1;  // past the end
     for (int e = threadIdx.x; e < lim; e += kThreads) {
       const int q = (r0 + e) / 5;
       const int dpos = r0 + e - 5 * q;
@@ -372,14 +402,25 @@ __global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) code[v] = (c4 >> (8 * v)) & 0xffu;
     }
-    uint64_t rb[4];
+    if (FAST) {
+      float y[4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      uint32_t f;
-      rb[v] = replay_one(xv[j].v[v], code[v], a.g, err, f);
-      flips += (i0 + v < a.n) ? f : 0u;
+      for (int v = 0; v < 4; ++v) {
+        uint32_t f;
+        y[v] = replay32(xv[j].v[v], code[v], err, f);
+        flips += f;  // padding lanes carry x = 0, code 1: never a flip
+      }
+      store_out<OUT>(a.out, i0, a.n, y);
+    } else {
+      uint64_t rb[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint32_t f;
+        rb[v] = replay_one(xv[j].v[v], code[v], a.g, err, f);
+        flips += f;
+      }
+      store_out<OUT>(a.out, i0, a.n, rb);
     }
-    store_out<OUT>(a.out, i0, a.n, rb);
   }
   report_err(a.err, err);
   const uint32_t w = warp_sum_u32(flips);
@@ -483,29 +524,40 @@ bool valid_b(int b_r) { return b_r >= 10 && b_r <= 32; }
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 int64_t num_tiles_for(int64_t n) { return (n + kTile - 1) / kTile; }
 
-template <int OUT, bool S, bool C, bool P>
+template <int OUT, bool S, bool C, bool P, bool F>
 void launch_rl(const RoundLogArgs& a, int64_t tiles, cudaStream_t st) {
   size_t smem = (S ? (size_t)kTile * sizeof(uint64_t) : 0) + (P ? (size_t)kTile + 8 : 0);
-  auto k = round_log_kernel<OUT, S, C, P>;
+  auto k = round_log_kernel<OUT, S, C, P, F>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<(unsigned)tiles, kThreads, smem, st>>>(a);
 }
 
 typedef void (*rl_fn)(const RoundLogArgs&, int64_t, cudaStream_t);
 
-template <int OUT>
-rl_fn pick_rl(bool s, bool c, bool p) {
-  const int key = (s ? 4 : 0) | (c ? 2 : 0) | (p ? 1 : 0);
+template <int OUT, bool F>
+rl_fn pick_rl2(int key) {
   switch (key) {
-    case 0: return launch_rl<OUT, false, false, false>;
-    case 1: return launch_rl<OUT, false, false, true>;
-    case 2: return launch_rl<OUT, false, true, false>;
-    case 3: return launch_rl<OUT, false, true, true>;
-    case 4: return launch_rl<OUT, true, false, false>;
-    case 5: return launch_rl<OUT, true, false, true>;
-    case 6: return launch_rl<OUT, true, true, false>;
-    default: return launch_rl<OUT, true, true, true>;
+    case 0: return launch_rl<OUT, false, false, false, F>;
+    case 1: return launch_rl<OUT, false, false, true, F>;
+    case 2: return launch_rl<OUT, false, true, false, F>;
+    case 3: return launch_rl<OUT, false, true, true, F>;
+    case 4: return launch_rl<OUT, true, false, false, F>;
+    case 5: return launch_rl<OUT, true, false, true, F>;
+    case 6: return launch_rl<OUT, true, true, false, F>;
+    default: return launch_rl<OUT, true, true, true, F>;
   }
+}
+
+rl_fn pick_rl(int out_kind, bool fast, bool s, bool c, bool p) {
+  const int key = (s ? 4 : 0) | (c ? 2 : 0) | (p ? 1 : 0);
+  if (fast) {
+    return out_kind == VT_OUT_F32 ? pick_rl2<VT_OUT_F32, true>(key)
+         : out_kind == VT_OUT_F64 ? pick_rl2<VT_OUT_F64, true>(key)
+                                  : pick_rl2<VT_OUT_NONE, true>(key);
+  }
+  return out_kind == VT_OUT_F32 ? pick_rl2<VT_OUT_F32, false>(key)
+       : out_kind == VT_OUT_F64 ? pick_rl2<VT_OUT_F64, false>(key)
+                                : pick_rl2<VT_OUT_NONE, false>(key);
 }
 
 }  // namespace
@@ -555,34 +607,41 @@ extern "C" int vt_round_log(const double* x, int64_t n, int b_r, double tau, int
   a.err = err;
   a.num_tiles = tiles;
   a.status = nullptr;
-  a.ticket = nullptr;
+  a.thr32 = (int)std::min<int64_t>(std::max<int64_t>(a.g.thr, 0), INT32_MAX);
   if (sparse) {
     if (!ws || ws_bytes < vt_round_log_workspace(n)) {
       vt_set_error("vt_round_log: workspace too small");
       return VT_EINVAL;
     }
     a.status = static_cast<uint64_t*>(ws);
-    a.ticket = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + tiles * 8);
-    if (cudaMemsetAsync(ws, 0, (size_t)tiles * 8 + 4, st) != cudaSuccess) return vt_check_launch("memset");
+    if (cudaMemsetAsync(ws, 0, (size_t)tiles * 8, st) != cudaSuccess) return vt_check_launch("memset");
   }
-  rl_fn f = out_kind == VT_OUT_F32 ? pick_rl<VT_OUT_F32>(sparse != nullptr, codes != nullptr, packed != nullptr)
-          : out_kind == VT_OUT_F64 ? pick_rl<VT_OUT_F64>(sparse != nullptr, codes != nullptr, packed != nullptr)
-                                   : pick_rl<VT_OUT_NONE>(sparse != nullptr, codes != nullptr, packed != nullptr);
+  rl_fn f = pick_rl(out_kind, b_r == 32, sparse != nullptr, codes != nullptr, packed != nullptr);
   f(a, tiles, st);
   return vt_check_launch("round_log_kernel");
 }
 
 namespace {
-template <int OUT, int L>
+template <int OUT, int L, bool F>
 void launch_rp(const ReplayArgs& a, int64_t tiles, cudaStream_t st) {
-  replay_kernel<OUT, L><<<(unsigned)tiles, kThreads, 0, st>>>(a);
+  replay_kernel<OUT, L, F><<<(unsigned)tiles, kThreads, 0, st>>>(a);
 }
 typedef void (*rp_fn)(const ReplayArgs&, int64_t, cudaStream_t);
-template <int OUT>
-rp_fn pick_rp(int lk) {
-  return lk == VT_LOG_SPARSE ? launch_rp<OUT, VT_LOG_SPARSE>
-       : lk == VT_LOG_CODES  ? launch_rp<OUT, VT_LOG_CODES>
-                             : launch_rp<OUT, VT_LOG_PACKED>;
+template <int OUT, bool F>
+rp_fn pick_rp2(int lk) {
+  return lk == VT_LOG_SPARSE ? launch_rp<OUT, VT_LOG_SPARSE, F>
+       : lk == VT_LOG_CODES  ? launch_rp<OUT, VT_LOG_CODES, F>
+                             : launch_rp<OUT, VT_LOG_PACKED, F>;
+}
+rp_fn pick_rp(int out_kind, bool fast, int lk) {
+  if (fast) {
+    return out_kind == VT_OUT_F32 ? pick_rp2<VT_OUT_F32, true>(lk)
+         : out_kind == VT_OUT_F64 ? pick_rp2<VT_OUT_F64, true>(lk)
+                                  : pick_rp2<VT_OUT_NONE, true>(lk);
+  }
+  return out_kind == VT_OUT_F32 ? pick_rp2<VT_OUT_F32, false>(lk)
+       : out_kind == VT_OUT_F64 ? pick_rp2<VT_OUT_F64, false>(lk)
+                                : pick_rp2<VT_OUT_NONE, false>(lk);
 }
 }  // namespace
 
@@ -630,9 +689,7 @@ extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, cons
     if (rc) return rc;
     a.offs = offs;
   }
-  rp_fn f = out_kind == VT_OUT_F32 ? pick_rp<VT_OUT_F32>(log_kind)
-          : out_kind == VT_OUT_F64 ? pick_rp<VT_OUT_F64>(log_kind)
-                                   : pick_rp<VT_OUT_NONE>(log_kind);
+  rp_fn f = pick_rp(out_kind, b_r == 32, log_kind);
   f(a, tiles, st);
   return vt_check_launch("replay_kernel");
 }

@@ -1,0 +1,161 @@
+"""Contiguous sharding of the hot path across the GPUs of one box.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  The
+path shards naturally:
+
+* round-and-log: rank r owns elements [lo_r, hi_r) (boundaries on the
+  640-element warp grid) and emits sparse entries with GLOBAL indices;
+  the only exchange is an all-gather of the per-rank entry counts, whose
+  exclusive prefix places each rank's slice in the global log (concatenation
+  in rank order is the reference order).  The log itself stays sharded.
+* replay: each rank consumes its own slice; corrections are all-reduced.
+* Merkle: leaves are grouped in blocks of 2^K; each rank hashes a
+  contiguous run of blocks and builds levels 0..K locally, all ranks
+  all-gather the block roots and build the top levels redundantly.  Every
+  node of ``merkle.build`` over the full leaf list is reproduced (the
+  promotion rule only acts at the right edge, which is the last rank's).
+
+The combination logic is pure host arithmetic over tensors (``*_plan`` /
+``combine_*``) so it is unit-tested with the gloo backend on CPU; the
+device work is the same single-GPU kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+SHARD_ALIGN = 640  # lcm(5 codes per .vtrl byte, 128 elements per warp slot)
+BLOCK_LEAVES_LOG2 = 12
+
+
+def shard_range(n: int, rank: int, world: int, align: int = SHARD_ALIGN) -> tuple[int, int]:
+    """Contiguous [lo, hi) of rank; interior boundaries are multiples of align,
+    the last rank takes the remainder."""
+    units = (n + align - 1) // align
+    per, extra = divmod(units, world)
+    lo_u = rank * per + min(rank, extra)
+    hi_u = lo_u + per + (1 if rank < extra else 0)
+    return min(lo_u * align, n), min(hi_u * align, n)
+
+
+def exclusive_offsets(counts: torch.Tensor) -> torch.Tensor:
+    return torch.cumsum(counts, 0) - counts
+
+
+def all_gather_counts(count: int | torch.Tensor, group=None, device=None) -> torch.Tensor:
+    """All ranks' int64 counts (one tiny NCCL all-gather over NVLink)."""
+    world = dist.get_world_size(group)
+    if isinstance(count, torch.Tensor):
+        mine = count.reshape(1).to(torch.int64)
+    else:
+        mine = torch.tensor([int(count)], dtype=torch.int64, device=device)
+    out = torch.empty(world, dtype=torch.int64, device=mine.device)
+    dist.all_gather_into_tensor(out, mine, group=group)
+    return out
+
+
+@dataclass
+class ShardedLog:
+    """This rank's slice of the global sparse log plus the global layout."""
+
+    local: object          # ops.SparseLog with global indices
+    offset: int            # position of local.words[0] in the global log
+    total: int             # global entry count
+    counts: torch.Tensor   # per-rank counts
+
+
+def round_and_log_sharded(x_local: torch.Tensor, b_r: int, tau: float, global_base: int,
+                          group=None, **kw):
+    from . import ops
+    y, log = ops.round_and_log(x_local, b_r, tau, global_base=global_base, **kw)
+    counts = all_gather_counts(log.count, group, device=x_local.device)
+    offs = exclusive_offsets(counts)
+    rank = dist.get_rank(group)
+    return y, ShardedLog(log, int(offs[rank]), int(counts.sum()), counts)
+
+
+def replay_sharded(xa_local: torch.Tensor, b_r: int, slog: ShardedLog, global_base: int,
+                   group=None, **kw):
+    from . import ops
+    y, corr = ops.replay(xa_local, b_r, slog.local, global_base=global_base, **kw)
+    t = torch.tensor([corr], dtype=torch.int64, device=xa_local.device)
+    dist.all_reduce(t, group=group)
+    return y, int(t.item())
+
+
+# ---------------------------------------------------------------------------
+# Merkle
+# ---------------------------------------------------------------------------
+
+def leaf_block_range(n_leaves: int, rank: int, world: int, k: int = BLOCK_LEAVES_LOG2) -> tuple[int, int]:
+    """Leaves [lo, hi) of rank: whole 2^k-leaf blocks, contiguous."""
+    blocks = (n_leaves + (1 << k) - 1) >> k
+    per, extra = divmod(blocks, world)
+    b_lo = rank * per + min(rank, extra)
+    b_hi = b_lo + per + (1 if rank < extra else 0)
+    return min(b_lo << k, n_leaves), min(b_hi << k, n_leaves)
+
+
+def local_levels(leaves: torch.Tensor, k: int, hash_level) -> list[torch.Tensor]:
+    """Levels 0..k over a run of whole 2^k blocks (the last may be partial,
+    in which case it is the global right edge and promotion applies)."""
+    levels = [leaves]
+    cur = leaves
+    for _ in range(k):
+        if cur.shape[0] <= 1 and len(levels) > 1:
+            levels.append(cur)
+            continue
+        cur = hash_level(cur)
+        levels.append(cur)
+    return levels
+
+
+def combine_top(block_roots: torch.Tensor, hash_level) -> list[torch.Tensor]:
+    """Levels above the block roots (built redundantly on every rank)."""
+    levels = [block_roots]
+    cur = block_roots
+    while cur.shape[0] > 1:
+        cur = hash_level(cur)
+        levels.append(cur)
+    return levels
+
+
+def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes: int = 4096,
+                   k: int = BLOCK_LEAVES_LOG2, group=None, hash_leaves=None, hash_level=None):
+    """Per-rank lower levels (0..k) + all-gathered block roots + top levels.
+
+    Returns (local_levels, top_levels).  Global level L (L <= k) of the full
+    tree is the rank-order concatenation of every rank's local level L
+    (ranks own whole blocks); levels above k are the top levels.
+    """
+    if hash_leaves is None or hash_level is None:
+        from . import merkle as mk
+        hash_leaves = hash_leaves or (lambda b: mk.sha256_leaves(b, leaf_bytes))
+        hash_level = hash_level or _device_level
+    world = dist.get_world_size(group)
+    leaves = hash_leaves(w_local_bytes)
+    lv = local_levels(leaves, k, hash_level) if leaves.shape[0] else [leaves]
+    # each rank contributes its block roots; ranks own whole blocks, so the
+    # number of roots per rank is known from the plan
+    n_blocks = [(hi - lo + (1 << k) - 1) >> k
+                for lo, hi in (leaf_block_range(n_leaves_total, r, world, k) for r in range(world))]
+    mine = lv[-1] if leaves.shape[0] else leaves.new_zeros((0, 32))
+    width = max(n_blocks)
+    pad = torch.zeros((width, 32), dtype=torch.uint8, device=mine.device)
+    pad[: mine.shape[0]] = mine
+    gathered = torch.empty((world * width, 32), dtype=torch.uint8, device=mine.device)
+    dist.all_gather_into_tensor(gathered, pad, group=group)
+    roots = torch.cat([gathered[r * width: r * width + n_blocks[r]] for r in range(world)])
+    return lv, combine_top(roots, hash_level)
+
+
+def _device_level(cur: torch.Tensor) -> torch.Tensor:
+    from . import _device as D
+    from . import _lib
+    m = int(cur.shape[0])
+    out = torch.empty(((m + 1) // 2, 32), dtype=torch.uint8, device=cur.device)
+    _lib.call("vt_merkle_level", D.ptr(cur.contiguous()), m, D.ptr(out), D.stream_ptr())
+    return out

@@ -119,6 +119,113 @@ def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtyp
     return (y.reshape(shape) if out is None else y), cnt[0]
 
 
+class _HostPipe:
+    """Double-buffered device staging for host-resident tensors: H2D copies,
+    kernels and D2H copies run on three streams so PCIe traffic in both
+    directions overlaps the HBM-bound kernels chunk by chunk."""
+
+    def __init__(self, chunk: int, device):
+        self.chunk = chunk
+        self.dev = device
+        self.s_in = torch.cuda.Stream(device)
+        self.s_run = torch.cuda.Stream(device)
+        self.s_out = torch.cuda.Stream(device)
+        self.xbuf = [torch.empty(chunk, dtype=torch.float64, device=device) for _ in range(2)]
+        self.ybuf = [torch.empty(chunk, dtype=torch.float32, device=device) for _ in range(2)]
+        self.ev_loaded = [torch.cuda.Event() for _ in range(2)]
+        self.ev_xfree = [torch.cuda.Event() for _ in range(2)]
+        self.ev_done = [torch.cuda.Event() for _ in range(2)]
+        self.ev_yfree = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_xfree + self.ev_yfree:
+            e.record(torch.cuda.current_stream(device))
+
+    def run(self, x_h: torch.Tensor, y_h: torch.Tensor, kernel) -> None:
+        n = x_h.numel()
+        for i, lo in enumerate(range(0, n, self.chunk)):
+            hi = min(n, lo + self.chunk)
+            k = i & 1
+            xb = self.xbuf[k][: hi - lo]
+            yb = self.ybuf[k][: hi - lo]
+            with torch.cuda.stream(self.s_in):
+                self.s_in.wait_event(self.ev_xfree[k])
+                xb.copy_(x_h[lo:hi], non_blocking=True)
+                self.ev_loaded[k].record(self.s_in)
+            with torch.cuda.stream(self.s_run):
+                self.s_run.wait_event(self.ev_loaded[k])
+                self.s_run.wait_event(self.ev_yfree[k])
+                kernel(xb, yb, lo)
+                self.ev_xfree[k].record(self.s_run)
+                self.ev_done[k].record(self.s_run)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_done[k])
+                y_h[lo:hi].copy_(yb, non_blocking=True)
+                self.ev_yfree[k].record(self.s_out)
+        torch.cuda.current_stream(self.dev).wait_stream(self.s_out)
+        torch.cuda.current_stream(self.dev).wait_stream(self.s_run)
+
+
+_PIPES: dict = {}
+
+
+def round_and_log_replay_host(xt_h: torch.Tensor, xa_h: torch.Tensor, b_r: int, tau: float,
+                              yt_h: torch.Tensor, ya_h: torch.Tensor, log_h: torch.Tensor,
+                              global_base: int = 0, chunk: int = 1 << 22) -> tuple[int, int, int]:
+    """End-to-end trainer + auditor step from pinned host memory.
+
+    Trainer: chunked H2D of the FP64 tensor, fused round-and-log (log chunks
+    appended on the device through cursor chaining, global indices), D2H of
+    the FP32 output, then D2H of the sparse log.  Auditor: chunked H2D of its
+    FP64 tensor, fused replay against the device log, D2H of the FP32 output.
+    Returns (log entries, corrections, log bytes copied to the host).
+    """
+    _check_b(b_r)
+    dev = D.require_cuda()
+    n = xt_h.numel()
+    key = (dev.index, chunk)
+    pipe = _PIPES.get(key)
+    if pipe is None:
+        pipe = _PIPES[key] = _HostPipe(chunk, dev)
+    words = D.workspace(8 * max(n // 4, 1024), "host_log").view(torch.int64)
+    n_chunks = (n + chunk - 1) // chunk
+    cursors = torch.zeros(n_chunks + 1, dtype=torch.int64, device=dev)
+    ws_rl = [D.workspace(int(_lib.lib().vt_round_log_workspace(chunk)), f"hp_rl{k}") for k in range(2)]
+    fl = D.Flags()
+    fl_a = D.Flags()
+    cap = words.numel()
+
+    def rl(xb, yb, lo):
+        i = lo // chunk
+        ws = ws_rl[i & 1]
+        _lib.call("vt_round_log", D.ptr(xb), xb.numel(), b_r, float(tau), _lib.OUT_F32, D.ptr(yb),
+                  D.ptr(words), cap, int(global_base + lo), cursors.data_ptr() + 8 * i,
+                  cursors.data_ptr() + 8 * (i + 1), None, None, 0, None, fl.cnt_ptr, fl.err_ptr,
+                  D.ptr(ws), ws.numel(), D.stream_ptr())
+
+    torch.cuda.current_stream(dev).synchronize()
+    pipe.run(xt_h, yt_h, rl)
+    err, cnt = fl.read()  # syncs: the auditor needs the log length
+    D.raise_fpround(err)
+    count = cnt[0]
+    if count > cap or count > log_h.numel():
+        raise LogOverflow(f"sparse log needs {count} words")
+    log_h[:count].copy_(words[:count], non_blocking=True)
+    ws_rp = [D.workspace(int(_lib.lib().vt_replay_workspace(chunk)), f"hp_rp{k}") for k in range(2)]
+
+    def rp(xb, yb, lo):
+        i = lo // chunk
+        ws = ws_rp[i & 1]
+        _lib.call("vt_replay", D.ptr(xb), xb.numel(), b_r, _lib.LOG_SPARSE, D.ptr(words), count,
+                  int(global_base + lo), _lib.OUT_F32, D.ptr(yb), fl_a.cnt_ptr, fl_a.err_ptr,
+                  D.ptr(ws), ws.numel(), D.stream_ptr())
+
+    pipe.run(xa_h, ya_h, rp)
+    err_a, cnt_a = fl_a.read()
+    if err_a & _lib.ERR_BAD_SPARSE:
+        raise SparseLogError("sparse log is not strictly ascending")
+    D.raise_fpround(err_a)
+    return count, cnt_a[0], 8 * count
+
+
 def normalized_distance(x: torch.Tensor, b_r: int) -> torch.Tensor:
     """p = |x - rnd(x)| / max(scale(x), 2^-126) per element (fpround.py:171-173)."""
     _check_b(b_r)

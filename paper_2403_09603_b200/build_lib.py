@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvtrain_b200.so"
-SOURCES = ["vt_abi.cu", "vt_round.cu", "vt_codec.cu", "vt_tau.cu", "vt_sha256.cu"]
+SOURCES = ["vt_abi.cu", "vt_round.cu", "vt_stream.cu", "vt_codec.cu", "vt_tau.cu", "vt_sha256.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

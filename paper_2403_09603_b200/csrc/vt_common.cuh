@@ -200,6 +200,40 @@ __device__ __forceinline__ float round_dir32(double x, int thr32, double thr_sub
   return f;
 }
 
+// Branch-free variants for the common case 2^-126 <= |x| < FLT_MAX + half ulp.
+// `slow` is raised for anything else (FP32-subnormal range, overflow,
+// inf/nan, bad code); the caller then redoes the element group with the
+// exact general routines above / below.
+__device__ __forceinline__ bool outside_normal32(uint32_t ahi) {
+  return (ahi - 0x38100000u) >= (0x47efffffu - 0x38100000u);
+}
+
+__device__ __forceinline__ float round_dir32_fast(double x, int thr32, uint32_t& code, bool& slow) {
+  const float f = __double2float_rn(x);
+  const int hi = __double2hiint(x);
+  const uint32_t lo = (uint32_t)__double2loint(x);
+  slow |= outside_normal32((uint32_t)hi & 0x7fffffffu);
+  const uint32_t low = lo & 0x1fffffffu;
+  const bool up = (low + ((lo >> 29) & 1u)) > 0x10000000u;
+  const int d = (int)(up ? (0x20000000u - low) : low);
+  code = (d > thr32) ? ((up != (hi < 0)) ? 2u : 0u) : 1u;
+  return f;
+}
+
+__device__ __forceinline__ float replay32_fast(double x, uint32_t c, bool& slow, uint32_t& flip) {
+  const float f = __double2float_rn(x);
+  const int hi = __double2hiint(x);
+  const uint32_t lo = (uint32_t)__double2loint(x);
+  slow |= outside_normal32((uint32_t)hi & 0x7fffffffu) | (c > 2u);
+  const uint32_t low = lo & 0x1fffffffu;
+  const bool up = (low + ((lo >> 29) & 1u)) > 0x10000000u;
+  const bool r_above = up != (hi < 0);  // x < rnd(x) when off grid
+  const bool fl = (low != 0u) && ((c == 0u && r_above) || (c == 2u && !r_above));
+  flip = fl ? 1u : 0u;
+  // sign-magnitude: one FP32 ulp of magnitude is +-1 on the bit pattern
+  return fl ? __int_as_float(__float_as_int(f) + (up ? -1 : 1)) : f;
+}
+
 __device__ __forceinline__ float replay32(double x, uint32_t c, uint32_t& err, uint32_t& flip) {
   float f = __double2float_rn(x);
   const double r = (double)f;
@@ -262,6 +296,15 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 __device__ __forceinline__ void report_err(int32_t* err, uint32_t e) {
   if (e) atomicOr(reinterpret_cast<int*>(err), (int)e);
 }
+
+// persistent TMA-pipelined kernels of the north-star path (vt_stream.cu)
+size_t rl_stream_workspace(int64_t n);
+size_t rp_stream_workspace(int64_t n);
+int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
+              uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
+              int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
+int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
+              int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 
 }  // namespace vt
 

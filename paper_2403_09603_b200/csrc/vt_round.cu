@@ -122,42 +122,53 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
   return v;
 }
 
-// Decoupled look-back by one warp.  Returns the exclusive prefix of `tile`.
-__device__ __forceinline__ int64_t lookback(uint64_t* status, int64_t tile, uint64_t agg, int lane) {
+// Decoupled look-back by the whole CTA: every thread reads one predecessor
+// status word, so one L2 round trip covers 256 predecessors.  Returns the
+// exclusive prefix of `tile` (all threads).  Called by all threads.
+__device__ __forceinline__ int64_t lookback(uint64_t* status, int64_t tile, uint64_t agg) {
+  __shared__ int s_first;
+  __shared__ unsigned long long s_part[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tile == 0) {
-    if (lane == 0) st_relaxed_u64(status, kFlagInc | agg);
+    if (tid == 0) st_relaxed_u64(status, kFlagInc | agg);
     return 0;
   }
-  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | agg);
+  if (tid == 0) st_relaxed_u64(status + tile, kFlagAgg | agg);
   int64_t excl = 0;
   int64_t pred = tile - 1;
   while (true) {
-    const int64_t idx = pred - lane;
+    if (tid == 0) s_first = kThreads;
+    __syncthreads();
+    const int64_t idx = pred - tid;
     const uint64_t s = (idx >= 0) ? ld_relaxed_u64(status + idx) : kFlagInc;
     const uint64_t flag = s >> 62;
     const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
-    const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
-    const int first = inc ? (__ffs(inc) - 1) : 31;
-    const uint32_t upto = (2u << first) - 1u;  // lanes 0..first (all lanes if first == 31)
-    if (inv & upto) {
-      __nanosleep(20);
-      continue;
+    if (lane == 0 && inc) atomicMin(&s_first, warp * 32 + __ffs(inc) - 1);
+    __syncthreads();
+    const int first = s_first;  // nearest predecessor holding an inclusive prefix
+    if (__syncthreads_or(flag == 0 && tid <= first)) {
+      __nanosleep(32);
+      continue;  // some needed predecessor has not published yet
     }
-    uint64_t v = (lane <= first) ? (s & kValMask) : 0ull;
+    uint64_t v = (tid <= first) ? (s & kValMask) : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += (int64_t)v;
-    if (inc) break;
-    pred -= 32;
+    if (lane == 0) s_part[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) excl += (int64_t)s_part[k];
+    if (first < kThreads) break;
+    pred -= kThreads;
   }
-  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | ((uint64_t)excl + agg));
+  if (tid == 0) st_relaxed_u64(status + tile, kFlagInc | ((uint64_t)excl + agg));
   return excl;
 }
 
 template <int OUT, bool SPARSE, bool CODES, bool PACKED, bool FAST>
-__global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) round_log_kernel(const RoundLogArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_warp[kWarps];
+  __shared__ uint32_t s_total;
   __shared__ int64_t s_base;
 
   const int lane = threadIdx.x & 31;
@@ -183,8 +194,13 @@ __global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs 
     uint32_t code[4];
     if (FAST) {
       float f[4];
+      bool slow = false;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) f[v] = round_dir32(xv[j].v[v], a.thr32, a.g.thr_sub, code[v], err);
+      for (int v = 0; v < 4; ++v) f[v] = round_dir32_fast(xv[j].v[v], a.thr32, code[v], slow);
+      if (slow) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = round_dir32(xv[j].v[v], a.thr32, a.g.thr_sub, code[v], err);
+      }
       store_out<OUT>(a.out, i0, a.n, f);
     } else {
       uint64_t rb[4];
@@ -251,14 +267,17 @@ __global__ void __launch_bounds__(kThreads) round_log_kernel(const RoundLogArgs 
       const uint32_t total = __shfl_sync(0xffffffffu, incl, kWarps - 1);
       __syncwarp();
       if (lane < kWarps) s_warp[lane] = incl - c;
-      const int64_t excl = lookback(a.status, tile, total, lane);
-      if (lane == 0) {
-        const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
-        s_base = cur + excl;
-        if (tile == a.num_tiles - 1) {
-          atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)total));
-          if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)total;
-        }
+      if (lane == 0) s_total = total;
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    const int64_t excl = lookback(a.status, tile, total);
+    if (threadIdx.x == 0) {
+      const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
+      s_base = cur + excl;
+      if (tile == a.num_tiles - 1) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)total));
+        if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)total;
       }
     }
     __syncthreads();
@@ -334,7 +353,7 @@ __global__ void log_tile_offsets_kernel(const uint64_t* __restrict__ w, int64_t 
 }
 
 template <int OUT, int LOGK, bool FAST>
-__global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a) {
   __shared__ __align__(16) uint8_t cs[kTile];
   __shared__ uint32_t s_warp[kWarps];
   const int lane = threadIdx.x & 31;
@@ -404,12 +423,15 @@ __global__ void __launch_bounds__(kThreads) replay_kernel(const ReplayArgs a) {
     }
     if (FAST) {
       float y[4];
+      uint32_t fl[4];
+      bool slow = false;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint32_t f;
-        y[v] = replay32(xv[j].v[v], code[v], err, f);
-        flips += f;  // padding lanes carry x = 0, code 1: never a flip
+      for (int v = 0; v < 4; ++v) y[v] = replay32_fast(xv[j].v[v], code[v], slow, fl[v]);
+      if (slow) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) y[v] = replay32(xv[j].v[v], code[v], err, fl[v]);
       }
+      flips += fl[0] + fl[1] + fl[2] + fl[3];  // padding lanes carry x = 0, code 1: never a flip
       store_out<OUT>(a.out, i0, a.n, y);
     } else {
       uint64_t rb[4];
@@ -565,7 +587,7 @@ rl_fn pick_rl(int out_kind, bool fast, bool s, bool c, bool p) {
 extern "C" int vt_tile_elems(void) { return kTile; }
 
 extern "C" size_t vt_round_log_workspace(int64_t n) {
-  return (size_t)(num_tiles_for(n) * 8 + 256);
+  return std::max((size_t)(num_tiles_for(n) * 8 + 256), rl_stream_workspace(n));
 }
 
 extern "C" int vt_round_log(const double* x, int64_t n, int b_r, double tau, int out_kind, void* out,
@@ -613,6 +635,10 @@ extern "C" int vt_round_log(const double* x, int64_t n, int b_r, double tau, int
       vt_set_error("vt_round_log: workspace too small");
       return VT_EINVAL;
     }
+    if (!codes && !packed) {  // north-star path: persistent TMA streaming + look-back expand
+      return rl_stream(x, n, a.g, a.thr32, b_r == 32, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
+                       cursor_out, counters, err, ws, st);
+    }
     a.status = static_cast<uint64_t*>(ws);
     if (cudaMemsetAsync(ws, 0, (size_t)tiles * 8, st) != cudaSuccess) return vt_check_launch("memset");
   }
@@ -645,7 +671,9 @@ rp_fn pick_rp(int out_kind, bool fast, int lk) {
 }
 }  // namespace
 
-extern "C" size_t vt_replay_workspace(int64_t n) { return (size_t)((num_tiles_for(n) + 1) * 8 + 256); }
+extern "C" size_t vt_replay_workspace(int64_t n) {
+  return std::max((size_t)((num_tiles_for(n) + 1) * 8 + 256), rp_stream_workspace(n));
+}
 
 extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, const void* log,
                          int64_t log_len, int64_t log_base, int out_kind, void* out,
@@ -681,6 +709,8 @@ extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, cons
       vt_set_error("vt_replay: workspace too small");
       return VT_EINVAL;
     }
+    return rp_stream(x, n, a.g, b_r == 32, out_kind, out, static_cast<const uint64_t*>(log), log_len, log_base,
+                     counters, err, ws, st);
     int64_t* offs = static_cast<int64_t*>(ws);
     const int64_t threads = tiles + 1;
     log_tile_offsets_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(

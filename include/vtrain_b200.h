@@ -87,7 +87,10 @@ size_t vt_round_log_workspace(int64_t n);
  *            [head + 5g, head + 5g + 5) with head = (5 - log_pos % 5) % 5
  *            (clipped to n); edge_codes[0..7] receives the head codes then
  *            the tail codes (elements after the last full group).
- * counters[0] = number of codes != 1 (directed count / sparse entry count).
+ * counters[0] += number of codes != 1 (directed count / sparse entry count).
+ * Workspace (>= vt_round_log_workspace(n) bytes) must be zero-filled before
+ * its first use and then belong to this entry point on one stream: it keeps
+ * an epoch counter so the look-back status words need no clearing per call.
  */
 int vt_round_log(const double *x, int64_t n, int b_r, double tau, int out_kind, void *out,
                  uint64_t *sparse, int64_t sparse_cap, int64_t global_base,

@@ -67,7 +67,7 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
     key = (torch.cuda.current_device(), stream_ptr(), tag)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device="cuda")  # zero-filled: see vt_round_log
         _WS[key] = ws
     return ws
 

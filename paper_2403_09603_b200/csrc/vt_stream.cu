@@ -150,27 +150,54 @@ __device__ __forceinline__ void* tile_out(void* out, int64_t tbase) {
   return out;
 }
 
+
 // ---------------------------------------------------------------------------
-// trainer: streaming pass
+// cross-CTA decoupled look-back with epoch-tagged status words
+//
+// status word = epoch (20 bits) | flag (2 bits) | value (42 bits).  A word
+// whose epoch differs from the current call's is "not yet published", so the
+// status array never needs clearing between calls: the workspace header keeps
+// the epoch, every CTA reads it at start, and the last CTA bumps it after its
+// own look-back (which completes only after every other CTA has published,
+// hence after every CTA has read the old epoch).
 // ---------------------------------------------------------------------------
 
-struct RLStreamArgs {
+constexpr int kEpochShift = 44;
+constexpr uint64_t kEpochMask = (1ull << 20) - 1;
+constexpr uint64_t kLBAgg = 1ull << 42;
+constexpr uint64_t kLBInc = 2ull << 42;
+constexpr uint64_t kLBVal = (1ull << 42) - 1;
+
+struct WsHeader {
+  uint32_t epoch;
+  uint32_t pad[15];
+};
+
+__device__ __forceinline__ uint64_t lb_word(uint32_t epoch, uint64_t flag, uint64_t v) {
+  return ((uint64_t)epoch << kEpochShift) | flag | (v & kLBVal);
+}
+
+// ---------------------------------------------------------------------------
+// trainer: streaming pass (strided persistent tiles) + expand pass
+// ---------------------------------------------------------------------------
+
+struct RLArgs {
   const double* x;
   int64_t n;
   Grid g;
   int thr32;
   void* out;
-  uint16_t* scratch;  // [num_tiles][kSTile] staged local entries
-  uint32_t* counts;   // [num_tiles]
   int64_t num_tiles;
+  uint32_t* counts;   // [num_tiles] logged entries per tile
+  uint16_t* scratch;  // [num_tiles][kSTile] staged entries: tile offset | up << 15
   int32_t* err;
 };
 
-// One tile of the trainer pass: round, classify, store, stage logged
-// elements (warp-local order == element order).  Returns the warp's count.
+// One tile: round, classify, store, stage logged elements (warp-local order
+// == element order).  Returns the warp's count.
 template <int OUT, bool FAST, bool FULL>
-__device__ __forceinline__ uint32_t rl_tile(const RLStreamArgs& a, const double* src, void* o, int lim,
-                                            uint16_t* stw, int warp, int lane, uint32_t lt, uint32_t& err) {
+__device__ __forceinline__ uint32_t rl_tile(const RLArgs& a, const double* src, void* o, int lim, uint16_t* stw,
+                                            int warp, int lane, uint32_t lt, uint32_t& err) {
   uint32_t wcnt = 0;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
@@ -194,7 +221,6 @@ __device__ __forceinline__ uint32_t rl_tile(const RLStreamArgs& a, const double*
     const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 1u);
     const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 1u);
     // branch-free staging: unlogged elements write into the trash slot
-    // (index kSWarpElems of this warp's stage row)
     const uint32_t r0 = wcnt + __popc(b0 & lt) + __popc(b1 & lt);
     const uint32_t r1 = r0 + (c0 != 1u);
     stw[(c0 != 1u) ? r0 : kSWarpElems] = (uint16_t)(e0 | ((c0 == 2u) ? 0x8000 : 0));
@@ -204,8 +230,10 @@ __device__ __forceinline__ uint32_t rl_tile(const RLStreamArgs& a, const double*
   return wcnt;
 }
 
+// Tiles t = blockIdx.x + k * gridDim.x: at any moment the CTAs of the grid
+// stream one contiguous window of x.  No cross-CTA waits.
 template <int OUT, bool FAST>
-__global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLStreamArgs a) {
+__global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ uint32_t s_cnt[2][kWarps];
@@ -213,6 +241,7 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLStreamA
   uint16_t* st16 = reinterpret_cast<uint16_t*>(sm + kRingBytes);  // [2][kWarps][kStageRow]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x;
   const int64_t full_tiles = a.n / kSTile;
   const uint64_t pol = evict_first_policy();
   if (tid == 0) {
@@ -221,12 +250,12 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLStreamA
   }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < kStages; ++s) issue_tile(ring, a.x, blockIdx.x + (int64_t)s * gridDim.x, full_tiles, s, pol);
+    for (int s = 0; s < kStages; ++s) issue_tile(ring, a.x, blockIdx.x + s * G, full_tiles, s, pol);
 
   const uint32_t lt = lanemask_lt();
   uint32_t err = 0;
   for (int64_t k = 0;; ++k) {
-    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int64_t t = blockIdx.x + k * G;
     if (t >= a.num_tiles) break;
     const int s = (int)(k % kStages);
     const int buf = (int)(k & 1);
@@ -238,10 +267,10 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLStreamA
         ? rl_tile<OUT, FAST, true>(a, src, o, kSTile, stw, warp, lane, lt, err)
         : rl_tile<OUT, FAST, false>(a, src, o, (int)(a.n - tbase), stw, warp, lane, lt, err);
     if (lane == 0) s_cnt[buf][warp] = wcnt;
-    __syncthreads();  // ring slot s fully consumed; warp counts visible
+    __syncthreads();  // ring slot s consumed; warp counts visible
     if (tid == 0) {
       fence_proxy_async();
-      issue_tile(ring, a.x, t + (int64_t)kStages * gridDim.x, full_tiles, s, pol);
+      issue_tile(ring, a.x, t + kStages * G, full_tiles, s, pol);
     }
     uint32_t off = 0, total = 0;
 #pragma unroll
@@ -250,118 +279,149 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLStreamA
       off += (w < warp) ? c : 0u;
       total += c;
     }
-    uint16_t* dst = a.scratch + t * kSTile + off;
+    uint16_t* dst = a.scratch + tbase + off;
     for (uint32_t i = lane; i < wcnt; i += 32) dst[i] = stw[i];
     if (tid == 0) a.counts[t] = total;
   }
   report_err(a.err, err);
 }
 
-// ---------------------------------------------------------------------------
-// trainer: expand staged entries into the global log
-// ---------------------------------------------------------------------------
+// Scan: exclusive prefix of the per-tile counts by single-pass decoupled
+// look-back (CTA per kScanTiles counts), giving every tile the global log
+// position of its first entry.
+constexpr int kScanPer = 8;                        // counts per thread
+constexpr int kScanTiles = kSThreads * kScanPer;  // 2048 counts per CTA
 
-constexpr uint64_t kSFlagAgg = 1ull << 62;
-constexpr uint64_t kSFlagInc = 2ull << 62;
-constexpr uint64_t kSValMask = (1ull << 62) - 1;
-
-struct ExpandArgs {
-  const uint16_t* scratch;
+struct ScanArgs {
   const uint32_t* counts;
   int64_t num_tiles;
-  uint64_t* status;  // [num_groups], zeroed
-  int64_t global_base;
+  WsHeader* hdr;
+  uint64_t* status;  // [num_scan_ctas] epoch-tagged
+  int64_t* toffs;    // [num_tiles] global log position of each tile's entries
   const int64_t* cursor_in;
   int64_t* cursor_out;
-  uint64_t* sparse;
-  int64_t cap;
   int64_t* counters;
 };
 
-__global__ void __launch_bounds__(kSThreads) rl_expand_kernel(const ExpandArgs a) {
-  __shared__ uint32_t s_off[kGroupTiles + 1];
+__global__ void __launch_bounds__(kSThreads) rl_scan_kernel(const ScanArgs a) {
+  __shared__ uint32_t s_warp[kWarps];
   __shared__ int64_t s_base;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t group = blockIdx.x;  // 1-D grid: dispatched in order, look-back is safe
-  const int64_t t0 = group * kGroupTiles;
-  const int nt = (int)std::min<int64_t>(kGroupTiles, a.num_tiles - t0);
-  if (tid < 32) {
-    // exclusive scan of the group's (<= 64) tile counts by warp 0
-    const uint32_t c0 = (lane < nt) ? a.counts[t0 + lane] : 0u;
-    const uint32_t c1 = (lane + 32 < nt) ? a.counts[t0 + lane + 32] : 0u;
-    uint32_t i0 = c0, i1 = c1;
+  __shared__ uint32_t s_epoch;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t chunk = blockIdx.x;  // 1-D grid: dispatched in order, look-back is safe
+  const int64_t t0 = chunk * kScanTiles + (int64_t)tid * kScanPer;
+  uint32_t c[kScanPer];
+  uint32_t sum = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u0 = __shfl_up_sync(0xffffffffu, i0, o);
-      const uint32_t u1 = __shfl_up_sync(0xffffffffu, i1, o);
-      if (lane >= o) {
-        i0 += u0;
-        i1 += u1;
-      }
-    }
-    const uint32_t tot0 = __shfl_sync(0xffffffffu, i0, 31);
-    s_off[lane] = i0 - c0;
-    s_off[lane + 32] = tot0 + i1 - c1;
-    const uint64_t agg = (uint64_t)tot0 + __shfl_sync(0xffffffffu, i1, 31);
-    if (lane == 0) s_off[kGroupTiles] = (uint32_t)agg;
-    // decoupled look-back over groups, 32 predecessors per round trip
+  for (int m = 0; m < kScanPer; ++m) {
+    c[m] = (t0 + m < a.num_tiles) ? a.counts[t0 + m] : 0u;
+    sum += c[m];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  if (tid == 0) s_epoch = ((*(volatile uint32_t*)&a.hdr->epoch) + 1u) & (uint32_t)kEpochMask;
+  __syncthreads();
+  uint32_t wpre = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    wpre += (w < warp) ? s_warp[w] : 0u;
+    agg += s_warp[w];
+  }
+  const uint32_t epoch = s_epoch;
+  if (warp == 0) {
     int64_t excl = 0;
-    if (group == 0) {
-      if (lane == 0) st_relaxed_u64(a.status, kSFlagInc | agg);
+    if (chunk == 0) {
+      if (lane == 0) st_relaxed_u64(a.status, lb_word(epoch, kLBInc, agg));
     } else {
-      if (lane == 0) st_relaxed_u64(a.status + group, kSFlagAgg | agg);
-      int64_t pred = group - 1;
+      if (lane == 0) st_relaxed_u64(a.status + chunk, lb_word(epoch, kLBAgg, agg));
+      int64_t pred = chunk - 1;
       while (true) {
         const int64_t idx = pred - lane;
-        const uint64_t s = (idx >= 0) ? ld_relaxed_u64(a.status + idx) : kSFlagInc;
-        const uint64_t flag = s >> 62;
-        const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
+        uint64_t s = lb_word(epoch, kLBInc, 0);
+        if (idx >= 0) s = ld_relaxed_u64(a.status + idx);
+        const bool valid = ((s >> kEpochShift) & kEpochMask) == epoch;
+        const uint64_t flag = valid ? ((s >> 42) & 3ull) : 0ull;
+        const uint32_t incm = __ballot_sync(0xffffffffu, flag == 2);
         const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
-        const int first = inc ? (__ffs(inc) - 1) : 31;
+        const int first = incm ? (__ffs(incm) - 1) : 31;
         const uint32_t upto = (2u << first) - 1u;
         if (inv & upto) {
-          __nanosleep(16);
+          __nanosleep(32);
           continue;
         }
-        uint64_t v = (lane <= first) ? (s & kSValMask) : 0ull;
+        uint64_t v = (lane <= first) ? (s & kLBVal) : 0ull;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         excl += (int64_t)v;
-        if (inc) break;
+        if (incm) break;
         pred -= 32;
       }
-      if (lane == 0) st_relaxed_u64(a.status + group, kSFlagInc | ((uint64_t)excl + agg));
+      if (lane == 0) st_relaxed_u64(a.status + chunk, lb_word(epoch, kLBInc, (uint64_t)excl + agg));
     }
     if (lane == 0) {
       const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
       s_base = cur + excl;
-      if (t0 + nt == a.num_tiles) {
+      if ((chunk + 1) * kScanTiles >= a.num_tiles) {
         atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)agg));
         if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)agg;
+        *(volatile uint32_t*)&a.hdr->epoch = epoch;
       }
     }
   }
   __syncthreads();
-  const int64_t base = s_base;
-  const int warp = tid >> 5;
-  // one warp per tile, unrolled so several independent loads are in flight
-  for (int k = warp; k < nt; k += kWarps) {
-    const int64_t t = t0 + k;
-    const uint32_t cnt = s_off[k + 1] - s_off[k];
-    const uint16_t* src = a.scratch + t * kSTile;
-    const int64_t out0 = base + s_off[k];
-    const uint64_t w0 = (uint64_t)(a.global_base + t * kSTile) << 1;
-    if (out0 + cnt <= a.cap) {
-#pragma unroll 4
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint32_t e = __ldg(src + i);
-        a.sparse[out0 + i] = w0 + ((uint64_t)(e & 0x7fffu) << 1) + (e >> 15);
+  int64_t off = s_base + wpre + (inc - sum);
+#pragma unroll
+  for (int m = 0; m < kScanPer; ++m) {
+    if (t0 + m < a.num_tiles) a.toffs[t0 + m] = off;
+    off += c[m];
+  }
+}
+
+// Expand: warp per tile, no waits -- the staged 16-bit entries become
+// global (index << 1 | up) words at the tile's scanned position.
+constexpr int kExpTilesPerCta = kWarps;
+
+struct ExpandArgs {
+  const uint16_t* scratch;
+  const uint32_t* counts;
+  const int64_t* toffs;
+  int64_t num_tiles;
+  int64_t global_base;
+  uint64_t* sparse;
+  int64_t cap;
+};
+
+__global__ void __launch_bounds__(kSThreads) rl_expand_kernel(const ExpandArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * kExpTilesPerCta + warp;
+  if (t >= a.num_tiles) return;
+  const uint32_t cnt = a.counts[t];
+  const int64_t out0 = a.toffs[t];
+  const uint16_t* src = a.scratch + t * kSTile;
+  const uint64_t w0 = (uint64_t)(a.global_base + t * kSTile) << 1;
+  if (out0 + cnt <= a.cap) {
+    for (uint32_t i0 = 0; i0 < cnt; i0 += 4 * 32) {
+      uint32_t e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * 32 + lane;
+        e[u] = (i < cnt) ? (uint32_t)__ldg(src + i) : 0u;
       }
-    } else {
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint32_t e = __ldg(src + i);
-        if (out0 + i < a.cap) a.sparse[out0 + i] = w0 + ((uint64_t)(e & 0x7fffu) << 1) + (e >> 15);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * 32 + lane;
+        if (i < cnt) a.sparse[out0 + i] = w0 + ((uint64_t)(e[u] & 0x7fffu) << 1) + (e[u] >> 15);
       }
+    }
+  } else {
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const uint32_t e = __ldg(src + i);
+      if (out0 + i < a.cap) a.sparse[out0 + i] = w0 + ((uint64_t)(e & 0x7fffu) << 1) + (e >> 15);
     }
   }
 }
@@ -370,41 +430,44 @@ __global__ void __launch_bounds__(kSThreads) rl_expand_kernel(const ExpandArgs a
 // auditor: streaming replay against the sparse log
 // ---------------------------------------------------------------------------
 
-struct RPStreamArgs {
+struct RPArgs {
   const double* x;
   int64_t n;
   Grid g;
   const uint64_t* log;
+  int64_t n_words;
   int64_t log_base;
-  const int64_t* offs;  // [num_tiles + 1] word ranges per tile
   void* out;
   int64_t num_tiles;
+  int64_t tiles_per_cta;
   int64_t* counters;
   int32_t* err;
 };
 
-__global__ void rp_tile_offsets_kernel(const uint64_t* __restrict__ w, int64_t n_words, int64_t base, int64_t n,
-                                       int64_t num_tiles, int64_t* __restrict__ offs, int64_t* counters) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > num_tiles) return;
-  const int64_t key = base + std::min<int64_t>(t * kSTile, n);
-  int64_t lo = 0, hi = n_words;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)(__ldg(w + mid) >> 1) < key) lo = mid + 1;
-    else hi = mid;
+// lower_bound over the sorted word indices by one warp, 32 probes per step
+__device__ int64_t warp_lower_bound(const uint64_t* w, int64_t n, int64_t key, int lane) {
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const bool lt = (p < hi) && ((int64_t)(__ldg(w + p) >> 1) < key);
+    const int c = __popc(__ballot_sync(0xffffffffu, lt));
+    if (c == 0) return lo;
+    const int64_t nlo = lo + (int64_t)(c - 1) * step + 1;
+    hi = std::min<int64_t>(hi, lo + (int64_t)c * step);
+    lo = nlo;
   }
-  offs[t] = lo;
-  if (t == 0) counters[1] = lo;
-  if (t == num_tiles) counters[2] = lo;
+  const int64_t p = lo + lane;
+  const bool lt = (p < hi) && ((int64_t)(__ldg(w + p) >> 1) < key);
+  return lo + __popc(__ballot_sync(0xffffffffu, lt));
 }
 
 // One tile of the auditor pass.  Each thread reads the codes of its own
 // elements from the map and resets them to 1, so the map is all-ignore
 // again for the next tile without an extra barrier.
 template <int OUT, bool FAST, bool FULL>
-__device__ __forceinline__ uint32_t rp_tile(const RPStreamArgs& a, const double* src, uint8_t* cs, void* o,
-                                            int lim, int warp, int lane, uint32_t& err) {
+__device__ __forceinline__ uint32_t rp_tile(const RPArgs& a, const double* src, uint8_t* cs, void* o, int lim,
+                                            int warp, int lane, uint32_t& err) {
   uint32_t flips = 0;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
@@ -434,23 +497,35 @@ __device__ __forceinline__ uint32_t rp_tile(const RPStreamArgs& a, const double*
   return flips;
 }
 
-__device__ __forceinline__ void scatter_entry(uint8_t* cs, uint64_t word, uint64_t prev, int64_t i, int64_t key0,
-                                              uint32_t& err) {
-  const int64_t idx = (int64_t)(word >> 1) - key0;
-  const bool ordered = (i == 0) || ((prev >> 1) < (word >> 1));
-  if (idx >= 0 && idx < kSTile && ordered) cs[idx] = (word & 1ull) ? 2 : 0;
-  else err |= VT_ERR_BAD_SPARSE;
+// Consume this tile's log words from the window [cur, cur + kSThreads)
+// (prefetched in w/prev), scatter them into the code map; returns how many
+// words belonged to the tile.  Entries must be a sorted prefix of the window.
+__device__ __forceinline__ int scatter_window(uint8_t* cs, uint64_t w, uint64_t prev, int64_t i, int64_t n_words,
+                                              int64_t key0, int64_t key1, uint32_t& err) {
+  const bool have = i < n_words;
+  const int64_t idx = (int64_t)(w >> 1);
+  const bool in = have && idx < key1;
+  const int cnt = __syncthreads_count(in);
+  if (in) {
+    const bool ordered = (i == 0) || ((prev >> 1) < (w >> 1));
+    if (idx >= key0 && ordered && (int)threadIdx.x < cnt) cs[idx - key0] = (w & 1ull) ? 2 : 0;
+    else err |= VT_ERR_BAD_SPARSE;
+  }
+  return cnt;
 }
 
 template <int OUT, bool FAST>
-__global__ void __launch_bounds__(kSThreads, 3) rp_stream_kernel(const RPStreamArgs a) {
+__global__ void __launch_bounds__(kSThreads, 3) rp_fused_kernel(const RPArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ uint32_t s_red[kWarps];
+  __shared__ int64_t s_lo;
   Ring ring{reinterpret_cast<double*>(sm), bars};
   uint8_t* cs = sm + kRingBytes;  // [kSTile] code map, all 1 between tiles
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t T0 = (int64_t)blockIdx.x * a.tiles_per_cta;
+  const int64_t T1 = std::min<int64_t>(T0 + a.tiles_per_cta, a.num_tiles);
   const int64_t full_tiles = a.n / kSTile;
   const uint64_t pol = evict_first_policy();
   if (tid == 0) {
@@ -460,66 +535,62 @@ __global__ void __launch_bounds__(kSThreads, 3) rp_stream_kernel(const RPStreamA
   reinterpret_cast<uint2*>(cs)[tid] = make_uint2(0x01010101u, 0x01010101u);
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < kStages; ++s) issue_tile(ring, a.x, blockIdx.x + (int64_t)s * gridDim.x, full_tiles, s, pol);
-
-  // Log prefetch pipeline: the word range of tile k+2 and the first 256
-  // words (plus predecessors, for the order check) of tile k+1 are loaded
-  // while tile k is processed.
-  const int64_t G = gridDim.x;
-  int64_t t0 = blockIdx.x;
-  int64_t p_lo = 0, p_hi = 0, q_lo = 0, q_hi = 0;
-  uint64_t p_w = 0, p_prev = 0;
-  if (t0 < a.num_tiles) {
-    p_lo = a.offs[t0];
-    p_hi = a.offs[t0 + 1];
-    const int64_t i = p_lo + tid;
-    if (i < p_hi) {
-      p_w = __ldg(a.log + i);
-      p_prev = i ? __ldg(a.log + i - 1) : 0ull;
-    }
+    for (int s = 0; s < kStages && T0 + s < T1; ++s) issue_tile(ring, a.x, T0 + s, full_tiles, s, pol);
+  if (warp == 0) {
+    const int64_t lo = warp_lower_bound(a.log, a.n_words, a.log_base + T0 * kSTile, lane);
+    if (lane == 0) s_lo = lo;
   }
-  if (t0 + G < a.num_tiles) {
-    q_lo = a.offs[t0 + G];
-    q_hi = a.offs[t0 + G + 1];
+  __syncthreads();
+  int64_t cur = s_lo;  // first log word of the current tile (block-uniform)
+  if (blockIdx.x == 0 && tid == 0) a.counters[1] = cur;
+  uint64_t pw = 0, pp = 0;
+  {
+    const int64_t i = cur + tid;
+    if (i < a.n_words) {
+      pw = __ldg(a.log + i);
+      pp = i ? __ldg(a.log + i - 1) : 0ull;
+    }
   }
 
   uint32_t err = 0, flips = 0;
-  for (int64_t k = 0;; ++k) {
-    const int64_t t = blockIdx.x + k * G;
-    if (t >= a.num_tiles) break;
+  for (int64_t t = T0; t < T1; ++t) {
+    const int64_t k = t - T0;
     const int s = (int)(k % kStages);
     const int64_t tbase = t * kSTile;
-    const int64_t c_lo = p_lo, c_hi = p_hi;
-    const uint64_t c_w = p_w, c_prev = p_prev;
-    p_lo = q_lo;
-    p_hi = q_hi;
-    p_w = p_prev = 0;
-    {
-      const int64_t i = p_lo + tid;
-      if (i < p_hi) {
-        p_w = __ldg(a.log + i);
-        p_prev = i ? __ldg(a.log + i - 1) : 0ull;
+    const int64_t key0 = a.log_base + tbase;
+    const int64_t key1 = a.log_base + std::min<int64_t>(tbase + kSTile, a.n);
+    int cnt = scatter_window(cs, pw, pp, cur + tid, a.n_words, key0, key1, err);
+    cur += cnt;
+    while (cnt == kSThreads) {  // more than one window of entries in this tile
+      const int64_t i = cur + tid;
+      uint64_t w = 0, p = 0;
+      if (i < a.n_words) {
+        w = __ldg(a.log + i);
+        p = __ldg(a.log + i - 1);
+      }
+      cnt = scatter_window(cs, w, p, i, a.n_words, key0, key1, err);
+      cur += cnt;
+    }
+    {  // prefetch the next tile's window while this tile computes
+      const int64_t i = cur + tid;
+      pw = pp = 0;
+      if (i < a.n_words) {
+        pw = __ldg(a.log + i);
+        pp = i ? __ldg(a.log + i - 1) : 0ull;
       }
     }
-    if (t + 2 * G < a.num_tiles) {
-      q_lo = a.offs[t + 2 * G];
-      q_hi = a.offs[t + 2 * G + 1];
-    }
-    const int64_t key0 = a.log_base + tbase;
-    int64_t i = c_lo + tid;
-    if (i < c_hi) scatter_entry(cs, c_w, c_prev, i, key0, err);
-    for (i += kSThreads; i < c_hi; i += kSThreads) scatter_entry(cs, __ldg(a.log + i), __ldg(a.log + i - 1), i, key0, err);
     const double* src = acquire_tile(ring, a.x, a.n, t, full_tiles, s, (uint32_t)((k / kStages) & 1));
     __syncthreads();  // code map complete, x tile resident
     void* o = tile_out<OUT>(a.out, tbase);
     flips += (t < full_tiles) ? rp_tile<OUT, FAST, true>(a, src, cs, o, kSTile, warp, lane, err)
                               : rp_tile<OUT, FAST, false>(a, src, cs, o, (int)(a.n - tbase), warp, lane, err);
     __syncthreads();  // ring slot s consumed, code map reset
-    if (tid == 0) {
+    if (tid == 0 && t + kStages < T1) {
       fence_proxy_async();
-      issue_tile(ring, a.x, t + (int64_t)kStages * G, full_tiles, s, pol);
+      issue_tile(ring, a.x, t + kStages, full_tiles, s, pol);
     }
   }
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) a.counters[2] = cur;
   report_err(a.err, err);
   uint32_t v = flips;
 #pragma unroll
@@ -540,24 +611,28 @@ __global__ void __launch_bounds__(kSThreads, 3) rp_stream_kernel(const RPStreamA
 
 int64_t stream_tiles(int64_t n) { return (n + kSTile - 1) / kSTile; }
 
+// [header 64 B][status: scan CTAs x 8][counts: T x 4][toffs: T x 8][scratch: T x kSTile x 2]
 size_t rl_stream_workspace(int64_t n) {
   const int64_t t = stream_tiles(n);
-  const int64_t groups = (t + kGroupTiles - 1) / kGroupTiles;
-  return (size_t)(groups * 8 + t * 4 + 256) + (size_t)t * kSTile * 2 + 256;
+  const int64_t chunks = (t + kScanTiles - 1) / kScanTiles;
+  return (size_t)(64 + chunks * 8 + t * 12 + 512) + (size_t)t * kSTile * 2 + 256;
 }
 
-size_t rp_stream_workspace(int64_t n) { return (size_t)(stream_tiles(n) + 1) * 8 + 256; }
+size_t rp_stream_workspace(int64_t n) {
+  (void)n;
+  return 0;
+}
 
 static int resident_ctas(const void* fn, size_t smem) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSThreads, smem);
-  return std::max(1, per) * sms;
+  return std::max(1, per * sms);
 }
 
 template <int OUT, bool FAST>
-static int launch_rl_stream(const RLStreamArgs& a, const ExpandArgs& e, cudaStream_t st) {
+static int launch_rl(const RLArgs& a, const ScanArgs& sc, const ExpandArgs& e, cudaStream_t st) {
   const size_t smem = kRingBytes + 2 * kWarps * kStageRow * sizeof(uint16_t);
   auto k = rl_stream_kernel<OUT, FAST>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -565,8 +640,11 @@ static int launch_rl_stream(const RLStreamArgs& a, const ExpandArgs& e, cudaStre
   k<<<grid, kSThreads, smem, st>>>(a);
   int rc = vt_check_launch("rl_stream_kernel");
   if (rc) return rc;
-  const int64_t groups = (a.num_tiles + kGroupTiles - 1) / kGroupTiles;
-  rl_expand_kernel<<<(unsigned)groups, kSThreads, 0, st>>>(e);
+  const int64_t chunks = (a.num_tiles + kScanTiles - 1) / kScanTiles;
+  rl_scan_kernel<<<(unsigned)chunks, kSThreads, 0, st>>>(sc);
+  if ((rc = vt_check_launch("rl_scan_kernel"))) return rc;
+  const int64_t ectas = (a.num_tiles + kExpTilesPerCta - 1) / kExpTilesPerCta;
+  rl_expand_kernel<<<(unsigned)ectas, kSThreads, 0, st>>>(e);
   return vt_check_launch("rl_expand_kernel");
 }
 
@@ -574,51 +652,56 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st) {
   const int64_t tiles = stream_tiles(n);
-  const int64_t groups = (tiles + kGroupTiles - 1) / kGroupTiles;
+  const int64_t chunks = (tiles + kScanTiles - 1) / kScanTiles;
   uint8_t* w = static_cast<uint8_t*>(ws);
-  uint64_t* status = reinterpret_cast<uint64_t*>(w);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(w + groups * 8);
-  uint16_t* scratch = reinterpret_cast<uint16_t*>(w + ((groups * 8 + tiles * 4 + 255) & ~(int64_t)255));
-  if (cudaMemsetAsync(status, 0, (size_t)groups * 8, st) != cudaSuccess) return vt_check_launch("memset");
-  RLStreamArgs a{x, n, g, thr32, out, scratch, counts, tiles, err};
-  ExpandArgs e{scratch, counts, tiles, status, global_base, cursor_in, cursor_out, sparse, cap, counters};
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(w);
+  uint64_t* status = reinterpret_cast<uint64_t*>(w + 64);
+  int64_t* toffs = reinterpret_cast<int64_t*>(w + ((64 + chunks * 8 + 255) & ~(int64_t)255));
+  uint32_t* counts = reinterpret_cast<uint32_t*>(toffs + tiles);
+  uint16_t* scratch = reinterpret_cast<uint16_t*>(
+      w + ((((64 + chunks * 8 + 255) & ~(int64_t)255) + tiles * 12 + 255) & ~(int64_t)255));
+  RLArgs a{x, n, g, thr32, out, tiles, counts, scratch, err};
+  ScanArgs sc{counts, tiles, hdr, status, toffs, cursor_in, cursor_out, counters};
+  ExpandArgs e{scratch, counts, toffs, tiles, global_base, sparse, cap};
   if (fast) {
-    return out_kind == VT_OUT_F32 ? launch_rl_stream<VT_OUT_F32, true>(a, e, st)
-         : out_kind == VT_OUT_F64 ? launch_rl_stream<VT_OUT_F64, true>(a, e, st)
-                                  : launch_rl_stream<VT_OUT_NONE, true>(a, e, st);
+    return out_kind == VT_OUT_F32 ? launch_rl<VT_OUT_F32, true>(a, sc, e, st)
+         : out_kind == VT_OUT_F64 ? launch_rl<VT_OUT_F64, true>(a, sc, e, st)
+                                  : launch_rl<VT_OUT_NONE, true>(a, sc, e, st);
   }
-  return out_kind == VT_OUT_F32 ? launch_rl_stream<VT_OUT_F32, false>(a, e, st)
-       : out_kind == VT_OUT_F64 ? launch_rl_stream<VT_OUT_F64, false>(a, e, st)
-                                : launch_rl_stream<VT_OUT_NONE, false>(a, e, st);
+  return out_kind == VT_OUT_F32 ? launch_rl<VT_OUT_F32, false>(a, sc, e, st)
+       : out_kind == VT_OUT_F64 ? launch_rl<VT_OUT_F64, false>(a, sc, e, st)
+                                : launch_rl<VT_OUT_NONE, false>(a, sc, e, st);
+}
+
+template <typename Args>
+static void split_tiles(Args& a, int resident) {
+  const int64_t grid = std::min<int64_t>(a.num_tiles, resident);
+  a.tiles_per_cta = (a.num_tiles + grid - 1) / grid;
 }
 
 template <int OUT, bool FAST>
-static int launch_rp_stream(const RPStreamArgs& a, cudaStream_t st) {
+static int launch_rp(RPArgs a, cudaStream_t st) {
   const size_t smem = kRingBytes + kSTile;
-  auto k = rp_stream_kernel<OUT, FAST>;
+  auto k = rp_fused_kernel<OUT, FAST>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = (int)std::min<int64_t>(a.num_tiles, resident_ctas((const void*)k, smem));
+  split_tiles(a, resident_ctas((const void*)k, smem));
+  const int grid = (int)((a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta);
   k<<<grid, kSThreads, smem, st>>>(a);
-  return vt_check_launch("rp_stream_kernel");
+  return vt_check_launch("rp_fused_kernel");
 }
 
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st) {
-  const int64_t tiles = stream_tiles(n);
-  int64_t* offs = static_cast<int64_t*>(ws);
-  rp_tile_offsets_kernel<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, st>>>(log, n_words, log_base, n, tiles, offs,
-                                                                              counters);
-  int rc = vt_check_launch("rp_tile_offsets_kernel");
-  if (rc) return rc;
-  RPStreamArgs a{x, n, g, log, log_base, offs, out, tiles, counters, err};
+  (void)ws;
+  RPArgs a{x, n, g, log, n_words, log_base, out, stream_tiles(n), 1, counters, err};
   if (fast) {
-    return out_kind == VT_OUT_F32 ? launch_rp_stream<VT_OUT_F32, true>(a, st)
-         : out_kind == VT_OUT_F64 ? launch_rp_stream<VT_OUT_F64, true>(a, st)
-                                  : launch_rp_stream<VT_OUT_NONE, true>(a, st);
+    return out_kind == VT_OUT_F32 ? launch_rp<VT_OUT_F32, true>(a, st)
+         : out_kind == VT_OUT_F64 ? launch_rp<VT_OUT_F64, true>(a, st)
+                                  : launch_rp<VT_OUT_NONE, true>(a, st);
   }
-  return out_kind == VT_OUT_F32 ? launch_rp_stream<VT_OUT_F32, false>(a, st)
-       : out_kind == VT_OUT_F64 ? launch_rp_stream<VT_OUT_F64, false>(a, st)
-                                : launch_rp_stream<VT_OUT_NONE, false>(a, st);
+  return out_kind == VT_OUT_F32 ? launch_rp<VT_OUT_F32, false>(a, st)
+       : out_kind == VT_OUT_F64 ? launch_rp<VT_OUT_F64, false>(a, st)
+                                : launch_rp<VT_OUT_NONE, false>(a, st);
 }
 
 }  // namespace vt

@@ -63,11 +63,15 @@ def back(t: torch.Tensor, host: bool, shape: tuple):
 
 
 def workspace(nbytes: int, tag: str) -> torch.Tensor:
-    """Per (device, stream, tag) scratch buffer, grown on demand."""
-    key = (torch.cuda.current_device(), stream_ptr(), tag)
+    """Per (device, tag) scratch buffer, grown on demand.  Operators that may
+    run concurrently on different streams use different tags.  The leading
+    1 MiB (epoch header + look-back status words of vt_round_log) is
+    zero-filled once at allocation; the rest needs no initialisation."""
+    key = (torch.cuda.current_device(), tag)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device="cuda")  # zero-filled: see vt_round_log
+        ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+        ws[: 1 << 20].zero_()
         _WS[key] = ws
     return ws
 

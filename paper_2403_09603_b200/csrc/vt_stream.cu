@@ -635,8 +635,12 @@ template <int OUT, bool FAST>
 static int launch_rl(const RLArgs& a, const ScanArgs& sc, const ExpandArgs& e, cudaStream_t st) {
   const size_t smem = kRingBytes + 2 * kWarps * kStageRow * sizeof(uint16_t);
   auto k = rl_stream_kernel<OUT, FAST>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = (int)std::min<int64_t>(a.num_tiles, resident_ctas((const void*)k, smem));
+  static int resident = 0;  // one process per GPU: attribute + occupancy queried once
+  if (!resident) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    resident = resident_ctas((const void*)k, smem);
+  }
+  const int grid = (int)std::min<int64_t>(a.num_tiles, resident);
   k<<<grid, kSThreads, smem, st>>>(a);
   int rc = vt_check_launch("rl_stream_kernel");
   if (rc) return rc;
@@ -683,8 +687,12 @@ template <int OUT, bool FAST>
 static int launch_rp(RPArgs a, cudaStream_t st) {
   const size_t smem = kRingBytes + kSTile;
   auto k = rp_fused_kernel<OUT, FAST>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  split_tiles(a, resident_ctas((const void*)k, smem));
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    resident = resident_ctas((const void*)k, smem);
+  }
+  split_tiles(a, resident);
   const int grid = (int)((a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta);
   k<<<grid, kSThreads, smem, st>>>(a);
   return vt_check_launch("rp_fused_kernel");

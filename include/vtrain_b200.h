@@ -29,7 +29,7 @@
  *   vt_log_validate   <- the byte check of _unpack_block     roundlog.py:75-76
  *   vt_log_histogram  <- roundlog.LogReader.histogram        roundlog.py:203-206
  *   vt_tau_kth_key    <- protocol.search_tau predicate       protocol.py:494-506 (budget form,
- *                        SURVEY.md Appendix A.4)
+ *   vt_tau_budget_key    SURVEY.md Appendix A.4)
  *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
@@ -139,6 +139,16 @@ size_t vt_tau_workspace(int64_t n);
  */
 int vt_tau_kth_key(const double *x, int64_t n, int b_r, int64_t rank, uint64_t *key_out,
                    int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * Budget form: *key_out = FP64 bits of v', the (budget+1)-th
+ * largest p clamped for a bisection inside (tau_lo, tau_hi): tau_lo if
+ * v <= tau_lo, +inf if v > tau_hi, else v exactly.  Two streaming passes.
+ * *status_out (device int32) = 1 when done, 2 when the selected digit held
+ * more candidates than the workspace: the caller then uses vt_tau_kth_key.
+ */
+int vt_tau_budget_key(const double *x, int64_t n, int b_r, int64_t budget, double tau_lo,
+                      double tau_hi, uint64_t *key_out, int32_t *status_out, int32_t *err,
+                      void *ws, size_t ws_bytes, vt_stream_t stream);
 /* out[0] = min over s[n] ignoring NaN (+inf if none), *nan_flag |= 1 if any NaN */
 int vt_min_f64(const double *s, int64_t n, double *out, int32_t *nan_flag, vt_stream_t stream);
 

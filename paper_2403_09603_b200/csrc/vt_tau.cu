@@ -14,6 +14,7 @@
 // (match_any-aggregated atomics), then a one-CTA select kernel narrows the
 // prefix on the device, so no host round trip happens between passes.
 #include <algorithm>
+#include <cstring>
 
 #include "vt_common.cuh"
 
@@ -183,13 +184,298 @@ __global__ void min_final_kernel(double* out) {
   *out = __longlong_as_double((long long)b);
 }
 
+// ---------------------------------------------------------------------------
+// Budget selection (the fast path of the budget search).
+//
+// The bisection only ever compares v with midpoints strictly inside
+// (tau_lo, tau_hi), so v may be clamped: v <= tau_lo -> tau_lo, v > tau_hi ->
+// +inf.  Keys inside (tau_lo, tau_hi] are offsets o = key - lo_key - 1 in
+// [0, W); they are resolved from the top in 13-bit digits.  Each full
+// streaming pass over x histograms the next digit inside the selected
+// prefix (spread-out bins: plain shared atomics) and, as soon as the
+// selected digit holds at most kCandCap keys, compacts them instead; a
+// one-CTA kernel then finishes the selection on the candidates.  Typical
+// data needs two passes; a distribution with a hot digit (e.g. many exact
+// midpoints) takes one more.  Level selection runs on the device, so no
+// host round trip happens until the final key.
+// ---------------------------------------------------------------------------
+
+constexpr int kBudBits = 13;
+constexpr int kBudBins = 1 << kBudBits;
+constexpr int kBudMaxLevels = 5;
+constexpr int64_t kCandCap = 1 << 16;
+
+struct BudState {
+  uint64_t lo_key, hi_key;
+  uint64_t cnt_above;  // keys > hi_key
+  uint64_t cand;       // candidates appended
+  uint64_t prefix;     // fixed offset bits (under pmask)
+  uint64_t pmask;
+  int64_t rank;        // remaining 0-based rank from the top inside the prefix
+  uint64_t bin_count;  // keys inside the prefix
+  int level;           // next digit level to histogram
+  int compacting;      // the current pass compacts instead of histogramming
+  int status;          // 0 running, 1 done (key written)
+  int nlevels;
+  int shift[kBudMaxLevels];
+  int bits[kBudMaxLevels];
+};
+
+__global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                       BudState* st, uint32_t* __restrict__ hist,
+                                                       uint64_t* __restrict__ cand, int32_t* errp) {
+  __shared__ uint32_t sh[kBudBins];
+  __shared__ unsigned long long s_above;
+  if (st->status != 0) return;
+  const int level = st->level;
+  const bool compact = st->compacting != 0;
+  const bool first = level == 0 && !compact;
+  const uint64_t lo = st->lo_key, hi = st->hi_key, prefix = st->prefix, pmask = st->pmask;
+  const int sh_lv = compact ? 0 : st->shift[level];
+  const uint32_t dmask = compact ? 0u : ((1u << st->bits[level]) - 1u);
+  if (!compact) {
+    for (int i = threadIdx.x; i < kBudBins; i += 256) sh[i] = 0;
+  }
+  if (threadIdx.x == 0) s_above = 0;
+  __syncthreads();
+  uint32_t err = 0, above = 0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * 256; base < n; base += (int64_t)gridDim.x * 256) {
+    const int64_t i = base + threadIdx.x;
+    bool in = false;
+    uint64_t k = 0;
+    if (i < n) {
+      k = dist_key(__ldg(x + i), g, err);
+      if (k > hi) above += first ? 1u : 0u;
+      else in = k > lo && ((k - lo - 1) & pmask) == prefix;
+    }
+    if (compact) {
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(&st->cand), (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (in) {
+          const uint64_t slot = pos + __popc(m & ((1u << lane) - 1u));
+          if ((int64_t)slot < kCandCap) cand[slot] = k;
+        }
+      }
+    } else if (in) {
+      atomicAdd(&sh[(uint32_t)((k - lo - 1) >> sh_lv) & dmask], 1u);
+    }
+  }
+  report_err(errp, err);
+  if (first) {
+    for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+    if (lane == 0 && above) atomicAdd(&s_above, (unsigned long long)above);
+  }
+  __syncthreads();
+  if (!compact) {
+    for (int i = threadIdx.x; i < kBudBins; i += 256)
+      if (sh[i]) atomicAdd(&hist[(size_t)level * kBudBins + i], sh[i]);
+  }
+  if (first && threadIdx.x == 0 && s_above)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->cnt_above), s_above);
+}
+
+// Pick the digit of the rank-th largest key (descending scan by one CTA).
+__device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int& bin, int64_t& above_out) {
+  __shared__ unsigned long long s_warp[kSelThreads / 32];
+  __shared__ int s_bin;
+  __shared__ long long s_above;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (nbins + kSelThreads - 1) / kSelThreads;
+  const int hi = nbins - t * per;
+  unsigned long long mine = 0;
+  for (int k = 0; k < per; ++k) {
+    const int b = hi - 1 - k;
+    if (b >= 0) mine += hist[b];
+  }
+  unsigned long long incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  if (t == 0) s_bin = -1;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long v = s_warp[lane];
+    unsigned long long w = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    s_warp[lane] = w - v;
+  }
+  __syncthreads();
+  const unsigned long long above = s_warp[warp] + incl - mine;
+  if ((long long)above <= rank && rank < (long long)(above + mine)) {
+    unsigned long long acc = above;
+    for (int k = 0; k < per; ++k) {
+      const int b = hi - 1 - k;
+      if (b < 0) break;
+      const unsigned long long c = hist[b];
+      if (rank < (long long)(acc + c)) {
+        s_bin = b;
+        s_above = (long long)acc;
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+  bin = s_bin;
+  above_out = s_above;
+}
+
+// After a pass: either finish from the candidates, or select the digit of
+// this level and decide whether the next pass compacts or histograms.
+__global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, const uint32_t* __restrict__ hist,
+                                                               const uint64_t* __restrict__ cand, int64_t budget,
+                                                               uint64_t* key_out) {
+  __shared__ uint32_t sh[kBudBins];
+  if (st->status != 0) return;
+  const uint64_t lo1 = st->lo_key + 1;
+  if (st->compacting) {  // exact select among the compacted candidates
+    const int64_t m = (int64_t)st->cand;
+    uint64_t prefix = st->prefix, pmask = st->pmask;
+    int64_t rank = st->rank;
+    for (int lv = st->level; lv < st->nlevels; ++lv) {
+      const int sh_lv = st->shift[lv], bits = st->bits[lv];
+      for (int i = threadIdx.x; i < kBudBins; i += kSelThreads) sh[i] = 0;
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < m; i += kSelThreads) {
+        const uint64_t o = cand[i] - lo1;
+        if ((o & pmask) == prefix) atomicAdd(&sh[(o >> sh_lv) & ((1u << bits) - 1u)], 1u);
+      }
+      __syncthreads();
+      int bin;
+      int64_t above;
+      select_digit(sh, 1 << bits, rank, bin, above);
+      prefix |= (uint64_t)bin << sh_lv;
+      pmask |= ((1ull << bits) - 1ull) << sh_lv;
+      rank -= above;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      *key_out = lo1 + prefix;
+      st->status = 1;
+    }
+    return;
+  }
+  const int level = st->level;
+  int64_t rank = st->rank;
+  if (level == 0) {
+    const uint64_t above_hi = st->cnt_above;
+    if ((int64_t)above_hi > budget) {  // more than budget keys above tau_hi: v > tau_hi
+      if (threadIdx.x == 0) {
+        *key_out = 0x7ff0000000000000ull;
+        st->status = 1;
+      }
+      return;
+    }
+    rank = budget - (int64_t)above_hi;
+  }
+  int bin;
+  int64_t above;
+  select_digit(hist + (size_t)level * kBudBins, 1 << st->bits[level], rank, bin, above);
+  if (threadIdx.x == 0) {
+    if (bin < 0) {  // fewer than budget+1 keys above tau_lo: v <= tau_lo
+      *key_out = st->lo_key;
+      st->status = 1;
+      return;
+    }
+    const int sh_lv = st->shift[level];
+    st->prefix |= (uint64_t)bin << sh_lv;
+    st->pmask |= ((1ull << st->bits[level]) - 1ull) << sh_lv;
+    st->rank = rank - above;
+    st->bin_count = hist[(size_t)level * kBudBins + bin];
+    st->level = level + 1;
+    if (level + 1 >= st->nlevels) {  // every offset bit fixed
+      *key_out = lo1 + st->prefix;
+      st->status = 1;
+    } else if ((int64_t)st->bin_count <= kCandCap) {
+      st->compacting = 1;
+    }
+  }
+}
+
+__global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out) {
+  st->lo_key = lo_key;
+  st->hi_key = hi_key;
+  st->cnt_above = 0;
+  st->cand = 0;
+  st->prefix = 0;
+  st->pmask = 0;
+  st->rank = 0;
+  st->bin_count = 0;
+  st->level = 0;
+  st->compacting = 0;
+  st->status = 0;
+  const uint64_t width = hi_key - lo_key;  // offsets 0 .. width-1
+  int top = 64 - __clzll((long long)(width - 1));
+  if (width <= 1) top = 1;
+  int nl = 0;
+  while (top > 0 && nl < kBudMaxLevels) {
+    const int b = top < kBudBits ? top : kBudBits;
+    top -= b;
+    st->shift[nl] = top;
+    st->bits[nl] = b;
+    ++nl;
+  }
+  st->nlevels = nl;
+  *key_out = 0;
+}
+
 }  // namespace vt
 
 using namespace vt;
 
 extern "C" size_t vt_tau_workspace(int64_t n) {
   (void)n;
-  return (size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256;
+  const size_t radix = (size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256;
+  const size_t budget = 512 + (size_t)kBudMaxLevels * kBudBins * 4 + (size_t)kCandCap * 8;
+  return std::max(radix, budget);
+}
+
+extern "C" int vt_tau_budget_key(const double* x, int64_t n, int b_r, int64_t budget, double tau_lo,
+                                 double tau_hi, uint64_t* key_out, int32_t* status_out, int32_t* err, void* ws,
+                                 size_t ws_bytes, vt_stream_t stream) {
+  if (n < 0 || b_r < 10 || b_r > 32 || budget < 0 || !key_out || !status_out || !err || !ws ||
+      ws_bytes < vt_tau_workspace(n) || !(tau_lo > 0.0) || !(tau_hi > tau_lo)) {
+    vt_set_error("vt_tau_budget_key: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  BudState* st = reinterpret_cast<BudState*>(w);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(w + 512);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(w + 512 + (size_t)kBudMaxLevels * kBudBins * 4);
+  uint64_t lo_key, hi_key;
+  memcpy(&lo_key, &tau_lo, 8);
+  memcpy(&hi_key, &tau_hi, 8);
+  if (cudaMemsetAsync(hist, 0, (size_t)kBudMaxLevels * kBudBins * 4, s) != cudaSuccess)
+    return vt_check_launch("memset");
+  bud_init_kernel<<<1, 1, 0, s>>>(st, lo_key, hi_key, key_out);
+  int rc = vt_check_launch("bud_init_kernel");
+  if (rc) return rc;
+  const Grid g = make_grid(b_r, 0.0);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, 148 * 8));
+  // level passes: at most nlevels histogram passes plus one compaction pass;
+  // kernels return at once when the state says done
+  for (int p = 0; p <= kBudMaxLevels; ++p) {
+    if (n > 0) {
+      bud_pass_kernel<<<blocks, 256, 0, s>>>(x, n, g, st, hist, cand, err);
+      if ((rc = vt_check_launch("bud_pass_kernel"))) return rc;
+    }
+    bud_step_kernel<<<1, kSelThreads, 0, s>>>(st, hist, cand, budget, key_out);
+    if ((rc = vt_check_launch("bud_step_kernel"))) return rc;
+  }
+  if (cudaMemcpyAsync(status_out, &st->status, 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return vt_check_launch("status copy");
+  return VT_OK;
 }
 
 namespace {

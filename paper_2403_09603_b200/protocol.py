@@ -151,11 +151,32 @@ def kth_largest_distance(x, b_r: int, rank: int) -> float:
     return float(np.array([key.item()], dtype=np.int64).view(np.float64)[0])
 
 
+def budget_key(x, b_r: int, budget: int) -> float:
+    """v' = the (budget+1)-th largest p, clamped for a bisection strictly inside
+    tau_bounds(b_r) (two-pass device select; exact 5-pass select as fallback)."""
+    _check_b(b_r)
+    lower, upper = tau_bounds(b_r)
+    t, _, _ = D.to_device_f64(x)
+    n = t.numel()
+    if budget >= n:
+        return lower
+    ws = D.workspace(int(_lib.lib().vt_tau_workspace(n)), "tau")
+    out = torch.zeros(2, dtype=torch.int64, device=t.device)  # [key, status]
+    f = D.Flags()
+    _lib.call("vt_tau_budget_key", D.ptr(t), n, b_r, int(budget), lower, upper, D.ptr(out),
+              out.data_ptr() + 8, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
+    key, status = out.tolist()
+    D.raise_fpround(f.read()[0])
+    if (status & 0xFFFFFFFF) != 1:
+        return kth_largest_distance(x, b_r, int(budget))
+    return float(np.array([key], dtype=np.int64).view(np.float64)[0])
+
+
 def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
     """Per-tensor adaptive threshold: the search_tau skeleton with predicate
     count(p > tau) <= budget, feasible -> upper = tau, returns ``upper``."""
     lower, upper = tau_bounds(b_r)
-    v = kth_largest_distance(x, b_r, int(budget))
+    v = budget_key(x, b_r, int(budget))
     for _ in range(iters):
         tau = (lower + upper) / 2.0
         if v <= tau:
@@ -166,4 +187,4 @@ def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
 
 
 __all__ = ["AuditFailure", "GpuAuditorChannel", "GpuPlainChannel", "GpuTrainerChannel",
-           "LogExhaustedError", "kth_largest_distance", "search_tau", "search_tau_budget"]
+           "LogExhaustedError", "budget_key", "kth_largest_distance", "search_tau", "search_tau_budget"]

@@ -59,6 +59,27 @@ def test_budget_matches_oracle_random(oracle):
         assert protocol.search_tau_budget(x, 32, B) == oracle.search_tau_budget(x, 32, B)
 
 
+def test_budget_key_clamps_and_fallback(oracle):
+    """Both early exits (v above / below the bisection range) and the exact
+    fallback when one digit holds more candidates than the buffer."""
+    from paper_2403_09603_b200 import protocol
+    lo, hi = oracle.tau_bounds(32)
+    # all p identical (2^21 copies of one value): the selected digit overflows
+    x = np.full(1 << 21, 1.0 + 0.4 * 2.0 ** -23)
+    x[::3] = 1.0 + 0.45 * 2.0 ** -23
+    for B in (0, 5000, 700_000, 699_050):
+        assert protocol.search_tau_budget(x, 32, B) == oracle.search_tau_budget(x, 32, B), B
+    # every p below tau_lo (values near the grid): v <= tau_lo
+    y = 1.0 + np.random.default_rng(1).uniform(0, 0.2, size=100_000) * 2.0 ** -23
+    assert protocol.search_tau_budget(y, 32, 10) == oracle.search_tau_budget(y, 32, 10)
+    # many p at the top (near midpoints): v > tau_hi impossible (p <= 2^-24) but
+    # exactly-tied midpoints sit at p == tau_hi
+    z = (np.random.default_rng(2).integers(1 << 23, 1 << 24, size=100_000) + 0.5) * 2.0 ** -23
+    for B in (0, 10, 99_999):
+        assert protocol.search_tau_budget(z, 32, B) == oracle.search_tau_budget(z, 32, B), B
+    assert protocol.budget_key(z, 32, 10) == hi
+
+
 def test_normalized_distance(oracle):
     import torch
     from paper_2403_09603_b200 import ops

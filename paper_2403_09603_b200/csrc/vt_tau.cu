@@ -240,29 +240,42 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
   __syncthreads();
   uint32_t err = 0, above = 0;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * 256; base < n; base += (int64_t)gridDim.x * 256) {
-    const int64_t i = base + threadIdx.x;
-    bool in = false;
-    uint64_t k = 0;
-    if (i < n) {
-      k = dist_key(__ldg(x + i), g, err);
-      if (k > hi) above += first ? 1u : 0u;
-      else in = k > lo && ((k - lo - 1) & pmask) == prefix;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+  // four consecutive elements per thread per step (one 256-bit load)
+  for (int64_t base = (int64_t)blockIdx.x * 1024; base < n; base += (int64_t)gridDim.x * 1024) {
+    const int64_t i0 = base + 4 * threadIdx.x;
+    D4 xv;
+    if (vec && i0 + 3 < n) {
+      xv = ldg_stream4(x + i0);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xv.v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
     }
-    if (compact) {
-      const uint32_t m = __ballot_sync(0xffffffffu, in);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        unsigned long long pos = 0;
-        if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(&st->cand), (unsigned long long)__popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (in) {
-          const uint64_t slot = pos + __popc(m & ((1u << lane) - 1u));
-          if ((int64_t)slot < kCandCap) cand[slot] = k;
-        }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      bool in = false;
+      uint64_t k = 0;
+      if (i0 + v < n) {
+        k = dist_key(xv.v[v], g, err);
+        if (k > hi) above += first ? 1u : 0u;
+        else in = k > lo && ((k - lo - 1) & pmask) == prefix;
       }
-    } else if (in) {
-      atomicAdd(&sh[(uint32_t)((k - lo - 1) >> sh_lv) & dmask], 1u);
+      if (compact) {
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long pos = 0;
+          if (lane == leader)
+            pos = atomicAdd(reinterpret_cast<unsigned long long*>(&st->cand), (unsigned long long)__popc(m));
+          pos = __shfl_sync(0xffffffffu, pos, leader);
+          if (in) {
+            const uint64_t slot = pos + __popc(m & ((1u << lane) - 1u));
+            if ((int64_t)slot < kCandCap) cand[slot] = k;
+          }
+        }
+      } else if (in) {
+        atomicAdd(&sh[(uint32_t)((k - lo - 1) >> sh_lv) & dmask], 1u);
+      }
     }
   }
   report_err(errp, err);

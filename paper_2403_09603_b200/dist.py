@@ -45,6 +45,18 @@ def exclusive_offsets(counts: torch.Tensor) -> torch.Tensor:
     return torch.cumsum(counts, 0) - counts
 
 
+def _all_gather_flat(out: torch.Tensor, mine: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor on NCCL; list form on backends without it (gloo)."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, mine, group=group)
+    else:
+        parts = list(out.chunk(dist.get_world_size(group)))
+        tmp = [torch.empty_like(p) for p in parts]
+        dist.all_gather(tmp, mine, group=group)
+        for p, t in zip(parts, tmp):
+            p.copy_(t)
+
+
 def all_gather_counts(count: int | torch.Tensor, group=None, device=None) -> torch.Tensor:
     """All ranks' int64 counts (one tiny NCCL all-gather over NVLink)."""
     world = dist.get_world_size(group)
@@ -53,7 +65,7 @@ def all_gather_counts(count: int | torch.Tensor, group=None, device=None) -> tor
     else:
         mine = torch.tensor([int(count)], dtype=torch.int64, device=device)
     out = torch.empty(world, dtype=torch.int64, device=mine.device)
-    dist.all_gather_into_tensor(out, mine, group=group)
+    _all_gather_flat(out, mine, group)
     return out
 
 
@@ -147,7 +159,7 @@ def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes:
     pad = torch.zeros((width, 32), dtype=torch.uint8, device=mine.device)
     pad[: mine.shape[0]] = mine
     gathered = torch.empty((world * width, 32), dtype=torch.uint8, device=mine.device)
-    dist.all_gather_into_tensor(gathered, pad, group=group)
+    _all_gather_flat(gathered, pad, group)
     roots = torch.cat([gathered[r * width: r * width + n_blocks[r]] for r in range(world)])
     return lv, combine_top(roots, hash_level)
 

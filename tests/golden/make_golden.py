@@ -251,7 +251,51 @@ def golden_configs() -> None:
     (HERE / "config_golden.json").write_text(json.dumps({"config0": c0, "config1": c1}, indent=1))
 
 
+def golden_channel_traces() -> None:
+    """Record every channel call of real reference train + audit runs.
+
+    A recording wrapper sits in the channel seam of ``protocol._run``
+    (protocol.py:239-307) around the reference ``_TrainerChannel`` /
+    ``_AuditorChannel``; the fixture stores each call's input tensor, tau,
+    output and counts, plus the .vtrl file digest.  On the GPU box the same
+    inputs are replayed through the GPU channels (no reference needed)."""
+    from vtrain.cli import load_config
+
+    class Rec:
+        def __init__(self, inner):
+            self.inner, self.calls = inner, []
+
+        def process(self, values, tau):
+            out, directed, corr = self.inner.process(values, tau)
+            self.calls.append((np.array(values, dtype=np.float64), float(tau), np.array(out), directed, corr))
+            return out, directed, corr
+
+    arrays = {}
+    meta = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name in ("tiny", "logreg"):
+            cfg = load_config(Path("/root/reference/pkg/configs") / f"{name}.json")
+            log = Path(td) / f"{name}.vtrl"
+            w = rl.LogWriter(log, cfg.b_r)
+            tr = Rec(pr._TrainerChannel(w, cfg.b_r))
+            tree_t, *_ = pr._run(cfg, pr.get_profile(cfg.trainer_profile), tr, False)
+            w.close()
+            au = Rec(pr._AuditorChannel(rl.LogReader(log), cfg.b_r))
+            tree_a, *_ = pr._run(cfg, pr.get_profile("pairwise"), au, False)
+            meta[name] = {"b_r": cfg.b_r, "vtrl_sha": sha(log.read_bytes()), "root": tree_t.root.hex(),
+                          "audit_root": tree_a.root.hex(), "n_calls": len(tr.calls),
+                          "directed": [c[3] for c in tr.calls], "corrections": [c[4] for c in au.calls],
+                          "taus": [c[1] for c in tr.calls], "shapes": [list(c[0].shape) for c in tr.calls]}
+            for role, rec in (("t", tr), ("a", au)):
+                arrays[f"{name}_{role}_in"] = np.concatenate([c[0].reshape(-1) for c in rec.calls])
+                # outputs are grid values (FP32-exact): stored as FP32, lossless
+                arrays[f"{name}_{role}_out"] = np.concatenate([c[2].reshape(-1) for c in rec.calls]).astype(np.float32)
+    np.savez_compressed(HERE / "channel_traces.npz", **arrays)
+    (HERE / "channel_traces.json").write_text(json.dumps(meta))
+
+
 if __name__ == "__main__":
+    golden_channel_traces()
     golden_fpround()
     golden_errors()
     golden_roundlog()

@@ -281,7 +281,11 @@ def run_ours(args) -> None:
         "cpu_baseline": cpu,
     }
     if args.sweep:
-        line["sweep"] = sweep(args)
+        line["sweep"] = sweep(args.sweep)
+    if args.extras:
+        line["extras"] = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
+                          "configs[2]_resnet50_budget": config2(),
+                          "configs[4]_merkle_1.5B": config4_merkle()}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -332,43 +336,122 @@ def run_e2e(args, n, tau, base, dev):
             "path": "ops.round_and_log_replay_host (chunked H2D / kernel / D2H on 3 streams)"}
 
 
-def sweep(args):
+def _time(fn, reps: int, warm: int = 2) -> float:
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def sweep(log2s) -> dict:
+    """configs[4] size sweep: round-and-log and replay at 2^20 .. 2^32 (config-0
+    distribution, Bernoulli 10% midpoints; 2^20 is L2-resident)."""
     import torch
 
     from paper_2403_09603_b200 import ops, workloads
+    peak, _ = peaks()
     out = {}
-    for lg in args.sweep:
+    for lg in log2s:
         n = 1 << lg
-        x = workloads.config0_x_torch(n, seed=lg)
+        x = workloads.config0_x_torch_bernoulli(n, seed=lg)
         y = torch.empty(n, dtype=torch.float32, device="cuda")
         words = torch.empty(max(n // 4, 1024), dtype=torch.int64, device="cuda")
-        p = ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
-        _, log = p.finish()
-        for _ in range(3):
-            ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
-        s.record()
-        for _ in range(reps):
-            ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)
-        e.record()
-        torch.cuda.synchronize()
-        ms = s.elapsed_time(e) / reps
+        _, log = ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False).finish()
+        reps = 10 if lg <= 30 else 4
+        ms = _time(lambda: ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False), reps)
         ya = torch.empty_like(y)
         lw = log.words
-        s.record()
-        for _ in range(reps):
-            ops.replay(x, 32, lw, out=ya, check=False)
-        e.record()
-        torch.cuda.synchronize()
-        ms2 = s.elapsed_time(e) / reps
+        ms2 = _time(lambda: ops.replay(x, 32, lw, out=ya, check=False), reps)
         b = n * (8 + 4 + 8 * log.count / n)
-        out[f"2^{lg}"] = {"round_log_gbs": round(b / ms / 1e6, 1), "replay_gbs": round(b / ms2 / 1e6, 1),
+        out[f"2^{lg}"] = {"round_log_gbs": round(b / ms / 1e6, 1), "round_log_frac": round(b / ms / 1e6 / peak, 4),
+                          "replay_gbs": round(b / ms2 / 1e6, 1), "replay_frac": round(b / ms2 / 1e6 / peak, 4),
                           "round_log_ms": round(ms, 4), "replay_ms": round(ms2, 4),
-                          "l2_resident": n * 8 < 126e6}
+                          "logged_fraction": round(log.count / n, 5), "l2_resident": n * 8 < 126e6}
         del x, y, words, ya, lw, log
         torch.cuda.empty_cache()
     return out
+
+
+def config2() -> dict:
+    """configs[2]: 161 ResNet-50-shaped FP64 tensors (N(0, sigma_t), sigma_t
+    log-uniform in [1e-3, 10]); per tensor the budget search (B = 0.5% of n)
+    then round-and-log at that tau."""
+    import numpy as np
+    import torch
+
+    from paper_2403_09603_b200 import ops, protocol, workloads
+    shapes = workloads.resnet50_tensors()
+    sig = workloads.config2_sigmas(len(shapes))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2)
+    xs = [torch.randn(int(np.prod(s)), dtype=torch.float64, device="cuda", generator=g) * float(sig[i])
+          for i, (_, s) in enumerate(shapes)]
+    total = sum(x.numel() for x in xs)
+    ys = torch.empty(total, dtype=torch.float32, device="cuda")
+    budgets = [int(0.005 * x.numel()) for x in xs]
+    words = torch.empty(sum(budgets) + len(xs), dtype=torch.int64, device="cuda")
+    state = {}
+
+    def run():
+        off = woff = 0
+        taus, pend = [], []
+        for x, B in zip(xs, budgets):
+            n = x.numel()
+            tau = protocol.search_tau_budget(x, 32, B)
+            pend.append(ops.round_and_log(x, 32, tau, out=ys[off:off + n], log_out=words[woff:woff + B + 1],
+                                          check=False))
+            taus.append(tau)
+            off += n
+            woff += B + 1
+        state["taus"], state["pend"] = taus, pend
+
+    ms = _time(run, reps=3, warm=1)
+    counts = [p.flags.read()[1][0] for p in state["pend"]]
+    assert all(c <= B for c, B in zip(counts, budgets))
+    t = np.array(state["taus"]) / 2.0 ** -24
+    logged = sum(counts)
+    return {"tensors": len(xs), "elements": total, "ms_per_sweep": round(ms, 3),
+            "g_elements_per_s": round(total / ms / 1e6, 2),
+            "round_log_gbs_equiv": round(total * (8 + 4 + 8 * logged / total) / ms / 1e6, 1),
+            "logged_fraction": round(logged / total, 6), "tau_over_2^-24": [round(float(t.min()), 6), round(float(t.max()), 6)],
+            "note": "search (2-3 streaming passes) + round-and-log per tensor, host bisection between them"}
+
+
+def config4_merkle() -> dict:
+    """configs[4]: SHA-256 Merkle tree over 1.5e9 FP32 params (4 KiB leaves)."""
+    import torch
+
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, merkle
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    n = 1_500_000_000
+    w = torch.randn(n, device="cuda", generator=g) * 0.02
+    ms = _time(lambda: merkle.merkle_chunked(w), reps=3, warm=1)
+    t = merkle.merkle_chunked(w)
+    leaves = t.levels_device[0].shape[0]
+    nodes = t.n_nodes() - leaves
+    comps = leaves * (4096 // 64 + 1) + nodes * 2
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    blocks, reps = 148 * 32, 64
+    pk_ms = _time(lambda: _lib.call("vt_sha256_peak_bench", D.ptr(sink), blocks, reps, D.stream_ptr()), reps=3)
+    peak_cps = blocks * 128 * reps / (pk_ms * 1e-3)
+    cps = comps / (ms * 1e-3)
+    return {"params": n, "leaves": int(leaves), "internal_nodes": int(nodes), "levels": len(t.levels_device),
+            "ms": round(ms, 3), "hashed_gbs": round(n * 4 / ms / 1e6, 1),
+            "compressions_per_s": round(cps / 1e9, 3), "unit_cps": "G compressions/s",
+            "int_ops_per_s": round(cps * 1400 / 1e12, 2), "unit_ops": "T int ops/s (analytic 1400 / compression)",
+            "sha256_compute_ceiling_cps": round(peak_cps / 1e9, 3),
+            "frac_of_sha256_int_peak": round(cps / peak_cps, 4),
+            "peak_note": "ceiling = the same compress() on register-resident messages (vt_sha256_peak_bench)",
+            "root": t.root_hex[:16]}
 
 
 # ---------------------------------------------------------------------------
@@ -483,6 +566,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also run configs[2], configs[4] and the size sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

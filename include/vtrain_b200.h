@@ -166,6 +166,9 @@ int64_t vt_merkle_node_count(int64_t n_leaves);
  */
 int vt_merkle_build(const uint8_t *data, int64_t nbytes, int64_t leaf_bytes, uint8_t *nodes,
                     int64_t nodes_cap, vt_stream_t stream);
+/* measurement support: blocks x 128 threads x reps compressions of
+ * register-resident messages (compute-only SHA-256 ceiling of this chip) */
+int vt_sha256_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t stream);
 
 #ifdef __cplusplus
 }

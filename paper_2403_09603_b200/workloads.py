@@ -63,6 +63,44 @@ def config1_pair(n: int, seed: int = 1) -> tuple[np.ndarray, np.ndarray]:
     return x, xa
 
 
+def resnet50_tensors(batch: int = 32, image: int = 224) -> list[tuple[str, tuple[int, ...]]]:
+    """The 161 FP64 tensors of BASELINE configs[2]: the 107
+    conv / BN / fc forward outputs and the 54 conv / fc input gradients of
+    one ResNet-50 step (bottleneck blocks [3, 4, 6, 3], widths 64..512,
+    expansion 4, stride on the 3x3 conv), NCHW shapes."""
+    fwd: list[tuple[str, tuple[int, ...]]] = []
+    grads: list[tuple[str, tuple[int, ...]]] = []
+
+    def conv(name, cin, cout, h, stride, k):
+        ho = (h + 2 * (k // 2) - k) // stride + 1
+        grads.append((f"grad_in:{name}", (batch, cin, h, h)))
+        fwd.append((f"out:{name}", (batch, cout, ho, ho)))
+        fwd.append((f"out:{name}.bn", (batch, cout, ho, ho)))
+        return ho
+
+    h = conv("conv1", 3, 64, image, 2, 7)
+    h = (h + 2 - 3) // 2 + 1  # max pool 3x3 / 2
+    cin = 64
+    for li, (blocks, width) in enumerate(zip((3, 4, 6, 3), (64, 128, 256, 512))):
+        for b in range(blocks):
+            stride = 2 if (b == 0 and li > 0) else 1
+            name = f"layer{li + 1}.{b}"
+            h1 = conv(f"{name}.conv1", cin, width, h, 1, 1)
+            h2 = conv(f"{name}.conv2", width, width, h1, stride, 3)
+            conv(f"{name}.conv3", width, 4 * width, h2, 1, 1)
+            if b == 0:
+                conv(f"{name}.downsample", cin, 4 * width, h, stride, 1)
+            cin, h = 4 * width, h2
+    grads.append(("grad_in:fc", (batch, cin)))
+    fwd.append(("out:fc", (batch, 1000)))
+    return fwd + grads
+
+
+def config2_sigmas(n_tensors: int, seed: int = 2) -> np.ndarray:
+    """sigma_t = 10^U(-3, 1) per tensor (log-uniform in [1e-3, 10])."""
+    return 10.0 ** np.random.default_rng(seed).uniform(-3.0, 1.0, size=n_tensors)
+
+
 def _torch_bracket(v):
     import torch
     f = v.float()
@@ -87,6 +125,23 @@ def config0_x_torch(n: int, seed: int = 0, device="cuda"):
         u = torch.rand(k, dtype=torch.float64, device=device, generator=g) * 2.0 - 1.0
         lo, hi = _torch_bracket(x[sel])
         x[sel] = (lo + hi) * 0.5 * (1.0 + u * 2.0 ** -40)
+    return x
+
+
+def config0_x_torch_bernoulli(n: int, seed: int = 0, device="cuda"):
+    """Config-0 distribution with an i.i.d. 10% midpoint mask instead of an
+    exact-size subset (no randperm; used for the 2^20..2^32 size sweep)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.randn(n, dtype=torch.float64, device=device, generator=g)
+    chunk = 1 << 26
+    for lo in range(0, n, chunk):
+        xs = x[lo:lo + chunk]
+        m = torch.rand(xs.numel(), device=device, generator=g) < MID_FRACTION
+        u = torch.rand(xs.numel(), dtype=torch.float64, device=device, generator=g) * 2.0 - 1.0
+        lo_, hi_ = _torch_bracket(xs)
+        xs.copy_(torch.where(m, (lo_ + hi_) * 0.5 * (1.0 + u * 2.0 ** -40), xs))
     return x
 
 

@@ -282,7 +282,7 @@ def run_ours(args) -> None:
     }
     if args.sweep:
         line["sweep"] = sweep(args.sweep)
-    if args.extras:
+    if args.extras and world == 1:
         line["extras"] = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
                           "configs[2]_resnet50_budget": config2(),
                           "configs[4]_merkle_1.5B": config4_merkle()}
@@ -436,15 +436,16 @@ def config4_merkle() -> dict:
     w = torch.randn(n, device="cuda", generator=g) * 0.02
     ms = _time(lambda: merkle.merkle_chunked(w), reps=3, warm=1)
     t = merkle.merkle_chunked(w)
-    leaves = t.levels_device[0].shape[0]
-    nodes = t.n_nodes() - leaves
+    sizes = [int(l.shape[0]) for l in t.levels_device]
+    leaves = sizes[0]
+    nodes = sum(m // 2 for m in sizes[:-1])  # hashed internal nodes (promoted copies excluded)
     comps = leaves * (4096 // 64 + 1) + nodes * 2
     sink = torch.zeros(1, dtype=torch.int32, device="cuda")
     blocks, reps = 148 * 32, 64
     pk_ms = _time(lambda: _lib.call("vt_sha256_peak_bench", D.ptr(sink), blocks, reps, D.stream_ptr()), reps=3)
     peak_cps = blocks * 128 * reps / (pk_ms * 1e-3)
     cps = comps / (ms * 1e-3)
-    return {"params": n, "leaves": int(leaves), "internal_nodes": int(nodes), "levels": len(t.levels_device),
+    return {"params": n, "leaves": int(leaves), "hashed_internal_nodes": int(nodes), "levels": len(sizes),
             "ms": round(ms, 3), "hashed_gbs": round(n * 4 / ms / 1e6, 1),
             "compressions_per_s": round(cps / 1e9, 3), "unit_cps": "G compressions/s",
             "int_ops_per_s": round(cps * 1400 / 1e12, 2), "unit_ops": "T int ops/s (analytic 1400 / compression)",
@@ -566,7 +567,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also run configs[2], configs[4] and the size sweep")
+    ap.add_argument("--no-extras", dest="extras", action="store_false",
+                    help="skip configs[2], configs[4] and the 2^20..2^32 size sweep (run by default at N=1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -149,6 +149,19 @@ int vt_tau_kth_key(const double *x, int64_t n, int b_r, int64_t rank, uint64_t *
 int vt_tau_budget_key(const double *x, int64_t n, int b_r, int64_t budget, double tau_lo,
                       double tau_hi, uint64_t *key_out, int32_t *status_out, int32_t *err,
                       void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * Per-tensor adaptive round-and-log with no host round trip: budget select
+ * (vt_tau_budget_key), the 30-step search_tau-skeleton bisection on the
+ * device, then the sparse round-and-log at that tau.  *tau_out (device
+ * double) receives the chosen tau.  Workspace 256-byte aligned, zero-filled
+ * before first use.
+ */
+size_t vt_round_log_adaptive_workspace(int64_t n);
+int vt_round_log_adaptive(const double *x, int64_t n, int b_r, int64_t budget, int iters,
+                          int out_kind, void *out, uint64_t *sparse, int64_t sparse_cap,
+                          int64_t global_base, const int64_t *cursor_in, int64_t *cursor_out,
+                          double *tau_out, int64_t *counters, int32_t *err, void *ws,
+                          size_t ws_bytes, vt_stream_t stream);
 /* out[0] = min over s[n] ignoring NaN (+inf if none), *nan_flag |= 1 if any NaN */
 int vt_min_f64(const double *s, int64_t n, double *out, int32_t *nan_flag, vt_stream_t stream);
 

@@ -71,7 +71,7 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
-        ws[: 1 << 20].zero_()
+        ws[: 8 << 20].zero_()
         _WS[key] = ws
     return ws
 

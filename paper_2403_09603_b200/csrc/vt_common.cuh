@@ -81,6 +81,35 @@ inline Grid make_grid(int b_r, double tau) {
   return g;
 }
 
+// Thresholds derived from a tau that lives on the device (adaptive path:
+// the bisection result never visits the host).  Same mapping as make_grid.
+struct DevThr {
+  double tau;
+  int64_t thr;
+  double thr_sub;
+  int32_t thr32;
+  int32_t _pad;
+};
+
+__host__ __device__ inline DevThr thresholds_for(double tau) {
+  DevThr d;
+  d.tau = tau;
+  if (tau != tau) {
+    d.thr = INT64_MAX;
+  } else if (tau < 0.0) {
+    d.thr = -1;
+  } else if (tau < 0x1p-800) {
+    d.thr = 0;
+  } else {
+    const double t = floor(ldexp(tau, 52));
+    d.thr = (t >= 0x1p62) ? INT64_MAX : (int64_t)t;
+  }
+  d.thr_sub = 0x1p-126 * tau;
+  d.thr32 = (int32_t)(d.thr < 0 ? 0 : (d.thr > INT32_MAX ? INT32_MAX : d.thr));
+  d._pad = 0;
+  return d;
+}
+
 // ---------------------------------------------------------------------------
 // element primitives
 // ---------------------------------------------------------------------------
@@ -300,9 +329,10 @@ __device__ __forceinline__ void report_err(int32_t* err, uint32_t e) {
 // persistent TMA-pipelined kernels of the north-star path (vt_stream.cu)
 size_t rl_stream_workspace(int64_t n);
 size_t rp_stream_workspace(int64_t n);
+// dthr: nullable device thresholds overriding g.thr / g.thr_sub / thr32
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
-              int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
+              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 

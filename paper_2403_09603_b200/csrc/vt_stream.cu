@@ -191,13 +191,14 @@ struct RLArgs {
   uint32_t* counts;   // [num_tiles] logged entries per tile
   uint16_t* scratch;  // [num_tiles][kSTile] staged entries: tile offset | up << 15
   int32_t* err;
+  const DevThr* dthr;  // adaptive path: thresholds from the device bisection
 };
 
 // One tile: round, classify, store, stage logged elements (warp-local order
 // == element order).  Returns the warp's count.
 template <int OUT, bool FAST, bool FULL>
-__device__ __forceinline__ uint32_t rl_tile(const RLArgs& a, const double* src, void* o, int lim, uint16_t* stw,
-                                            int warp, int lane, uint32_t lt, uint32_t& err) {
+__device__ __forceinline__ uint32_t rl_tile(const Grid& g, int thr32, const double* src, void* o, int lim,
+                                            uint16_t* stw, int warp, int lane, uint32_t lt, uint32_t& err) {
   uint32_t wcnt = 0;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
@@ -206,16 +207,16 @@ __device__ __forceinline__ uint32_t rl_tile(const RLArgs& a, const double* src, 
     uint32_t c0, c1;
     if (FAST) {
       bool slow = false;
-      float f0 = round_dir32_fast(xv.x, a.thr32, c0, slow);
-      float f1 = round_dir32_fast(xv.y, a.thr32, c1, slow);
+      float f0 = round_dir32_fast(xv.x, thr32, c0, slow);
+      float f1 = round_dir32_fast(xv.y, thr32, c1, slow);
       if (slow) {
-        f0 = round_dir32(xv.x, a.thr32, a.g.thr_sub, c0, err);
-        f1 = round_dir32(xv.y, a.thr32, a.g.thr_sub, c1, err);
+        f0 = round_dir32(xv.x, thr32, g.thr_sub, c0, err);
+        f1 = round_dir32(xv.y, thr32, g.thr_sub, c1, err);
       }
       store2<OUT, FULL>(o, e0, lim, f0, f1);
     } else {
-      const uint64_t r0 = round_dir(xv.x, a.g, c0, err);
-      const uint64_t r1 = round_dir(xv.y, a.g, c1, err);
+      const uint64_t r0 = round_dir(xv.x, g, c0, err);
+      const uint64_t r1 = round_dir(xv.y, g, c1, err);
       store2<OUT, FULL>(o, e0, lim, r0, r1);
     }
     const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 1u);
@@ -254,6 +255,13 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLArgs a)
 
   const uint32_t lt = lanemask_lt();
   uint32_t err = 0;
+  Grid g = a.g;
+  int thr32 = a.thr32;
+  if (a.dthr) {  // adaptive: tau was bisected on the device
+    g.thr = a.dthr->thr;
+    g.thr_sub = a.dthr->thr_sub;
+    thr32 = a.dthr->thr32;
+  }
   for (int64_t k = 0;; ++k) {
     const int64_t t = blockIdx.x + k * G;
     if (t >= a.num_tiles) break;
@@ -264,8 +272,8 @@ __global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLArgs a)
     uint16_t* stw = st16 + (buf * kWarps + warp) * kStageRow;
     void* o = tile_out<OUT>(a.out, tbase);
     const uint32_t wcnt = (t < full_tiles)
-        ? rl_tile<OUT, FAST, true>(a, src, o, kSTile, stw, warp, lane, lt, err)
-        : rl_tile<OUT, FAST, false>(a, src, o, (int)(a.n - tbase), stw, warp, lane, lt, err);
+        ? rl_tile<OUT, FAST, true>(g, thr32, src, o, kSTile, stw, warp, lane, lt, err)
+        : rl_tile<OUT, FAST, false>(g, thr32, src, o, (int)(a.n - tbase), stw, warp, lane, lt, err);
     if (lane == 0) s_cnt[buf][warp] = wcnt;
     __syncthreads();  // ring slot s consumed; warp counts visible
     if (tid == 0) {
@@ -654,7 +662,7 @@ static int launch_rl(const RLArgs& a, const ScanArgs& sc, const ExpandArgs& e, c
 
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
-              int64_t* counters, int32_t* err, void* ws, cudaStream_t st) {
+              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr) {
   const int64_t tiles = stream_tiles(n);
   const int64_t chunks = (tiles + kScanTiles - 1) / kScanTiles;
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -664,7 +672,7 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
   uint32_t* counts = reinterpret_cast<uint32_t*>(toffs + tiles);
   uint16_t* scratch = reinterpret_cast<uint16_t*>(
       w + ((((64 + chunks * 8 + 255) & ~(int64_t)255) + tiles * 12 + 255) & ~(int64_t)255));
-  RLArgs a{x, n, g, thr32, out, tiles, counts, scratch, err};
+  RLArgs a{x, n, g, thr32, out, tiles, counts, scratch, err, dthr};
   ScanArgs sc{counts, tiles, hdr, status, toffs, cursor_in, cursor_out, counters};
   ExpandArgs e{scratch, counts, toffs, tiles, global_base, sparse, cap};
   if (fast) {

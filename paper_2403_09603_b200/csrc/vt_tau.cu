@@ -491,6 +491,68 @@ extern "C" int vt_tau_budget_key(const double* x, int64_t n, int b_r, int64_t bu
   return VT_OK;
 }
 
+namespace vt {
+// The search_tau skeleton (protocol.py:494-506) in budget form, on one
+// thread: identical IEEE FP64 operations to the host loop, so the same tau.
+__global__ void budget_bisect_kernel(const uint64_t* key, double lower, double upper, int iters, DevThr* out) {
+  const double v = __longlong_as_double((long long)*key);
+  for (int i = 0; i < iters; ++i) {
+    const double tau = __dmul_rn(__dadd_rn(lower, upper), 0.5);
+    if (v <= tau) upper = tau;
+    else lower = tau;
+  }
+  *out = thresholds_for(upper);
+}
+}  // namespace vt
+
+extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) {
+  return 256 + vt_tau_workspace(n) + vt_round_log_workspace(n);
+}
+
+extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_t budget, int iters, int out_kind,
+                                     void* out, uint64_t* sparse, int64_t sparse_cap, int64_t global_base,
+                                     const int64_t* cursor_in, int64_t* cursor_out, double* tau_out,
+                                     int64_t* counters, int32_t* err, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (n <= 0 || b_r < 10 || b_r > 32 || budget < 0 || iters < 0 || !tau_out || !sparse || !ws ||
+      ws_bytes < vt_round_log_adaptive_workspace(n) || reinterpret_cast<uintptr_t>(ws) % 256) {
+    vt_set_error("vt_round_log_adaptive: bad argument (n > 0, 256-byte aligned workspace)");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  DevThr* dthr = reinterpret_cast<DevThr*>(w);
+  uint64_t* key = reinterpret_cast<uint64_t*>(w + 64);
+  int32_t* status = reinterpret_cast<int32_t*>(w + 72);
+  void* tws = w + 256;
+  const size_t tws_bytes = vt_tau_workspace(n);
+  void* rws = w + 256 + ((tws_bytes + 255) & ~(size_t)255);
+  // the round-and-log workspace keeps an epoch header at its start: keep it
+  // at a fixed place (it must stay zero-filled until first use)
+  const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
+  int rc = vt_tau_budget_key(x, n, b_r, budget, lo, hi, key, status, err, tws, tws_bytes, stream);
+  if (rc) return rc;
+  budget_bisect_kernel<<<1, 1, 0, s>>>(key, lo, hi, iters, dthr);
+  if ((rc = vt_check_launch("budget_bisect_kernel"))) return rc;
+  if (cudaMemcpyAsync(tau_out, &dthr->tau, 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return vt_check_launch("tau copy");
+  const Grid g = make_grid(b_r, lo);  // thresholds come from dthr
+  const size_t rws_bytes = ws_bytes - (static_cast<uint8_t*>(rws) - w);
+  if (rws_bytes < vt_round_log_workspace(n)) {
+    vt_set_error("vt_round_log_adaptive: workspace too small");
+    return VT_EINVAL;
+  }
+  if (out_kind == VT_OUT_F32 && (reinterpret_cast<uintptr_t>(out) & 15)) {
+    vt_set_error("vt_round_log_adaptive: misaligned output");
+    return VT_EINVAL;
+  }
+  if ((reinterpret_cast<uintptr_t>(x) & 31) || (out_kind == VT_OUT_F64 && (reinterpret_cast<uintptr_t>(out) & 31))) {
+    vt_set_error("vt_round_log_adaptive: misaligned x / output");
+    return VT_EINVAL;
+  }
+  return rl_stream(x, n, g, 0, b_r == 32, out_kind, out, sparse, sparse_cap, global_base, cursor_in, cursor_out,
+                   counters, err, rws, s, dthr);
+}
+
 namespace {
 template <int P>
 int run_pass(const double* x, int64_t n, const Grid& g, SelectState* st, uint32_t* hist,

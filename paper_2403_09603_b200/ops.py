@@ -119,6 +119,51 @@ def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtyp
     return (y.reshape(shape) if out is None else y), cnt[0]
 
 
+@dataclass
+class PendingAdaptive:
+    """Result of round_and_log_adaptive(check=False): buffers + device tau."""
+
+    y: torch.Tensor
+    words: torch.Tensor
+    tau: torch.Tensor  # float64[1] on the device
+    flags: D.Flags
+
+    def finish(self) -> tuple[torch.Tensor, SparseLog, float]:
+        err, cnt = self.flags.read()
+        D.raise_fpround(err)
+        if cnt[0] > self.words.numel():
+            raise LogOverflow(f"sparse log needs {cnt[0]} words, capacity {self.words.numel()}")
+        return self.y, SparseLog(self.words[: cnt[0]], cnt[0]), float(self.tau.item())
+
+
+def round_and_log_adaptive(x: torch.Tensor, b_r: int, budget: int, *, iters: int = 30,
+                           out_dtype=torch.float32, global_base: int = 0, out: torch.Tensor | None = None,
+                           log_out: torch.Tensor | None = None, check: bool = True, tag: str = "adaptive"):
+    """Per-tensor adaptive threshold + round-and-log, all on the device.
+
+    tau = protocol.search_tau_budget(x, b_r, budget, iters) (bit-identical:
+    same selection, same FP64 bisection run by one device thread), then the
+    sparse round-and-log at tau.  No host synchronisation unless check=True,
+    so a whole model's worth of tensors can be queued or graph-captured."""
+    _check_b(b_r)
+    D.require_cuda()
+    shape = tuple(x.shape) if x.dim() else (1,)
+    t = D.aligned_f64(x.reshape(-1))
+    n = t.numel()
+    kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
+    y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
+    words = log_out if log_out is not None else torch.empty(max(budget + 1, 1), dtype=torch.int64, device=t.device)
+    tau = torch.empty(1, dtype=torch.float64, device=t.device)
+    ws = D.workspace(int(_lib.lib().vt_round_log_adaptive_workspace(n)), tag)
+    f = D.Flags()
+    if n:
+        _lib.call("vt_round_log_adaptive", D.ptr(t), n, b_r, int(budget), int(iters), kind, D.ptr(y), D.ptr(words),
+                  words.numel(), int(global_base), None, None, D.ptr(tau), f.cnt_ptr, f.err_ptr, D.ptr(ws),
+                  ws.numel(), D.stream_ptr())
+    pending = PendingAdaptive(y.reshape(shape) if out is None else y, words, tau, f)
+    return pending.finish() if check else pending
+
+
 class _HostPipe:
     """Double-buffered device staging for host-resident tensors: H2D copies,
     kernels and D2H copies run on three streams so PCIe traffic in both

@@ -7,6 +7,8 @@ import hashlib
 import numpy as np
 import pytest
 
+from conftest import bits
+
 pytestmark = pytest.mark.gpu
 
 
@@ -78,6 +80,25 @@ def test_budget_key_clamps_and_fallback(oracle):
     for B in (0, 10, 99_999):
         assert protocol.search_tau_budget(z, 32, B) == oracle.search_tau_budget(z, 32, B), B
     assert protocol.budget_key(z, 32, 10) == hi
+
+
+def test_round_and_log_adaptive_matches_host_search(oracle):
+    """Device bisection + fused round-and-log == oracle budget search, then
+    oracle direction codes at that tau (log <= budget)."""
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    cases = [np.random.default_rng(60).normal(0, 10.0 ** -2.5, size=200_003),
+             np.random.default_rng(61).normal(0, 3.0, size=4096 * 3 + 5),
+             workloads.config0_x(100_000, 62)]
+    for x in cases:
+        B = int(0.005 * x.size)
+        y, log, tau = ops.round_and_log_adaptive(torch.from_numpy(x).cuda(), 32, B)
+        t_or = oracle.search_tau_budget(x, 32, B)
+        assert tau == t_or
+        codes = oracle.direction_array(x, 32, t_or)
+        assert np.array_equal(log.words.cpu().numpy().view(np.uint64), oracle.sparse_from_codes(codes))
+        assert log.count <= B
+        assert np.array_equal(bits(y.cpu().numpy()), bits(oracle.rnd_array(x, 32).astype(np.float32)))
 
 
 def test_normalized_distance(oracle):

@@ -285,6 +285,7 @@ def run_ours(args) -> None:
     if args.extras and world == 1:
         line["extras"] = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
                           "configs[2]_resnet50_budget": config2(),
+                          "configs[3]_gpt2_fp64_step": config3_gpt2(),
                           "configs[4]_merkle_1.5B": config4_merkle()}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -438,6 +439,44 @@ def config2() -> dict:
             "round_log_gbs_equiv": round(total * (8 + 4 + 8 * logged / total) / ms / 1e6, 1),
             "logged_fraction": round(logged / total, 6), "tau_over_2^-24": [round(float(t.min()), 6), round(float(t.max()), 6)],
             "note": "search (2-3 streaming passes) + round-and-log per tensor, host bisection between them"}
+
+
+def config3_gpt2(steps: int = 3) -> dict:
+    """configs[3]: one GPT-2-small FP64 training step (batch 8 x 1024 tokens,
+    random init, SGD) with every leaf-module output and input gradient passed
+    through the adaptive round-and-log (hooks.RoundAndLogHooks), against the
+    same step without the hooks."""
+    import torch
+
+    from paper_2403_09603_b200 import hooks, workloads
+    model = workloads.gpt2_small_fp64()
+    opt = torch.optim.SGD(model.parameters(), lr=1e-4)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    idx = torch.randint(0, 50257, (8, 1024), device="cuda", generator=g)
+    tgt = torch.randint(0, 50257, (8, 1024), device="cuda", generator=g)
+
+    def step():
+        opt.zero_grad(set_to_none=True)
+        logits = model(idx)
+        loss = torch.nn.functional.cross_entropy(logits.view(-1, logits.shape[-1]), tgt.view(-1))
+        loss.backward()
+        opt.step()
+        return loss
+
+    ms_plain = _time(step, reps=steps, warm=1)
+    hk = hooks.RoundAndLogHooks(model)
+    step()
+    info = hk.collect()
+    ms_hooked = _time(step, reps=steps, warm=0)
+    hk.collect()
+    hk.remove()
+    return {"model": "GPT-2 small FP64 (12x768, 12 heads, vocab 50257), random init", "batch": [8, 1024],
+            "step_ms_plain": round(ms_plain, 2), "step_ms_round_and_log": round(ms_hooked, 2),
+            "trainer_overhead": round(ms_hooked / ms_plain, 4), "hooked_tensors": info["tensors"],
+            "hooked_fwd": info["fwd"], "hooked_bwd": info["bwd"], "hooked_elements": info["elements"],
+            "logged_entries": info["logged"], "budget": "0.5% per tensor",
+            "paper_trainer_overhead": "1.2-1.4x (PAPER.md:402, A40 / Titan XP / 2080 Ti)"}
 
 
 def config4_merkle() -> dict:

@@ -96,6 +96,61 @@ def resnet50_tensors(batch: int = 32, image: int = 224) -> list[tuple[str, tuple
     return fwd + grads
 
 
+def gpt2_small_fp64(device="cuda", vocab: int = 50257, d: int = 768, layers: int = 12, heads: int = 12,
+                    ctx: int = 1024, seed: int = 3):
+    """BASELINE configs[3] model: GPT-2 small (117M: 12 layers, d=768, 12
+    heads, vocab 50257) in FP64 with random init (no checkpoint).  Every
+    leaf module is a hook point: wte, wpe, and per block ln_1, c_attn,
+    c_proj, ln_2, c_fc, gelu, c_fc_proj; then ln_f and lm_head (tied to wte).
+    Attention itself is the functional causal SDPA."""
+    import torch
+    import torch.nn as nn
+    import torch.nn.functional as F
+
+    class Block(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.ln_1 = nn.LayerNorm(d)
+            self.c_attn = nn.Linear(d, 3 * d)
+            self.c_proj = nn.Linear(d, d)
+            self.ln_2 = nn.LayerNorm(d)
+            self.c_fc = nn.Linear(d, 4 * d)
+            self.gelu = nn.GELU(approximate="tanh")
+            self.c_fc_proj = nn.Linear(4 * d, d)
+
+        def forward(self, x):
+            b, t, _ = x.shape
+            q, k, v = self.c_attn(self.ln_1(x)).split(d, dim=2)
+            q, k, v = (z.view(b, t, heads, d // heads).transpose(1, 2) for z in (q, k, v))
+            a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+            x = x + self.c_proj(a.transpose(1, 2).reshape(b, t, d))
+            return x + self.c_fc_proj(self.gelu(self.c_fc(self.ln_2(x))))
+
+    class GPT2(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.wte = nn.Embedding(vocab, d)
+            self.wpe = nn.Embedding(ctx, d)
+            self.h = nn.ModuleList(Block() for _ in range(layers))
+            self.ln_f = nn.LayerNorm(d)
+            self.lm_head = nn.Linear(d, vocab, bias=False)
+            self.lm_head.weight = self.wte.weight
+
+        def forward(self, idx):
+            pos = torch.arange(idx.shape[1], device=idx.device)
+            x = self.wte(idx) + self.wpe(pos)
+            for blk in self.h:
+                x = blk(x)
+            return self.lm_head(self.ln_f(x))
+
+    torch.manual_seed(seed)
+    m = GPT2()
+    for name, p in m.named_parameters():
+        if name.endswith("weight") and p.dim() == 2:
+            torch.nn.init.normal_(p, 0.0, 0.02)
+    return m.to(device=device, dtype=torch.float64)
+
+
 def config2_sigmas(n_tensors: int, seed: int = 2) -> np.ndarray:
     """sigma_t = 10^U(-3, 1) per tensor (log-uniform in [1e-3, 10])."""
     return 10.0 ** np.random.default_rng(seed).uniform(-3.0, 1.0, size=n_tensors)

@@ -148,7 +148,9 @@ def gpt2_small_fp64(device="cuda", vocab: int = 50257, d: int = 768, layers: int
     for name, p in m.named_parameters():
         if name.endswith("weight") and p.dim() == 2:
             torch.nn.init.normal_(p, 0.0, 0.02)
-    return m.to(device=device, dtype=torch.float64)
+    m = m.to(device=device, dtype=torch.float64)
+    m.lm_head.weight = m.wte.weight  # keep the GPT-2 weight tying after the move
+    return m
 
 
 def config2_sigmas(n_tensors: int, seed: int = 2) -> np.ndarray:

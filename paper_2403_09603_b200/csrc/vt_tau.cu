@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
   uint32_t err = 0, above = 0;
   const int lane = threadIdx.x & 31;
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+  // fast path valid for b_r = 32 over the default bisection range (2^-25, 2^-24]
+  const bool fast32 = g.drop == 29 && lo == 0x3E60000000000000ull && hi == 0x3E70000000000000ull;
   // four consecutive elements per thread per step (one 256-bit load)
   for (int64_t base = (int64_t)blockIdx.x * 1024; base < n; base += (int64_t)gridDim.x * 1024) {
     const int64_t i0 = base + 4 * threadIdx.x;
@@ -256,9 +258,24 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
       bool in = false;
       uint64_t k = 0;
       if (i0 + v < n) {
-        k = dist_key(xv.v[v], g, err);
-        if (k > hi) above += first ? 1u : 0u;
-        else in = k > lo && ((k - lo - 1) & pmask) == prefix;
+        const double xe = xv.v[v];
+        const int hi32 = __double2hiint(xe);
+        if (fast32 && !outside_normal32((uint32_t)hi32 & 0x7fffffffu)) {
+          // b_r = 32, 2^-126 <= |x| < FLT_MAX: p = d * 2^-52 with d the distance
+          // in dropped-bit units (d <= 2^28, so never above tau_hi = 2^-24);
+          // inside (2^-25, 2^-24] iff d > 2^27, at key offset (d - 2^27) * 2^25 - 1
+          const uint32_t lo32 = (uint32_t)__double2loint(xe);
+          const uint32_t low = lo32 & 0x1fffffffu;
+          const bool up = (low + ((lo32 >> 29) & 1u)) > 0x10000000u;
+          const uint32_t d = up ? (0x20000000u - low) : low;
+          const uint64_t o = ((uint64_t)(d - 0x08000000u) << 25) - 1ull;
+          in = d > 0x08000000u && (o & pmask) == prefix;
+          k = lo + 1ull + o;
+        } else {
+          k = dist_key(xe, g, err);
+          if (k > hi) above += first ? 1u : 0u;
+          else in = k > lo && ((k - lo - 1) & pmask) == prefix;
+        }
       }
       if (compact) {
         const uint32_t m = __ballot_sync(0xffffffffu, in);

@@ -276,6 +276,32 @@ def test_special_values_fused(oracle, b_r):
         assert np.array_equal(_sparse_np(log), want), tau
 
 
+def test_host_pipeline_e2e(oracle):
+    """The e2e path of bench.py (pinned host buffers, chunked H2D / kernels /
+    D2H on three streams, log chunks chained through device cursors)."""
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    n = (1 << 21) + 12345
+    xt, xa = workloads.config1_pair(n, 11)
+    tau = workloads.TAU_CONFIG0
+    xt_h = torch.from_numpy(xt).pin_memory()
+    xa_h = torch.from_numpy(xa).pin_memory()
+    yt_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    ya_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    log_h = torch.empty(n // 4, dtype=torch.int64).pin_memory()
+    count, corr, _ = ops.round_and_log_replay_host(xt_h, xa_h, 32, tau, yt_h, ya_h, log_h, global_base=777,
+                                                   chunk=1 << 19)
+    torch.cuda.synchronize()
+    codes = oracle.direction_array(xt, 32, tau)
+    want = oracle.sparse_from_codes(codes, base=777)
+    assert count == want.size
+    assert np.array_equal(log_h[:count].numpy().view(np.uint64), want)
+    assert np.array_equal(bits(yt_h.numpy()), bits(oracle.rnd_array(xt, 32).astype(np.float32)))
+    ya_want = oracle.rev_array(xa, 32, codes)
+    assert np.array_equal(bits(ya_h.numpy()), bits(ya_want.astype(np.float32)))
+    assert corr == int(np.count_nonzero(ya_want != oracle.rnd_array(xa, 32)))
+
+
 @pytest.mark.slow
 def test_large_properties():
     """2^27 elements: sortedness, count consistency, replay idempotence."""

@@ -162,6 +162,14 @@ int vt_round_log_adaptive(const double *x, int64_t n, int b_r, int64_t budget, i
                           int64_t global_base, const int64_t *cursor_in, int64_t *cursor_out,
                           double *tau_out, int64_t *counters, int32_t *err, void *ws,
                           size_t ws_bytes, vt_stream_t stream);
+/*
+ * Straddle samples of protocol.collect_divergence_samples (protocol.py:483-490)
+ * for two profiles' outputs y1, y2: *count = number of samples (2 per
+ * straddling element), *out_min = their minimum (+inf if none),
+ * *nan_flag |= 1 if any sample is NaN.  Feeds search_tau's all(p >= tau).
+ */
+int vt_straddle_min(const double *y1, const double *y2, int64_t n, int b_r, double *out_min,
+                    int64_t *count, int32_t *nan_flag, int32_t *err, vt_stream_t stream);
 /* out[0] = min over s[n] ignoring NaN (+inf if none), *nan_flag |= 1 if any NaN */
 int vt_min_f64(const double *s, int64_t n, double *out, int32_t *nan_flag, vt_stream_t stream);
 

@@ -284,6 +284,20 @@ def search_tau(samples, b_r: int, iters: int) -> float:
     return t
 
 
+def straddle_samples(y1, y2, b_r: int) -> list[float]:
+    """protocol.py:483-490: where two profiles' outputs round to different
+    grid points from opposite sides, both normalized distances."""
+    a, b = _as_f64(y1).reshape(-1), _as_f64(y2).reshape(-1)
+    r1, r2 = rnd_array(a, b_r), rnd_array(b, b_r)
+    st = (r1 != r2) & (((a > r1) & (b < r2)) | ((a < r1) & (b > r2)))
+    out: list[float] = []
+    if st.any():
+        for y, r in ((a, r1), (b, r2)):
+            scale = np.maximum(exponent_scale_array(y[st]), SCALE_FLOOR)
+            out.extend((np.abs(y[st] - r[st]) / scale).tolist())
+    return out
+
+
 def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
     """North-star budget search: the search_tau skeleton
     (same bounds, same midpoint) with predicate count(p > tau) <= budget;

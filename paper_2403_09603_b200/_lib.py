@@ -55,6 +55,7 @@ EXPORTS: dict[str, tuple] = {
     "vt_round_log_adaptive_workspace": (_sz, [_i64]),
     "vt_round_log_adaptive": (_i32, [_p, _i64, _i32, _i64, _i32, _i32, _p, _p, _i64, _i64, _p, _p, _p, _p, _p,
                                      _p, _sz, _p]),
+    "vt_straddle_min": (_i32, [_p, _p, _i64, _i32, _p, _p, _p, _p, _p]),
     "vt_min_f64": (_i32, [_p, _i64, _p, _p, _p]),
     "vt_sha256_leaves": (_i32, [_p, _i64, _i64, _p, _p]),
     "vt_merkle_level": (_i32, [_p, _i64, _p, _p]),

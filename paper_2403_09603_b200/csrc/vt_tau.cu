@@ -509,6 +509,61 @@ extern "C" int vt_tau_budget_key(const double* x, int64_t n, int b_r, int64_t bu
 }
 
 namespace vt {
+// Straddle samples of protocol.collect_divergence_samples (protocol.py:483-490)
+// reduced on the fly: for every element where the two profiles' outputs
+// round to different grid points from opposite sides, both normalized
+// distances are samples; search_tau only needs their minimum (and whether
+// any is NaN), so nothing is materialised.
+__global__ void straddle_min_kernel(const double* __restrict__ y1, const double* __restrict__ y2, int64_t n,
+                                    Grid g, double* out_min, unsigned long long* count, int32_t* nanp,
+                                    int32_t* errp) {
+  unsigned long long best = ~0ull;
+  uint32_t cnt = 0, err = 0;
+  bool nan = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = __ldg(y1 + i), b = __ldg(y2 + i);
+    const double r1 = __longlong_as_double((long long)round_only(a, g, err));
+    const double r2 = __longlong_as_double((long long)round_only(b, g, err));
+    const bool straddle = (r1 != r2) && (((a > r1) && (b < r2)) || ((a < r1) && (b > r2)));
+    if (straddle) {
+      cnt += 2;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double y = s ? b : a, r = s ? r2 : r1;
+        int e = 0;
+        (void)frexp(y, &e);
+        double scale = (y == 0.0) ? 0x1p-126 : ldexp(1.0, e - 1);
+        scale = scale < 0x1p-126 ? 0x1p-126 : scale;
+        const double p = __ddiv_rn(fabs(__dsub_rn(y, r)), scale);
+        if (p != p) nan = true;
+        else best = min(best, (unsigned long long)__double_as_longlong(p) | 0x8000000000000000ull);
+      }
+    }
+  }
+  report_err(errp, err);
+  for (int o = 16; o > 0; o >>= 1) {
+    best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (best != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(out_min), best);
+    if (cnt) atomicAdd(count, (unsigned long long)cnt);
+  }
+  if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(reinterpret_cast<int*>(nanp), 1);
+}
+
+// p >= 0 always, so the order key is the bit pattern with the sign bit set
+__global__ void straddle_final_kernel(double* out_min) {
+  const unsigned long long k = *reinterpret_cast<unsigned long long*>(out_min);
+  *out_min = (k == ~0ull) ? __longlong_as_double(0x7ff0000000000000ll)
+                          : __longlong_as_double((long long)(k & 0x7fffffffffffffffull));
+}
+
+__global__ void straddle_init_kernel(double* out_min, unsigned long long* count) {
+  *reinterpret_cast<unsigned long long*>(out_min) = ~0ull;
+  *count = 0;
+}
+
 // The search_tau skeleton (protocol.py:494-506) in budget form, on one
 // thread: identical IEEE FP64 operations to the host loop, so the same tau.
 __global__ void budget_bisect_kernel(const uint64_t* key, double lower, double upper, int iters, DevThr* out) {
@@ -521,6 +576,23 @@ __global__ void budget_bisect_kernel(const uint64_t* key, double lower, double u
   *out = thresholds_for(upper);
 }
 }  // namespace vt
+
+extern "C" int vt_straddle_min(const double* y1, const double* y2, int64_t n, int b_r, double* out_min,
+                               int64_t* count, int32_t* nan_flag, int32_t* err, vt_stream_t stream) {
+  if (n < 0 || b_r < 10 || b_r > 32 || !out_min || !count || !nan_flag || !err || (n && (!y1 || !y2))) {
+    vt_set_error("vt_straddle_min: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* c = reinterpret_cast<unsigned long long*>(count);
+  straddle_init_kernel<<<1, 1, 0, s>>>(out_min, c);
+  if (n) {
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    straddle_min_kernel<<<blocks, 256, 0, s>>>(y1, y2, n, make_grid(b_r, 0.0), out_min, c, nan_flag, err);
+  }
+  straddle_final_kernel<<<1, 1, 0, s>>>(out_min);
+  return vt_check_launch("straddle_min_kernel");
+}
 
 extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) {
   return 256 + vt_tau_workspace(n) + vt_round_log_workspace(n);

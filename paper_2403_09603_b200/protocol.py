@@ -134,6 +134,45 @@ def search_tau(samples, b_r: int, iters: int) -> float:
     return tau
 
 
+def straddle_min(y1, y2, b_r: int) -> tuple[float, int, bool]:
+    """(min sample, sample count, any NaN) of the straddle samples that
+    collect_divergence_samples (protocol.py:483-490) draws from two profiles'
+    outputs of the same layer on the same inputs."""
+    _check_b(b_r)
+    t1, _, s1 = D.to_device_f64(y1)
+    t2, _, s2 = D.to_device_f64(y2)
+    if s1 != s2:
+        raise ValueError(f"output shapes differ: {s1} vs {s2}")
+    out = torch.empty(2, dtype=torch.float64, device=t1.device)
+    f = D.Flags()
+    _lib.call("vt_straddle_min", D.ptr(t1), D.ptr(t2), t1.numel(), b_r, D.ptr(out), out.data_ptr() + 8,
+              f.cnt_ptr, f.err_ptr, D.stream_ptr())
+    err, cnt = f.read()
+    D.raise_fpround(err)
+    m, c = out.tolist()
+    return m, int(np.array([c], dtype=np.float64).view(np.int64)[0]), bool(cnt[0] & 1)
+
+
+def threshold_from_outputs(y1, y2, b_r: int, iters: int) -> float:
+    """protocol.threshold_search (protocol.py:509-516) once the layer has been
+    run under both profiles: search_tau over the straddle samples, with the
+    all(p >= tau) predicate evaluated as min(samples) >= tau on the device."""
+    if iters < 1:
+        raise ValueError("n_samples and iters must be >= 1")
+    lower, upper = tau_bounds(b_r)
+    m, count, has_nan = straddle_min(y1, y2, b_r)
+    if count == 0:
+        return upper
+    tau = lower
+    for _ in range(iters):
+        tau = (lower + upper) / 2.0
+        if (not has_nan) and m >= tau:
+            lower = tau
+        else:
+            upper = tau
+    return tau
+
+
 def kth_largest_distance(x, b_r: int, rank: int) -> float:
     """(rank+1)-th largest p = |x - rnd(x)| / max(scale, 2^-126), exactly."""
     _check_b(b_r)

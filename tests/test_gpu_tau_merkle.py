@@ -101,6 +101,24 @@ def test_round_and_log_adaptive_matches_host_search(oracle):
         assert np.array_equal(bits(y.cpu().numpy()), bits(oracle.rnd_array(x, 32).astype(np.float32)))
 
 
+@pytest.mark.parametrize("b_r", (26, 32))
+def test_straddle_threshold_vs_oracle(oracle, b_r):
+    """§8f3: threshold_search's sample reduction on the device."""
+    from paper_2403_09603_b200 import protocol
+    rng = np.random.default_rng(70 + b_r)
+    n = 300_000
+    y1 = rng.normal(size=n) * np.exp2(rng.integers(-12, 4, size=n))
+    # a second "profile": a few ulps of reduction-order noise
+    y2 = y1 + y1 * rng.integers(-64, 65, size=n) * 2.0 ** -53
+    s = oracle.straddle_samples(y1, y2, b_r)
+    m, count, nan = protocol.straddle_min(y1, y2, b_r)
+    assert count == len(s) > 0 and not nan
+    assert m == min(s)
+    for iters in (1, 10, 30):
+        assert protocol.threshold_from_outputs(y1, y2, b_r, iters) == oracle.search_tau(s, b_r, iters)
+    assert protocol.threshold_from_outputs(y1, y1, b_r, 10) == oracle.tau_bounds(b_r)[1]
+
+
 def test_normalized_distance(oracle):
     import torch
     from paper_2403_09603_b200 import ops

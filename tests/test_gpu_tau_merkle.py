@@ -108,8 +108,8 @@ def test_straddle_threshold_vs_oracle(oracle, b_r):
     rng = np.random.default_rng(70 + b_r)
     n = 300_000
     y1 = rng.normal(size=n) * np.exp2(rng.integers(-12, 4, size=n))
-    # a second "profile": a few ulps of reduction-order noise
-    y2 = y1 + y1 * rng.integers(-64, 65, size=n) * 2.0 ** -53
+    # a second "profile": reduction-order noise ~2^-7 of the grid spacing
+    y2 = y1 + y1 * rng.uniform(-1.0, 1.0, size=n) * 2.0 ** (2 - b_r)
     s = oracle.straddle_samples(y1, y2, b_r)
     m, count, nan = protocol.straddle_min(y1, y2, b_r)
     assert count == len(s) > 0 and not nan

@@ -64,14 +64,13 @@ def back(t: torch.Tensor, host: bool, shape: tuple):
 
 def workspace(nbytes: int, tag: str) -> torch.Tensor:
     """Per (device, tag) scratch buffer, grown on demand.  Operators that may
-    run concurrently on different streams use different tags.  The leading
-    1 MiB (epoch header + look-back status words of vt_round_log) is
-    zero-filled once at allocation; the rest needs no initialisation."""
+    run concurrently on different streams use different tags.  Zero-filled
+    once at allocation (vt_round_log keeps an epoch header and epoch-tagged
+    status words in it that must start out zero)."""
     key = (torch.cuda.current_device(), tag)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
-        ws[: 8 << 20].zero_()
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
         _WS[key] = ws
     return ws
 

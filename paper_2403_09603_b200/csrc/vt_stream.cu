@@ -203,9 +203,12 @@ template <int OUT, bool FAST, bool FULL>
 __device__ __forceinline__ uint32_t rl_tile(const Grid& g, int thr32, const double* src, void* o, int lim,
                                             uint16_t* stw, int warp, int lane, uint32_t lt, uint32_t& err) {
   uint32_t wcnt = 0;
+  const int eb = warp * kSWarpElems + lane * 2;  // this lane's first element in the tile
+  const uint32_t st_base = smem_u32(stw);       // shared-window address of the warp's stage row
+  const uint32_t trash = st_base + 2u * kSWarpElems;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
-    const int e0 = warp * kSWarpElems + j * 64 + lane * 2;
+    const int e0 = eb + j * 64;
     const double2 xv = *reinterpret_cast<const double2*>(src + e0);
     uint32_t c0, c1;
     if (FAST) {
@@ -222,13 +225,17 @@ __device__ __forceinline__ uint32_t rl_tile(const Grid& g, int thr32, const doub
       const uint64_t r1 = round_dir(xv.y, g, c1, err);
       store2<OUT, FULL>(o, e0, lim, r0, r1);
     }
-    const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 1u);
-    const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 1u);
+    const bool l0 = c0 != 1u, l1 = c1 != 1u;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, l0);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, l1);
     // branch-free staging: unlogged elements write into the trash slot
     const uint32_t r0 = wcnt + __popc(b0 & lt) + __popc(b1 & lt);
-    const uint32_t r1 = r0 + (c0 != 1u);
-    stw[(c0 != 1u) ? r0 : kSWarpElems] = (uint16_t)(e0 | ((c0 == 2u) ? 0x8000 : 0));
-    stw[(c1 != 1u) ? r1 : kSWarpElems] = (uint16_t)((e0 + 1) | ((c1 == 2u) ? 0x8000 : 0));
+    const uint32_t a0 = l0 ? st_base + 2u * r0 : trash;
+    const uint32_t a1 = l1 ? st_base + 2u * (r0 + (l0 ? 1u : 0u)) : trash;
+    const uint32_t v0 = (uint32_t)e0 | ((c0 == 2u) ? 0x8000u : 0u);
+    const uint32_t v1 = (uint32_t)(e0 + 1) | ((c1 == 2u) ? 0x8000u : 0u);
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"((uint16_t)v0) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"((uint16_t)v1) : "memory");
     wcnt += __popc(b0) + __popc(b1);
   }
   return wcnt;

@@ -438,7 +438,8 @@ def config2() -> dict:
             "g_elements_per_s": round(total / ms / 1e6, 2),
             "round_log_gbs_equiv": round(total * (8 + 4 + 8 * logged / total) / ms / 1e6, 1),
             "logged_fraction": round(logged / total, 6), "tau_over_2^-24": [round(float(t.min()), 6), round(float(t.max()), 6)],
-            "note": "search (2-3 streaming passes) + round-and-log per tensor, host bisection between them"}
+            "note": "per tensor: budget select (2-3 streaming passes) + device bisection + round-and-log "
+                    "(ops.round_and_log_adaptive), all 161 tensors in one CUDA graph"}
 
 
 def config3_gpt2(steps: int = 3) -> dict:

@@ -266,8 +266,8 @@ def run_ours(args) -> None:
                    "auditor_equals_trainer_bitwise": ok_equal,
                    "launch": "cuda graphs (one per operator)" if graphs else "eager"},
         "roofline": {"bound": "hbm",
-                     "kernel": "round-and-log op: rl_stream_kernel (TMA-pipelined rnd + direction + tile staging) "
-                               "+ rl_scan_kernel (decoupled look-back) + rl_expand_kernel",
+                     "kernel": "round-and-log op: rl_fused_kernel (single pass: TMA-pipelined rnd + direction + "
+                               "ballot staging, in-kernel decoupled look-back, final log words)",
                      "achieved": round(rl_ach, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(rl_ach / peak, 4), "traffic": traffic_for("round_log", n),
                      "algorithmic_bytes_per_launch": int(rl_bytes), "avg_launch_ms": round(rl_ms, 4),
@@ -276,7 +276,7 @@ def run_ours(args) -> None:
                                       "avg_launch_ms": round(rp_ms, 4), "algorithmic_bytes_per_launch": int(rp_bytes),
                                       "traffic": traffic_for("replay", n)}},
         "clocks": clk.summary(),
-        "gpu_launches": 4 * args.steps,  # rl_stream + rl_scan + rl_expand + rp_fused per step
+        "gpu_launches": 2 * args.steps,  # rl_fused + rp_fused per step
         "e2e": e2e,
         "cpu_baseline": cpu,
     }

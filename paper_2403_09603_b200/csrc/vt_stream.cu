@@ -1,27 +1,21 @@
 // Persistent, TMA-pipelined streaming kernels for the north-star path
 // (sparse log, FP32 / FP64 output):
 //
-//   rl_stream_kernel   trainer round-and-log (protocol._TrainerChannel.process,
-//                      pkg/src/vtrain/protocol.py:198-202) -- rounds every element,
-//                      and stages each tile's logged elements as 16-bit local
-//                      entries (11-bit offset | up << 15) + a per-tile count;
-//   rl_scan_kernel     block-level decoupled look-back prefix sum over the tile
-//                      counts (the global log position of every tile);
-//   rl_expand_kernel   expands the staged entries into the global ascending
-//                      uint64 log (global_index << 1 | up);
+//   rl_fused_kernel    trainer round-and-log (protocol._TrainerChannel.process,
+//                      pkg/src/vtrain/protocol.py:198-202) in ONE pass: rounds
+//                      every element, and writes the ascending uint64 log
+//                      (global_index << 1 | up) at its global position, found by
+//                      an in-kernel decoupled look-back over 8192-element
+//                      super-tiles (warp-specialised; see the section below);
 //   rp_fused_kernel    auditor replay (protocol._AuditorChannel.process,
 //                      protocol.py:212-216) -- scatters the tile's log slice into a
 //                      shared-memory code map and replays every element.
 //
-// Streaming CTAs are persistent (grid = resident CTAs): the trainer walks
-// tiles blockIdx.x, blockIdx.x + gridDim.x, ..., the auditor a contiguous
-// range of tiles; the FP64 input of the next kStages tiles is in flight at
-// all times through cp.async.bulk (TMA bulk copies, L2 evict-first) into a
-// shared-memory ring guarded by mbarriers, so HBM streams continuously while
-// the SM computes.  No CTA ever waits on another CTA in a streaming pass; the
-// only cross-CTA wait is the look-back of the small scan pass.  (A single-
-// launch variant that resolves each tile's log position a few waves later
-// from epoch-tagged tile counts was measured 12-20% slower and dropped.)
+// Streaming CTAs are persistent (grid = resident CTAs): the trainer draws
+// super-tiles from an atomic ticket counter, the auditor walks a contiguous
+// range of tiles; the FP64 input of the next tiles is in flight at all times
+// through cp.async.bulk (TMA bulk copies, L2 evict-first) into a shared-memory
+// ring guarded by mbarriers, so HBM streams continuously while the SM computes.
 #include <algorithm>
 
 #include "vt_common.cuh"
@@ -33,8 +27,6 @@ constexpr int kSTile = 2048;  // elements per tile (16 KiB of FP64)
 constexpr int kStages = 4;
 constexpr int kSWarpElems = kSTile / kWarps;  // 256
 constexpr int kSSlots = kSWarpElems / 64;     // 4 slots x 32 lanes x 2 elements
-constexpr int kGroupTiles = 64;               // tiles per expand CTA
-constexpr int kStageRow = kSWarpElems + 8;    // per-warp staging row + trash slot
 constexpr size_t kRingBytes = (size_t)kStages * kSTile * sizeof(double);
 
 // ---------------------------------------------------------------------------
@@ -160,9 +152,8 @@ __device__ __forceinline__ void* tile_out(void* out, int64_t tbase) {
 // status word = epoch (20 bits) | flag (2 bits) | value (42 bits).  A word
 // whose epoch differs from the current call's is "not yet published", so the
 // status array never needs clearing between calls: the workspace header keeps
-// the epoch, every CTA reads it at start, and the last CTA bumps it after its
-// own look-back (which completes only after every other CTA has published,
-// hence after every CTA has read the old epoch).
+// the epoch, every CTA reads it at start, and the last CTA to finish bumps it
+// (after every CTA has read the old one).
 // ---------------------------------------------------------------------------
 
 constexpr int kEpochShift = 44;
@@ -171,275 +162,414 @@ constexpr uint64_t kLBAgg = 1ull << 42;
 constexpr uint64_t kLBInc = 2ull << 42;
 constexpr uint64_t kLBVal = (1ull << 42) - 1;
 
-struct WsHeader {
-  uint32_t epoch;
-  uint32_t pad[15];
-};
-
 __device__ __forceinline__ uint64_t lb_word(uint32_t epoch, uint64_t flag, uint64_t v) {
   return ((uint64_t)epoch << kEpochShift) | flag | (v & kLBVal);
 }
 
 // ---------------------------------------------------------------------------
-// trainer: streaming pass (strided persistent tiles) + expand pass
+// trainer, single pass: warp-specialised round-and-log with an in-kernel
+// decoupled look-back
+//
+//   warps 0..7  compute: round every element of a 2048-element tile staged by
+//               TMA, store y, and ballot two masks per 64-element group
+//               (logged, UP) into a shared-memory mask slot -- no compaction,
+//               no per-element shared stores;
+//   warp 8      log writer: per 8192-element super-tile (4 tiles), popc the
+//               masks, publish the super-tile count, look back over the
+//               predecessors' epoch-tagged status words for its global log
+//               position, and write the final (index << 1 | up) words
+//               (staged in shared memory, then coalesced stores);
+//   warp 9      producer: grabs super-tile tickets (atomic counter: a CTA
+//               only ever waits on lower tickets, which running CTAs hold, so
+//               the kernel cannot deadlock even when not all CTAs are
+//               resident) and keeps kStages TMA bulk copies in flight.
+//
+// Compute warps never wait on another CTA: the look-back latency is absorbed
+// by kMaskSlots super-tiles of mask slack.  The CTA that finishes last
+// resets the ticket counter and bumps the epoch for the next call.
 // ---------------------------------------------------------------------------
 
-struct RLArgs {
+constexpr int kSuper = 4;                        // tiles per super-tile / status word
+constexpr int kMaskSlots = 3;                    // super-tiles of masks in flight
+constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
+constexpr int kRow = 64;                         // staged entries per warp-tile (else from masks)
+constexpr int kRows = kSuper * kWarps;           // warp-tiles per super-tile
+constexpr int kFCompute = kSThreads;             // 8 compute warps
+constexpr int kFThreads = kFCompute + 64;        // + log warp + producer warp
+constexpr int kLogWarp = kWarps;                 // warp 8
+constexpr int kProdWarp = kWarps + 1;            // warp 9
+constexpr int kGroups = kSTile / 64;             // 32 groups of 64 elements per tile
+
+struct FusedHeader {
+  uint32_t epoch;
+  uint32_t ticket;  // next super-tile to hand out
+  uint32_t done;    // CTAs finished
+  uint32_t pad[13];
+};
+
+struct FusedSmem {
+  double ring[kFStages][kSTile];
+  uint4 masks[kMaskSlots][kSuper][kGroups];    // {logged even, logged odd, up even, up odd} lanes
+  uint16_t rows[kMaskSlots][kRows][kRow];      // staged entries: super-tile offset << 1 | up
+  uint32_t cnts[kMaskSlots][kRows];            // entries per warp-tile (tile-major)
+  uint32_t rpos[kMaskSlots][kRows];            // log warp: row start inside the super-tile
+  int64_t sbase[kMaskSlots];                   // log warp: global log position of the super-tile
+  int64_t slot_id[kMaskSlots];
+  int64_t ids[4];
+  uint32_t slot_cnt[kMaskSlots];  // (warps arrived << 24) + logged entries, by the compute warps
+  uint64_t full[kFStages], empty[kFStages], mfull[kMaskSlots], ofull[kMaskSlots];
+  uint32_t epoch;
+};
+
+struct RLFArgs {
   const double* x;
   int64_t n;
   Grid g;
   int thr32;
   void* out;
   int64_t num_tiles;
-  uint32_t* counts;   // [num_tiles] logged entries per tile
-  uint16_t* scratch;  // [num_tiles][kSTile] staged entries: tile offset | up << 15
+  int64_t num_super;
+  FusedHeader* hdr;
+  uint64_t* status;  // [num_super] epoch-tagged look-back words
+  uint64_t* sparse;
+  int64_t cap;
+  int64_t global_base;
+  const int64_t* cursor_in;
+  int64_t* cursor_out;
+  int64_t* counters;
   int32_t* err;
-  const DevThr* dthr;  // adaptive path: thresholds from the device bisection
+  const DevThr* dthr;
 };
 
-// One tile: round, classify, store, stage logged elements (warp-local order
-// == element order).  Returns the warp's count.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// bit i of x (< 2^16) -> bit 2i
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// One tile, compute warp: round, store, ballot.  `gx` non-null = partial
+// tile read straight from global memory (elements >= lim are zero, which is
+// on the grid and never logged).
 template <int OUT, bool FAST, bool FULL>
-__device__ __forceinline__ uint32_t rl_tile(const Grid& g, int thr32, const double* src, void* o, int lim,
-                                            uint16_t* stw, int warp, int lane, uint32_t lt, uint32_t& err) {
+__device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_t w8, int thr32, const double* src,
+                                         void* o, int lim, uint4* mslot, uint16_t* row, uint32_t sbase, int warp,
+                                         int lane, uint32_t lt, uint32_t& err) {
   uint32_t wcnt = 0;
-  const int eb = warp * kSWarpElems + lane * 2;  // this lane's first element in the tile
-  const uint32_t st_base = smem_u32(stw);       // shared-window address of the warp's stage row
-  const uint32_t trash = st_base + 2u * kSWarpElems;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
-    const int e0 = eb + j * 64;
-    const double2 xv = *reinterpret_cast<const double2*>(src + e0);
-    uint32_t c0, c1;
+    const int e0 = warp * kSWarpElems + j * 64 + lane * 2;
+    double2 xv;
+    if (FULL) {
+      xv = *reinterpret_cast<const double2*>(src + e0);
+    } else {
+      xv.x = (e0 < lim) ? src[e0] : 0.0;
+      xv.y = (e0 + 1 < lim) ? src[e0 + 1] : 0.0;
+    }
+    bool l0, l1, u0, u1;
     if (FAST) {
-      bool slow = false;
-      float f0 = round_dir32_fast(xv.x, thr32, c0, slow);
-      float f1 = round_dir32_fast(xv.y, thr32, c1, slow);
-      if (slow) {
+      float f0 = __double2float_rn(xv.x), f1 = __double2float_rn(xv.y);
+      const uint32_t lo0 = (uint32_t)__double2loint(xv.x), lo1 = (uint32_t)__double2loint(xv.y);
+      const uint32_t hi0 = (uint32_t)__double2hiint(xv.x), hi1 = (uint32_t)__double2hiint(xv.y);
+      // normal range: logged <=> thr32 < low29 < 2^29 - thr32 (SURVEY App. B.2,
+      // d = min(low, 2^29 - low) split by the rounding side); the magnitude
+      // rounded up iff the FP32 lsb differs from the FP64 bit 29, and the
+      // code is UP iff that XOR the sign.
+      l0 = (lo0 << 3) - c8 < w8;
+      l1 = (lo1 << 3) - c8 < w8;
+      const uint32_t fb0 = (uint32_t)__float_as_int(f0), fb1 = (uint32_t)__float_as_int(f1);
+      u0 = (int32_t)((fb0 << 31) ^ (lo0 << 2) ^ fb0) < 0;
+      u1 = (int32_t)((fb1 << 31) ^ (lo1 << 2) ^ fb1) < 0;
+      if (outside_normal32(hi0 & 0x7fffffffu) | outside_normal32(hi1 & 0x7fffffffu)) {
+        uint32_t c0, c1;
         f0 = round_dir32(xv.x, thr32, g.thr_sub, c0, err);
         f1 = round_dir32(xv.y, thr32, g.thr_sub, c1, err);
+        l0 = c0 != 1u;
+        l1 = c1 != 1u;
+        u0 = c0 == 2u;
+        u1 = c1 == 2u;
       }
       store2<OUT, FULL>(o, e0, lim, f0, f1);
     } else {
+      uint32_t c0, c1;
       const uint64_t r0 = round_dir(xv.x, g, c0, err);
       const uint64_t r1 = round_dir(xv.y, g, c1, err);
       store2<OUT, FULL>(o, e0, lim, r0, r1);
+      l0 = c0 != 1u;
+      l1 = c1 != 1u;
+      u0 = c0 == 2u;
+      u1 = c1 == 2u;
     }
-    const bool l0 = c0 != 1u, l1 = c1 != 1u;
-    const uint32_t b0 = __ballot_sync(0xffffffffu, l0);
-    const uint32_t b1 = __ballot_sync(0xffffffffu, l1);
-    // branch-free staging: unlogged elements write into the trash slot
-    const uint32_t r0 = wcnt + __popc(b0 & lt) + __popc(b1 & lt);
-    const uint32_t a0 = l0 ? st_base + 2u * r0 : trash;
-    const uint32_t a1 = l1 ? st_base + 2u * (r0 + (l0 ? 1u : 0u)) : trash;
-    const uint32_t v0 = (uint32_t)e0 | ((c0 == 2u) ? 0x8000u : 0u);
-    const uint32_t v1 = (uint32_t)(e0 + 1) | ((c1 == 2u) ? 0x8000u : 0u);
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"((uint16_t)v0) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"((uint16_t)v1) : "memory");
-    wcnt += __popc(b0) + __popc(b1);
+    const uint32_t L0 = __ballot_sync(0xffffffffu, l0), L1 = __ballot_sync(0xffffffffu, l1);
+    const uint32_t U0 = __ballot_sync(0xffffffffu, u0), U1 = __ballot_sync(0xffffffffu, u1);
+    if (lane == 0) mslot[warp * kSSlots + j] = make_uint4(L0, L1, U0, U1);
+    // ballot-rank staging of the warp-tile's entries (first kRow only)
+    const uint32_t r0 = wcnt + __popc(L0 & lt) + __popc(L1 & lt);
+    const uint32_t r1 = r0 + (l0 ? 1u : 0u);
+    const uint32_t v0 = ((sbase + (uint32_t)e0) << 1) | (u0 ? 1u : 0u);
+    if (l0 && r0 < (uint32_t)kRow) row[r0] = (uint16_t)v0;
+    if (l1 && r1 < (uint32_t)kRow) row[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+    wcnt += __popc(L0) + __popc(L1);
   }
   return wcnt;
 }
 
-// Tiles t = blockIdx.x + k * gridDim.x: at any moment the CTAs of the grid
-// stream one contiguous window of x.  No cross-CTA waits.
-template <int OUT, bool FAST>
-__global__ void __launch_bounds__(kSThreads, 3) rl_stream_kernel(const RLArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ uint32_t s_cnt[2][kWarps];
-  Ring ring{reinterpret_cast<double*>(sm), bars};
-  uint16_t* st16 = reinterpret_cast<uint16_t*>(sm + kRingBytes);  // [2][kWarps][kStageRow]
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t G = gridDim.x;
-  const int64_t full_tiles = a.n / kSTile;
-  const uint64_t pol = evict_first_policy();
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < kStages; ++s) issue_tile(ring, a.x, blockIdx.x + s * G, full_tiles, s, pol);
-
-  const uint32_t lt = lanemask_lt();
-  uint32_t err = 0;
-  Grid g = a.g;
-  int thr32 = a.thr32;
-  if (a.dthr) {  // adaptive: tau was bisected on the device
-    g.thr = a.dthr->thr;
-    g.thr_sub = a.dthr->thr_sub;
-    thr32 = a.dthr->thr32;
-  }
-  for (int64_t k = 0;; ++k) {
-    const int64_t t = blockIdx.x + k * G;
-    if (t >= a.num_tiles) break;
-    const int s = (int)(k % kStages);
-    const int buf = (int)(k & 1);
-    const double* src = acquire_tile(ring, a.x, a.n, t, full_tiles, s, (uint32_t)((k / kStages) & 1));
-    const int64_t tbase = t * kSTile;
-    uint16_t* stw = st16 + (buf * kWarps + warp) * kStageRow;
-    void* o = tile_out<OUT>(a.out, tbase);
-    const uint32_t wcnt = (t < full_tiles)
-        ? rl_tile<OUT, FAST, true>(g, thr32, src, o, kSTile, stw, warp, lane, lt, err)
-        : rl_tile<OUT, FAST, false>(g, thr32, src, o, (int)(a.n - tbase), stw, warp, lane, lt, err);
-    if (lane == 0) s_cnt[buf][warp] = wcnt;
-    __syncthreads();  // ring slot s consumed; warp counts visible
-    if (tid == 0) {
-      fence_proxy_async();
-      issue_tile(ring, a.x, t + kStages * G, full_tiles, s, pol);
-    }
-    uint32_t off = 0, total = 0;
+// Look-back by one warp over up to 128 predecessors per round trip (the
+// super-tile's own aggregate was published by its compute warps).  Valid
+// aggregates before the first unpublished word are kept, so every retry
+// starts at the first word still missing.  Returns the exclusive prefix of
+// super-tile s (same value in every lane) and publishes its inclusive prefix.
+__device__ __forceinline__ int64_t lookback128(uint64_t* status, int64_t s, uint64_t agg, uint32_t epoch,
+                                               int lane) {
+  if (s == 0) return 0;
+  int64_t excl = 0, pred = s - 1;
+  while (true) {
+    uint64_t w[4];
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_cnt[buf][w];
-      off += (w < warp) ? c : 0u;
-      total += c;
+    for (int m = 0; m < 4; ++m) {
+      const int64_t idx = pred - (m * 32 + lane);
+      w[m] = (idx >= 0) ? ld_relaxed_u64(status + idx) : lb_word(epoch, kLBInc, 0);
     }
-    uint16_t* dst = a.scratch + tbase + off;
-    for (uint32_t i = lane; i < wcnt; i += 32) dst[i] = stw[i];
-    if (tid == 0) a.counts[t] = total;
+    int p_inc = 128, p_inv = 128;  // first INC / first unpublished window position
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const bool valid = ((w[m] >> kEpochShift) & kEpochMask) == epoch;
+      const uint64_t flag = valid ? ((w[m] >> 42) & 3ull) : 0ull;
+      const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
+      const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
+      if (p_inc == 128 && inc) p_inc = m * 32 + __ffs(inc) - 1;
+      if (p_inv == 128 && inv) p_inv = m * 32 + __ffs(inv) - 1;
+    }
+    const bool done = p_inc < p_inv;
+    const int upto = done ? p_inc + 1 : p_inv;  // positions [0, upto) are summed
+    uint64_t v = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (m * 32 + lane < upto) v += w[m] & kLBVal;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += (int64_t)v;
+    if (done) break;
+    pred -= upto;
+    if (upto < 128) __nanosleep(32);
   }
-  report_err(a.err, err);
+  if (lane == 0) st_relaxed_u64(status + s, lb_word(epoch, kLBInc, (uint64_t)excl + agg));
+  return excl;
 }
 
-// Scan: exclusive prefix of the per-tile counts by single-pass decoupled
-// look-back (CTA per kScanTiles counts), giving every tile the global log
-// position of its first entry.
-constexpr int kScanPer = 8;                        // counts per thread
-constexpr int kScanTiles = kSThreads * kScanPer;  // 2048 counts per CTA
+// Log warp, overflow path: warp-tile q had more than kRow entries, so its
+// words come from the ballot masks, one 64-element group per step.
+// `dst` = the row's first log position, `lim` = positions still in capacity.
+__device__ __noinline__ void rlf_row_from_masks(const FusedSmem& S, int slot, int q, uint64_t gw, uint64_t* dst,
+                                                int64_t lim, int lane, uint32_t lt) {
+  const int tile = q / kWarps, w = q % kWarps;
+  uint32_t r = 0;
+  for (int j = 0; j < kSSlots; ++j) {
+    const uint4 m = S.masks[slot][tile][w * kSSlots + j];
+    const bool l0 = (m.x >> lane) & 1u, l1 = (m.y >> lane) & 1u;
+    const uint32_t r0 = r + __popc(m.x & lt) + __popc(m.y & lt);
+    const uint64_t e0 = (uint64_t)(tile * kSTile + w * kSWarpElems + j * 64 + lane * 2);
+    if (l0 && (int64_t)r0 < lim) dst[r0] = gw + (e0 << 1) + ((m.z >> lane) & 1u);
+    const uint32_t r1 = r0 + (l0 ? 1u : 0u);
+    if (l1 && (int64_t)r1 < lim) dst[r1] = gw + ((e0 + 1) << 1) + ((m.w >> lane) & 1u);
+    r += __popc(m.x) + __popc(m.y);
+  }
+}
 
-struct ScanArgs {
-  const uint32_t* counts;
-  int64_t num_tiles;
-  WsHeader* hdr;
-  uint64_t* status;  // [num_scan_ctas] epoch-tagged
-  int64_t* toffs;    // [num_tiles] global log position of each tile's entries
-  const int64_t* cursor_in;
-  int64_t* cursor_out;
-  int64_t* counters;
-};
-
-__global__ void __launch_bounds__(kSThreads) rl_scan_kernel(const ScanArgs a) {
-  __shared__ uint32_t s_warp[kWarps];
-  __shared__ int64_t s_base;
-  __shared__ uint32_t s_epoch;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t chunk = blockIdx.x;  // 1-D grid: dispatched in order, look-back is safe
-  const int64_t t0 = chunk * kScanTiles + (int64_t)tid * kScanPer;
-  uint32_t c[kScanPer];
-  uint32_t sum = 0;
+// Compute warp: once the log warp has placed ordinal k (super-tile s) of this
+// CTA (ofull), write this warp's four rows of it -- staged entries by
+// coalesced stores, an overflowing row from its ballot masks.
+__device__ __forceinline__ void rlf_write_rows(const RLFArgs& a, FusedSmem& S, int64_t k, int64_t s, int warp,
+                                               int lane, uint32_t lt) {
+  const int slot = (int)(k % kMaskSlots);
+  mbar_wait(S.ofull + slot, (uint32_t)((k / kMaskSlots) & 1));
+  const int64_t off = S.sbase[slot];
+  uint64_t* dst = a.sparse + off;
+  const int64_t lim = a.cap - off;  // positions >= lim are beyond the log capacity
+  const uint64_t gw = (uint64_t)(a.global_base + s * (int64_t)(kSuper * kSTile)) << 1;
 #pragma unroll
-  for (int m = 0; m < kScanPer; ++m) {
-    c[m] = (t0 + m < a.num_tiles) ? a.counts[t0 + m] : 0u;
-    sum += c[m];
-  }
-  uint32_t inc = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) s_warp[warp] = inc;
-  if (tid == 0) s_epoch = ((*(volatile uint32_t*)&a.hdr->epoch) + 1u) & (uint32_t)kEpochMask;
-  __syncthreads();
-  uint32_t wpre = 0, agg = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    wpre += (w < warp) ? s_warp[w] : 0u;
-    agg += s_warp[w];
-  }
-  const uint32_t epoch = s_epoch;
-  if (warp == 0) {
-    int64_t excl = 0;
-    if (chunk == 0) {
-      if (lane == 0) st_relaxed_u64(a.status, lb_word(epoch, kLBInc, agg));
+  for (int i = 0; i < kSuper; ++i) {
+    const int q = i * kWarps + warp;
+    if (s * kSuper + i >= a.num_tiles) break;
+    const uint32_t cq = S.cnts[slot][q];
+    const uint32_t pq = S.rpos[slot][q];
+    if (cq <= (uint32_t)kRow) {
+      const uint16_t* row = S.rows[slot][q];
+      if ((uint32_t)lane < cq && (int64_t)(pq + lane) < lim) dst[pq + lane] = gw + row[lane];
+      if (cq > 32u && (uint32_t)lane + 32u < cq && (int64_t)(pq + lane + 32) < lim)
+        dst[pq + lane + 32] = gw + row[lane + 32];
     } else {
-      if (lane == 0) st_relaxed_u64(a.status + chunk, lb_word(epoch, kLBAgg, agg));
-      int64_t pred = chunk - 1;
-      while (true) {
-        const int64_t idx = pred - lane;
-        uint64_t s = lb_word(epoch, kLBInc, 0);
-        if (idx >= 0) s = ld_relaxed_u64(a.status + idx);
-        const bool valid = ((s >> kEpochShift) & kEpochMask) == epoch;
-        const uint64_t flag = valid ? ((s >> 42) & 3ull) : 0ull;
-        const uint32_t incm = __ballot_sync(0xffffffffu, flag == 2);
-        const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
-        const int first = incm ? (__ffs(incm) - 1) : 31;
-        const uint32_t upto = (2u << first) - 1u;
-        if (inv & upto) {
-          __nanosleep(32);
-          continue;
-        }
-        uint64_t v = (lane <= first) ? (s & kLBVal) : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += (int64_t)v;
-        if (incm) break;
-        pred -= 32;
-      }
-      if (lane == 0) st_relaxed_u64(a.status + chunk, lb_word(epoch, kLBInc, (uint64_t)excl + agg));
+      rlf_row_from_masks(S, slot, q, gw, dst + pq, lim - (int64_t)pq, lane, lt);
     }
-    if (lane == 0) {
-      const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
-      s_base = cur + excl;
-      if ((chunk + 1) * kScanTiles >= a.num_tiles) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)agg));
-        if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)agg;
-        *(volatile uint32_t*)&a.hdr->epoch = epoch;
-      }
-    }
-  }
-  __syncthreads();
-  int64_t off = s_base + wpre + (inc - sum);
-#pragma unroll
-  for (int m = 0; m < kScanPer; ++m) {
-    if (t0 + m < a.num_tiles) a.toffs[t0 + m] = off;
-    off += c[m];
   }
 }
 
-// Expand: warp per tile, no waits -- the staged 16-bit entries become
-// global (index << 1 | up) words at the tile's scanned position.
-constexpr int kExpTilesPerCta = kWarps;
+template <int OUT, bool FAST>
+__global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t full_tiles = a.n / kSTile;
+  if (tid == 0) {
+    for (int s = 0; s < kFStages; ++s) {
+      mbar_init(S.full + s, 1);
+      mbar_init(S.empty + s, kWarps);
+    }
+    for (int m = 0; m < kMaskSlots; ++m) {
+      mbar_init(S.mfull + m, kWarps);
+      mbar_init(S.ofull + m, 1);
+    }
+    for (int m = 0; m < kMaskSlots; ++m) S.slot_cnt[m] = 0u;
+    fence_mbar_init();
+    S.epoch = ((*(volatile uint32_t*)&a.hdr->epoch) + 1u) & (uint32_t)kEpochMask;
+  }
+  __syncthreads();
 
-struct ExpandArgs {
-  const uint16_t* scratch;
-  const uint32_t* counts;
-  const int64_t* toffs;
-  int64_t num_tiles;
-  int64_t global_base;
-  uint64_t* sparse;
-  int64_t cap;
-};
-
-__global__ void __launch_bounds__(kSThreads) rl_expand_kernel(const ExpandArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t t = (int64_t)blockIdx.x * kExpTilesPerCta + warp;
-  if (t >= a.num_tiles) return;
-  const uint32_t cnt = a.counts[t];
-  const int64_t out0 = a.toffs[t];
-  const uint16_t* src = a.scratch + t * kSTile;
-  const uint64_t w0 = (uint64_t)(a.global_base + t * kSTile) << 1;
-  if (out0 + cnt <= a.cap) {
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 4 * 32) {
-      uint32_t e[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = i0 + u * 32 + lane;
-        e[u] = (i < cnt) ? (uint32_t)__ldg(src + i) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = i0 + u * 32 + lane;
-        if (i < cnt) a.sparse[out0 + i] = w0 + ((uint64_t)(e[u] & 0x7fffu) << 1) + (e[u] >> 15);
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+      for (int64_t k = 0;; ++k) {
+        if (s >= a.num_super) s = -1;
+        int64_t nxt = -1;
+#pragma unroll 1
+        for (int i = 0; i < kSuper; ++i) {
+          const int64_t q = k * kSuper + i;
+          const int st = (int)(q % kFStages);
+          mbar_wait(S.empty + st, (uint32_t)(((q / kFStages) & 1) ^ 1));
+          if (i == 0) {
+            S.ids[k & 3] = s;
+            if (s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+          }
+          const int64_t t = s * kSuper + i;
+          if (s >= 0 && t < full_tiles) {
+            fence_proxy_async();
+            tma_load(S.ring[st], a.x + t * kSTile, kSTile * sizeof(double), S.full + st, pol);
+          } else {
+            mbar_arrive(S.full + st);
+          }
+          if (s < 0) break;
+        }
+        if (s < 0) break;
+        s = nxt;
       }
     }
-  } else {
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t e = __ldg(src + i);
-      if (out0 + i < a.cap) a.sparse[out0 + i] = w0 + ((uint64_t)(e & 0x7fffu) << 1) + (e >> 15);
+    __syncwarp();
+  } else if (warp == kLogWarp) {  // scan + look-back only; compute warps write the words
+    const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
+    const uint32_t epoch = S.epoch;
+    for (int64_t k = 0;; ++k) {
+      const int slot = (int)(k % kMaskSlots);
+      mbar_wait(S.mfull + slot, (uint32_t)((k / kMaskSlots) & 1));
+      const int64_t s = S.slot_id[slot];
+      if (s < 0) break;
+      // lane = warp-tile (tile-major): exclusive position of each row inside the super-tile
+      const uint32_t c = (s * kSuper + lane / kWarps < a.num_tiles) ? S.cnts[slot][lane] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
+      S.rpos[slot][lane] = inc - c;
+      const int64_t excl = lookback128(a.status, s, agg, epoch, lane);
+      if (lane == 0) {
+        if (s == a.num_super - 1) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)agg));
+          if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)agg;
+        }
+        S.sbase[slot] = cur + excl;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(S.ofull + slot);
+    }
+  } else {  // compute warps
+    uint32_t err = 0;
+    Grid g = a.g;
+    int thr32 = a.thr32;
+    if (a.dthr) {
+      g.thr = a.dthr->thr;
+      g.thr_sub = a.dthr->thr_sub;
+      thr32 = a.dthr->thr32;
+    }
+    const uint32_t lt = lanemask_lt();
+    const uint32_t c8 = ((uint32_t)thr32 + 1u) << 3;
+    const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
+    const uint32_t epoch = S.epoch;
+    int64_t h1 = -1, h2 = -1, h3 = -1;  // super-tiles of ordinals k-1, k-2, k-3
+    for (int64_t k = 0;; ++k) {
+      // this warp's rows of ordinal k - 3 leave slot k % kMaskSlots before it is reused
+      if (k >= kMaskSlots) rlf_write_rows(a, S, k - kMaskSlots, h3, warp, lane, lt);
+      const int slot = (int)(k % kMaskSlots);
+      int64_t s = -1;
+      uint32_t wcnt = 0;
+#pragma unroll 1
+      for (int i = 0; i < kSuper; ++i) {
+        const int64_t q = k * kSuper + i;
+        const int st = (int)(q % kFStages);
+        mbar_wait(S.full + st, (uint32_t)((q / kFStages) & 1));
+        if (i == 0) {
+          s = S.ids[k & 3];
+          if (s < 0) break;
+        }
+        const int64_t t = s * kSuper + i;
+        if (t < a.num_tiles) {
+          const int64_t tbase = t * kSTile;
+          void* o = tile_out<OUT>(a.out, tbase);
+          uint16_t* row = S.rows[slot][i * kWarps + warp];
+          const uint32_t tc =
+              (t < full_tiles)
+                  ? rlf_tile<OUT, FAST, true>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
+                                              (uint32_t)(i * kSTile), warp, lane, lt, err)
+                  : rlf_tile<OUT, FAST, false>(g, c8, w8, thr32, a.x + tbase, o, (int)(a.n - tbase),
+                                               S.masks[slot][i], row, (uint32_t)(i * kSTile), warp, lane, lt, err);
+          if (lane == 0) S.cnts[slot][i * kWarps + warp] = tc;
+          wcnt += tc;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(S.empty + st);
+      }
+      if (lane == 0) {
+        if (s >= 0) {  // the last warp of the super-tile publishes its aggregate right away
+          const uint32_t prev = atomicAdd(&S.slot_cnt[slot], wcnt + (1u << 24));
+          if ((prev >> 24) == kWarps - 1) {
+            const uint64_t agg = (prev & 0xffffffu) + wcnt;
+            st_relaxed_u64(a.status + s, lb_word(epoch, s == 0 ? kLBInc : kLBAgg, agg));
+            S.slot_cnt[slot] = 0u;
+          }
+        }
+        if (warp == 0) S.slot_id[slot] = s;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(S.mfull + slot);
+      if (s < 0) {  // drain ordinals k - 2, k - 1
+        if (k >= 2) rlf_write_rows(a, S, k - 2, h2, warp, lane, lt);
+        if (k >= 1) rlf_write_rows(a, S, k - 1, h1, warp, lane, lt);
+        break;
+      }
+      h3 = h2;
+      h2 = h1;
+      h1 = s;
+    }
+    report_err(a.err, err);
+  }
+
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&a.hdr->done, 1u);
+    if (prev == gridDim.x - 1) {  // every CTA has drawn its last ticket and read the epoch
+      a.hdr->ticket = 0u;
+      a.hdr->done = 0u;
+      a.hdr->epoch = S.epoch;
+      __threadfence();
     }
   }
 }
@@ -630,11 +760,12 @@ __global__ void __launch_bounds__(kSThreads, 3) rp_fused_kernel(const RPArgs a) 
 int64_t stream_tiles(int64_t n) { return (n + kSTile - 1) / kSTile; }
 
 // [header 64 B][status: scan CTAs x 8][counts: T x 4][toffs: T x 8][scratch: T x kSTile x 2]
-size_t rl_stream_workspace(int64_t n) {
-  const int64_t t = stream_tiles(n);
-  const int64_t chunks = (t + kScanTiles - 1) / kScanTiles;
-  return (size_t)(64 + chunks * 8 + t * 12 + 512) + (size_t)t * kSTile * 2 + 256;
-}
+static int64_t super_tiles(int64_t n) { return (stream_tiles(n) + kSuper - 1) / kSuper; }
+
+// fused: [header 64 B][status: super-tiles x 8]
+static size_t rl_fused_workspace(int64_t n) { return (size_t)(64 + super_tiles(n) * 8 + 256); }
+
+size_t rl_stream_workspace(int64_t n) { return rl_fused_workspace(n); }
 
 size_t rp_stream_workspace(int64_t n) {
   (void)n;
@@ -650,49 +781,39 @@ static int resident_ctas(const void* fn, size_t smem) {
 }
 
 template <int OUT, bool FAST>
-static int launch_rl(const RLArgs& a, const ScanArgs& sc, const ExpandArgs& e, cudaStream_t st) {
-  const size_t smem = kRingBytes + 2 * kWarps * kStageRow * sizeof(uint16_t);
-  auto k = rl_stream_kernel<OUT, FAST>;
-  static int resident = 0;  // one process per GPU: attribute + occupancy queried once
+static int launch_rlf(const RLFArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(FusedSmem);
+  static_assert(sizeof(FusedSmem) <= 74 * 1024, "three fused CTAs per SM");
+  auto k = rl_fused_kernel<OUT, FAST>;
+  static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    resident = resident_ctas((const void*)k, smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kFThreads, smem);
+    resident = std::max(1, per * sms);
   }
-  const int grid = (int)std::min<int64_t>(a.num_tiles, resident);
-  k<<<grid, kSThreads, smem, st>>>(a);
-  int rc = vt_check_launch("rl_stream_kernel");
-  if (rc) return rc;
-  const int64_t chunks = (a.num_tiles + kScanTiles - 1) / kScanTiles;
-  rl_scan_kernel<<<(unsigned)chunks, kSThreads, 0, st>>>(sc);
-  if ((rc = vt_check_launch("rl_scan_kernel"))) return rc;
-  const int64_t ectas = (a.num_tiles + kExpTilesPerCta - 1) / kExpTilesPerCta;
-  rl_expand_kernel<<<(unsigned)ectas, kSThreads, 0, st>>>(e);
-  return vt_check_launch("rl_expand_kernel");
+  const int grid = (int)std::min<int64_t>(a.num_super, resident);
+  k<<<grid, kFThreads, smem, st>>>(a);
+  return vt_check_launch("rl_fused_kernel");
 }
 
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr) {
-  const int64_t tiles = stream_tiles(n);
-  const int64_t chunks = (tiles + kScanTiles - 1) / kScanTiles;
   uint8_t* w = static_cast<uint8_t*>(ws);
-  WsHeader* hdr = reinterpret_cast<WsHeader*>(w);
-  uint64_t* status = reinterpret_cast<uint64_t*>(w + 64);
-  int64_t* toffs = reinterpret_cast<int64_t*>(w + ((64 + chunks * 8 + 255) & ~(int64_t)255));
-  uint32_t* counts = reinterpret_cast<uint32_t*>(toffs + tiles);
-  uint16_t* scratch = reinterpret_cast<uint16_t*>(
-      w + ((((64 + chunks * 8 + 255) & ~(int64_t)255) + tiles * 12 + 255) & ~(int64_t)255));
-  RLArgs a{x, n, g, thr32, out, tiles, counts, scratch, err, dthr};
-  ScanArgs sc{counts, tiles, hdr, status, toffs, cursor_in, cursor_out, counters};
-  ExpandArgs e{scratch, counts, toffs, tiles, global_base, sparse, cap};
+  RLFArgs f{x, n, g, thr32, out, stream_tiles(n), super_tiles(n), reinterpret_cast<FusedHeader*>(w),
+            reinterpret_cast<uint64_t*>(w + 64), sparse, cap, global_base, cursor_in, cursor_out, counters, err,
+            dthr};
   if (fast) {
-    return out_kind == VT_OUT_F32 ? launch_rl<VT_OUT_F32, true>(a, sc, e, st)
-         : out_kind == VT_OUT_F64 ? launch_rl<VT_OUT_F64, true>(a, sc, e, st)
-                                  : launch_rl<VT_OUT_NONE, true>(a, sc, e, st);
+    return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, true>(f, st)
+         : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, true>(f, st)
+                                  : launch_rlf<VT_OUT_NONE, true>(f, st);
   }
-  return out_kind == VT_OUT_F32 ? launch_rl<VT_OUT_F32, false>(a, sc, e, st)
-       : out_kind == VT_OUT_F64 ? launch_rl<VT_OUT_F64, false>(a, sc, e, st)
-                                : launch_rl<VT_OUT_NONE, false>(a, sc, e, st);
+  return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, false>(f, st)
+       : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, false>(f, st)
+                                : launch_rlf<VT_OUT_NONE, false>(f, st);
 }
 
 template <typename Args>

@@ -17,7 +17,7 @@ for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
     b = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
     t = float(r[hdr.index("gpu__time_duration.sum")])
-    key = ("round_log" if any(k in name for k in ("rl_stream", "rl_expand", "rl_scan"))
+    key = ("round_log" if any(k in name for k in ("rl_fused", "rl_stream", "rl_expand", "rl_scan"))
            else "replay" if any(k in name for k in ("rp_fused", "rp_stream", "rp_tile")) else name)
     acc.setdefault(key, {}).setdefault(name.split("(")[0], []).append((b, t, r[-1]))
 out = {}

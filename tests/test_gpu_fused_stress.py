@@ -1,0 +1,127 @@
+"""GPU stress of the single-pass round-and-log kernel (rl_fused_kernel):
+super-tile / tile boundaries, dense logs (the staged-row overflow paths),
+repeated calls on one workspace (epoch + ticket reset), and two streams
+running the kernel concurrently (ticketed super-tiles must not deadlock or
+mix when the grids are not co-resident).  Everything is checked against the
+oracle (vtrain fpround.direction_array / rnd_array restated) bit for bit."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+SUPER = 8192  # elements per look-back super-tile
+TILE = 2048
+
+
+def _check(oracle, x, tau, base, y, log):
+    codes = oracle.direction_array(x, 32, tau)
+    want = oracle.sparse_from_codes(codes, base=base)
+    assert log.count == want.size
+    assert np.array_equal(log.words[: log.count].cpu().numpy().view(np.uint64), want)
+    assert np.array_equal(bits(y.cpu().numpy()), bits(oracle.rnd_array(x, 32).astype(np.float32)))
+
+
+@pytest.mark.parametrize("n", [TILE - 1, TILE, TILE + 1, SUPER - 1, SUPER, SUPER + 1, 3 * SUPER + 5,
+                               444 * SUPER - 1, 450 * SUPER + TILE + 17])
+def test_super_tile_boundaries(oracle, n):
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    x = workloads.config0_x(n, seed=n % 1000)
+    tau = workloads.TAU_CONFIG0
+    y, log = ops.round_and_log(torch.from_numpy(x).cuda(), 32, tau, global_base=3 * n + 1)
+    _check(oracle, x, tau, 3 * n + 1, y, log)
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.3, 0.2, 0.15])
+def test_dense_logs(oracle, frac):
+    """Logged fractions whose 256-element warp-tiles overflow the 64-entry
+    staged rows (frac >= 0.3) or need their second half (0.15-0.2)."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    n = 37 * SUPER + 1234
+    x = np.random.default_rng(11).normal(0.0, 3.0, n)
+    # p ~ U[0, 2^-24] for N(0, s) data: logged iff p > tau
+    tau = 0.0 if frac == 1.0 else (1.0 - frac) * 2.0 ** -24
+    y, log = ops.round_and_log(torch.from_numpy(x).cuda(), 32, tau, global_base=5)
+    _check(oracle, x, tau, 5, y, log)
+    assert abs(log.count / n - frac) < 0.02
+
+
+def test_dense_general_grid(oracle):
+    """b_r < 32 (non-fast path) with a dense log."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    n = 9 * SUPER + 77
+    x = np.random.default_rng(12).normal(0.0, 1.0, n)
+    y, log = ops.round_and_log(torch.from_numpy(x).cuda(), 26, 0.0, out_dtype=torch.float64)
+    codes = oracle.direction_array(x, 26, 0.0)
+    assert np.array_equal(log.words[: log.count].cpu().numpy().view(np.uint64), oracle.sparse_from_codes(codes))
+    assert np.array_equal(bits(y.cpu().numpy()), bits(oracle.rnd_array(x, 26)))
+
+
+def test_repeated_calls_one_workspace(oracle):
+    """Epoch-tagged status words and the ticket counter survive many calls of
+    varying size on the same workspace."""
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    tau = workloads.TAU_CONFIG0
+    sizes = [SUPER * 600 + 3, 5000, SUPER * 17, 1, SUPER * 600 + 3, 123457]
+    xs = [workloads.config0_x(n, seed=i) for i, n in enumerate(sizes)]
+    want = [oracle.sparse_from_codes(oracle.direction_array(x, 32, tau)) for x in xs]
+    xd = [torch.from_numpy(x).cuda() for x in xs]
+    for rep in range(40):
+        i = rep % len(sizes)
+        _, log = ops.round_and_log(xd[i], 32, tau)
+        assert log.count == want[i].size, (rep, i)
+        if rep % 7 == 0 or sizes[i] < 10000:
+            assert np.array_equal(log.words[: log.count].cpu().numpy().view(np.uint64), want[i])
+        else:
+            w = log.words[: log.count]
+            assert int(w[0]) == int(want[i][0]) and int(w[-1]) == int(want[i][-1])
+            assert bool((w[1:] > w[:-1]).all())
+
+
+@pytest.mark.timeout(300)
+def test_two_streams_concurrent():
+    """Two grids of resident size on two streams at once: CTAs of one grid may
+    wait for SMs held by the other, so super-tiles are handed out by ticket
+    and a CTA only ever waits on lower tickets.  Results must equal the
+    sequential ones."""
+    import torch
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, ops, workloads
+    tau = workloads.TAU_CONFIG0
+    n = 1 << 24
+    xs = [workloads.config0_x_torch(n, s) for s in (21, 22)]
+    ref = []
+    for x in xs:
+        y, log = ops.round_and_log(x, 32, tau)
+        ref.append((y.clone(), log.words[: log.count].clone()))
+    lib = _lib.lib()
+    streams = [torch.cuda.Stream() for _ in xs]
+    wss = [torch.zeros(int(lib.vt_round_log_workspace(n)), dtype=torch.uint8, device="cuda") for _ in xs]
+    ys = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in xs]
+    words = [torch.empty(n // 4, dtype=torch.int64, device="cuda") for _ in xs]
+    flags = [D.Flags() for _ in xs]
+    torch.cuda.synchronize()
+    for rep in range(25):
+        for fl in flags:
+            fl.buf.zero_()
+        torch.cuda.synchronize()
+        for i, x in enumerate(xs):
+            with torch.cuda.stream(streams[i]):
+                _lib.call("vt_round_log", D.ptr(x), n, 32, float(tau), _lib.OUT_F32, D.ptr(ys[i]),
+                          D.ptr(words[i]), words[i].numel(), 0, None, None, None, None, 0, None,
+                          flags[i].cnt_ptr, flags[i].err_ptr, D.ptr(wss[i]), wss[i].numel(),
+                          streams[i].cuda_stream)
+        torch.cuda.synchronize()
+        for i in range(len(xs)):
+            err, cnt = flags[i].read()
+            assert err == 0 and cnt[0] == ref[i][1].numel(), (rep, i, cnt[0])
+            assert torch.equal(words[i][: cnt[0]], ref[i][1])
+            assert torch.equal(ys[i].view(torch.int32), ref[i][0].view(torch.int32))

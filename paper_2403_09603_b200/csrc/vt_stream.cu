@@ -189,6 +189,24 @@ __device__ __forceinline__ uint64_t lb_word(uint32_t epoch, uint64_t flag, uint6
 // resets the ticket counter and bumps the epoch for the next call.
 // ---------------------------------------------------------------------------
 
+#ifdef VT_TIMELINE  // development builds only (tools/timeline.py): per-CTA globaltimer stamps
+__device__ uint64_t g_tl[1024][64];
+__device__ __forceinline__ void tl_mark(int i) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (i < 64) g_tl[blockIdx.x & 1023][i] = t;
+}
+__device__ __forceinline__ void tl_put(int i, uint64_t v) { g_tl[blockIdx.x & 1023][i] = v; }
+extern "C" int vt_debug_timeline(uint64_t* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_tl, sizeof(g_tl));
+}
+#define TL(i) tl_mark(i)
+#define TLV(i, v) tl_put(i, v)
+#else
+#define TL(i)
+#define TLV(i, v)
+#endif
+
 constexpr int kSuper = 4;                        // tiles per super-tile / status word
 constexpr int kMaskSlots = 3;                    // super-tiles of masks in flight
 constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
@@ -228,7 +246,8 @@ struct RLFArgs {
   int thr32;
   void* out;
   int64_t num_tiles;
-  int64_t num_super;
+  int64_t num_super;  // tickets: n4 super-tiles of kSuper tiles, then one per remaining tile
+  int64_t n4;
   FusedHeader* hdr;
   uint64_t* status;  // [num_super] epoch-tagged look-back words
   uint64_t* sparse;
@@ -240,6 +259,13 @@ struct RLFArgs {
   int32_t* err;
   const DevThr* dthr;
 };
+
+// Ticket s -> its first tile and tile count: n4 super-tiles of kSuper tiles,
+// then the remaining (< kSuper) tiles one per ticket.
+__device__ __forceinline__ int64_t st_first(const RLFArgs& a, int64_t s) {
+  return s < a.n4 ? s * kSuper : a.n4 * kSuper + (s - a.n4);
+}
+__device__ __forceinline__ int st_ntiles(const RLFArgs& a, int64_t s) { return s < a.n4 ? kSuper : 1; }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -389,14 +415,16 @@ __device__ __forceinline__ void rlf_write_rows(const RLFArgs& a, FusedSmem& S, i
                                                int lane, uint32_t lt) {
   const int slot = (int)(k % kMaskSlots);
   mbar_wait(S.ofull + slot, (uint32_t)((k / kMaskSlots) & 1));
+  if (warp == 0 && lane == 0 && k + kMaskSlots < 14) TL(5 + 4 * (int)(k + kMaskSlots));
   const int64_t off = S.sbase[slot];
   uint64_t* dst = a.sparse + off;
   const int64_t lim = a.cap - off;  // positions >= lim are beyond the log capacity
-  const uint64_t gw = (uint64_t)(a.global_base + s * (int64_t)(kSuper * kSTile)) << 1;
+  const uint64_t gw = (uint64_t)(a.global_base + st_first(a, s) * kSTile) << 1;
+  const int nt = st_ntiles(a, s);
 #pragma unroll
   for (int i = 0; i < kSuper; ++i) {
     const int q = i * kWarps + warp;
-    if (s * kSuper + i >= a.num_tiles) break;
+    if (i >= nt) break;
     const uint32_t cq = S.cnts[slot][q];
     const uint32_t pq = S.rpos[slot][q];
     if (cq <= (uint32_t)kRow) {
@@ -415,6 +443,12 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
   extern __shared__ __align__(128) uint8_t smraw[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    TL(0);
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TLV(63, smid);
+  }
   const int64_t full_tiles = a.n / kSTile;
   if (tid == 0) {
     for (int s = 0; s < kFStages; ++s) {
@@ -435,26 +469,27 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+      int64_t q = 0;  // ring sequence number
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
         int64_t nxt = -1;
+        const int nt = (s >= 0) ? st_ntiles(a, s) : 1;
+        const int64_t t0 = (s >= 0) ? st_first(a, s) : 0;
 #pragma unroll 1
-        for (int i = 0; i < kSuper; ++i) {
-          const int64_t q = k * kSuper + i;
+        for (int i = 0; i < nt; ++i, ++q) {
           const int st = (int)(q % kFStages);
           mbar_wait(S.empty + st, (uint32_t)(((q / kFStages) & 1) ^ 1));
-          if (i == 0) {
-            S.ids[k & 3] = s;
-            if (s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
-          }
-          const int64_t t = s * kSuper + i;
+          if (i == 0) S.ids[k & 3] = s;
+          // draw the next ticket with this ordinal's last tile: late enough that
+          // the grid runs dry together, early enough to hide the atomic
+          if (i == nt - 1 && s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+          const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
             fence_proxy_async();
             tma_load(S.ring[st], a.x + t * kSTile, kSTile * sizeof(double), S.full + st, pol);
           } else {
             mbar_arrive(S.full + st);
           }
-          if (s < 0) break;
         }
         if (s < 0) break;
         s = nxt;
@@ -470,7 +505,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       const int64_t s = S.slot_id[slot];
       if (s < 0) break;
       // lane = warp-tile (tile-major): exclusive position of each row inside the super-tile
-      const uint32_t c = (s * kSuper + lane / kWarps < a.num_tiles) ? S.cnts[slot][lane] : 0u;
+      const uint32_t c = (lane / kWarps < st_ntiles(a, s)) ? S.cnts[slot][lane] : 0u;
       uint32_t inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -504,23 +539,32 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
     const uint32_t epoch = S.epoch;
     int64_t h1 = -1, h2 = -1, h3 = -1;  // super-tiles of ordinals k-1, k-2, k-3
+    int64_t q = 0;                      // ring sequence number
     for (int64_t k = 0;; ++k) {
       // this warp's rows of ordinal k - 3 leave slot k % kMaskSlots before it is reused
+      if (warp == 0 && lane == 0 && k < 14) TL(4 + 4 * (int)k);
       if (k >= kMaskSlots) rlf_write_rows(a, S, k - kMaskSlots, h3, warp, lane, lt);
+      if (warp == 0 && lane == 0 && k < 14) TL(6 + 4 * (int)k);
       const int slot = (int)(k % kMaskSlots);
-      int64_t s = -1;
+      int64_t s = -1, t0 = 0;
+      int nt = 1;
       uint32_t wcnt = 0;
 #pragma unroll 1
-      for (int i = 0; i < kSuper; ++i) {
-        const int64_t q = k * kSuper + i;
+      for (int i = 0; i < nt; ++i, ++q) {
         const int st = (int)(q % kFStages);
         mbar_wait(S.full + st, (uint32_t)((q / kFStages) & 1));
+        if (q == 0 && warp == 0 && lane == 0) TL(1);
         if (i == 0) {
           s = S.ids[k & 3];
-          if (s < 0) break;
+          if (s < 0) {
+            ++q;
+            break;
+          }
+          nt = st_ntiles(a, s);
+          t0 = st_first(a, s);
         }
-        const int64_t t = s * kSuper + i;
-        if (t < a.num_tiles) {
+        const int64_t t = t0 + i;
+        {
           const int64_t tbase = t * kSTile;
           void* o = tile_out<OUT>(a.out, tbase);
           uint16_t* row = S.rows[slot][i * kWarps + warp];
@@ -549,9 +593,18 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(S.mfull + slot);
+      if (warp == 0 && lane == 0 && k < 14) TL(7 + 4 * (int)k);
+      if (warp == 0 && lane == 0 && s >= 0) {
+        TL(58);
+        TLV(56, (uint64_t)k + 1);
+        TLV(55, (uint64_t)s);
+      }
+      if (warp == 0 && lane == 0 && s < 0) TL(60);
       if (s < 0) {  // drain ordinals k - 2, k - 1
         if (k >= 2) rlf_write_rows(a, S, k - 2, h2, warp, lane, lt);
+        if (warp == 0 && lane == 0) TL(61);
         if (k >= 1) rlf_write_rows(a, S, k - 1, h1, warp, lane, lt);
+        if (warp == 0 && lane == 0) TL(62);
         break;
       }
       h3 = h2;
@@ -561,8 +614,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     report_err(a.err, err);
   }
 
+  if (tid == 0) TL(2);
   __syncthreads();
   if (tid == 0) {
+    TL(3);
     __threadfence();
     const uint32_t prev = atomicAdd(&a.hdr->done, 1u);
     if (prev == gridDim.x - 1) {  // every CTA has drawn its last ticket and read the epoch
@@ -759,11 +814,8 @@ __global__ void __launch_bounds__(kSThreads, 3) rp_fused_kernel(const RPArgs a) 
 
 int64_t stream_tiles(int64_t n) { return (n + kSTile - 1) / kSTile; }
 
-// [header 64 B][status: scan CTAs x 8][counts: T x 4][toffs: T x 8][scratch: T x kSTile x 2]
-static int64_t super_tiles(int64_t n) { return (stream_tiles(n) + kSuper - 1) / kSuper; }
-
-// fused: [header 64 B][status: super-tiles x 8]
-static size_t rl_fused_workspace(int64_t n) { return (size_t)(64 + super_tiles(n) * 8 + 256); }
+// fused: [header 64 B][status: one word per ticket (at most one per tile)]
+static size_t rl_fused_workspace(int64_t n) { return (size_t)(64 + stream_tiles(n) * 8 + 256); }
 
 size_t rl_stream_workspace(int64_t n) { return rl_fused_workspace(n); }
 
@@ -781,7 +833,7 @@ static int resident_ctas(const void* fn, size_t smem) {
 }
 
 template <int OUT, bool FAST>
-static int launch_rlf(const RLFArgs& a, cudaStream_t st) {
+static int launch_rlf(RLFArgs a, cudaStream_t st) {
   const size_t smem = sizeof(FusedSmem);
   static_assert(sizeof(FusedSmem) <= 74 * 1024, "three fused CTAs per SM");
   auto k = rl_fused_kernel<OUT, FAST>;
@@ -794,6 +846,8 @@ static int launch_rlf(const RLFArgs& a, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kFThreads, smem);
     resident = std::max(1, per * sms);
   }
+  a.n4 = a.num_tiles / kSuper;
+  a.num_super = a.n4 + a.num_tiles % kSuper;
   const int grid = (int)std::min<int64_t>(a.num_super, resident);
   k<<<grid, kFThreads, smem, st>>>(a);
   return vt_check_launch("rl_fused_kernel");
@@ -803,7 +857,7 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr) {
   uint8_t* w = static_cast<uint8_t*>(ws);
-  RLFArgs f{x, n, g, thr32, out, stream_tiles(n), super_tiles(n), reinterpret_cast<FusedHeader*>(w),
+  RLFArgs f{x, n, g, thr32, out, stream_tiles(n), 0, 0, reinterpret_cast<FusedHeader*>(w),
             reinterpret_cast<uint64_t*>(w + 64), sparse, cap, global_base, cursor_in, cursor_out, counters, err,
             dthr};
   if (fast) {

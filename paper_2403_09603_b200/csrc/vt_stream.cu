@@ -24,10 +24,8 @@ namespace vt {
 
 constexpr int kSThreads = 256;
 constexpr int kSTile = 2048;  // elements per tile (16 KiB of FP64)
-constexpr int kStages = 4;
 constexpr int kSWarpElems = kSTile / kWarps;  // 256
 constexpr int kSSlots = kSWarpElems / 64;     // 4 slots x 32 lanes x 2 elements
-constexpr size_t kRingBytes = (size_t)kStages * kSTile * sizeof(double);
 
 // ---------------------------------------------------------------------------
 // TMA bulk copy + mbarrier helpers
@@ -75,31 +73,6 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
-}
-
-// Stage the tile's FP64 input in ring slot `s`: full tiles by TMA (issued
-// ahead of time), the partial last tile by plain loads here.
-struct Ring {
-  double* xs;
-  uint64_t* bars;
-};
-
-__device__ __forceinline__ const double* acquire_tile(const Ring& r, const double* x, int64_t n, int64_t t,
-                                                      int64_t full_tiles, int s, uint32_t phase) {
-  double* dst = r.xs + (size_t)s * kSTile;
-  if (t < full_tiles) {
-    mbar_wait(r.bars + s, phase);
-  } else {
-    const int64_t base = t * kSTile;
-    for (int e = threadIdx.x; e < kSTile; e += kSThreads) dst[e] = (base + e < n) ? x[base + e] : 0.0;
-    __syncthreads();
-  }
-  return dst;
-}
-
-__device__ __forceinline__ void issue_tile(const Ring& r, const double* x, int64_t t, int64_t full_tiles, int s,
-                                           uint64_t pol) {
-  if (t < full_tiles) tma_load(r.xs + (size_t)s * kSTile, x + t * kSTile, kSTile * sizeof(double), r.bars + s, pol);
 }
 
 // Output stores relative to the tile: `o` points at the tile's first output
@@ -182,7 +155,7 @@ __device__ __forceinline__ uint64_t lb_word(uint32_t epoch, uint64_t flag, uint6
 //   warp 9      producer: grabs super-tile tickets (atomic counter: a CTA
 //               only ever waits on lower tickets, which running CTAs hold, so
 //               the kernel cannot deadlock even when not all CTAs are
-//               resident) and keeps kStages TMA bulk copies in flight.
+//               resident) and keeps kFStages TMA bulk copies in flight.
 //
 // Compute warps never wait on another CTA: the look-back latency is absorbed
 // by kMaskSlots super-tiles of mask slack.  The CTA that finishes last
@@ -642,14 +615,44 @@ struct RPArgs {
   int64_t log_base;
   void* out;
   int64_t num_tiles;
-  int64_t tiles_per_cta;
+  int64_t num_super;  // tickets, as for the trainer: n4 chunks of kSuper tiles, then single tiles
+  int64_t n4;
+  FusedHeader* hdr;   // ticket + done counters
   int64_t* counters;
   int32_t* err;
 };
 
-// lower_bound over the sorted word indices by one warp, 32 probes per step
-__device__ int64_t warp_lower_bound(const uint64_t* w, int64_t n, int64_t key, int lane) {
-  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+constexpr int kRStages = 4;
+constexpr int kRThreads = kSThreads + 64;  // 8 compute warps + producer warp + log-search warp
+constexpr int kRIds = 8;                   // ordinals in flight between the three roles
+
+struct ReplaySmem {
+  double ring[kRStages][kSTile];
+  uint8_t cmap[kSTile];             // code map of the current tile, all 1 between tiles
+  int64_t ids[kRIds], curs[kRIds];  // ticket (producer) and first log word (search warp) of ordinal k
+  uint64_t full[kRStages], empty[kRStages], tfull[kRIds], nfull[kRIds];
+  uint32_t red[kWarps];
+};
+
+__device__ __forceinline__ int64_t rp_first(const RPArgs& a, int64_t s) {
+  return s < a.n4 ? s * kSuper : a.n4 * kSuper + (s - a.n4);
+}
+__device__ __forceinline__ int rp_ntiles(const RPArgs& a, int64_t s) { return s < a.n4 ? kSuper : 1; }
+
+// named barrier over the 256 compute threads (barrier 0 is the whole CTA)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ int compute_sync_count(bool p) {
+  int r;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tbar.red.popc.u32 %0, 1, 256, q;\n}"
+               : "=r"(r)
+               : "r"((uint32_t)p)
+               : "memory");
+  return r;
+}
+
+// lower_bound over the sorted word indices by one warp, 32 probes per step;
+// the answer is known to lie in [lo, hi]
+__device__ int64_t warp_lower_bound(const uint64_t* w, int64_t lo, int64_t hi, int64_t key, int lane) {
   while (hi - lo > 32) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t p = lo + lane * step;
@@ -663,6 +666,27 @@ __device__ int64_t warp_lower_bound(const uint64_t* w, int64_t n, int64_t key, i
   const int64_t p = lo + lane;
   const bool lt = (p < hi) && ((int64_t)(__ldg(w + p) >> 1) < key);
   return lo + __popc(__ballot_sync(0xffffffffu, lt));
+}
+
+// First log word with index >= key.  Entries are spread over the tensor's
+// index range: for uniformly scattered entries the word count below key is
+// binomial around the interpolated position, with sd <= sqrt(nw) / 2, so 32
+// probes spaced sqrt(nw) / 8 (+-4 sd) usually bracket the answer; otherwise
+// (skewed logs) the bracket is one side of the probes.  Then the 32-ary search.
+__device__ int64_t log_lower_bound(const RPArgs& a, int64_t key, int lane) {
+  const int64_t nw = a.n_words;
+  if (nw == 0) return 0;
+  const int64_t d = std::max<int64_t>(64, (int64_t)(sqrt((double)nw) * 0.125));
+  const int64_t g = (int64_t)((double)(key - a.log_base) / (double)a.n * (double)nw);
+  const int64_t p = g + (int64_t)(lane - 16) * d;
+  const bool lt = (p < 0) || (p < nw && (int64_t)(__ldg(a.log + p) >> 1) < key);
+  const int c = __popc(__ballot_sync(0xffffffffu, lt));
+  const int64_t p0 = g - 16 * d;
+  int64_t lo = (c == 0) ? 0 : p0 + (int64_t)(c - 1) * d + 1;
+  int64_t hi = (c == 32) ? nw : p0 + (int64_t)c * d;
+  lo = std::max<int64_t>(lo, 0);
+  hi = std::min<int64_t>(std::max<int64_t>(hi, lo), nw);
+  return warp_lower_bound(a.log, lo, hi, key, lane);
 }
 
 // One tile of the auditor pass.  Each thread reads the codes of its own
@@ -708,7 +732,7 @@ __device__ __forceinline__ int scatter_window(uint8_t* cs, uint64_t w, uint64_t 
   const bool have = i < n_words;
   const int64_t idx = (int64_t)(w >> 1);
   const bool in = have && idx < key1;
-  const int cnt = __syncthreads_count(in);
+  const int cnt = compute_sync_count(in);
   if (in) {
     const bool ordered = (i == 0) || ((prev >> 1) < (w >> 1));
     if (idx >= key0 && ordered && (int)threadIdx.x < cnt) cs[idx - key0] = (w & 1ull) ? 2 : 0;
@@ -717,94 +741,174 @@ __device__ __forceinline__ int scatter_window(uint8_t* cs, uint64_t w, uint64_t 
   return cnt;
 }
 
+// Auditor kernel, warp-specialised like the trainer's: the producer warp
+// draws tickets (super-tiles of kSuper tiles) and keeps kRStages TMA copies in
+// flight; the search warp finds each ordinal's first log word
+// (log_lower_bound) as soon as its ticket is known and publishes it (nfull);
+// the compute warps scatter each tile's log slice into the code map and
+// replay the tile, prefetching the next tile's window of log words while the
+// current one computes (across ordinals too, through nfull).
 template <int OUT, bool FAST>
-__global__ void __launch_bounds__(kSThreads, 3) rp_fused_kernel(const RPArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ uint32_t s_red[kWarps];
-  __shared__ int64_t s_lo;
-  Ring ring{reinterpret_cast<double*>(sm), bars};
-  uint8_t* cs = sm + kRingBytes;  // [kSTile] code map, all 1 between tiles
-
+__global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  ReplaySmem& S = *reinterpret_cast<ReplaySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t T0 = (int64_t)blockIdx.x * a.tiles_per_cta;
-  const int64_t T1 = std::min<int64_t>(T0 + a.tiles_per_cta, a.num_tiles);
   const int64_t full_tiles = a.n / kSTile;
-  const uint64_t pol = evict_first_policy();
+  if (tid == 0) TL(0);
+  if (tid < kSThreads) reinterpret_cast<uint2*>(S.cmap)[tid] = make_uint2(0x01010101u, 0x01010101u);
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    for (int st = 0; st < kRStages; ++st) {
+      mbar_init(S.full + st, 1);
+      mbar_init(S.empty + st, 1);
+    }
+    for (int m = 0; m < kRIds; ++m) {
+      mbar_init(S.tfull + m, 1);
+      mbar_init(S.nfull + m, 1);
+    }
     fence_mbar_init();
   }
-  reinterpret_cast<uint2*>(cs)[tid] = make_uint2(0x01010101u, 0x01010101u);
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < kStages && T0 + s < T1; ++s) issue_tile(ring, a.x, T0 + s, full_tiles, s, pol);
-  if (warp == 0) {
-    const int64_t lo = warp_lower_bound(a.log, a.n_words, a.log_base + T0 * kSTile, lane);
-    if (lane == 0) s_lo = lo;
-  }
-  __syncthreads();
-  int64_t cur = s_lo;  // first log word of the current tile (block-uniform)
-  if (blockIdx.x == 0 && tid == 0) a.counters[1] = cur;
-  uint64_t pw = 0, pp = 0;
-  {
-    const int64_t i = cur + tid;
-    if (i < a.n_words) {
-      pw = __ldg(a.log + i);
-      pp = i ? __ldg(a.log + i - 1) : 0ull;
-    }
-  }
 
-  uint32_t err = 0, flips = 0;
-  for (int64_t t = T0; t < T1; ++t) {
-    const int64_t k = t - T0;
-    const int s = (int)(k % kStages);
-    const int64_t tbase = t * kSTile;
-    const int64_t key0 = a.log_base + tbase;
-    const int64_t key1 = a.log_base + std::min<int64_t>(tbase + kSTile, a.n);
-    int cnt = scatter_window(cs, pw, pp, cur + tid, a.n_words, key0, key1, err);
-    cur += cnt;
-    while (cnt == kSThreads) {  // more than one window of entries in this tile
-      const int64_t i = cur + tid;
-      uint64_t w = 0, p = 0;
-      if (i < a.n_words) {
-        w = __ldg(a.log + i);
-        p = __ldg(a.log + i - 1);
+  if (warp == kWarps) {  // producer: tickets and TMA
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+      int64_t q = 0;
+      for (int64_t k = 0;; ++k) {
+        if (s >= a.num_super) s = -1;
+        S.ids[k % kRIds] = s;
+        mbar_arrive(S.tfull + (k % kRIds));
+        const int nt = (s >= 0) ? rp_ntiles(a, s) : 1;
+        const int64_t t0 = (s >= 0) ? rp_first(a, s) : 0;
+        int64_t nxt = -1;
+#pragma unroll 1
+        for (int i = 0; i < nt; ++i, ++q) {
+          const int st = (int)(q % kRStages);
+          mbar_wait(S.empty + st, (uint32_t)(((q / kRStages) & 1) ^ 1));
+          if (i == nt - 1 && s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+          const int64_t t = t0 + i;
+          if (s >= 0 && t < full_tiles) {
+            fence_proxy_async();
+            tma_load(S.ring[st], a.x + t * kSTile, kSTile * sizeof(double), S.full + st, pol);
+          } else {
+            mbar_arrive(S.full + st);
+          }
+        }
+        if (s < 0) break;
+        s = nxt;
       }
-      cnt = scatter_window(cs, w, p, i, a.n_words, key0, key1, err);
-      cur += cnt;
     }
-    {  // prefetch the next tile's window while this tile computes
-      const int64_t i = cur + tid;
-      pw = pp = 0;
-      if (i < a.n_words) {
-        pw = __ldg(a.log + i);
-        pp = i ? __ldg(a.log + i - 1) : 0ull;
+    __syncwarp();
+  } else if (warp == kWarps + 1) {  // log search: each ordinal's first log word, ahead of the compute warps
+    for (int64_t k = 0;; ++k) {
+      const int m = (int)(k % kRIds);
+      mbar_wait(S.tfull + m, (uint32_t)((k / kRIds) & 1));
+      const int64_t s = S.ids[m];
+      const int64_t cur = (s >= 0) ? log_lower_bound(a, a.log_base + rp_first(a, s) * kSTile, lane) : 0;
+      if (lane == 0) {
+        S.curs[m] = cur;
+        mbar_arrive(S.nfull + m);
+      }
+      if (s < 0) break;
+    }
+  } else {  // compute warps
+    uint32_t err = 0, flips = 0;
+    int64_t q = 0;
+    uint64_t pw = 0, pp = 0;  // prefetched window for the next tile (word at cur + tid, its predecessor)
+    bool pref = false;
+    int64_t cur = 0;
+    for (int64_t k = 0;; ++k) {
+      mbar_wait(S.nfull + (k % kRIds), (uint32_t)((k / kRIds) & 1));
+      const int64_t s = S.ids[k % kRIds];
+      if (s < 0) break;
+      const int nt = rp_ntiles(a, s);
+      const int64_t t0 = rp_first(a, s);
+      if (!pref) {
+        cur = S.curs[k % kRIds];
+        const int64_t i = cur + tid;
+        pw = pp = 0;
+        if (i < a.n_words) {
+          pw = __ldg(a.log + i);
+          pp = i ? __ldg(a.log + i - 1) : 0ull;
+        }
+      }
+      if (s == 0 && tid == 0) a.counters[1] = cur;
+#pragma unroll 1
+      for (int i = 0; i < nt; ++i, ++q) {
+        const int64_t t = t0 + i;
+        const int64_t tbase = t * kSTile;
+        const int64_t key0 = a.log_base + tbase;
+        const int64_t key1 = a.log_base + std::min<int64_t>(tbase + kSTile, a.n);
+        int cnt = scatter_window(S.cmap, pw, pp, cur + tid, a.n_words, key0, key1, err);
+        cur += cnt;
+        while (cnt == kSThreads) {  // more than one window of entries in this tile
+          const int64_t j = cur + tid;
+          uint64_t w = 0, p = 0;
+          if (j < a.n_words) {
+            w = __ldg(a.log + j);
+            p = __ldg(a.log + j - 1);
+          }
+          cnt = scatter_window(S.cmap, w, p, j, a.n_words, key0, key1, err);
+          cur += cnt;
+        }
+        // prefetch the next tile's window while this tile computes
+        pref = true;
+        int64_t ncur = cur;
+        if (i == nt - 1) {  // next ordinal: its first word comes from the producer's search
+          mbar_wait(S.nfull + ((k + 1) % kRIds), (uint32_t)(((k + 1) / kRIds) & 1));
+          if (S.ids[(k + 1) % kRIds] >= 0) ncur = S.curs[(k + 1) % kRIds];
+          if (s == a.num_super - 1 && tid == 0) a.counters[2] = cur;
+        }
+        {
+          const int64_t j = ncur + tid;
+          pw = pp = 0;
+          if (j < a.n_words) {
+            pw = __ldg(a.log + j);
+            pp = j ? __ldg(a.log + j - 1) : 0ull;
+          }
+        }
+        const int st = (int)(q % kRStages);
+        const double* src = S.ring[st];
+        if (t < full_tiles) {
+          mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1));
+        } else {  // partial last tile: plain loads into the (unused) ring slot
+          mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1));
+          double* dst = S.ring[st];
+          for (int e = tid; e < kSTile; e += kSThreads) dst[e] = (tbase + e < a.n) ? a.x[tbase + e] : 0.0;
+        }
+        if (tid == 0 && q == 0) TL(1);
+        compute_sync();  // code map complete, x tile resident
+        void* o = tile_out<OUT>(a.out, tbase);
+        flips += (t < full_tiles) ? rp_tile<OUT, FAST, true>(a, src, S.cmap, o, kSTile, warp, lane, err)
+                                  : rp_tile<OUT, FAST, false>(a, src, S.cmap, o, (int)(a.n - tbase), warp, lane, err);
+        compute_sync();  // ring slot consumed, code map reset
+        if (tid == 0) mbar_arrive(S.empty + (int)(q % kRStages));
+        cur = ncur;
       }
     }
-    const double* src = acquire_tile(ring, a.x, a.n, t, full_tiles, s, (uint32_t)((k / kStages) & 1));
-    __syncthreads();  // code map complete, x tile resident
-    void* o = tile_out<OUT>(a.out, tbase);
-    flips += (t < full_tiles) ? rp_tile<OUT, FAST, true>(a, src, cs, o, kSTile, warp, lane, err)
-                              : rp_tile<OUT, FAST, false>(a, src, cs, o, (int)(a.n - tbase), warp, lane, err);
-    __syncthreads();  // ring slot s consumed, code map reset
-    if (tid == 0 && t + kStages < T1) {
-      fence_proxy_async();
-      issue_tile(ring, a.x, t + kStages, full_tiles, s, pol);
+    report_err(a.err, err);
+    uint32_t v = flips;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) S.red[warp] = v;
+    compute_sync();
+    if (tid == 0) {
+      uint32_t tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) tot += S.red[w];
+      if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)tot);
     }
   }
-  if (blockIdx.x == gridDim.x - 1 && tid == 0) a.counters[2] = cur;
-  report_err(a.err, err);
-  uint32_t v = flips;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) s_red[warp] = v;
   __syncthreads();
   if (tid == 0) {
-    uint32_t tot = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) tot += s_red[w];
-    if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)tot);
+    TL(3);
+    __threadfence();
+    const uint32_t prev = atomicAdd(&a.hdr->done, 1u);
+    if (prev == gridDim.x - 1) {  // every CTA has drawn its last ticket
+      a.hdr->ticket = 0u;
+      a.hdr->done = 0u;
+      __threadfence();
+    }
   }
 }
 
@@ -821,15 +925,7 @@ size_t rl_stream_workspace(int64_t n) { return rl_fused_workspace(n); }
 
 size_t rp_stream_workspace(int64_t n) {
   (void)n;
-  return 0;
-}
-
-static int resident_ctas(const void* fn, size_t smem) {
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSThreads, smem);
-  return std::max(1, per * sms);
+  return 64;  // ticket header
 }
 
 template <int OUT, bool FAST>
@@ -870,31 +966,31 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
                                 : launch_rlf<VT_OUT_NONE, false>(f, st);
 }
 
-template <typename Args>
-static void split_tiles(Args& a, int resident) {
-  const int64_t grid = std::min<int64_t>(a.num_tiles, resident);
-  a.tiles_per_cta = (a.num_tiles + grid - 1) / grid;
-}
-
 template <int OUT, bool FAST>
 static int launch_rp(RPArgs a, cudaStream_t st) {
-  const size_t smem = kRingBytes + kSTile;
+  const size_t smem = sizeof(ReplaySmem);
+  static_assert(sizeof(ReplaySmem) <= 74 * 1024, "three replay CTAs per SM");
   auto k = rp_fused_kernel<OUT, FAST>;
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    resident = resident_ctas((const void*)k, smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRThreads, smem);
+    resident = std::max(1, per * sms);
   }
-  split_tiles(a, resident);
-  const int grid = (int)((a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta);
-  k<<<grid, kSThreads, smem, st>>>(a);
+  a.n4 = a.num_tiles / kSuper;
+  a.num_super = a.n4 + a.num_tiles % kSuper;
+  const int grid = (int)std::min<int64_t>(a.num_super, resident);
+  k<<<grid, kRThreads, smem, st>>>(a);
   return vt_check_launch("rp_fused_kernel");
 }
 
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st) {
-  (void)ws;
-  RPArgs a{x, n, g, log, n_words, log_base, out, stream_tiles(n), 1, counters, err};
+  RPArgs a{x, n, g, log, n_words, log_base, out, stream_tiles(n), 0, 0, static_cast<FusedHeader*>(ws), counters,
+           err};
   if (fast) {
     return out_kind == VT_OUT_F32 ? launch_rp<VT_OUT_F32, true>(a, st)
          : out_kind == VT_OUT_F64 ? launch_rp<VT_OUT_F64, true>(a, st)

@@ -107,6 +107,9 @@ size_t vt_replay_workspace(int64_t n);
  * log_kind PACKED: log = payload bytes, log_base = stream position of x[0],
  *   log_len = payload byte count (bounds).
  * counters[0] = corrections (elements whose output differs from rnd(x)).
+ * Workspace (>= vt_replay_workspace(n) bytes, SPARSE only) must be zero-filled
+ * before its first use and then belong to this entry point on one stream: it
+ * holds the ticket counter of the persistent kernel.
  */
 int vt_replay(const double *x, int64_t n, int b_r, int log_kind, const void *log,
               int64_t log_len, int64_t log_base, int out_kind, void *out, int64_t *counters,

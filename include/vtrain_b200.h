@@ -34,6 +34,8 @@
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
  *   vt_merkle_build   <- merkle.build over chunked leaves    merkle.py:55-72
+ *   vt_serialize_f32  <- the FP32 serialization + finiteness check of
+ *                        merkle.hash_weights                 merkle.py:155-166
  */
 #ifndef VTRAIN_B200_H
 #define VTRAIN_B200_H
@@ -190,6 +192,15 @@ int64_t vt_merkle_node_count(int64_t n_leaves);
  */
 int vt_merkle_build(const uint8_t *data, int64_t nbytes, int64_t leaf_bytes, uint8_t *nodes,
                     int64_t nodes_cap, vt_stream_t stream);
+/*
+ * Canonical checkpoint bytes: out[n] = (float)x[n] (RNE, overflow -> +-inf,
+ * little-endian), *first_bad = min(*first_bad, index_base + first index i of
+ * a non-finite x[i]).  The caller initialises *first_bad (e.g. to INT64_MAX)
+ * and passes the chunk's offset in the tensor as index_base.
+ * x 32-byte aligned, out 16-byte aligned.
+ */
+int vt_serialize_f32(const double *x, int64_t n, float *out, int64_t index_base, int64_t *first_bad,
+                     vt_stream_t stream);
 /* measurement support: blocks x 128 threads x reps compressions of
  * register-resident messages (compute-only SHA-256 ceiling of this chip) */
 int vt_sha256_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t stream);

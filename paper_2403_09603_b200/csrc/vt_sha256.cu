@@ -335,3 +335,54 @@ extern "C" int vt_sha256_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt
   vt::sha256_peak_kernel<<<(unsigned)blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps);
   return vt_check_launch("sha256_peak_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Canonical checkpoint serialization (merkle.hash_weights, merkle.py:155-166):
+// FP64 -> FP32 round-to-nearest-even, little-endian (the device's own byte
+// order), overflow to +-inf exactly like numpy's astype('<f4'); the first
+// non-finite FP64 element is reported (the reference checks finiteness on
+// the FP64 values before casting).  Streaming: 256-bit loads, 128-bit stores.
+// ---------------------------------------------------------------------------
+namespace vt {
+__global__ void __launch_bounds__(256) serialize_f32_kernel(const double* __restrict__ x, int64_t n,
+                                                            float* __restrict__ out, int64_t index_base,
+                                                            unsigned long long* first_bad) {
+  unsigned long long bad = ~0ull;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 3 < n) {
+      const D4 v = ldg_stream4(x + i);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (!isfinite(v.v[k]) && bad == ~0ull) bad = (unsigned long long)(i + k);
+      *reinterpret_cast<float4*>(out + i) = make_float4(__double2float_rn(v.v[0]), __double2float_rn(v.v[1]),
+                                                        __double2float_rn(v.v[2]), __double2float_rn(v.v[3]));
+    } else {
+      for (int64_t k = i; k < n; ++k) {
+        const double e = x[k];
+        if (!isfinite(e) && bad == ~0ull) bad = (unsigned long long)k;
+        out[k] = __double2float_rn(e);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b < bad ? b : bad;
+  }
+  if ((threadIdx.x & 31) == 0 && bad != ~0ull) atomicMin(first_bad, bad + (unsigned long long)index_base);
+}
+}  // namespace vt
+
+extern "C" int vt_serialize_f32(const double* x, int64_t n, float* out, int64_t index_base, int64_t* first_bad,
+                                vt_stream_t stream) {
+  if (n < 0 || index_base < 0 || !first_bad || (n > 0 && (!x || !out)) || (reinterpret_cast<uintptr_t>(x) & 31) ||
+      (reinterpret_cast<uintptr_t>(out) & 15)) {
+    vt_set_error("vt_serialize_f32: bad argument (x 32-byte, out 16-byte aligned)");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  const int64_t blocks = std::min<int64_t>((n + 1023) / 1024, 148 * 8);
+  vt::serialize_f32_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, n, out, index_base, reinterpret_cast<unsigned long long*>(first_bad));
+  return vt_check_launch("serialize_f32_kernel");
+}

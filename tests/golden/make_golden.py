@@ -224,6 +224,62 @@ def golden_merkle() -> None:
                                                           "hash_weights": hw}))
 
 
+def golden_merkle_game() -> None:
+    """merkle.node / path / verify_path / first_divergence and hash_weights
+    (merkle.py:75-166) on seeded inputs, for the device-level drop-ins."""
+    rng = np.random.default_rng(17)
+    trees = []
+    for n in (1, 2, 3, 5, 8, 13, 40, 257):
+        leaves = [hashlib.sha256(f"t{n}-{i}".encode()).digest() for i in range(n)]
+        t = mk.build(leaves)
+        nodes = []
+        for lv in range(len(t.levels)):
+            for ix in sorted({0, len(t.levels[lv]) - 1, len(t.levels[lv]) // 2}):
+                nodes.append([lv, ix, mk.node(t, lv, ix).hex()])
+        paths = []
+        for li in sorted({0, n - 1, n // 2, (7 * n) // 11}):
+            pth = mk.path(t, li)
+            paths.append({"leaf_index": li, "leaf": pth.leaf.hex(),
+                          "siblings": [[d.hex(), side] for d, side in pth.siblings],
+                          "verifies": mk.verify_path(pth, t.root)})
+        # a second tree diverging at planted leaves: reference first_divergence
+        div = []
+        for planted in sorted({0, n - 1, n // 3}):
+            other = list(leaves)
+            for j in range(planted, n, max(1, n // 4)):
+                other[j] = hashlib.sha256(f"x{n}-{j}".encode()).digest()
+            div.append({"planted": planted, "other": [d.hex() for d in other],
+                        "first": mk.first_divergence(t, mk.build(other))})
+        trees.append({"n": n, "seed_tag": f"t{n}", "nodes": nodes, "paths": paths, "divergence": div})
+    errors = {}
+    t3 = mk.build([hashlib.sha256(b"e%d" % i).digest() for i in range(3)])
+    for name, fn in (("level", lambda: mk.node(t3, 5, 0)), ("index", lambda: mk.node(t3, 1, 2)),
+                     ("path", lambda: mk.path(t3, 3))):
+        try:
+            fn()
+        except IndexError as e:
+            errors[name] = str(e)
+    w1 = rng.normal(0.0, 0.02, size=(37, 41))
+    w2 = rng.normal(0.0, 1.0, size=100_003)
+    w3 = np.array([1e300, -1e300, 3.4028235e38, 1e-45, -0.0, 2.0 ** -149, 2.0 ** -150], dtype=np.float64)
+    hw = {"pair": mk.hash_weights([w1, w2]).hex(), "specials": mk.hash_weights([w3]).hex(),
+          "f32_input": mk.hash_weights([w1.astype(np.float32)]).hex(),
+          "w1_sha": sha(w1.tobytes()), "w2_sha": sha(w2.tobytes())}
+    bad = np.zeros(50, dtype=np.float64)
+    bad[17] = np.inf
+    bad[31] = np.nan
+    try:
+        mk.hash_weights([w1, bad])
+    except ValueError as e:
+        hw["nonfinite_error"] = str(e)
+    try:
+        mk.hash_weights([w1], b_m=16)
+    except ValueError as e:
+        hw["b_m_error"] = str(e)
+    (HERE / "merkle_game_golden.json").write_text(json.dumps({"trees": trees, "errors": errors,
+                                                               "hash_weights": hw}))
+
+
 def golden_configs() -> None:
     """Config 0 / config 1 at 2^20 through the reference functions, as digests."""
     n = 1 << 20
@@ -301,5 +357,6 @@ if __name__ == "__main__":
     golden_roundlog()
     golden_tau()
     golden_merkle()
+    golden_merkle_game()
     golden_configs()
     print("golden fixtures written to", HERE)

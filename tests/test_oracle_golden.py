@@ -157,3 +157,24 @@ def test_config_digests(golden, oracle):
     assert hashlib.sha256(xa.tobytes()).hexdigest() == c1["xa_sha"]
     ya = oracle.rev_array(xa, 32, oracle.direction_array(xt, 32, tau))
     assert hashlib.sha256(ya.astype(np.float32).tobytes()).hexdigest() == c1["auditor_f32_sha"]
+
+
+def test_oracle_hash_weights_game_golden(oracle):
+    """The oracle's hash_weights restatement against the reference's digests
+    (merkle.py:155-166): FP64 pair, FP32 specials / overflow, FP32 input."""
+    import json
+    from conftest import GOLDEN
+    hw = json.loads((GOLDEN / "merkle_game_golden.json").read_text())["hash_weights"]
+    rng = np.random.default_rng(17)
+    w1 = rng.normal(0.0, 0.02, size=(37, 41))
+    w2 = rng.normal(0.0, 1.0, size=100_003)
+    assert oracle.hash_weights([w1, w2]).hex() == hw["pair"]
+    w3 = np.array([1e300, -1e300, 3.4028235e38, 1e-45, -0.0, 2.0 ** -149, 2.0 ** -150], dtype=np.float64)
+    with np.errstate(over="ignore"):
+        assert oracle.hash_weights([w3]).hex() == hw["specials"]
+    assert oracle.hash_weights([w1.astype(np.float32)]).hex() == hw["f32_input"]
+    bad = np.zeros(50, dtype=np.float64)
+    bad[17] = np.inf
+    with pytest.raises(ValueError) as e:
+        oracle.hash_weights([w1, bad])
+    assert str(e.value) == hw["nonfinite_error"]

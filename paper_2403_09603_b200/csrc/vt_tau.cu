@@ -432,7 +432,11 @@ __global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, con
   }
 }
 
-__global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out) {
+__global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out,
+                                uint32_t* hist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kBudMaxLevels * kBudBins; i += gridDim.x * blockDim.x)
+    hist[i] = 0u;
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
   st->lo_key = lo_key;
   st->hi_key = hi_key;
   st->cnt_above = 0;
@@ -486,9 +490,7 @@ extern "C" int vt_tau_budget_key(const double* x, int64_t n, int b_r, int64_t bu
   uint64_t lo_key, hi_key;
   memcpy(&lo_key, &tau_lo, 8);
   memcpy(&hi_key, &tau_hi, 8);
-  if (cudaMemsetAsync(hist, 0, (size_t)kBudMaxLevels * kBudBins * 4, s) != cudaSuccess)
-    return vt_check_launch("memset");
-  bud_init_kernel<<<1, 1, 0, s>>>(st, lo_key, hi_key, key_out);
+  bud_init_kernel<<<(kBudMaxLevels * kBudBins + 255) / 256, 256, 0, s>>>(st, lo_key, hi_key, key_out, hist);
   int rc = vt_check_launch("bud_init_kernel");
   if (rc) return rc;
   const Grid g = make_grid(b_r, 0.0);
@@ -566,7 +568,8 @@ __global__ void straddle_init_kernel(double* out_min, unsigned long long* count)
 
 // The search_tau skeleton (protocol.py:494-506) in budget form, on one
 // thread: identical IEEE FP64 operations to the host loop, so the same tau.
-__global__ void budget_bisect_kernel(const uint64_t* key, double lower, double upper, int iters, DevThr* out) {
+__global__ void budget_bisect_kernel(const uint64_t* key, double lower, double upper, int iters, DevThr* out,
+                                     double* tau_out) {
   const double v = __longlong_as_double((long long)*key);
   for (int i = 0; i < iters; ++i) {
     const double tau = __dmul_rn(__dadd_rn(lower, upper), 0.5);
@@ -574,6 +577,7 @@ __global__ void budget_bisect_kernel(const uint64_t* key, double lower, double u
     else lower = tau;
   }
   *out = thresholds_for(upper);
+  *tau_out = upper;
 }
 }  // namespace vt
 
@@ -620,10 +624,8 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
   int rc = vt_tau_budget_key(x, n, b_r, budget, lo, hi, key, status, err, tws, tws_bytes, stream);
   if (rc) return rc;
-  budget_bisect_kernel<<<1, 1, 0, s>>>(key, lo, hi, iters, dthr);
+  budget_bisect_kernel<<<1, 1, 0, s>>>(key, lo, hi, iters, dthr, tau_out);
   if ((rc = vt_check_launch("budget_bisect_kernel"))) return rc;
-  if (cudaMemcpyAsync(tau_out, &dthr->tau, 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return vt_check_launch("tau copy");
   const Grid g = make_grid(b_r, lo);  // thresholds come from dthr
   const size_t rws_bytes = ws_bytes - (static_cast<uint8_t*>(rws) - w);
   if (rws_bytes < vt_round_log_workspace(n)) {

@@ -329,10 +329,12 @@ __device__ __forceinline__ void report_err(int32_t* err, uint32_t e) {
 // persistent TMA-pipelined kernels of the north-star path (vt_stream.cu)
 size_t rl_stream_workspace(int64_t n);
 size_t rp_stream_workspace(int64_t n);
-// dthr: nullable device thresholds overriding g.thr / g.thr_sub / thr32
+// dthr: nullable device thresholds overriding g.thr / g.thr_sub / thr32;
+// gate: nullable device flag, the kernel does nothing while *gate == 0
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
-              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr);
+              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr,
+              const int32_t* gate = nullptr);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 

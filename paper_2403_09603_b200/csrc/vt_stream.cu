@@ -231,6 +231,7 @@ struct RLFArgs {
   int64_t* counters;
   int32_t* err;
   const DevThr* dthr;
+  const int32_t* gate;  // nullable: the kernel returns at once when *gate == 0
 };
 
 // Ticket s -> its first tile and tile count: n4 super-tiles of kSuper tiles,
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
   extern __shared__ __align__(128) uint8_t smraw[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.gate && *a.gate == 0) return;
   if (tid == 0) {
     TL(0);
     uint32_t smid;
@@ -951,11 +953,12 @@ static int launch_rlf(RLFArgs a, cudaStream_t st) {
 
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
-              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr) {
+              int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr,
+              const int32_t* gate) {
   uint8_t* w = static_cast<uint8_t*>(ws);
   RLFArgs f{x, n, g, thr32, out, stream_tiles(n), 0, 0, reinterpret_cast<FusedHeader*>(w),
             reinterpret_cast<uint64_t*>(w + 64), sparse, cap, global_base, cursor_in, cursor_out, counters, err,
-            dthr};
+            dthr, gate};
   if (fast) {
     return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, true>(f, st)
          : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, true>(f, st)

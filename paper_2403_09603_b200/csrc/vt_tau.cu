@@ -221,12 +221,12 @@ struct BudState {
   int bits[kBudMaxLevels];
 };
 
-__global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                       BudState* st, uint32_t* __restrict__ hist,
-                                                       uint64_t* __restrict__ cand, int32_t* errp) {
-  __shared__ uint32_t sh[kBudBins];
+// One streaming pass of the budget selection by the calling CTA (256
+// threads); `sh` = kBudBins words of shared memory.
+__device__ void bud_pass_body(const double* __restrict__ x, int64_t n, const Grid& g, BudState* st,
+                              uint32_t* __restrict__ hist, uint64_t* __restrict__ cand, int32_t* errp,
+                              uint32_t* sh) {
   __shared__ unsigned long long s_above;
-  if (st->status != 0) return;
   const int level = st->level;
   const bool compact = st->compacting != 0;
   const bool first = level == 0 && !compact;
@@ -309,13 +309,23 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
     atomicAdd(reinterpret_cast<unsigned long long*>(&st->cnt_above), s_above);
 }
 
-// Pick the digit of the rank-th largest key (descending scan by one CTA).
+__global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                       BudState* st, uint32_t* __restrict__ hist,
+                                                       uint64_t* __restrict__ cand, int32_t* errp) {
+  __shared__ uint32_t sh[kBudBins];
+  if (st->status != 0) return;
+  bud_pass_body(x, n, g, st, hist, cand, errp, sh);
+}
+
+// Pick the digit of the rank-th largest key (descending scan by one CTA of
+// up to kSelThreads threads).
 __device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int& bin, int64_t& above_out) {
   __shared__ unsigned long long s_warp[kSelThreads / 32];
   __shared__ int s_bin;
   __shared__ long long s_above;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int per = (nbins + kSelThreads - 1) / kSelThreads;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
+  const int per = (nbins + nthr - 1) / nthr;
   const int hi = nbins - t * per;
   unsigned long long mine = 0;
   for (int k = 0; k < per; ++k) {
@@ -331,13 +341,13 @@ __device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int&
   if (t == 0) s_bin = -1;
   __syncthreads();
   if (warp == 0) {
-    const unsigned long long v = s_warp[lane];
+    const unsigned long long v = lane < nwarps ? s_warp[lane] : 0ull;
     unsigned long long w = v;
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += u;
     }
-    s_warp[lane] = w - v;
+    if (lane < nwarps) s_warp[lane] = w - v;
   }
   __syncthreads();
   const unsigned long long above = s_warp[warp] + incl - mine;
@@ -362,11 +372,8 @@ __device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int&
 
 // After a pass: either finish from the candidates, or select the digit of
 // this level and decide whether the next pass compacts or histograms.
-__global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, const uint32_t* __restrict__ hist,
-                                                               const uint64_t* __restrict__ cand, int64_t budget,
-                                                               uint64_t* key_out) {
-  __shared__ uint32_t sh[kBudBins];
-  if (st->status != 0) return;
+__device__ void bud_step_body(BudState* st, const uint32_t* __restrict__ hist, const uint64_t* __restrict__ cand,
+                              int64_t budget, uint64_t* key_out, uint32_t* sh) {
   const uint64_t lo1 = st->lo_key + 1;
   if (st->compacting) {  // exact select among the compacted candidates
     const int64_t m = (int64_t)st->cand;
@@ -374,9 +381,9 @@ __global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, con
     int64_t rank = st->rank;
     for (int lv = st->level; lv < st->nlevels; ++lv) {
       const int sh_lv = st->shift[lv], bits = st->bits[lv];
-      for (int i = threadIdx.x; i < kBudBins; i += kSelThreads) sh[i] = 0;
+      for (int i = threadIdx.x; i < kBudBins; i += blockDim.x) sh[i] = 0;
       __syncthreads();
-      for (int64_t i = threadIdx.x; i < m; i += kSelThreads) {
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
         const uint64_t o = cand[i] - lo1;
         if ((o & pmask) == prefix) atomicAdd(&sh[(o >> sh_lv) & ((1u << bits) - 1u)], 1u);
       }
@@ -432,11 +439,16 @@ __global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, con
   }
 }
 
-__global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out,
-                                uint32_t* hist) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kBudMaxLevels * kBudBins; i += gridDim.x * blockDim.x)
-    hist[i] = 0u;
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+__global__ void __launch_bounds__(kSelThreads) bud_step_kernel(BudState* st, const uint32_t* __restrict__ hist,
+                                                               const uint64_t* __restrict__ cand, int64_t budget,
+                                                               uint64_t* key_out) {
+  __shared__ uint32_t sh[kBudBins];
+  if (st->status != 0) return;
+  bud_step_body(st, hist, cand, budget, key_out, sh);
+}
+
+// one thread: fresh selection state for keys in (lo_key, hi_key]
+__device__ void bud_init_body(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out) {
   st->lo_key = lo_key;
   st->hi_key = hi_key;
   st->cnt_above = 0;
@@ -461,6 +473,13 @@ __global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, 
   }
   st->nlevels = nl;
   *key_out = 0;
+}
+
+__global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, uint64_t* key_out,
+                                uint32_t* hist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kBudMaxLevels * kBudBins; i += gridDim.x * blockDim.x)
+    hist[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) bud_init_body(st, lo_key, hi_key, key_out);
 }
 
 }  // namespace vt
@@ -598,9 +617,382 @@ extern "C" int vt_straddle_min(const double* y1, const double* y2, int64_t n, in
   return vt_check_launch("straddle_min_kernel");
 }
 
-extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) {
-  return 256 + vt_tau_workspace(n) + vt_round_log_workspace(n);
+namespace vt {
+// ---------------------------------------------------------------------------
+// One-pass adaptive round-and-log (the budget search of SURVEY.md A.4 without
+// extra streaming passes over x in the common case).
+//
+//   1. rl_fused at a candidate threshold L below the expected tau (about
+//      kCandFactor x budget elements have p > L when the dropped mantissa
+//      bits are uniform): y (final: rnd does not depend on tau) plus the
+//      ascending candidate words (local index << 1 | up);
+//   2. adapt_hist_kernel: gather each candidate's key (FP64 bits of p) from
+//      x, histogram its top digit above L; the last CTA picks the digit of
+//      the (budget+1)-th largest key;
+//   3. adapt_select_kernel: compact the keys of that digit; the last CTA
+//      finishes the exact selection in shared memory and runs the FP64
+//      bisection (protocol.py:494-506 skeleton) -> tau;
+//   4. adapt_filter_kernel: the log is exactly the candidates with p > tau,
+//      kept in order by a ticketed decoupled look-back.
+// If fewer than budget+1 candidates exist (v <= L) or they overflow the
+// buffer, the exact selection over x (the multi-pass radix select above) and
+// a second rl_fused at the device tau run instead; in the common case those
+// kernels return at once.
+// ---------------------------------------------------------------------------
+
+constexpr int kCandFactor = 3;
+constexpr int kAdBins = 1 << 13;
+constexpr int kAdThreads = 256;
+constexpr int kFChunk = 2048;  // candidates per filter ticket
+
+struct AdaptHdr {
+  int32_t fallback;    // 1: the exact path runs (written by adapt_hist_kernel every call)
+  uint32_t arrived;    // CTAs done (hist, select kernels; reset by the last one)
+  int64_t ccount;      // candidates (cursor_out of the rounding pass)
+  int64_t scratch;     // the rounding pass's counters[0] (unused)
+  uint64_t above;      // keys > hi_key
+  int64_t rank;        // remaining rank inside the selected digit
+  uint64_t digit;      // selected top digit of (key - L_key - 1)
+  uint64_t bin_count;  // keys in that digit
+  int32_t done;        // 1: decided at the top digit (v > tau_hi)
+  int32_t pad;
+  uint64_t cand2;      // keys compacted by adapt_select_kernel
+  uint32_t f_epoch, f_ticket, f_done, f_pad;
+};
+
+// keys are FP64 bit patterns of p >= 0, so integer order is numeric order
+__device__ __forceinline__ bool last_cta(uint32_t* arrived) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(arrived, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
 }
+
+__global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __restrict__ x, Grid g,
+                                                                const uint64_t* __restrict__ cw,
+                                                                uint64_t* __restrict__ ck, int64_t cap,
+                                                                int64_t budget, uint64_t L_key, uint64_t hi_key,
+                                                                int s0, AdaptHdr* h, uint32_t* __restrict__ hist,
+                                                                uint64_t* __restrict__ fstatus) {
+  __shared__ uint32_t sh[kAdBins];
+  __shared__ unsigned long long s_above;
+  const int64_t M = h->ccount;
+  if (M > cap || M < budget + 1) {  // v <= L, or too many candidates: the exact path decides
+    if (blockIdx.x == 0 && threadIdx.x == 0) h->fallback = 1;
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) h->fallback = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < (M + kFChunk - 1) / kFChunk;
+       i += (int64_t)gridDim.x * kAdThreads)
+    fstatus[i] = 0ull;  // the filter's look-back words for this call's chunks
+  for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0;
+  if (threadIdx.x == 0) s_above = 0;
+  __syncthreads();
+  uint32_t err = 0, above = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < M; i += (int64_t)gridDim.x * kAdThreads) {
+    const uint64_t key = dist_key(__ldg(x + (cw[i] >> 1)), g, err);
+    ck[i] = key;
+    if (key > hi_key) ++above;
+    else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
+  }
+  for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, (unsigned long long)above);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAdBins; i += kAdThreads)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  if (threadIdx.x == 0 && s_above) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above), s_above);
+  if (!last_cta(&h->arrived)) return;
+  // last CTA: the digit of the (budget+1)-th largest key
+  const int64_t above_hi = (int64_t)h->above;
+  if (above_hi > budget) {
+    if (threadIdx.x == 0) h->done = 1;
+  } else {
+    int bin;
+    int64_t above_bin;
+    select_digit(hist, kAdBins, budget - above_hi, bin, above_bin);
+    if (threadIdx.x == 0) {
+      h->done = 0;
+      h->digit = (uint64_t)bin;
+      h->rank = budget - above_hi - above_bin;
+      h->bin_count = hist[bin];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) hist[i] = 0u;  // clean for the next call
+  if (threadIdx.x == 0) {
+    h->above = 0;
+    h->arrived = 0;
+  }
+}
+
+// One FP64 bisection thread: the search_tau skeleton on the selected key.
+__device__ void bisect_to(uint64_t key, double lower, double upper, int iters, DevThr* out, double* tau_out) {
+  const double v = __longlong_as_double((long long)key);
+  for (int i = 0; i < iters; ++i) {
+    const double tau = __dmul_rn(__dadd_rn(lower, upper), 0.5);
+    if (v <= tau) upper = tau;
+    else lower = tau;
+  }
+  *out = thresholds_for(upper);
+  *tau_out = upper;
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t* __restrict__ ck, uint64_t L_key,
+                                                                  uint64_t hi_key, int s0, AdaptHdr* h,
+                                                                  uint64_t* __restrict__ cand2, double lower,
+                                                                  double upper, int iters, DevThr* dthr,
+                                                                  double* tau_out, uint64_t* key_out) {
+  __shared__ uint32_t sh[kAdBins];
+  if (h->fallback) return;
+  if (h->done) {  // more than budget keys above tau_hi: v > tau_hi
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *key_out = 0x7ff0000000000000ull;
+      bisect_to(0x7ff0000000000000ull, lower, upper, iters, dthr, tau_out);
+    }
+    return;
+  }
+  const int64_t M = h->ccount;
+  const uint64_t digit = h->digit;
+  const uint64_t lo1 = L_key + 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    uint64_t key = 0;
+    bool in = false;
+    if (i < M) {
+      key = ck[i];
+      in = key <= hi_key && key >= lo1 && ((key - lo1) >> s0) == digit;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key - lo1;
+    }
+  }
+  if (!last_cta(&h->arrived)) return;
+  // last CTA: exact selection of the rank-th largest among the digit's keys
+  const int64_t m = (int64_t)h->cand2;
+  int64_t rank = h->rank;
+  uint64_t low = 0, lmask = 0;
+  for (int top = s0; top > 0;) {
+    const int bits = top < 13 ? top : 13;
+    top -= bits;
+    for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < m; i += kAdThreads) {
+      const uint64_t o = cand2[i];
+      if ((o & lmask) == low) atomicAdd(&sh[(uint32_t)(o >> top) & ((1u << bits) - 1u)], 1u);
+    }
+    __syncthreads();
+    int bin;
+    int64_t above;
+    select_digit(sh, 1 << bits, rank, bin, above);
+    low |= (uint64_t)bin << top;
+    lmask |= ((1ull << bits) - 1ull) << top;
+    rank -= above;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t key = lo1 + ((digit << s0) | low);
+    *key_out = key;
+    bisect_to(key, lower, upper, iters, dthr, tau_out);
+    h->cand2 = 0;
+    h->arrived = 0;
+  }
+}
+
+// The log: candidates with p > tau, in order.  Persistent CTAs draw chunk
+// tickets; each chunk's kept count goes through an epoch-tagged decoupled
+// look-back over the chunk status words (the status word format of the
+// round-and-log kernel).
+constexpr int kLBShift = 44;
+constexpr uint64_t kLBEpoch = (1ull << 20) - 1;
+constexpr uint64_t kLBA = 1ull << 42, kLBI = 2ull << 42, kLBV = (1ull << 42) - 1;
+__device__ __forceinline__ uint64_t lbw(uint32_t e, uint64_t f, uint64_t v) {
+  return ((uint64_t)e << kLBShift) | f | (v & kLBV);
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t* __restrict__ cw,
+                                                                  const uint64_t* __restrict__ ck, AdaptHdr* h,
+                                                                  const DevThr* dthr, uint64_t* sparse, int64_t cap,
+                                                                  int64_t global_base, const int64_t* cursor_in,
+                                                                  int64_t* cursor_out, int64_t* counters,
+                                                                  uint64_t* status) {
+  constexpr int kPer = kFChunk / kAdThreads;  // 8 candidates per thread
+  __shared__ uint32_t s_warp[kAdThreads / 32];
+  __shared__ int64_t s_t, s_base;
+  __shared__ uint32_t s_epoch;
+  if (h->fallback) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t M = h->ccount;
+  const int64_t nchunks = (M + kFChunk - 1) / kFChunk;
+  const uint64_t tau_key = (uint64_t)__double_as_longlong(dthr->tau);
+  const int64_t cur = cursor_in ? *cursor_in : 0;
+  if (tid == 0) s_epoch = ((*(volatile uint32_t*)&h->f_epoch) + 1u) & (uint32_t)kLBEpoch;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  while (true) {
+    if (tid == 0) s_t = (int64_t)atomicAdd(&h->f_ticket, 1u);
+    __syncthreads();
+    const int64_t t = s_t;
+    __syncthreads();
+    if (t >= nchunks) break;
+    const int64_t c0 = t * kFChunk + (int64_t)tid * kPer;
+    uint32_t keep = 0, cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const bool kp = c0 + k < M && ck[c0 + k] > tau_key;
+      keep |= kp ? (1u << k) : 0u;
+      cnt += kp ? 1u : 0u;
+    }
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kAdThreads / 32; ++w) {
+      wpre += (w < warp) ? s_warp[w] : 0u;
+      agg += s_warp[w];
+    }
+    if (warp == 0) {  // publish + look-back (32 predecessors per round trip)
+      int64_t excl = 0;
+      if (t == 0) {
+        if (lane == 0) st_relaxed_u64(status, lbw(epoch, kLBI, agg));
+      } else {
+        if (lane == 0) st_relaxed_u64(status + t, lbw(epoch, kLBA, agg));
+        int64_t pred = t - 1;
+        while (true) {
+          const int64_t idx = pred - lane;
+          uint64_t w = lbw(epoch, kLBI, 0);
+          if (idx >= 0) w = ld_relaxed_u64(status + idx);
+          const bool valid = ((w >> kLBShift) & kLBEpoch) == epoch;
+          const uint64_t flag = valid ? ((w >> 42) & 3ull) : 0ull;
+          const uint32_t incm = __ballot_sync(0xffffffffu, flag == 2);
+          const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
+          const int first = incm ? (__ffs(incm) - 1) : 31;
+          if (inv & ((2u << first) - 1u)) {
+            __nanosleep(32);
+            continue;
+          }
+          uint64_t v = (lane <= first) ? (w & kLBV) : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          excl += (int64_t)v;
+          if (incm) break;
+          pred -= 32;
+        }
+        if (lane == 0) st_relaxed_u64(status + t, lbw(epoch, kLBI, (uint64_t)excl + agg));
+      }
+      if (lane == 0) {
+        s_base = cur + excl;
+        if (t == nchunks - 1) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(counters), (unsigned long long)(excl + (int64_t)agg));
+          if (cursor_out) *cursor_out = cur + excl + (int64_t)agg;
+        }
+      }
+    }
+    __syncthreads();
+    int64_t pos = s_base + wpre + (inc - cnt);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      if (keep & (1u << k)) {
+        const uint64_t w = cw[c0 + k];
+        if (pos < cap) sparse[pos] = ((uint64_t)(global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+        ++pos;
+      }
+    }
+  }
+  if (last_cta(&h->f_done)) {
+    if (tid == 0) {
+      h->f_ticket = 0u;
+      h->f_done = 0u;
+      h->f_epoch = epoch;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void adapt_force_exact_kernel(AdaptHdr* h) { h->fallback = 1; }
+
+// Exact fallback, gated on h->fallback (the kernels return at once in the
+// common case): the multi-pass budget selection over x, each pass followed
+// by the selection step in its last CTA, the final step running the FP64
+// bisection.
+__global__ void adapt_fb_init_kernel(const AdaptHdr* h, BudState* st, uint32_t* hist, uint64_t lo_key,
+                                     uint64_t hi_key, uint64_t* key_out) {
+  if (!h->fallback) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kBudMaxLevels * kBudBins; i += gridDim.x * blockDim.x)
+    hist[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) bud_init_body(st, lo_key, hi_key, key_out);
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                                   AdaptHdr* h, BudState* st, uint32_t* hist,
+                                                                   uint64_t* cand, int64_t budget, double lower,
+                                                                   double upper, int iters, uint64_t* key_out,
+                                                                   DevThr* dthr, double* tau_out, int32_t* errp) {
+  __shared__ uint32_t sh[kBudBins];
+  if (!h->fallback || st->status != 0) return;
+  bud_pass_body(x, n, g, st, hist, cand, errp, sh);
+  if (!last_cta(&h->arrived)) return;
+  if (threadIdx.x == 0) h->arrived = 0u;
+  bud_step_body(st, hist, cand, budget, key_out, sh);
+  __syncthreads();
+  if (threadIdx.x == 0 && st->status != 0) bisect_to(*key_out, lower, upper, iters, dthr, tau_out);
+}
+}  // namespace vt
+
+namespace {
+// Adaptive workspace: [header 256 B: DevThr, key, status, AdaptHdr]
+// [candidate digit histogram] [tau workspace (exact fallback)] [round-and-log
+// workspace] [filter status] [candidate words | keys | digit keys: cap each].
+// Everything that outlives a call (the headers, the self-cleaning histogram,
+// the round-and-log epoch header) sits at offsets independent of n, because
+// one workspace serves calls of any size; the filter status words are
+// cleared by adapt_hist_kernel for the chunks a call uses.
+struct AdaptLayout {
+  size_t tau, rl, hist, cw, ck, c2, fst, total;
+  int64_t cap;
+};
+size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
+AdaptLayout adapt_layout(int64_t n) {
+  AdaptLayout L;
+  L.cap = std::max<int64_t>(8192, (n + 15) / 16);
+  size_t o = 256;
+  L.hist = o;
+  o += al256((size_t)kAdBins * 4);
+  L.tau = o;
+  o += al256(vt_tau_workspace(n));  // size independent of n
+  L.rl = o;
+  o += al256(vt_round_log_workspace(n));
+  L.fst = o;
+  o += al256((size_t)((L.cap + kFChunk - 1) / kFChunk) * 8);
+  L.cw = o;
+  o += al256((size_t)L.cap * 8);
+  L.ck = o;
+  o += al256((size_t)L.cap * 8);
+  L.c2 = o;
+  o += al256((size_t)L.cap * 8);
+  L.total = o;
+  return L;
+}
+int adapt_grid(int64_t work, int per) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + per - 1) / per, 148 * 4));
+}
+}  // namespace
+
+extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) { return adapt_layout(n).total; }
 
 extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_t budget, int iters, int out_kind,
                                      void* out, uint64_t* sparse, int64_t sparse_cap, int64_t global_base,
@@ -611,37 +1003,82 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
     vt_set_error("vt_round_log_adaptive: bad argument (n > 0, 256-byte aligned workspace)");
     return VT_EINVAL;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  DevThr* dthr = reinterpret_cast<DevThr*>(w);
-  uint64_t* key = reinterpret_cast<uint64_t*>(w + 64);
-  int32_t* status = reinterpret_cast<int32_t*>(w + 72);
-  void* tws = w + 256;
-  const size_t tws_bytes = vt_tau_workspace(n);
-  void* rws = w + 256 + ((tws_bytes + 255) & ~(size_t)255);
-  // the round-and-log workspace keeps an epoch header at its start: keep it
-  // at a fixed place (it must stay zero-filled until first use)
-  const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
-  int rc = vt_tau_budget_key(x, n, b_r, budget, lo, hi, key, status, err, tws, tws_bytes, stream);
-  if (rc) return rc;
-  budget_bisect_kernel<<<1, 1, 0, s>>>(key, lo, hi, iters, dthr, tau_out);
-  if ((rc = vt_check_launch("budget_bisect_kernel"))) return rc;
-  const Grid g = make_grid(b_r, lo);  // thresholds come from dthr
-  const size_t rws_bytes = ws_bytes - (static_cast<uint8_t*>(rws) - w);
-  if (rws_bytes < vt_round_log_workspace(n)) {
-    vt_set_error("vt_round_log_adaptive: workspace too small");
-    return VT_EINVAL;
-  }
-  if (out_kind == VT_OUT_F32 && (reinterpret_cast<uintptr_t>(out) & 15)) {
-    vt_set_error("vt_round_log_adaptive: misaligned output");
-    return VT_EINVAL;
-  }
-  if ((reinterpret_cast<uintptr_t>(x) & 31) || (out_kind == VT_OUT_F64 && (reinterpret_cast<uintptr_t>(out) & 31))) {
+  if ((out_kind == VT_OUT_F32 && (reinterpret_cast<uintptr_t>(out) & 15)) ||
+      (reinterpret_cast<uintptr_t>(x) & 31) || (out_kind == VT_OUT_F64 && (reinterpret_cast<uintptr_t>(out) & 31))) {
     vt_set_error("vt_round_log_adaptive: misaligned x / output");
     return VT_EINVAL;
   }
-  return rl_stream(x, n, g, 0, b_r == 32, out_kind, out, sparse, sparse_cap, global_base, cursor_in, cursor_out,
-                   counters, err, rws, s, dthr);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const AdaptLayout lay = adapt_layout(n);
+  DevThr* dthr = reinterpret_cast<DevThr*>(w);
+  uint64_t* key = reinterpret_cast<uint64_t*>(w + 64);
+  AdaptHdr* h = reinterpret_cast<AdaptHdr*>(w + 128);
+  uint8_t* tws = w + lay.tau;
+  BudState* st = reinterpret_cast<BudState*>(tws);
+  uint32_t* bhist = reinterpret_cast<uint32_t*>(tws + 512);
+  uint64_t* bcand = reinterpret_cast<uint64_t*>(tws + 512 + (size_t)kBudMaxLevels * kBudBins * 4);
+  void* rws = w + lay.rl;
+  uint32_t* ahist = reinterpret_cast<uint32_t*>(w + lay.hist);
+  uint64_t* cw = reinterpret_cast<uint64_t*>(w + lay.cw);
+  uint64_t* ck = reinterpret_cast<uint64_t*>(w + lay.ck);
+  uint64_t* c2 = reinterpret_cast<uint64_t*>(w + lay.c2);
+  uint64_t* fst = reinterpret_cast<uint64_t*>(w + lay.fst);
+  const bool fast = b_r == 32;
+  const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
+  uint64_t lo_key, hi_key;
+  memcpy(&lo_key, &lo, 8);
+  memcpy(&hi_key, &hi, 8);
+  // candidate threshold: about kCandFactor x (budget + 1) elements above it
+  // when p is uniform on [0, hi] (the dropped bits of real data are)
+  const double want = (double)kCandFactor * (double)(budget + 1) + 1024.0;
+  double L = hi * (1.0 - want / (double)n);
+  if (!(L > lo)) L = lo;
+  uint64_t L_key;
+  memcpy(&L_key, &L, 8);
+  const uint64_t W = hi_key - L_key;  // key offsets 0 .. W - 1 above L
+  const int wbits = W > 1 ? 64 - __builtin_clzll(W - 1) : 1;
+  const int s0 = std::max(0, wbits - 13);
+  const Grid gL = make_grid(b_r, L);
+  const int thrL = (int)std::min<int64_t>(std::max<int64_t>(gL.thr, 0), INT32_MAX);
+  const Grid g0 = make_grid(b_r, 0.0);
+
+  // In place (y overwrites x) the candidates' keys could not be gathered
+  // after the rounding pass: select on x first (the exact path), then round.
+  const size_t ybytes = out_kind == VT_OUT_F64 ? 8 : out_kind == VT_OUT_F32 ? 4 : 0;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(out);
+  const bool aliased = ybytes && ya < xa + (uintptr_t)n * 8 && xa < ya + (uintptr_t)n * ybytes;
+  int rc = 0;
+  if (aliased) {
+    adapt_force_exact_kernel<<<1, 1, 0, s>>>(h);
+    if ((rc = vt_check_launch("adapt_force_exact_kernel"))) return rc;
+  } else {
+    // 1. rounding pass: y + candidate words (local index << 1 | up) with p > L
+    rc = rl_stream(x, n, gL, thrL, fast, out_kind, out, cw, lay.cap, 0, nullptr, &h->ccount, &h->scratch, err,
+                   rws, s);
+    if (rc) return rc;
+    // 2-3. exact selection of the (budget+1)-th largest p among the candidates, bisection
+    const int gc = adapt_grid(lay.cap, kAdThreads * 8);
+    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst);
+    if ((rc = vt_check_launch("adapt_hist_kernel"))) return rc;
+    adapt_select_kernel<<<gc, kAdThreads, 0, s>>>(ck, L_key, hi_key, s0, h, c2, lo, hi, iters, dthr, tau_out, key);
+    if ((rc = vt_check_launch("adapt_select_kernel"))) return rc;
+    // 4. the log = candidates with p > tau, in order
+    adapt_filter_kernel<<<adapt_grid(lay.cap, kFChunk), kAdThreads, 0, s>>>(
+        cw, ck, h, dthr, sparse, sparse_cap, global_base, cursor_in, cursor_out, counters, fst);
+    if ((rc = vt_check_launch("adapt_filter_kernel"))) return rc;
+  }
+  // fallback (no-ops unless the candidates could not decide): exact selection over x, then a full pass
+  adapt_fb_init_kernel<<<(kBudMaxLevels * kBudBins + 255) / 256, 256, 0, s>>>(h, st, bhist, lo_key, hi_key, key);
+  if ((rc = vt_check_launch("adapt_fb_init_kernel"))) return rc;
+  const unsigned fb_blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, 148 * 8));
+  for (int p = 0; p <= kBudMaxLevels; ++p) {
+    adapt_fb_pass_kernel<<<fb_blocks, kAdThreads, 0, s>>>(x, n, g0, h, st, bhist, bcand, budget, lo, hi, iters, key,
+                                                          dthr, tau_out, err);
+    if ((rc = vt_check_launch("adapt_fb_pass_kernel"))) return rc;
+  }
+  return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
+                   cursor_out, counters, err, rws, s, dthr, &h->fallback);
 }
 
 namespace {

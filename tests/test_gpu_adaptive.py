@@ -1,0 +1,101 @@
+"""GPU parity of the one-pass adaptive round-and-log (ops.round_and_log_adaptive:
+candidates at a threshold below tau during the rounding pass, exact selection
+among them, FP64 bisection, ordered filter; exact multi-pass fallback) against
+the oracle's budget search (the protocol.search_tau skeleton of
+pkg/src/vtrain/protocol.py:494-506 in budget form) and the
+oracle direction codes at that tau (fpround.py:164-177)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(oracle, x, b_r, B, base=0, out_dtype=None):
+    import torch
+    from paper_2403_09603_b200 import ops
+    kw = {} if out_dtype is None else {"out_dtype": out_dtype}
+    y, log, tau = ops.round_and_log_adaptive(torch.from_numpy(x).cuda(), b_r, B, global_base=base, **kw)
+    t_or = oracle.search_tau_budget(x, b_r, B)
+    assert tau == t_or, (tau.hex(), t_or.hex())
+    codes = oracle.direction_array(x, b_r, t_or)
+    want = oracle.sparse_from_codes(codes, base=base)
+    assert log.count == want.size
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64), want)
+    r = oracle.rnd_array(x, b_r)
+    got = y.cpu().numpy()
+    assert np.array_equal(bits(got), bits(r if got.dtype == np.float64 else r.astype(np.float32)))
+    return log.count
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 5_000, 200_003, 4_000_037])
+def test_fast_path_sizes(oracle, n):
+    x = np.random.default_rng(n).normal(0.0, 0.7, size=n)
+    B = int(0.005 * n)
+    cnt = _check(oracle, x, 32, B, base=3 * n)
+    assert cnt <= B
+
+
+@pytest.mark.parametrize("B", [0, 1, 17, 2_500])
+def test_budgets(oracle, B):
+    x = np.random.default_rng(100 + B).normal(0.0, 5.0, size=500_000)
+    _check(oracle, x, 32, B)
+
+
+def test_fallbacks(oracle):
+    """Inputs the candidate threshold cannot decide: too few candidates
+    (mostly on-grid data), too many (exact midpoints, a 40% budget)."""
+    rng = np.random.default_rng(7)
+    n = 300_000
+    sparse = np.where(rng.random(n) < 0.9, np.round(rng.normal(0, 100, n)), rng.normal(0, 1, n))
+    _check(oracle, sparse, 32, int(0.005 * n))
+    from paper_2403_09603_b200 import workloads
+    _check(oracle, workloads.config0_x(n, 8), 32, int(0.005 * n))
+    _check(oracle, rng.normal(0, 1, n), 32, int(0.4 * n))
+
+
+def test_general_grid_and_fp64_out(oracle):
+    import torch
+    x = np.random.default_rng(9).normal(0.0, 2.0, size=123_457)
+    _check(oracle, x, 26, 600, out_dtype=torch.float64)
+    _check(oracle, x, 10, 600)
+
+
+def test_tiny_magnitudes(oracle):
+    """Values below 2^-126 (absolute grid, FP64 distance) mixed with normal ones."""
+    rng = np.random.default_rng(10)
+    x = rng.normal(0, 1, 100_000) * np.exp2(rng.integers(-160, 4, 100_000))
+    _check(oracle, x, 32, 500)
+
+
+def test_repeated_calls_share_workspace(oracle):
+    """The filter's epoch / ticket state and the candidate histograms are
+    reset by the kernels themselves: many calls of mixed sizes on one
+    workspace, including fallbacks in between."""
+    from paper_2403_09603_b200 import workloads
+    rng = np.random.default_rng(11)
+    xs = [rng.normal(0, 1, 250_000), workloads.config0_x(60_000, 12), rng.normal(0, 1e-3, 31_000),
+          rng.normal(0, 1, 250_000)]
+    for rep in range(3):
+        for x in xs:
+            _check(oracle, x, 32, int(0.005 * x.size))
+
+
+def test_in_place_fp64(oracle):
+    """y written over x (the hooks' use): the selection runs on x before the
+    rounding pass overwrites it."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    x = np.random.default_rng(13).normal(0.0, 0.3, size=333_333)
+    xt = torch.from_numpy(x.copy()).cuda()
+    B = int(0.005 * x.size)
+    y, log, tau = ops.round_and_log_adaptive(xt, 32, B, out_dtype=torch.float64, out=xt)
+    t_or = oracle.search_tau_budget(x, 32, B)
+    assert tau == t_or
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
+                          oracle.sparse_from_codes(oracle.direction_array(x, 32, t_or)))
+    assert np.array_equal(bits(xt.cpu().numpy()), bits(oracle.rnd_array(x, 32)))

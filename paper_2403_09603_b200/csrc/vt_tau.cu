@@ -658,6 +658,7 @@ struct AdaptHdr {
   int32_t pad;
   uint64_t cand2;      // keys compacted by adapt_select_kernel
   uint32_t f_epoch, f_ticket, f_done, f_pad;
+  uint64_t above_lo;   // in-place calls: keys > lo_key (decides v <= tau_lo without a fallback)
 };
 
 // keys are FP64 bit patterns of p >= 0, so integer order is numeric order
@@ -676,12 +677,18 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
                                                                 uint64_t* __restrict__ ck, int64_t cap,
                                                                 int64_t budget, uint64_t L_key, uint64_t hi_key,
                                                                 int s0, AdaptHdr* h, uint32_t* __restrict__ hist,
-                                                                uint64_t* __restrict__ fstatus) {
+                                                                uint64_t* __restrict__ fstatus, bool gather) {
   __shared__ uint32_t sh[kAdBins];
   __shared__ unsigned long long s_above;
   const int64_t M = h->ccount;
   if (M > cap || M < budget + 1) {  // v <= L, or too many candidates: the exact path decides
-    if (blockIdx.x == 0 && threadIdx.x == 0) h->fallback = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      // unless at most budget keys exceed tau_lo at all (in-place calls count
+      // them): then v <= tau_lo and the bisection result is fixed
+      const bool low = !gather && M <= cap && (int64_t)h->above_lo <= budget;
+      h->fallback = low ? 0 : 1;
+      h->done = low ? 2 : 0;
+    }
     return;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) h->fallback = 0;
@@ -693,8 +700,13 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
   __syncthreads();
   uint32_t err = 0, above = 0;
   for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < M; i += (int64_t)gridDim.x * kAdThreads) {
-    const uint64_t key = dist_key(__ldg(x + (cw[i] >> 1)), g, err);
-    ck[i] = key;
+    uint64_t key;
+    if (gather) {
+      key = dist_key(__ldg(x + (cw[i] >> 1)), g, err);
+      ck[i] = key;
+    } else {
+      key = ck[i];
+    }
     if (key > hi_key) ++above;
     else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
   }
@@ -747,10 +759,13 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t
                                                                   double* tau_out, uint64_t* key_out) {
   __shared__ uint32_t sh[kAdBins];
   if (h->fallback) return;
-  if (h->done) {  // more than budget keys above tau_hi: v > tau_hi
+  if (h->done) {  // 1: more than budget keys above tau_hi (v > tau_hi); 2: v <= tau_lo
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      *key_out = 0x7ff0000000000000ull;
-      bisect_to(0x7ff0000000000000ull, lower, upper, iters, dthr, tau_out);
+      const uint64_t v = h->done == 1 ? 0x7ff0000000000000ull : (uint64_t)__double_as_longlong(lower);
+      *key_out = v;
+      bisect_to(v, lower, upper, iters, dthr, tau_out);
+      h->done = 0;
+      h->above_lo = 0;
     }
     return;
   }
@@ -804,6 +819,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t
     bisect_to(key, lower, upper, iters, dthr, tau_out);
     h->cand2 = 0;
     h->arrived = 0;
+    h->above_lo = 0;
   }
 }
 
@@ -923,7 +939,66 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t
   }
 }
 
-__global__ void adapt_force_exact_kernel(AdaptHdr* h) { h->fallback = 1; }
+// In-place calls: one streaming read of x appends the keys above L
+// (unordered, warp-aggregated); the rounding pass then runs at the selected
+// tau and writes the ordered log itself.
+__global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                                uint64_t L_key, uint64_t lo_key,
+                                                                uint64_t* __restrict__ ck, int64_t cap, AdaptHdr* h,
+                                                                int32_t* errp) {
+  // keys are staged per CTA and appended with one global atomic per flush:
+  // a global atomic per warp ballot serialises on the counter's L2 slice
+  constexpr int kBuf = 2048;  // one step adds at most 1024
+  __shared__ uint64_t sbuf[kBuf];
+  __shared__ uint32_t scount;
+  __shared__ unsigned long long sbase;
+  uint32_t err = 0, above_lo = 0;
+  const int lane = threadIdx.x & 31;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+  if (threadIdx.x == 0) scount = 0;
+  __syncthreads();
+  auto flush = [&]() {
+    const uint32_t c = scount;
+    if (threadIdx.x == 0) sbase = atomicAdd(reinterpret_cast<unsigned long long*>(&h->ccount), (unsigned long long)c);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < c; i += kAdThreads)
+      if ((int64_t)(sbase + i) < cap) ck[sbase + i] = sbuf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) scount = 0;
+    __syncthreads();
+  };
+  for (int64_t base = (int64_t)blockIdx.x * 1024; base < n; base += (int64_t)gridDim.x * 1024) {
+    const int64_t i0 = base + 4 * threadIdx.x;
+    D4 xv;
+    if (vec && i0 + 3 < n) {
+      xv = ldg_stream4(x + i0);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xv.v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint64_t key = (i0 + v < n) ? dist_key(xv.v[v], g, err) : 0ull;
+      const bool in = key > L_key;
+      above_lo += key > lo_key ? 1u : 0u;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t pos = 0;
+        if (lane == leader) pos = atomicAdd(&scount, (uint32_t)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (in) sbuf[pos + __popc(m & ((1u << lane) - 1u))] = key;
+      }
+    }
+    __syncthreads();
+    if (scount >= kBuf - 1024) flush();
+  }
+  if (scount) flush();
+  report_err(errp, err);
+  for (int o = 16; o > 0; o >>= 1) above_lo += __shfl_xor_sync(0xffffffffu, above_lo, o);
+  if (lane == 0 && above_lo)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), (unsigned long long)above_lo);
+}
 
 // Exact fallback, gated on h->fallback (the kernels return at once in the
 // common case): the multi-pass budget selection over x, each pass followed
@@ -937,13 +1012,14 @@ __global__ void adapt_fb_init_kernel(const AdaptHdr* h, BudState* st, uint32_t* 
   if (blockIdx.x == 0 && threadIdx.x == 0) bud_init_body(st, lo_key, hi_key, key_out);
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
+__global__ void __launch_bounds__(kAdThreads, 6) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
                                                                    AdaptHdr* h, BudState* st, uint32_t* hist,
                                                                    uint64_t* cand, int64_t budget, double lower,
                                                                    double upper, int iters, uint64_t* key_out,
                                                                    DevThr* dthr, double* tau_out, int32_t* errp) {
   __shared__ uint32_t sh[kBudBins];
   if (!h->fallback || st->status != 0) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) h->above_lo = 0;
   bud_pass_body(x, n, g, st, hist, cand, errp, sh);
   if (!last_cta(&h->arrived)) return;
   if (threadIdx.x == 0) h->arrived = 0u;
@@ -1044,22 +1120,31 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   const Grid g0 = make_grid(b_r, 0.0);
 
   // In place (y overwrites x) the candidates' keys could not be gathered
-  // after the rounding pass: select on x first (the exact path), then round.
+  // after the rounding pass: their keys come from a read of x first.
   const size_t ybytes = out_kind == VT_OUT_F64 ? 8 : out_kind == VT_OUT_F32 ? 4 : 0;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(out);
   const bool aliased = ybytes && ya < xa + (uintptr_t)n * 8 && xa < ya + (uintptr_t)n * ybytes;
   int rc = 0;
+  const int gc = adapt_grid(lay.cap, kAdThreads * 8);
   if (aliased) {
-    adapt_force_exact_kernel<<<1, 1, 0, s>>>(h);
-    if ((rc = vt_check_launch("adapt_force_exact_kernel"))) return rc;
+    // 1'. keys above L (unordered), 2-3. selection among them, bisection
+    if (cudaMemsetAsync(&h->ccount, 0, sizeof(int64_t), s) != cudaSuccess) return vt_check_launch("memset");
+    const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 148 * 8));
+    adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, ck, lay.cap, h, err);
+    if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
+    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,
+                                                false);
+    if ((rc = vt_check_launch("adapt_hist_kernel"))) return rc;
+    adapt_select_kernel<<<gc, kAdThreads, 0, s>>>(ck, L_key, hi_key, s0, h, c2, lo, hi, iters, dthr, tau_out, key);
+    if ((rc = vt_check_launch("adapt_select_kernel"))) return rc;
   } else {
     // 1. rounding pass: y + candidate words (local index << 1 | up) with p > L
     rc = rl_stream(x, n, gL, thrL, fast, out_kind, out, cw, lay.cap, 0, nullptr, &h->ccount, &h->scratch, err,
                    rws, s);
     if (rc) return rc;
     // 2-3. exact selection of the (budget+1)-th largest p among the candidates, bisection
-    const int gc = adapt_grid(lay.cap, kAdThreads * 8);
-    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst);
+    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,
+                                                true);
     if ((rc = vt_check_launch("adapt_hist_kernel"))) return rc;
     adapt_select_kernel<<<gc, kAdThreads, 0, s>>>(ck, L_key, hi_key, s0, h, c2, lo, hi, iters, dthr, tau_out, key);
     if ((rc = vt_check_launch("adapt_select_kernel"))) return rc;
@@ -1077,8 +1162,9 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
                                                           dthr, tau_out, err);
     if ((rc = vt_check_launch("adapt_fb_pass_kernel"))) return rc;
   }
+  // the rounding pass at the device tau: always for in-place calls, else only after a fallback
   return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
-                   cursor_out, counters, err, rws, s, dthr, &h->fallback);
+                   cursor_out, counters, err, rws, s, dthr, aliased ? nullptr : &h->fallback);
 }
 
 namespace {

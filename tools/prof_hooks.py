@@ -1,5 +1,6 @@
 """configs[3] hook cost breakdown (development aid): the adaptive round-and-log
-alone on the 174 GPT-2 hooked tensor sizes, eager and graph-captured."""
+alone on the 174 GPT-2 hooked tensor sizes -- in place on fresh data (the
+hooks' call) and out of place -- timed with CUDA events around the ops only."""
 import sys, json
 sys.path.insert(0, ".")
 import torch
@@ -17,18 +18,33 @@ hk.collect(); hk.remove()
 del model, logits
 torch.cuda.empty_cache()
 mx = max(sizes)
-buf = torch.randn(mx, dtype=torch.float64, device="cuda", generator=g)
-def run():
-    for n in sizes:
-        x = buf[:n]
-        ops.round_and_log_adaptive(x, 32, int(0.005 * n), out_dtype=torch.float64, out=x, check=False, tag="hooks_fwd")
-def t(fn, reps=3):
-    fn(); torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps): fn()
-    e.record(); torch.cuda.synchronize()
-    return s.elapsed_time(e) / reps
-ms = t(run)
-print(json.dumps({"tensors": len(sizes), "elements": sum(sizes), "max": mx, "eager_ms": round(ms, 3),
-                  "gb_28B": round(sum(sizes) * 28 / 1e9, 2)}))
+src = torch.randn(mx, dtype=torch.float64, device="cuda", generator=g)
+work = torch.empty_like(src)
+out = torch.empty_like(src)
+
+
+def timed(inplace: bool, reps: int = 3) -> float:
+    res = []
+    for r in range(reps + 1):
+        evs = []
+        for n in sizes:
+            if inplace:
+                work[:n].copy_(src[:n])  # fresh (unrounded) data, outside the timed spans
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            if inplace:
+                ops.round_and_log_adaptive(work[:n], 32, int(0.005 * n), out_dtype=torch.float64, out=work[:n],
+                                           check=False, tag="hooks_fwd")
+            else:
+                ops.round_and_log_adaptive(src[:n], 32, int(0.005 * n), out_dtype=torch.float64, out=out[:n],
+                                           check=False, tag="hooks_fwd")
+            e.record()
+            evs.append((s, e))
+        torch.cuda.synchronize()
+        if r:
+            res.append(sum(a.elapsed_time(b) for a, b in evs))
+    return sum(res) / len(res)
+
+
+print(json.dumps({"tensors": len(sizes), "elements": sum(sizes), "max": mx,
+                  "in_place_ms": round(timed(True), 3), "out_of_place_ms": round(timed(False), 3)}))

@@ -330,28 +330,12 @@ struct ReplayArgs {
   int64_t log_len;
   int64_t log_base;
   void* out;
-  const int64_t* offs;  // SPARSE: per-tile [lo, hi) word ranges
   int64_t* counters;
   int32_t* err;
 };
 
-__global__ void log_tile_offsets_kernel(const uint64_t* __restrict__ w, int64_t n_words,
-                                        int64_t base, int64_t n, int64_t num_tiles,
-                                        int64_t* __restrict__ offs, int64_t* counters) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > num_tiles) return;
-  const int64_t key = base + std::min<int64_t>(t * kTile, n);
-  int64_t lo = 0, hi = n_words;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)(w[mid] >> 1) < key) lo = mid + 1;
-    else hi = mid;
-  }
-  offs[t] = lo;
-  if (t == 0) counters[1] = lo;
-  if (t == num_tiles) counters[2] = lo;
-}
-
+// Dense-log replay (ternary codes, or the .vtrl payload); the sparse log
+// goes through the persistent rp_fused_kernel (vt_stream.cu).
 template <int OUT, int LOGK, bool FAST>
 __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a) {
   __shared__ __align__(16) uint8_t cs[kTile];
@@ -366,22 +350,7 @@ __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a)
   load_slots(a.x, a.n, wbase, lane, xv);
   uint32_t err = 0;
 
-  if (LOGK == VT_LOG_SPARSE) {
-    uint4* c4 = reinterpret_cast<uint4*>(cs);
-    for (int k = threadIdx.x; k < kTile / 16; k += kThreads) c4[k] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-    __syncthreads();
-    const uint64_t* w = static_cast<const uint64_t*>(a.log);
-    const int64_t lo = a.offs[tile], hi = a.offs[tile + 1];
-    const int64_t t0 = a.log_base + tile_base;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-      const uint64_t word = w[i];
-      const int64_t idx = (int64_t)(word >> 1) - t0;
-      const bool ordered = (i == 0) || ((w[i - 1] >> 1) < (word >> 1));
-      if (idx >= 0 && idx < kTile && ordered) cs[idx] = (word & 1ull) ? 2 : 0;
-      else err |= VT_ERR_BAD_SPARSE;
-    }
-    __syncthreads();
-  } else if (LOGK == VT_LOG_PACKED) {
+  if (LOGK == VT_LOG_PACKED) {
     const uint8_t* p = static_cast<const uint8_t*>(a.log);
     const int64_t pos0 = a.log_base + tile_base;
     const int64_t b0 = pos0 / 5;
@@ -655,9 +624,7 @@ void launch_rp(const ReplayArgs& a, int64_t tiles, cudaStream_t st) {
 typedef void (*rp_fn)(const ReplayArgs&, int64_t, cudaStream_t);
 template <int OUT, bool F>
 rp_fn pick_rp2(int lk) {
-  return lk == VT_LOG_SPARSE ? launch_rp<OUT, VT_LOG_SPARSE, F>
-       : lk == VT_LOG_CODES  ? launch_rp<OUT, VT_LOG_CODES, F>
-                             : launch_rp<OUT, VT_LOG_PACKED, F>;
+  return lk == VT_LOG_CODES ? launch_rp<OUT, VT_LOG_CODES, F> : launch_rp<OUT, VT_LOG_PACKED, F>;
 }
 rp_fn pick_rp(int out_kind, bool fast, int lk) {
   if (fast) {
@@ -671,9 +638,7 @@ rp_fn pick_rp(int out_kind, bool fast, int lk) {
 }
 }  // namespace
 
-extern "C" size_t vt_replay_workspace(int64_t n) {
-  return std::max((size_t)((num_tiles_for(n) + 1) * 8 + 256), rp_stream_workspace(n));
-}
+extern "C" size_t vt_replay_workspace(int64_t n) { return rp_stream_workspace(n); }
 
 extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, const void* log,
                          int64_t log_len, int64_t log_base, int out_kind, void* out,
@@ -703,7 +668,6 @@ extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, cons
   a.out = out;
   a.counters = counters;
   a.err = err;
-  a.offs = nullptr;
   if (log_kind == VT_LOG_SPARSE) {
     if (!ws || ws_bytes < vt_replay_workspace(n)) {
       vt_set_error("vt_replay: workspace too small");
@@ -711,13 +675,6 @@ extern "C" int vt_replay(const double* x, int64_t n, int b_r, int log_kind, cons
     }
     return rp_stream(x, n, a.g, b_r == 32, out_kind, out, static_cast<const uint64_t*>(log), log_len, log_base,
                      counters, err, ws, st);
-    int64_t* offs = static_cast<int64_t*>(ws);
-    const int64_t threads = tiles + 1;
-    log_tile_offsets_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint64_t*>(log), log_len, log_base, n, tiles, offs, counters);
-    int rc = vt_check_launch("log_tile_offsets_kernel");
-    if (rc) return rc;
-    a.offs = offs;
   }
   rp_fn f = pick_rp(out_kind, b_r == 32, log_kind);
   f(a, tiles, st);

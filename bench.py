@@ -237,7 +237,7 @@ def run_ours(args) -> None:
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, n, tau, base, dev)
+        e2e = run_e2e(args, n, tau, base, dev, world)
 
     if rank != 0:
         if world > 1:
@@ -292,11 +292,13 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def run_e2e(args, n, tau, base, dev):
+def run_e2e(args, n, tau, base, dev, world: int = 1):
     """Same step through the public API with pinned host buffers: H2D of both
-    FP64 inputs, both kernels, D2H of both FP32 outputs and the sparse log."""
+    FP64 inputs, both kernels, D2H of both FP32 outputs and the sparse log.
+    Whole job: every rank's bytes over the slowest rank's time."""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     from paper_2403_09603_b200 import ops, workloads
 
@@ -330,10 +332,17 @@ def run_e2e(args, n, tau, base, dev):
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
     cnt = res["log"]
-    f = cnt / n
-    v = n * (8 + 4 + 8 * f) * 2 / (ms * 1e-3) / 1e9
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([cnt], dtype=torch.int64, device=dev)
+        dist.all_reduce(c)
+        cnt = int(c.item())
+    f = cnt / (n * world)
+    v = world * n * (8 + 4 + 8 * f) * 2 / (ms * 1e-3) / 1e9
     return {"value": round(v, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
-            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n + 8 * cnt,
+            "h2d_bytes_per_step": 16 * n * world, "d2h_bytes_per_step": 8 * n * world + 8 * cnt,
             "path": "ops.round_and_log_replay_host (chunked H2D / kernel / D2H on 3 streams)"}
 
 

@@ -341,8 +341,23 @@ def run_e2e(args, n, tau, base, dev, world: int = 1):
         cnt = int(c.item())
     f = cnt / (n * world)
     v = world * n * (8 + 4 + 8 * f) * 2 / (ms * 1e-3) / 1e9
+    # the link this leg is bound by: a plain pinned 1 GiB host -> device copy on this box
+    big_h = torch.empty(1 << 27, dtype=torch.float64, pin_memory=True)
+    big_d = torch.empty(1 << 27, dtype=torch.float64, device=dev)
+    big_d.copy_(big_h, non_blocking=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(3):
+        big_d.copy_(big_h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    h2d_peak = 3 * big_h.numel() * 8 / (s.elapsed_time(e) * 1e-3) / 1e9
+    h2d_rate = 16 * n / (ms * 1e-3) / 1e9
+    del big_h, big_d
     return {"value": round(v, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": 16 * n * world, "d2h_bytes_per_step": 8 * n * world + 8 * cnt,
+            "h2d_gbs_per_gpu": round(h2d_rate, 1), "h2d_copy_peak_gbs": round(h2d_peak, 1),
+            "h2d_frac_of_copy_peak": round(h2d_rate / h2d_peak, 3),
             "path": "ops.round_and_log_replay_host (chunked H2D / kernel / D2H on 3 streams)"}
 
 

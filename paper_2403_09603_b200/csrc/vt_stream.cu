@@ -195,7 +195,8 @@ struct FusedHeader {
   uint32_t epoch;
   uint32_t ticket;  // next super-tile to hand out
   uint32_t done;    // CTAs finished
-  uint32_t pad[13];
+  uint32_t hwm;     // most status words any call has written
+  uint32_t pad[12];
 };
 
 struct FusedSmem {
@@ -591,16 +592,30 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
 
   if (tid == 0) TL(2);
   __syncthreads();
+  __shared__ uint32_t s_last;
   if (tid == 0) {
     TL(3);
     __threadfence();
-    const uint32_t prev = atomicAdd(&a.hdr->done, 1u);
-    if (prev == gridDim.x - 1) {  // every CTA has drawn its last ticket and read the epoch
-      a.hdr->ticket = 0u;
-      a.hdr->done = 0u;
-      a.hdr->epoch = S.epoch;
-      __threadfence();
-    }
+    s_last = atomicAdd(&a.hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // the last CTA out: every CTA has drawn its last ticket and read the epoch
+  const uint32_t hwm = max(a.hdr->hwm, (uint32_t)a.num_super);
+  if (S.epoch == (uint32_t)kEpochMask) {
+    // the next epoch value wraps: clear every status word any call has
+    // written, so no word from 2^20 calls ago can pass for a current one
+    __threadfence();
+    for (uint32_t i = tid; i < hwm; i += blockDim.x) a.status[i] = 0ull;
+    __threadfence();
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.hdr->ticket = 0u;
+    a.hdr->done = 0u;
+    a.hdr->hwm = hwm;
+    a.hdr->epoch = S.epoch == (uint32_t)kEpochMask ? 0u : S.epoch;
+    __threadfence();
   }
 }
 

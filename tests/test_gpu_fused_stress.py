@@ -125,3 +125,43 @@ def test_two_streams_concurrent():
             assert err == 0 and cnt[0] == ref[i][1].numel(), (rep, i, cnt[0])
             assert torch.equal(words[i][: cnt[0]], ref[i][1])
             assert torch.equal(ys[i].view(torch.int32), ref[i][0].view(torch.int32))
+
+
+def test_epoch_wrap_clears_stale_status(oracle):
+    """The look-back status words carry a 20-bit epoch.  Plant words that
+    would pass for the first epoch after the wrap (as a call 2^20 calls
+    earlier could have left them) and run across the wrap: the call holding
+    the last epoch value must clear them first."""
+    import torch
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, workloads
+    lib = _lib.lib()
+    tau = workloads.TAU_CONFIG0
+    big, small = 300 * SUPER + 77, 3 * SUPER
+    ws = torch.zeros(int(lib.vt_round_log_workspace(big)), dtype=torch.uint8, device="cuda")
+    hdr = ws[:64].view(torch.int32)
+    status = ws[64:64 + 8 * 320].view(torch.int64)
+    mask = (1 << 20) - 1
+    hdr[0] = mask - 1        # the next call runs with the last epoch value
+    hdr[3] = 320             # high-water mark: some earlier call wrote 320 words
+    status[:] = (1 << 44) | (2 << 42) | 12345  # INC words tagged with epoch 1, garbage prefixes
+
+    def run(x):
+        n = x.numel()
+        y = torch.empty(n, dtype=torch.float32, device="cuda")
+        words = torch.empty(n // 4, dtype=torch.int64, device="cuda")
+        f = D.Flags()
+        _lib.call("vt_round_log", D.ptr(x), n, 32, float(tau), _lib.OUT_F32, D.ptr(y), D.ptr(words), words.numel(),
+                  0, None, None, None, None, 0, None, f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
+        err, cnt = f.read()
+        assert err == 0
+        return words[: cnt[0]].cpu().numpy().view(np.uint64)
+
+    xs = workloads.config0_x(small, 1)
+    xb = workloads.config0_x(big, 2)
+    want_s = oracle.sparse_from_codes(oracle.direction_array(xs, 32, tau))
+    want_b = oracle.sparse_from_codes(oracle.direction_array(xb, 32, tau))
+    assert np.array_equal(run(torch.from_numpy(xs).cuda()), want_s)  # epoch = mask: clears, wraps to 0
+    assert int(hdr[0]) == 0
+    assert np.array_equal(run(torch.from_numpy(xb).cuda()), want_b)  # epoch 1: planted words are gone
+    assert int(hdr[0]) == 1

@@ -328,8 +328,11 @@ def golden_channel_traces() -> None:
 
     arrays = {}
     meta = {}
+    # trend: only the prefix up to the last call with auditor corrections
+    # (calls 18 and 20 hold all 77 of the run's corrections; 102,144 elements)
+    prefix = {"tiny": None, "logreg": None, "trend": 21}
     with tempfile.TemporaryDirectory() as td:
-        for name in ("tiny", "logreg"):
+        for name in ("tiny", "logreg", "trend"):
             cfg = load_config(Path("/root/reference/pkg/configs") / f"{name}.json")
             log = Path(td) / f"{name}.vtrl"
             w = rl.LogWriter(log, cfg.b_r)
@@ -338,7 +341,18 @@ def golden_channel_traces() -> None:
             w.close()
             au = Rec(pr._AuditorChannel(rl.LogReader(log), cfg.b_r))
             tree_a, *_ = pr._run(cfg, pr.get_profile("pairwise"), au, False)
-            meta[name] = {"b_r": cfg.b_r, "vtrl_sha": sha(log.read_bytes()), "root": tree_t.root.hex(),
+            k = prefix[name]
+            vtrl_sha = sha(log.read_bytes())
+            if k is not None:  # .vtrl of the prefix: the reference writer over the prefix's codes
+                tr.calls, au.calls = tr.calls[:k], au.calls[:k]
+                plog = Path(td) / f"{name}_prefix.vtrl"
+                pw = rl.LogWriter(plog, cfg.b_r)
+                for c in tr.calls:
+                    pw.write_array(fp.direction_array(c[0], cfg.b_r, c[1]))
+                pw.close()
+                vtrl_sha = sha(plog.read_bytes())
+            meta[name] = {"b_r": cfg.b_r, "vtrl_sha": vtrl_sha, "root": tree_t.root.hex(),
+                          "prefix_calls": k, "total_corrections": int(sum(c[4] for c in au.calls)),
                           "audit_root": tree_a.root.hex(), "n_calls": len(tr.calls),
                           "directed": [c[3] for c in tr.calls], "corrections": [c[4] for c in au.calls],
                           "taus": [c[1] for c in tr.calls], "shapes": [list(c[0].shape) for c in tr.calls]}

@@ -1,6 +1,7 @@
 """Drop-in end to end: the exact channel-call sequences of real
-reference train + audit runs (tiny, logreg configs; recorded in the build
-container by tests/golden/make_golden.py) replayed through the GPU channels.
+reference train + audit runs (tiny, logreg, and the prefix of trend that holds
+all 77 of its auditor corrections; recorded in the build container by
+tests/golden/make_golden.py) replayed through the GPU channels.
 Outputs, directed / correction counts and the .vtrl file must match the
 reference bit for bit."""
 
@@ -32,7 +33,7 @@ def _split(flat, shapes):
     return out
 
 
-@pytest.mark.parametrize("name", ["tiny", "logreg"])
+@pytest.mark.parametrize("name", ["tiny", "logreg", "trend"])
 def test_reference_run_through_gpu_channels(traces, name, tmp_path):
     from paper_2403_09603_b200 import protocol, roundlog
     arr, meta = traces

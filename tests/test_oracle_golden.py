@@ -178,3 +178,32 @@ def test_oracle_hash_weights_game_golden(oracle):
     with pytest.raises(ValueError) as e:
         oracle.hash_weights([w1, bad])
     assert str(e.value) == hw["nonfinite_error"]
+
+
+@pytest.mark.parametrize("name", ["tiny", "logreg", "trend"])
+def test_oracle_replays_reference_channel_traces(oracle, name):
+    """The oracle restatement over the recorded channel calls of real
+    reference runs: trainer outputs, directed counts and .vtrl bytes;
+    auditor outputs and corrections (trend's prefix carries 77)."""
+    import json
+    from conftest import GOLDEN
+    arr = np.load(GOLDEN / "channel_traces.npz")
+    m = json.loads((GOLDEN / "channel_traces.json").read_text())[name]
+    sizes = [int(np.prod(s)) for s in m["shapes"]]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    t_in, t_out = arr[f"{name}_t_in"], arr[f"{name}_t_out"]
+    a_in, a_out = arr[f"{name}_a_in"], arr[f"{name}_a_out"]
+    codes_all = []
+    for i, tau in enumerate(m["taus"]):
+        x = t_in[offs[i]:offs[i + 1]]
+        c = oracle.direction_array(x, m["b_r"], tau)
+        codes_all.append(c)
+        assert np.array_equal(bits(oracle.rnd_array(x, m["b_r"]).astype(np.float32)), bits(t_out[offs[i]:offs[i + 1]]))
+        assert int(np.count_nonzero(c != 1)) == m["directed"][i]
+        xa = a_in[offs[i]:offs[i + 1]]
+        ya = oracle.rev_array(xa, m["b_r"], c)
+        assert np.array_equal(bits(ya.astype(np.float32)), bits(a_out[offs[i]:offs[i + 1]]))
+        assert int(np.count_nonzero(ya != oracle.rnd_array(xa, m["b_r"]))) == m["corrections"][i]
+    assert hashlib.sha256(oracle.vtrl_bytes(codes_all, m["b_r"])).hexdigest() == m["vtrl_sha"]
+    if name == "trend":
+        assert sum(m["corrections"]) == 77

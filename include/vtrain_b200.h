@@ -29,6 +29,7 @@
  *   vt_log_validate   <- the byte check of _unpack_block     roundlog.py:75-76
  *   vt_log_histogram  <- roundlog.LogReader.histogram        roundlog.py:203-206
  *   vt_tau_kth_key    <- protocol.search_tau predicate       protocol.py:494-506 (budget form,
+ *   vt_tau_kth_begin/hist/select: the same, one pass at a time (sharded tensors)
  *   vt_tau_budget_key    SURVEY.md Appendix A.4)
  *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
@@ -144,6 +145,20 @@ size_t vt_tau_workspace(int64_t n);
  */
 int vt_tau_kth_key(const double *x, int64_t n, int b_r, int64_t rank, uint64_t *key_out,
                    int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * The same order statistic for one tensor sharded across ranks: begin, then
+ * for pass 0..4: this rank's histogram (vt_tau_kth_hist), the caller sums
+ * it over the ranks in place (vt_tau_kth_hist_bins(pass) uint32 bins at byte
+ * offset vt_tau_kth_hist_offset(pass) of ws, e.g. ncclAllReduce), then the
+ * selection (vt_tau_kth_select), identical on every rank.  rank = global
+ * 0-based rank from the top; the caller handles rank >= total count.
+ */
+size_t vt_tau_kth_hist_offset(int pass);
+int vt_tau_kth_hist_bins(int pass);
+int vt_tau_kth_begin(int64_t rank, uint64_t *key_out, void *ws, size_t ws_bytes, vt_stream_t stream);
+int vt_tau_kth_hist(const double *x, int64_t n, int b_r, int pass, int32_t *err, void *ws, size_t ws_bytes,
+                    vt_stream_t stream);
+int vt_tau_kth_select(int pass, uint64_t *key_out, void *ws, size_t ws_bytes, vt_stream_t stream);
 /*
  * Budget form: *key_out = FP64 bits of v', the (budget+1)-th
  * largest p clamped for a bisection inside (tau_lo, tau_hi): tau_lo if

@@ -51,6 +51,11 @@ EXPORTS: dict[str, tuple] = {
     "vt_log_histogram": (_i32, [_p, _i64, _p, _p, _p]),
     "vt_tau_workspace": (_sz, [_i64]),
     "vt_tau_kth_key": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p, _sz, _p]),
+    "vt_tau_kth_hist_offset": (_sz, [_i32]),
+    "vt_tau_kth_hist_bins": (_i32, [_i32]),
+    "vt_tau_kth_begin": (_i32, [_i64, _p, _p, _sz, _p]),
+    "vt_tau_kth_hist": (_i32, [_p, _i64, _i32, _i32, _p, _p, _sz, _p]),
+    "vt_tau_kth_select": (_i32, [_i32, _p, _p, _sz, _p]),
     "vt_tau_budget_key": (_i32, [_p, _i64, _i32, _i64, _dbl, _dbl, _p, _p, _p, _p, _sz, _p]),
     "vt_round_log_adaptive_workspace": (_sz, [_i64]),
     "vt_round_log_adaptive": (_i32, [_p, _i64, _i32, _i64, _i32, _i32, _p, _p, _i64, _i64, _p, _p, _p, _p, _p,

@@ -1169,18 +1169,28 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
 
 namespace {
 template <int P>
-int run_pass(const double* x, int64_t n, const Grid& g, SelectState* st, uint32_t* hist,
-             uint64_t* key_out, int32_t* err, cudaStream_t s) {
+int hist_pass(const double* x, int64_t n, const Grid& g, SelectState* st, uint32_t* hist, int32_t* err,
+              cudaStream_t s) {
   constexpr size_t smem = sizeof(uint32_t) << pass_bits(P);
   auto hk = tau_hist_kernel<P>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t want = (n + kHistThreads * 8 - 1) / (kHistThreads * 8);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 148 * 2));
   hk<<<blocks, kHistThreads, smem, s>>>(x, n, g, st, hist + (size_t)P * kMaxBins, err);
-  int rc = vt_check_launch("tau_hist_kernel");
-  if (rc) return rc;
+  return vt_check_launch("tau_hist_kernel");
+}
+
+template <int P>
+int select_pass(SelectState* st, uint32_t* hist, uint64_t* key_out, cudaStream_t s) {
   tau_select_kernel<P><<<1, kSelThreads, 0, s>>>(hist + (size_t)P * kMaxBins, st, key_out);
   return vt_check_launch("tau_select_kernel");
+}
+
+template <int P>
+int run_pass(const double* x, int64_t n, const Grid& g, SelectState* st, uint32_t* hist,
+             uint64_t* key_out, int32_t* err, cudaStream_t s) {
+  int rc = hist_pass<P>(x, n, g, st, hist, err, s);
+  return rc ? rc : select_pass<P>(st, hist, key_out, s);
 }
 }  // namespace
 
@@ -1204,6 +1214,63 @@ extern "C" int vt_tau_kth_key(const double* x, int64_t n, int b_r, int64_t rank,
   if ((rc = run_pass<2>(x, n, g, st, hist, key_out, err, s))) return rc;
   if ((rc = run_pass<3>(x, n, g, st, hist, key_out, err, s))) return rc;
   return run_pass<4>(x, n, g, st, hist, key_out, err, s);
+}
+
+// Sharded exact order statistic (one tensor split across ranks): the passes
+// of vt_tau_kth_key one at a time, so the ranks can sum each pass's
+// histogram (ncclAllReduce) before every rank makes the same selection.
+extern "C" size_t vt_tau_kth_hist_offset(int pass) { return (size_t)pass * kMaxBins * sizeof(uint32_t); }
+extern "C" int vt_tau_kth_hist_bins(int pass) { return pass == 4 ? (1 << pass_bits(4)) : (1 << pass_bits(0)); }
+
+extern "C" int vt_tau_kth_begin(int64_t rank, uint64_t* key_out, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (rank < 0 || !key_out || !ws || ws_bytes < vt_tau_workspace(0)) {
+    vt_set_error("vt_tau_kth_begin: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* hist = static_cast<uint32_t*>(ws);
+  SelectState* st = reinterpret_cast<SelectState*>(static_cast<uint8_t*>(ws) + (size_t)kPasses * kMaxBins * 4);
+  if (cudaMemsetAsync(hist, 0, (size_t)kPasses * kMaxBins * 4, s) != cudaSuccess) return vt_check_launch("memset");
+  init_state_kernel<<<1, 1, 0, s>>>(st, rank, key_out);
+  return vt_check_launch("init_state_kernel");
+}
+
+extern "C" int vt_tau_kth_hist(const double* x, int64_t n, int b_r, int pass, int32_t* err, void* ws,
+                               size_t ws_bytes, vt_stream_t stream) {
+  if (n < 0 || b_r < 10 || b_r > 32 || pass < 0 || pass >= kPasses || !err || !ws || (n > 0 && !x) ||
+      ws_bytes < vt_tau_workspace(n)) {
+    vt_set_error("vt_tau_kth_hist: bad argument");
+    return VT_EINVAL;
+  }
+  if (n == 0) return VT_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* hist = static_cast<uint32_t*>(ws);
+  SelectState* st = reinterpret_cast<SelectState*>(static_cast<uint8_t*>(ws) + (size_t)kPasses * kMaxBins * 4);
+  const Grid g = make_grid(b_r, 0.0);
+  switch (pass) {
+    case 0: return hist_pass<0>(x, n, g, st, hist, err, s);
+    case 1: return hist_pass<1>(x, n, g, st, hist, err, s);
+    case 2: return hist_pass<2>(x, n, g, st, hist, err, s);
+    case 3: return hist_pass<3>(x, n, g, st, hist, err, s);
+    default: return hist_pass<4>(x, n, g, st, hist, err, s);
+  }
+}
+
+extern "C" int vt_tau_kth_select(int pass, uint64_t* key_out, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (pass < 0 || pass >= kPasses || !key_out || !ws || ws_bytes < vt_tau_workspace(0)) {
+    vt_set_error("vt_tau_kth_select: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* hist = static_cast<uint32_t*>(ws);
+  SelectState* st = reinterpret_cast<SelectState*>(static_cast<uint8_t*>(ws) + (size_t)kPasses * kMaxBins * 4);
+  switch (pass) {
+    case 0: return select_pass<0>(st, hist, key_out, s);
+    case 1: return select_pass<1>(st, hist, key_out, s);
+    case 2: return select_pass<2>(st, hist, key_out, s);
+    case 3: return select_pass<3>(st, hist, key_out, s);
+    default: return select_pass<4>(st, hist, key_out, s);
+  }
 }
 
 extern "C" int vt_min_f64(const double* s, int64_t n, double* out, int32_t* nan_flag, vt_stream_t stream) {

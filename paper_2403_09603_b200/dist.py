@@ -9,6 +9,11 @@ path shards naturally:
   exclusive prefix places each rank's slice in the global log (concatenation
   in rank order is the reference order).  The log itself stays sharded.
 * replay: each rank consumes its own slice; corrections are all-reduced.
+* adaptive threshold: independent tensors go to ranks whole, LPT-balanced
+  (``lpt_assign``; no collective beyond gathering the taus).  One tensor
+  sharded across ranks: the exact radix select runs pass by pass with the
+  pass histogram summed over the ranks (``ncclAllReduce``, 64 KiB) before
+  every rank makes the same selection (``search_tau_budget_sharded``).
 * Merkle: leaves are grouped in blocks of 2^K; each rank hashes a
   contiguous run of blocks and builds levels 0..K locally, all ranks
   all-gather the block roots and build the top levels redundantly.  Every
@@ -24,6 +29,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -96,6 +102,99 @@ def replay_sharded(xa_local: torch.Tensor, b_r: int, slog: ShardedLog, global_ba
     t = torch.tensor([corr], dtype=torch.int64, device=xa_local.device)
     dist.all_reduce(t, group=group)
     return y, int(t.item())
+
+
+# ---------------------------------------------------------------------------
+# adaptive threshold
+# ---------------------------------------------------------------------------
+
+def lpt_assign(sizes: list[int], world: int) -> list[int]:
+    """Owner rank of each independent tensor: longest processing time first
+    (largest tensor to the least loaded rank; ties to the lower index), so
+    the largest per-rank load is within one tensor of the best split."""
+    order = sorted(range(len(sizes)), key=lambda i: (-int(sizes[i]), i))
+    loads = [0] * world
+    owner = [0] * len(sizes)
+    for i in order:
+        r = min(range(world), key=lambda q: (loads[q], q))
+        owner[i] = r
+        loads[r] += int(sizes[i])
+    return owner
+
+
+class ShardedKth:
+    """One rank's side of the exact order statistic of p over a tensor
+    sharded across ranks (vt_tau_kth_begin / hist / select): pass by pass,
+    this rank's histogram, summed over the ranks by the caller, then the
+    same selection on every rank."""
+
+    PASSES = 5
+
+    def __init__(self, x_local: torch.Tensor, b_r: int, tag: str = "kth_sharded"):
+        from . import _device as D
+        from . import _lib
+        self.D, self.lib = D, _lib
+        self.t = D.aligned_f64(x_local.reshape(-1))
+        self.b_r = b_r
+        self.ws = D.workspace(int(_lib.lib().vt_tau_workspace(self.t.numel())), tag)
+        self.key = torch.zeros(1, dtype=torch.int64, device=self.t.device)
+        self.flags = D.Flags()
+
+    def begin(self, rank: int) -> None:
+        self.lib.call("vt_tau_kth_begin", int(rank), self.D.ptr(self.key), self.D.ptr(self.ws), self.ws.numel(),
+                      self.D.stream_ptr())
+
+    def local_hist(self, p: int) -> torch.Tensor:
+        """Run this rank's pass-p histogram; returns the (int32 view of the)
+        uint32 bins to be summed over the ranks in place."""
+        self.lib.call("vt_tau_kth_hist", self.D.ptr(self.t), self.t.numel(), self.b_r, p, self.flags.err_ptr,
+                      self.D.ptr(self.ws), self.ws.numel(), self.D.stream_ptr())
+        off = int(self.lib.lib().vt_tau_kth_hist_offset(p))
+        bins = int(self.lib.lib().vt_tau_kth_hist_bins(p))
+        return self.ws[off:off + 4 * bins].view(torch.int32)
+
+    def select(self, p: int) -> None:
+        self.lib.call("vt_tau_kth_select", p, self.D.ptr(self.key), self.D.ptr(self.ws), self.ws.numel(),
+                      self.D.stream_ptr())
+
+    def value(self) -> float:
+        self.D.raise_fpround(self.flags.read()[0])
+        return float(self.key.cpu().numpy().view(np.float64)[0])
+
+
+def kth_largest_distance_sharded(x_local: torch.Tensor, b_r: int, rank: int, group=None) -> float:
+    """(rank+1)-th largest p over the union of every rank's shard, exactly
+    (rank 0-based from the top); 0.0 when the union has at most rank elements."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    n = torch.tensor([x_local.numel()], dtype=torch.int64, device=x_local.device)
+    if world > 1:
+        dist.all_reduce(n, group=group)
+    if rank >= int(n.item()):
+        return 0.0
+    sk = ShardedKth(x_local, b_r)
+    sk.begin(rank)
+    for p in range(ShardedKth.PASSES):
+        h = sk.local_hist(p)
+        if world > 1:  # uint32 counts summed as int32: exact modulo 2^32
+            dist.all_reduce(h, group=group)
+        sk.select(p)
+    return sk.value()
+
+
+def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iters: int = 30, group=None) -> float:
+    """protocol.search_tau_budget over a tensor sharded across ranks: the same
+    FP64 bisection on the exact global (budget+1)-th largest p (every rank
+    gets the same tau)."""
+    from .fpround import tau_bounds
+    lower, upper = tau_bounds(b_r)
+    v = kth_largest_distance_sharded(x_local, b_r, int(budget), group)
+    for _ in range(iters):
+        tau = (lower + upper) / 2.0
+        if v <= tau:
+            upper = tau
+        else:
+            lower = tau
+    return upper
 
 
 # ---------------------------------------------------------------------------

@@ -181,3 +181,40 @@ def test_chunked_tree_vs_oracle_random(oracle):
         want = oracle.merkle_levels(oracle.chunk_leaves(w.tobytes(), 4096))
         assert t.levels == want, n_params
         assert t.root == want[-1][0]
+
+
+def test_sharded_budget_search_virtual_ranks(oracle):
+    """§8e: one tensor split over ranks.  Three virtual ranks in one process
+    run the per-pass histograms, their sum stands in for the all-reduce, and
+    every rank's selection must give the single-device order statistic and
+    the oracle's budget tau."""
+    import torch
+    from paper_2403_09603_b200 import dist as vd, protocol
+    x = np.random.default_rng(90).normal(0.0, 0.4, size=250_001)
+    x[::7] = np.round(x[::7] * 1000) / 1000  # some near-grid mass
+    cuts = [0, 61_000, 190_017, x.size]
+    shards = [torch.from_numpy(x[a:b].copy()).cuda() for a, b in zip(cuts, cuts[1:])]
+    for B in (0, 1_250, 40_000):
+        ks = [vd.ShardedKth(s, 32, tag=f"kth_v{r}") for r, s in enumerate(shards)]
+        for k in ks:
+            k.begin(B)
+        for p in range(vd.ShardedKth.PASSES):
+            hs = [k.local_hist(p) for k in ks]
+            total = sum(h.to(torch.int64) for h in hs).to(torch.int32)
+            for h in hs:
+                h.copy_(total)
+            for k in ks:
+                k.select(p)
+        vals = [k.value() for k in ks]
+        want = protocol.kth_largest_distance(x, 32, B)
+        assert all(v == want for v in vals), (B, vals, want)
+        lower, upper = oracle.tau_bounds(32)
+        for _ in range(30):
+            t = (lower + upper) / 2.0
+            if vals[0] <= t:
+                upper = t
+            else:
+                lower = t
+        assert upper == oracle.search_tau_budget(x, 32, B)
+    # world of one: the sharded entry point equals the single-device search
+    assert vd.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, 1_250) == oracle.search_tau_budget(x, 32, 1_250)

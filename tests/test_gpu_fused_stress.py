@@ -165,3 +165,46 @@ def test_epoch_wrap_clears_stale_status(oracle):
     assert int(hdr[0]) == 0
     assert np.array_equal(run(torch.from_numpy(xb).cuda()), want_b)  # epoch 1: planted words are gone
     assert int(hdr[0]) == 1
+
+
+def _torch_words(x, tau, base):
+    """Torch FP64 restatement of direction_array's predicate for b_r = 32
+    (fpround.py:164-177): p = |x - r| / max(2^E, 2^-126) > tau (exact: the
+    divisor is a power of two), UP iff x < r; words (base + i) << 1 | up."""
+    import torch
+    r = x.float().double()
+    _, e = torch.frexp(x)
+    scale = torch.clamp(torch.ldexp(torch.ones_like(x), (e - 1).to(torch.int32)), min=2.0 ** -126)
+    logged = (x - r).abs() / scale > tau
+    idx = torch.nonzero(logged).flatten()
+    return ((idx + base) << 1) | (x[idx] < r[idx]).to(torch.int64)
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(900)
+def test_max_size_properties():
+    """2^32 + 12345 elements (global indices past 32 bits, 524,290 tickets):
+    every log word against a torch FP64 restatement of the direction
+    predicate, chunk by chunk; FP32 output == x.float(); replay of the same
+    input reproduces it with no corrections."""
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    n = (1 << 32) + 12345
+    tau = workloads.TAU_CONFIG0
+    base = 7
+    x = workloads.config0_x_torch_bernoulli(n, seed=32)
+    y, log = ops.round_and_log(x, 32, tau, global_base=base, log_out=torch.empty(n // 8, dtype=torch.int64,
+                                                                                     device="cuda"))
+    assert 0.09 * n < log.count < 0.11 * n
+    pos = 0
+    chunk = 1 << 28
+    for lo in range(0, n, chunk):
+        xs = x[lo:lo + chunk]
+        assert torch.equal(y[lo:lo + chunk].view(torch.int32), xs.float().view(torch.int32))
+        want = _torch_words(xs, tau, base + lo)
+        got = log.words[pos:pos + want.numel()]
+        assert torch.equal(got, want), lo
+        pos += want.numel()
+    assert pos == log.count
+    y2, corr = ops.replay(x, 32, log, global_base=base)
+    assert corr == 0 and torch.equal(y2.view(torch.int32), y.view(torch.int32))

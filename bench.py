@@ -377,7 +377,9 @@ def _time(fn, reps: int, warm: int = 2) -> float:
 
 def sweep(log2s) -> dict:
     """configs[4] size sweep: round-and-log and replay at 2^20 .. 2^32 (config-0
-    distribution, Bernoulli 10% midpoints; 2^20 is L2-resident)."""
+    distribution, Bernoulli 10% midpoints; 2^20 is L2-resident).  Each operator
+    is captured in a CUDA graph and the graph replays are timed (as for the
+    headline); the eager per-call time (host overhead included) is kept too."""
     import torch
 
     from paper_2403_09603_b200 import ops, workloads
@@ -390,16 +392,30 @@ def sweep(log2s) -> dict:
         words = torch.empty(max(n // 4, 1024), dtype=torch.int64, device="cuda")
         _, log = ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False).finish()
         reps = 10 if lg <= 30 else 4
-        ms = _time(lambda: ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False), reps)
         ya = torch.empty_like(y)
         lw = log.words
-        ms2 = _time(lambda: ops.replay(x, 32, lw, out=ya, check=False), reps)
+        rl = lambda: ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)  # noqa: E731
+        rp = lambda: ops.replay(x, 32, lw, out=ya, check=False)  # noqa: E731
+        ms_e, ms2_e = _time(rl, reps), _time(rp, reps)
+        graphs = []
+        for fn in (rl, rp):
+            s_ = torch.cuda.Stream()
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                fn()
+            torch.cuda.current_stream().wait_stream(s_)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs.append(g)
+        ms, ms2 = _time(graphs[0].replay, reps), _time(graphs[1].replay, reps)
         b = n * (8 + 4 + 8 * log.count / n)
         out[f"2^{lg}"] = {"round_log_gbs": round(b / ms / 1e6, 1), "round_log_frac": round(b / ms / 1e6 / peak, 4),
                           "replay_gbs": round(b / ms2 / 1e6, 1), "replay_frac": round(b / ms2 / 1e6 / peak, 4),
                           "round_log_ms": round(ms, 4), "replay_ms": round(ms2, 4),
+                          "round_log_ms_eager": round(ms_e, 4), "replay_ms_eager": round(ms2_e, 4),
                           "logged_fraction": round(log.count / n, 5), "l2_resident": n * 8 < 126e6}
-        del x, y, words, ya, lw, log
+        del x, y, words, ya, lw, log, graphs
         torch.cuda.empty_cache()
     return out
 

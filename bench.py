@@ -287,6 +287,10 @@ def run_ours(args) -> None:
                           "configs[2]_resnet50_budget": config2(),
                           "configs[3]_gpt2_fp64_step": config3_gpt2(),
                           "configs[4]_merkle_1.5B": config4_merkle()}
+        if not args.no_cpu:
+            cores = len(os.sched_getaffinity(0))
+            line["extras"]["configs[4]_merkle_1.5B"]["cpu_baseline"] = cpu_merkle(1 << 16, cores)
+            line["extras"]["configs[2]_resnet50_budget"]["cpu_baseline"] = cpu_adaptive(1 << 22)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -607,11 +611,61 @@ def cpu_measure(total: int, chunk: int, procs: int):
     return {"gbs": gbs, "n": n, "wall_s": wall, "compute_s": compute, "eff_s": eff, "f": f}
 
 
+def _cpu_leaf_chunk(args):
+    lo, hi, leaf = args
+    import hashlib
+
+    import numpy as np
+    w = np.random.default_rng(lo).normal(0.0, 0.02, size=(hi - lo) * leaf // 4).astype("<f4").tobytes()
+    t0 = time.perf_counter()
+    out = [hashlib.sha256(w[i:i + leaf]).digest() for i in range(0, len(w), leaf)]
+    return out, time.perf_counter() - t0
+
+
+def cpu_merkle(n_leaves: int, procs: int, leaf: int = 4096) -> dict:
+    """Reference Merkle path on the host: hashlib (OpenSSL) SHA-256 of each
+    4 KiB leaf over all cores, then merkle.build's levels (one process)."""
+    import multiprocessing as mp
+    sys.path.insert(0, str(REPO / "oracle"))
+    import vt_oracle as O
+    per = (n_leaves + procs - 1) // procs
+    jobs = [(i * per, min(n_leaves, (i + 1) * per), leaf) for i in range(procs) if i * per < n_leaves]
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cpu_leaf_chunk, jobs)
+    leaves = [d for r in res for d in r[0]]
+    hash_s = max(r[1] for r in res)
+    t0 = time.perf_counter()
+    O.merkle_levels(leaves)
+    build_s = time.perf_counter() - t0
+    return {"value": round(n_leaves * leaf / (hash_s + build_s) / 1e9, 3), "unit": "GB/s hashed",
+            "cores": procs, "kind": "port", "sample": f"{n_leaves} leaves of {leaf} B (hashlib over {procs} "
+                                                       f"processes, then the level build)"}
+
+
+def cpu_adaptive(n: int) -> dict:
+    """Reference budget search + trainer channel on one host core: the
+    oracle's search_tau_budget (bisection on the exact order statistic) then
+    direction_array + rnd_array at that tau, on one N(0,1) tensor."""
+    import numpy as np
+    sys.path.insert(0, str(REPO / "oracle"))
+    import vt_oracle as O
+    x = np.random.default_rng(2).normal(0.0, 1.0, n)
+    t0 = time.perf_counter()
+    tau = O.search_tau_budget(x, 32, int(0.005 * n))
+    O.direction_array(x, 32, tau)
+    O.rnd_array(x, 32)
+    dt = time.perf_counter() - t0
+    return {"value": round(n / dt / 1e9, 4), "unit": "G elements/s", "cores": 1, "kind": "port",
+            "sample": f"one tensor of {n} elements"}
+
+
 def cpu_baseline(args):
     cores = len(os.sched_getaffinity(0))
     total = 1 << args.cpu_log2n
     r = cpu_measure(total, 1 << 20, cores)
+    r1 = cpu_measure(1 << 22, 1 << 20, 1)
     return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "value_1core": round(r1["gbs"], 4),
             "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair (trainer channel: direction_array + "
                       f"rnd_array + pack; auditor: rev_array + rnd_array count), chunks of 2^20 over "
                       f"{cores} processes, wall {r['wall_s']:.1f}s",

@@ -317,8 +317,23 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
   bud_pass_body(x, n, g, st, hist, cand, errp, sh);
 }
 
+// Copy a global histogram into shared memory with batches of independent
+// loads (the scan below would otherwise pay one memory round trip per bin).
+__device__ void stage_hist(const uint32_t* __restrict__ g, uint32_t* sh, int nbins) {
+  const int nthr = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < nbins; i0 += 8 * nthr) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (i0 + k * nthr < nbins) ? g[i0 + k * nthr] : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i0 + k * nthr < nbins) sh[i0 + k * nthr] = v[k];
+  }
+  __syncthreads();
+}
+
 // Pick the digit of the rank-th largest key (descending scan by one CTA of
-// up to kSelThreads threads).
+// up to kSelThreads threads) from a histogram in shared memory.
 __device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int& bin, int64_t& above_out) {
   __shared__ unsigned long long s_warp[kSelThreads / 32];
   __shared__ int s_bin;
@@ -334,20 +349,20 @@ __device__ void select_digit(const uint32_t* hist, int nbins, int64_t rank, int&
   }
   unsigned long long incl = mine;
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
   }
   if (lane == 31) s_warp[warp] = incl;
   if (t == 0) s_bin = -1;
   __syncthreads();
   if (warp == 0) {
-    const unsigned long long v = lane < nwarps ? s_warp[lane] : 0ull;
-    unsigned long long w = v;
+    const unsigned long long a = lane < nwarps ? s_warp[lane] : 0ull;
+    unsigned long long w = a;
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += u;
     }
-    if (lane < nwarps) s_warp[lane] = w - v;
+    if (lane < nwarps) s_warp[lane] = w - a;
   }
   __syncthreads();
   const unsigned long long above = s_warp[warp] + incl - mine;
@@ -417,7 +432,8 @@ __device__ void bud_step_body(BudState* st, const uint32_t* __restrict__ hist, c
   }
   int bin;
   int64_t above;
-  select_digit(hist + (size_t)level * kBudBins, 1 << st->bits[level], rank, bin, above);
+  stage_hist(hist + (size_t)level * kBudBins, sh, 1 << st->bits[level]);
+  select_digit(sh, 1 << st->bits[level], rank, bin, above);
   if (threadIdx.x == 0) {
     if (bin < 0) {  // fewer than budget+1 keys above tau_lo: v <= tau_lo
       *key_out = st->lo_key;
@@ -724,7 +740,8 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
   } else {
     int bin;
     int64_t above_bin;
-    select_digit(hist, kAdBins, budget - above_hi, bin, above_bin);
+    stage_hist(hist, sh, kAdBins);
+    select_digit(sh, kAdBins, budget - above_hi, bin, above_bin);
     if (threadIdx.x == 0) {
       h->done = 0;
       h->digit = (uint64_t)bin;
@@ -1012,7 +1029,7 @@ __global__ void adapt_fb_init_kernel(const AdaptHdr* h, BudState* st, uint32_t* 
   if (blockIdx.x == 0 && threadIdx.x == 0) bud_init_body(st, lo_key, hi_key, key_out);
 }
 
-__global__ void __launch_bounds__(kAdThreads, 6) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
+__global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
                                                                    AdaptHdr* h, BudState* st, uint32_t* hist,
                                                                    uint64_t* cand, int64_t budget, double lower,
                                                                    double upper, int iters, uint64_t* key_out,

@@ -61,3 +61,50 @@ def test_operator_fails_loudly_without_gpu():
     from paper_2403_09603_b200 import fpround
     with pytest.raises(RuntimeError, match="CUDA"):
         fpround.rnd_array([1.0], 32)
+
+
+# Every compute entry point rejects malformed arguments before touching the
+# device (VT_EINVAL = -1, vt_last_error names the entry point), so these
+# run without a GPU.  None = NULL pointer.
+BAD_CALLS = [
+    ("vt_round_log", (None, -1, 32, 0.0, 1, None, None, 0, 0, None, None, None, None, 0, None, None, None, None, 0,
+                      None)),
+    ("vt_replay", (None, 10, 9, 0, None, 0, 0, 1, None, None, None, None, 0, None)),
+    ("vt_grid_neighbors", (None, -1, 32, None, None, None, None)),
+    ("vt_exponent_scale", (None, -1, None, None, None)),
+    ("vt_is_on_grid", (None, 4, 33, None, None)),
+    ("vt_norm_distance", (None, 4, 9, None, None, None)),
+    ("vt_pack5", (None, -1, None, None, None)),
+    ("vt_unpack5", (None, -1, 5, None, None, None)),
+    ("vt_log_validate", (None, -1, None, None)),
+    ("vt_log_histogram", (None, -1, None, None, None)),
+    ("vt_tau_kth_key", (None, -1, 32, 0, None, None, None, 0, None)),
+    ("vt_tau_budget_key", (None, 10, 32, -1, 0.1, 0.2, None, None, None, None, 0, None)),
+    ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
+                               None)),
+    ("vt_straddle_min", (None, None, -1, 32, None, None, None, None, None)),
+    ("vt_min_f64", (None, -1, None, None, None)),
+    ("vt_sha256_leaves", (None, 0, 4096, None, None)),
+    ("vt_merkle_level", (None, 0, None, None)),
+    ("vt_merkle_build", (None, 0, 4096, None, 0, None)),
+    ("vt_sha256_peak_bench", (None, 0, 1, None)),
+    ("vt_serialize_f32", (None, -1, None, 0, None, None)),
+    ("vt_tau_kth_begin", (-1, None, None, 0, None)),
+    ("vt_tau_kth_hist", (None, 10, 32, 7, None, None, 0, None)),
+    ("vt_tau_kth_select", (9, None, None, 0, None)),
+]
+
+
+@pytest.mark.parametrize("name,args", BAD_CALLS, ids=[c[0] for c in BAD_CALLS])
+def test_entry_points_reject_bad_arguments(name, args):
+    from paper_2403_09603_b200 import _lib
+    lib = _lib.lib()
+    assert getattr(lib, name)(*args) == _lib.VT_EINVAL
+    assert lib.vt_last_error().decode().startswith(name)
+
+
+def test_every_compute_entry_point_is_covered():
+    host_only = {"vt_version", "vt_last_error", "vt_tile_elems", "vt_merkle_node_count", "vt_tau_kth_hist_offset",
+                 "vt_tau_kth_hist_bins"}
+    covered = {c[0] for c in BAD_CALLS}
+    assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}

@@ -443,7 +443,17 @@ def config2() -> dict:
     budgets = [int(0.005 * x.numel()) for x in xs]
     words = torch.empty(sum(budgets) + len(xs), dtype=torch.int64, device="cuda")
     state = {}
-    n_streams = 8  # independent tensors: kernels of different tensors overlap (own workspace per stream)
+
+    def run_batch():
+        # the whole sweep in one batched call: one fused rounding pass over all
+        # 161 tensors + batched selection / filter kernels (fixed launch count)
+        state["batch"] = ops.round_and_log_adaptive_batch(
+            xs, 32, budgets, outs=[ys[o:o + x.numel()] for o, x in zip(offs, xs)],
+            log_outs=[words[w:w + B + 1] for w, B in zip(woffs, budgets)], check=False)
+
+    offs = np.concatenate([[0], np.cumsum([x.numel() for x in xs])[:-1]]).tolist()
+    woffs = np.concatenate([[0], np.cumsum([B + 1 for B in budgets])[:-1]]).tolist()
+    n_streams = 8  # per-tensor calls: kernels of different tensors overlap (own workspace per stream)
     side = [torch.cuda.Stream() for _ in range(n_streams)]
 
     def run():
@@ -464,25 +474,34 @@ def config2() -> dict:
             main.wait_stream(s_)
         state["pend"] = pend
 
-    # the whole 161-tensor sweep (search + device bisection + round-and-log per
-    # tensor, ~20 launches each) is one CUDA graph: no host round trips
-    run()
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        run()
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
-    with torch.cuda.graph(graph):
-        run()
-    ms = _time(graph.replay, reps=5, warm=1)
-    ms_eager = _time(run, reps=2, warm=0)
-    counts = [p.flags.read()[1][0] for p in state["pend"]]
-    taus = [float(p.tau.item()) for p in state["pend"]]
+    def graphed(fn):
+        fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph):
+            fn()
+        return graph
+
+    g_calls = graphed(run)
+    ms_calls = _time(g_calls.replay, reps=5, warm=1)
+    ms_calls_eager = _time(run, reps=2, warm=0)
+    counts_calls = [p.flags.read()[1][0] for p in state["pend"]]
+    taus_calls = [float(p.tau.item()) for p in state["pend"]]
+    g_batch = graphed(run_batch)
+    ms = _time(g_batch.replay, reps=5, warm=1)
+    ms_eager = _time(run_batch, reps=2, warm=0)
+    res = state["batch"].finish()
+    counts = [r[1].count for r in res]
+    taus = [r[2] for r in res]
     assert all(c <= B for c, B in zip(counts, budgets))
-    # spot check: the device-chosen tau equals the host search on one tensor
+    # the batch equals the per-tensor calls, and the device tau the host search
+    assert counts == counts_calls and taus == taus_calls
     k = int(np.argmin([x.numel() for x in xs]))
     assert taus[k] == protocol.search_tau_budget(xs[k], 32, budgets[k])
     t = np.array(taus) / 2.0 ** -24
@@ -490,9 +509,11 @@ def config2() -> dict:
     return {"tensors": len(xs), "elements": total, "ms_per_sweep": round(ms, 3), "ms_per_sweep_eager": round(ms_eager, 3),
             "g_elements_per_s": round(total / ms / 1e6, 2),
             "round_log_gbs_equiv": round(total * (8 + 4 + 8 * logged / total) / ms / 1e6, 1),
+            "ms_per_tensor_calls_8_streams": round(ms_calls, 3), "ms_per_tensor_calls_eager": round(ms_calls_eager, 3),
             "logged_fraction": round(logged / total, 6), "tau_over_2^-24": [round(float(t.min()), 6), round(float(t.max()), 6)],
-            "note": "per tensor: budget select (2-3 streaming passes) + device bisection + round-and-log "
-                    "(ops.round_and_log_adaptive); all 161 tensors in one CUDA graph, 8 concurrent streams"}
+            "note": "ops.round_and_log_adaptive_batch: one fused rounding pass over all 161 tensors (candidates "
+                    "above a per-tensor threshold below tau) + batched exact selection, device bisection and "
+                    "ordered filter; CUDA graph. Per-tensor calls (8 streams, one graph) kept for comparison"}
 
 
 def config3_gpt2(steps: int = 3) -> dict:

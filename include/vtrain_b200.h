@@ -183,6 +183,34 @@ int vt_round_log_adaptive(const double *x, int64_t n, int b_r, int64_t budget, i
                           double *tau_out, int64_t *counters, int32_t *err, void *ws,
                           size_t ws_bytes, vt_stream_t stream);
 /*
+ * The same per-tensor adaptive round-and-log for many independent tensors in
+ * a fixed number of launches (one fused rounding pass over all of them, then
+ * batched selection / filter kernels), e.g. every intermediate of one step
+ * (BASELINE configs[2]).  Per segment, results are identical to
+ * vt_round_log_adaptive on that tensor: *tau_out, the log words
+ * (global_base + i) << 1 | up at log[0 .. flags[2]), the rounded output,
+ * and the error bits OR'ed into (int32_t)flags[0].  flags must be zeroed by
+ * the caller.  x 32-byte aligned, out 16 (FP32) / 32 (FP64) byte aligned, not
+ * overlapping x.  Workspace 256-byte aligned, zero-filled before first use,
+ * vt_round_log_adaptive_batch_workspace(ns, nseg) bytes for the sizes ns[].
+ * Replaces a loop of protocol.search_tau-style selection + _TrainerChannel
+ * .process calls (protocol.py:198-202, 494-506) over a step's tensors.
+ */
+typedef struct vt_adaptive_segment {
+  const double *x;
+  int64_t n;
+  int64_t budget;
+  void *out;
+  uint64_t *log;
+  int64_t log_cap;
+  int64_t global_base;
+  double *tau_out;
+  int64_t *flags;
+} vt_adaptive_segment;
+size_t vt_round_log_adaptive_batch_workspace(const int64_t *ns, int nseg);
+int vt_round_log_adaptive_batch(const vt_adaptive_segment *segs, int nseg, int b_r, int iters,
+                                int out_kind, void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
  * Straddle samples of protocol.collect_divergence_samples (protocol.py:483-490)
  * for two profiles' outputs y1, y2: *count = number of samples (2 per
  * straddling element), *out_min = their minimum (+inf if none),

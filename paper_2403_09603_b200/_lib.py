@@ -60,6 +60,8 @@ EXPORTS: dict[str, tuple] = {
     "vt_round_log_adaptive_workspace": (_sz, [_i64]),
     "vt_round_log_adaptive": (_i32, [_p, _i64, _i32, _i64, _i32, _i32, _p, _p, _i64, _i64, _p, _p, _p, _p, _p,
                                      _p, _sz, _p]),
+    "vt_round_log_adaptive_batch_workspace": (_sz, [_p, _i32]),
+    "vt_round_log_adaptive_batch": (_i32, [_p, _i32, _i32, _i32, _i32, _p, _sz, _p]),
     "vt_straddle_min": (_i32, [_p, _p, _i64, _i32, _p, _p, _p, _p, _p]),
     "vt_min_f64": (_i32, [_p, _i64, _p, _p, _p]),
     "vt_sha256_leaves": (_i32, [_p, _i64, _i64, _p, _p]),
@@ -69,6 +71,15 @@ EXPORTS: dict[str, tuple] = {
     "vt_sha256_peak_bench": (_i32, [_p, _i64, _i32, _p]),
     "vt_serialize_f32": (_i32, [_p, _i64, _p, _i64, _p, _p]),
 }
+
+
+
+class AdaptiveSegment(C.Structure):
+    """``vt_adaptive_segment`` of include/vtrain_b200.h."""
+
+    _fields_ = [("x", _p), ("n", _i64), ("budget", _i64), ("out", _p), ("log", _p), ("log_cap", _i64),
+                ("global_base", _i64), ("tau_out", _p), ("flags", _p)]
+
 
 _LIB: C.CDLL | None = None
 

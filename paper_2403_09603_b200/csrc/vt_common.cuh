@@ -338,6 +338,45 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 
+// Batched trainer pass: up to kMaxBatch tensors in one launch of the fused
+// round-and-log.  The table travels by value as a __grid_constant__ kernel
+// parameter (no descriptor upload, so batches are graph-capturable).  Each
+// tensor owns a contiguous run of tickets [tick0, tick0 + its super-tiles)
+// and the look-back words at the same offsets; its log is its own.
+constexpr int kMaxBatch = 224;
+
+struct RLSeg {
+  const double* x;
+  void* out;
+  uint64_t* sparse;
+  int64_t* cursor_out;  // nullable: entries written (the adaptive candidate count)
+  int64_t* counters;    // counters[0] += entries
+  int32_t* err;
+  const DevThr* dthr;   // nullable: thresholds from the device instead of thr / thr_sub / thr32
+  const int32_t* gate;  // nullable: the tensor is skipped while *gate == 0
+  int64_t n, cap, global_base, tick0;
+  int64_t thr;
+  double thr_sub;
+  int32_t thr32, pad;
+};
+
+struct RLBatch {
+  Grid g;            // b_r-dependent fields (thr / thr_sub per tensor)
+  void* hdr;         // FusedHeader + look-back words (vt_round_log_workspace layout)
+  const int32_t* any;  // nullable: the whole launch does nothing while *any == 0
+  int32_t nseg, pad;
+  int64_t total;     // tickets over all tensors
+  RLSeg seg[kMaxBatch];
+};
+
+__host__ __device__ inline int64_t rl_batch_tickets(int64_t n) {
+  const int64_t tiles = (n + 2047) / 2048;
+  return tiles / 4 + tiles % 4;
+}
+// the batch's look-back words come after a 64-byte header
+inline size_t rl_batch_workspace(int64_t total_tickets) { return (size_t)(64 + total_tickets * 8 + 256); }
+int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st);
+
 }  // namespace vt
 
 // host-side error bookkeeping shared by the ABI translation units

@@ -620,6 +620,260 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// trainer, batched: the same warp-specialised pipeline over many tensors in
+// one launch (configs[2]: 161 tensors of 32 K .. 25.7 M elements).  One
+// persistent grid streams every tensor back to back, so the per-tensor ramp
+// and drain of a separate launch is paid once per batch.
+//
+// Tickets run over all tensors: tensor j owns [tick0_j, tick0_j + its
+// super-tiles) and the look-back words at the same offsets, so the look-back
+// of a ticket stops at its tensor's first super-tile (local ticket 0 = INC 0)
+// and every tensor's log is ordered and positioned on its own.  A gated-off
+// tensor (fallback pass, *gate == 0) is skipped whole: the producer that
+// draws one of its tickets raises the counter to the next tensor's first
+// ticket (atomicMax), so only the tickets of skipped tensors are ever jumped.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int find_seg(const RLBatch& b, int64_t s) {
+  int lo = 0, hi = b.nseg - 1;  // last tensor with tick0 <= s
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.seg[mid].tick0 <= s) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// the fields rlf_write_rows / st_first / st_ntiles read, for tensor j
+__device__ __forceinline__ RLFArgs seg_view(const RLBatch& b, int j) {
+  RLFArgs v;
+  const RLSeg& sg = b.seg[j];
+  v.x = sg.x;
+  v.n = sg.n;
+  v.num_tiles = (sg.n + kSTile - 1) / kSTile;
+  v.n4 = v.num_tiles / kSuper;
+  v.num_super = v.n4 + v.num_tiles % kSuper;
+  v.sparse = sg.sparse;
+  v.cap = sg.cap;
+  v.global_base = sg.global_base;
+  return v;
+}
+
+template <int OUT, bool FAST>
+__global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_constant__ RLBatch b) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (b.any && *b.any == 0) return;
+  FusedHeader* hdr = static_cast<FusedHeader*>(b.hdr);
+  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(b.hdr) + 64);
+  if (tid == 0) {
+    for (int s = 0; s < kFStages; ++s) {
+      mbar_init(S.full + s, 1);
+      mbar_init(S.empty + s, kWarps);
+    }
+    for (int m = 0; m < kMaskSlots; ++m) {
+      mbar_init(S.mfull + m, kWarps);
+      mbar_init(S.ofull + m, 1);
+    }
+    for (int m = 0; m < kMaskSlots; ++m) S.slot_cnt[m] = 0u;
+    fence_mbar_init();
+    S.epoch = ((*(volatile uint32_t*)&hdr->epoch) + 1u) & (uint32_t)kEpochMask;
+  }
+  __syncthreads();
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      // the next ticket of a tensor that runs (skips gated-off tensors whole)
+      auto draw = [&]() -> int64_t {
+        while (true) {
+          const int64_t s = (int64_t)atomicAdd(&hdr->ticket, 1u);
+          if (s >= b.total) return -1;
+          const int j = find_seg(b, s);
+          const int32_t* gate = b.seg[j].gate;
+          if (!gate || *gate != 0) return s;
+          const int64_t next = j + 1 < b.nseg ? b.seg[j + 1].tick0 : b.total;
+          atomicMax(&hdr->ticket, (uint32_t)next);
+        }
+      };
+      int64_t s = draw();
+      int64_t q = 0;  // ring sequence number
+      for (int64_t k = 0;; ++k) {
+        int64_t nxt = -1;
+        int nt = 1;
+        int64_t t0 = 0, full_tiles = 0;
+        const double* x = nullptr;
+        if (s >= 0) {
+          const int j = find_seg(b, s);
+          const RLFArgs v = seg_view(b, j);
+          const int64_t ls = s - b.seg[j].tick0;
+          nt = st_ntiles(v, ls);
+          t0 = st_first(v, ls);
+          full_tiles = v.n / kSTile;
+          x = v.x;
+        }
+#pragma unroll 1
+        for (int i = 0; i < nt; ++i, ++q) {
+          const int st = (int)(q % kFStages);
+          mbar_wait(S.empty + st, (uint32_t)(((q / kFStages) & 1) ^ 1));
+          if (i == 0) S.ids[k & 3] = s;
+          if (i == nt - 1 && s >= 0) nxt = draw();
+          const int64_t t = t0 + i;
+          if (s >= 0 && t < full_tiles) {
+            fence_proxy_async();
+            tma_load(S.ring[st], x + t * kSTile, kSTile * sizeof(double), S.full + st, pol);
+          } else {
+            mbar_arrive(S.full + st);
+          }
+        }
+        if (s < 0) break;
+        s = nxt;
+      }
+    }
+    __syncwarp();
+  } else if (warp == kLogWarp) {
+    const uint32_t epoch = S.epoch;
+    for (int64_t k = 0;; ++k) {
+      const int slot = (int)(k % kMaskSlots);
+      mbar_wait(S.mfull + slot, (uint32_t)((k / kMaskSlots) & 1));
+      const int64_t s = S.slot_id[slot];
+      if (s < 0) break;
+      const int j = find_seg(b, s);
+      const RLSeg& sg = b.seg[j];
+      const RLFArgs v = seg_view(b, j);
+      const int64_t ls = s - sg.tick0;
+      const uint32_t c = (lane / kWarps < st_ntiles(v, ls)) ? S.cnts[slot][lane] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
+      S.rpos[slot][lane] = inc - c;
+      const int64_t excl = lookback128(status + sg.tick0, ls, agg, epoch, lane);
+      if (lane == 0) {
+        if (ls == v.num_super - 1) {
+          if (sg.counters)
+            atomicAdd(reinterpret_cast<unsigned long long*>(sg.counters), (unsigned long long)(excl + (int64_t)agg));
+          if (sg.cursor_out) *sg.cursor_out = excl + (int64_t)agg;
+        }
+        S.sbase[slot] = excl;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(S.ofull + slot);
+    }
+  } else {  // compute warps
+    const uint32_t lt = lanemask_lt();
+    const uint32_t epoch = S.epoch;
+    int64_t h1 = -1, h2 = -1, h3 = -1;  // tickets of ordinals k-1, k-2, k-3
+    int64_t q = 0;
+    auto write_rows = [&](int64_t kk, int64_t s) {
+      const int j = find_seg(b, s);
+      rlf_write_rows(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
+    };
+    for (int64_t k = 0;; ++k) {
+      if (k >= kMaskSlots) write_rows(k - kMaskSlots, h3);
+      const int slot = (int)(k % kMaskSlots);
+      int64_t s = -1, t0 = 0, ls = 0;
+      int nt = 1, j = 0;
+      uint32_t wcnt = 0;
+#pragma unroll 1
+      for (int i = 0; i < nt; ++i, ++q) {
+        const int st = (int)(q % kFStages);
+        mbar_wait(S.full + st, (uint32_t)((q / kFStages) & 1));
+        if (i == 0) {
+          s = S.ids[k & 3];
+          if (s < 0) {
+            ++q;
+            break;
+          }
+          j = find_seg(b, s);
+          ls = s - b.seg[j].tick0;
+          const RLFArgs v = seg_view(b, j);
+          nt = st_ntiles(v, ls);
+          t0 = st_first(v, ls);
+        }
+        const RLSeg& sg = b.seg[j];
+        uint32_t err = 0;
+        Grid g = b.g;
+        int thr32 = sg.thr32;
+        g.thr = sg.thr;
+        g.thr_sub = sg.thr_sub;
+        if (sg.dthr) {
+          g.thr = sg.dthr->thr;
+          g.thr_sub = sg.dthr->thr_sub;
+          thr32 = sg.dthr->thr32;
+        }
+        const uint32_t c8 = ((uint32_t)thr32 + 1u) << 3;
+        const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
+        const int64_t full_tiles = sg.n / kSTile;
+        const int64_t t = t0 + i;
+        const int64_t tbase = t * kSTile;
+        void* o = tile_out<OUT>(sg.out, tbase);
+        uint16_t* row = S.rows[slot][i * kWarps + warp];
+        const uint32_t tc =
+            (t < full_tiles)
+                ? rlf_tile<OUT, FAST, true>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
+                                            (uint32_t)(i * kSTile), warp, lane, lt, err)
+                : rlf_tile<OUT, FAST, false>(g, c8, w8, thr32, sg.x + tbase, o, (int)(sg.n - tbase),
+                                             S.masks[slot][i], row, (uint32_t)(i * kSTile), warp, lane, lt, err);
+        if (lane == 0) S.cnts[slot][i * kWarps + warp] = tc;
+        wcnt += tc;
+        report_err(sg.err, err);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(S.empty + st);
+      }
+      if (lane == 0) {
+        if (s >= 0) {
+          const uint32_t prev = atomicAdd(&S.slot_cnt[slot], wcnt + (1u << 24));
+          if ((prev >> 24) == kWarps - 1) {
+            const uint64_t agg = (prev & 0xffffffu) + wcnt;
+            st_relaxed_u64(status + s, lb_word(epoch, ls == 0 ? kLBInc : kLBAgg, agg));
+            S.slot_cnt[slot] = 0u;
+          }
+        }
+        if (warp == 0) S.slot_id[slot] = s;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(S.mfull + slot);
+      if (s < 0) {
+        if (k >= 2) write_rows(k - 2, h2);
+        if (k >= 1) write_rows(k - 1, h1);
+        break;
+      }
+      h3 = h2;
+      h2 = h1;
+      h1 = s;
+    }
+  }
+
+  __syncthreads();
+  __shared__ uint32_t s_last;
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(&hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const uint32_t hwm = max(hdr->hwm, (uint32_t)b.total);
+  if (S.epoch == (uint32_t)kEpochMask) {
+    __threadfence();
+    for (uint32_t i = tid; i < hwm; i += blockDim.x) status[i] = 0ull;
+    __threadfence();
+    __syncthreads();
+  }
+  if (tid == 0) {
+    hdr->ticket = 0u;
+    hdr->done = 0u;
+    hdr->hwm = hwm;
+    hdr->epoch = S.epoch == (uint32_t)kEpochMask ? 0u : S.epoch;
+    __threadfence();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // auditor: streaming replay against the sparse log
 // ---------------------------------------------------------------------------
 
@@ -982,6 +1236,36 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
   return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, false>(f, st)
        : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, false>(f, st)
                                 : launch_rlf<VT_OUT_NONE, false>(f, st);
+}
+
+template <int OUT, bool FAST>
+static int launch_rlb(const RLBatch& b, cudaStream_t st) {
+  static_assert(sizeof(RLBatch) <= 32000, "batch table must fit the kernel parameter space");
+  const size_t smem = sizeof(FusedSmem);
+  auto k = rl_batch_kernel<OUT, FAST>;
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kFThreads, smem);
+    resident = std::max(1, per * sms);
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(b.total, resident));
+  k<<<grid, kFThreads, smem, st>>>(b);
+  return vt_check_launch("rl_batch_kernel");
+}
+
+int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st) {
+  if (fast) {
+    return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, true>(b, st)
+         : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, true>(b, st)
+                                  : launch_rlb<VT_OUT_NONE, true>(b, st);
+  }
+  return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, false>(b, st)
+       : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, false>(b, st)
+                                : launch_rlb<VT_OUT_NONE, false>(b, st);
 }
 
 template <int OUT, bool FAST>

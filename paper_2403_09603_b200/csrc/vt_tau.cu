@@ -15,6 +15,7 @@
 // prefix on the device, so no host round trip happens between passes.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "vt_common.cuh"
 
@@ -225,7 +226,7 @@ struct BudState {
 // threads); `sh` = kBudBins words of shared memory.
 __device__ void bud_pass_body(const double* __restrict__ x, int64_t n, const Grid& g, BudState* st,
                               uint32_t* __restrict__ hist, uint64_t* __restrict__ cand, int32_t* errp,
-                              uint32_t* sh) {
+                              uint32_t* sh, int64_t blk, int64_t nblk) {
   __shared__ unsigned long long s_above;
   const int level = st->level;
   const bool compact = st->compacting != 0;
@@ -244,7 +245,7 @@ __device__ void bud_pass_body(const double* __restrict__ x, int64_t n, const Gri
   // fast path valid for b_r = 32 over the default bisection range (2^-25, 2^-24]
   const bool fast32 = g.drop == 29 && lo == 0x3E60000000000000ull && hi == 0x3E70000000000000ull;
   // four consecutive elements per thread per step (one 256-bit load)
-  for (int64_t base = (int64_t)blockIdx.x * 1024; base < n; base += (int64_t)gridDim.x * 1024) {
+  for (int64_t base = blk * 1024; base < n; base += nblk * 1024) {
     const int64_t i0 = base + 4 * threadIdx.x;
     D4 xv;
     if (vec && i0 + 3 < n) {
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(256) bud_pass_kernel(const double* __restrict_
                                                        uint64_t* __restrict__ cand, int32_t* errp) {
   __shared__ uint32_t sh[kBudBins];
   if (st->status != 0) return;
-  bud_pass_body(x, n, g, st, hist, cand, errp, sh);
+  bud_pass_body(x, n, g, st, hist, cand, errp, sh, blockIdx.x, gridDim.x);
 }
 
 // Copy a global histogram into shared memory with batches of independent
@@ -502,11 +503,18 @@ __global__ void bud_init_kernel(BudState* st, uint64_t lo_key, uint64_t hi_key, 
 
 using namespace vt;
 
+namespace vt {
+__host__ __device__ constexpr size_t tau_ws_bytes() {
+  return ((size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256) > (512 + (size_t)kBudMaxLevels * kBudBins * 4 +
+                                                                  (size_t)kCandCap * 8)
+             ? ((size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256)
+             : (512 + (size_t)kBudMaxLevels * kBudBins * 4 + (size_t)kCandCap * 8);
+}
+}  // namespace vt
+
 extern "C" size_t vt_tau_workspace(int64_t n) {
   (void)n;
-  const size_t radix = (size_t)kPasses * kMaxBins * sizeof(uint32_t) + 256;
-  const size_t budget = 512 + (size_t)kBudMaxLevels * kBudBins * 4 + (size_t)kCandCap * 8;
-  return std::max(radix, budget);
+  return tau_ws_bytes();
 }
 
 extern "C" int vt_tau_budget_key(const double* x, int64_t n, int b_r, int64_t budget, double tau_lo,
@@ -678,27 +686,29 @@ struct AdaptHdr {
 };
 
 // keys are FP64 bit patterns of p >= 0, so integer order is numeric order
-__device__ __forceinline__ bool last_cta(uint32_t* arrived) {
+__device__ __forceinline__ bool last_cta(uint32_t* arrived, uint32_t count) {
   __shared__ unsigned s_last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(arrived, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) s_last = atomicAdd(arrived, 1u) == count - 1;
   __syncthreads();
   if (s_last) __threadfence();
   return s_last != 0;
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __restrict__ x, Grid g,
-                                                                const uint64_t* __restrict__ cw,
-                                                                uint64_t* __restrict__ ck, int64_t cap,
-                                                                int64_t budget, uint64_t L_key, uint64_t hi_key,
-                                                                int s0, AdaptHdr* h, uint32_t* __restrict__ hist,
-                                                                uint64_t* __restrict__ fstatus, bool gather) {
+// blk / nblk: this CTA's index among the CTAs working on the tensor (the
+// whole grid for a single call, the tensor's share of a batched grid)
+__device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, const Grid& g,
+                                                const uint64_t* __restrict__ cw, uint64_t* __restrict__ ck,
+                                                int64_t cap, int64_t budget, uint64_t L_key, uint64_t hi_key, int s0,
+                                                AdaptHdr* h, uint32_t* __restrict__ hist,
+                                                uint64_t* __restrict__ fstatus, bool gather, int64_t blk,
+                                                int64_t nblk) {
   __shared__ uint32_t sh[kAdBins];
   __shared__ unsigned long long s_above;
   const int64_t M = h->ccount;
   if (M > cap || M < budget + 1) {  // v <= L, or too many candidates: the exact path decides
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blk == 0 && threadIdx.x == 0) {
       // unless at most budget keys exceed tau_lo at all (in-place calls count
       // them): then v <= tau_lo and the bisection result is fixed
       const bool low = !gather && M <= cap && (int64_t)h->above_lo <= budget;
@@ -707,24 +717,42 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
     }
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) h->fallback = 0;
-  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < (M + kFChunk - 1) / kFChunk;
-       i += (int64_t)gridDim.x * kAdThreads)
+  if (blk == 0 && threadIdx.x == 0) h->fallback = 0;
+  for (int64_t i = blk * kAdThreads + threadIdx.x; i < (M + kFChunk - 1) / kFChunk;
+       i += nblk * kAdThreads)
     fstatus[i] = 0ull;  // the filter's look-back words for this call's chunks
   for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0;
   if (threadIdx.x == 0) s_above = 0;
   __syncthreads();
   uint32_t err = 0, above = 0;
-  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < M; i += (int64_t)gridDim.x * kAdThreads) {
-    uint64_t key;
+  // kGU independent gathers in flight per thread: the candidates sit ~1/67
+  // apart in x, so every one is its own DRAM line and latency-bound
+  constexpr int kGU = 8;
+  const int64_t stride = nblk * kAdThreads;
+  for (int64_t i0 = blk * kAdThreads + threadIdx.x; i0 < M; i0 += kGU * stride) {
+    uint64_t key[kGU];
     if (gather) {
-      key = dist_key(__ldg(x + (cw[i] >> 1)), g, err);
-      ck[i] = key;
+      uint64_t w[kGU];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
+      double xv[kGU];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? __ldg(x + (w[u] >> 1)) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        key[u] = dist_key(xv[u], g, err);
+        if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];
+      }
     } else {
-      key = ck[i];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) key[u] = (i0 + u * stride < M) ? ck[i0 + u * stride] : 0ull;
     }
-    if (key > hi_key) ++above;
-    else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      if (i0 + u * stride >= M) break;
+      if (key[u] > hi_key) ++above;
+      else if (key[u] > L_key) atomicAdd(&sh[(uint32_t)((key[u] - L_key - 1) >> s0)], 1u);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
   if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, (unsigned long long)above);
@@ -732,7 +760,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
   for (int i = threadIdx.x; i < kAdBins; i += kAdThreads)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
   if (threadIdx.x == 0 && s_above) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above), s_above);
-  if (!last_cta(&h->arrived)) return;
+  if (!last_cta(&h->arrived, (uint32_t)nblk)) return;
   // last CTA: the digit of the (budget+1)-th largest key
   const int64_t above_hi = (int64_t)h->above;
   if (above_hi > budget) {
@@ -757,6 +785,15 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __
   }
 }
 
+__global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __restrict__ x, Grid g,
+                                                                const uint64_t* __restrict__ cw,
+                                                                uint64_t* __restrict__ ck, int64_t cap,
+                                                                int64_t budget, uint64_t L_key, uint64_t hi_key,
+                                                                int s0, AdaptHdr* h, uint32_t* __restrict__ hist,
+                                                                uint64_t* __restrict__ fstatus, bool gather) {
+  adapt_hist_body(x, g, cw, ck, cap, budget, L_key, hi_key, s0, h, hist, fstatus, gather, blockIdx.x, gridDim.x);
+}
+
 // One FP64 bisection thread: the search_tau skeleton on the selected key.
 __device__ void bisect_to(uint64_t key, double lower, double upper, int iters, DevThr* out, double* tau_out) {
   const double v = __longlong_as_double((long long)key);
@@ -769,15 +806,14 @@ __device__ void bisect_to(uint64_t key, double lower, double upper, int iters, D
   *tau_out = upper;
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t* __restrict__ ck, uint64_t L_key,
-                                                                  uint64_t hi_key, int s0, AdaptHdr* h,
-                                                                  uint64_t* __restrict__ cand2, double lower,
-                                                                  double upper, int iters, DevThr* dthr,
-                                                                  double* tau_out, uint64_t* key_out) {
+__device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ ck, uint64_t L_key, uint64_t hi_key,
+                                                  int s0, AdaptHdr* h, uint64_t* __restrict__ cand2, double lower,
+                                                  double upper, int iters, DevThr* dthr, double* tau_out,
+                                                  uint64_t* key_out, int64_t blk, int64_t nblk) {
   __shared__ uint32_t sh[kAdBins];
   if (h->fallback) return;
   if (h->done) {  // 1: more than budget keys above tau_hi (v > tau_hi); 2: v <= tau_lo
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blk == 0 && threadIdx.x == 0) {
       const uint64_t v = h->done == 1 ? 0x7ff0000000000000ull : (uint64_t)__double_as_longlong(lower);
       *key_out = v;
       bisect_to(v, lower, upper, iters, dthr, tau_out);
@@ -790,7 +826,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t
   const uint64_t digit = h->digit;
   const uint64_t lo1 = L_key + 1;
   const int lane = threadIdx.x & 31;
-  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
+  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += nblk * kAdThreads) {
     const int64_t i = i0 + threadIdx.x;
     uint64_t key = 0;
     bool in = false;
@@ -807,7 +843,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t
       if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key - lo1;
     }
   }
-  if (!last_cta(&h->arrived)) return;
+  if (!last_cta(&h->arrived, (uint32_t)nblk)) return;
   // last CTA: exact selection of the rank-th largest among the digit's keys
   const int64_t m = (int64_t)h->cand2;
   int64_t rank = h->rank;
@@ -840,6 +876,15 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t
   }
 }
 
+__global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t* __restrict__ ck, uint64_t L_key,
+                                                                  uint64_t hi_key, int s0, AdaptHdr* h,
+                                                                  uint64_t* __restrict__ cand2, double lower,
+                                                                  double upper, int iters, DevThr* dthr,
+                                                                  double* tau_out, uint64_t* key_out) {
+  adapt_select_body(ck, L_key, hi_key, s0, h, cand2, lower, upper, iters, dthr, tau_out, key_out, blockIdx.x,
+                    gridDim.x);
+}
+
 // The log: candidates with p > tau, in order.  Persistent CTAs draw chunk
 // tickets; each chunk's kept count goes through an epoch-tagged decoupled
 // look-back over the chunk status words (the status word format of the
@@ -851,12 +896,10 @@ __device__ __forceinline__ uint64_t lbw(uint32_t e, uint64_t f, uint64_t v) {
   return ((uint64_t)e << kLBShift) | f | (v & kLBV);
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t* __restrict__ cw,
-                                                                  const uint64_t* __restrict__ ck, AdaptHdr* h,
-                                                                  const DevThr* dthr, uint64_t* sparse, int64_t cap,
-                                                                  int64_t global_base, const int64_t* cursor_in,
-                                                                  int64_t* cursor_out, int64_t* counters,
-                                                                  uint64_t* status) {
+__device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ cw, const uint64_t* __restrict__ ck,
+                                                  AdaptHdr* h, const DevThr* dthr, uint64_t* sparse, int64_t cap,
+                                                  int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
+                                                  int64_t* counters, uint64_t* status, int64_t nblk) {
   constexpr int kPer = kFChunk / kAdThreads;  // 8 candidates per thread
   __shared__ uint32_t s_warp[kAdThreads / 32];
   __shared__ int64_t s_t, s_base;
@@ -946,7 +989,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t
       }
     }
   }
-  if (last_cta(&h->f_done)) {
+  if (last_cta(&h->f_done, (uint32_t)nblk)) {
     if (tid == 0) {
       h->f_ticket = 0u;
       h->f_done = 0u;
@@ -954,6 +997,15 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t
       __threadfence();
     }
   }
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t* __restrict__ cw,
+                                                                  const uint64_t* __restrict__ ck, AdaptHdr* h,
+                                                                  const DevThr* dthr, uint64_t* sparse, int64_t cap,
+                                                                  int64_t global_base, const int64_t* cursor_in,
+                                                                  int64_t* cursor_out, int64_t* counters,
+                                                                  uint64_t* status) {
+  adapt_filter_body(cw, ck, h, dthr, sparse, cap, global_base, cursor_in, cursor_out, counters, status, gridDim.x);
 }
 
 // In-place calls: one streaming read of x appends the keys above L
@@ -1037,8 +1089,8 @@ __global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_kernel(const doub
   __shared__ uint32_t sh[kBudBins];
   if (!h->fallback || st->status != 0) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) h->above_lo = 0;
-  bud_pass_body(x, n, g, st, hist, cand, errp, sh);
-  if (!last_cta(&h->arrived)) return;
+  bud_pass_body(x, n, g, st, hist, cand, errp, sh, blockIdx.x, gridDim.x);
+  if (!last_cta(&h->arrived, gridDim.x)) return;
   if (threadIdx.x == 0) h->arrived = 0u;
   bud_step_body(st, hist, cand, budget, key_out, sh);
   __syncthreads();
@@ -1046,7 +1098,7 @@ __global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_kernel(const doub
 }
 }  // namespace vt
 
-namespace {
+namespace vt {
 // Adaptive workspace: [header 256 B: DevThr, key, status, AdaptHdr]
 // [candidate digit histogram] [tau workspace (exact fallback)] [round-and-log
 // workspace] [filter status] [candidate words | keys | digit keys: cap each].
@@ -1058,17 +1110,19 @@ struct AdaptLayout {
   size_t tau, rl, hist, cw, ck, c2, fst, total;
   int64_t cap;
 };
-size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
-AdaptLayout adapt_layout(int64_t n) {
+__host__ __device__ inline size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
+// rl_bytes: the tensor's own round-and-log workspace (0 in a batch, whose
+// rounding passes share one)
+__host__ __device__ inline AdaptLayout adapt_layout_rl(int64_t n, size_t rl_bytes) {
   AdaptLayout L;
-  L.cap = std::max<int64_t>(8192, (n + 15) / 16);
+  L.cap = (n + 15) / 16 > 8192 ? (n + 15) / 16 : 8192;
   size_t o = 256;
   L.hist = o;
   o += al256((size_t)kAdBins * 4);
   L.tau = o;
-  o += al256(vt_tau_workspace(n));  // size independent of n
+  o += al256(tau_ws_bytes());
   L.rl = o;
-  o += al256(vt_round_log_workspace(n));
+  o += al256(rl_bytes);
   L.fst = o;
   o += al256((size_t)((L.cap + kFChunk - 1) / kFChunk) * 8);
   L.cw = o;
@@ -1080,6 +1134,39 @@ AdaptLayout adapt_layout(int64_t n) {
   L.total = o;
   return L;
 }
+
+struct AdPtrs {
+  DevThr* dthr;
+  uint64_t* key;
+  AdaptHdr* h;
+  BudState* st;
+  uint32_t *bhist, *ahist;
+  uint64_t *bcand, *cw, *ck, *c2, *fst;
+  int64_t cap;
+};
+
+__host__ __device__ inline AdPtrs adapt_ptrs(uint8_t* w, const AdaptLayout& lay) {
+  AdPtrs p;
+  p.dthr = reinterpret_cast<DevThr*>(w);
+  p.key = reinterpret_cast<uint64_t*>(w + 64);
+  p.h = reinterpret_cast<AdaptHdr*>(w + 128);
+  uint8_t* tws = w + lay.tau;
+  p.st = reinterpret_cast<BudState*>(tws);
+  p.bhist = reinterpret_cast<uint32_t*>(tws + 512);
+  p.bcand = reinterpret_cast<uint64_t*>(tws + 512 + (size_t)kBudMaxLevels * kBudBins * 4);
+  p.ahist = reinterpret_cast<uint32_t*>(w + lay.hist);
+  p.cw = reinterpret_cast<uint64_t*>(w + lay.cw);
+  p.ck = reinterpret_cast<uint64_t*>(w + lay.ck);
+  p.c2 = reinterpret_cast<uint64_t*>(w + lay.c2);
+  p.fst = reinterpret_cast<uint64_t*>(w + lay.fst);
+  p.cap = lay.cap;
+  return p;
+}
+
+}  // namespace vt
+
+namespace {
+AdaptLayout adapt_layout(int64_t n) { return adapt_layout_rl(n, vt_round_log_workspace(n)); }
 int adapt_grid(int64_t work, int per) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work + per - 1) / per, 148 * 4));
 }
@@ -1104,19 +1191,16 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
   const AdaptLayout lay = adapt_layout(n);
-  DevThr* dthr = reinterpret_cast<DevThr*>(w);
-  uint64_t* key = reinterpret_cast<uint64_t*>(w + 64);
-  AdaptHdr* h = reinterpret_cast<AdaptHdr*>(w + 128);
-  uint8_t* tws = w + lay.tau;
-  BudState* st = reinterpret_cast<BudState*>(tws);
-  uint32_t* bhist = reinterpret_cast<uint32_t*>(tws + 512);
-  uint64_t* bcand = reinterpret_cast<uint64_t*>(tws + 512 + (size_t)kBudMaxLevels * kBudBins * 4);
+  const AdPtrs P = adapt_ptrs(w, lay);
+  DevThr* dthr = P.dthr;
+  uint64_t* key = P.key;
+  AdaptHdr* h = P.h;
+  BudState* st = P.st;
+  uint32_t* bhist = P.bhist;
+  uint64_t* bcand = P.bcand;
   void* rws = w + lay.rl;
-  uint32_t* ahist = reinterpret_cast<uint32_t*>(w + lay.hist);
-  uint64_t* cw = reinterpret_cast<uint64_t*>(w + lay.cw);
-  uint64_t* ck = reinterpret_cast<uint64_t*>(w + lay.ck);
-  uint64_t* c2 = reinterpret_cast<uint64_t*>(w + lay.c2);
-  uint64_t* fst = reinterpret_cast<uint64_t*>(w + lay.fst);
+  uint32_t* ahist = P.ahist;
+  uint64_t *cw = P.cw, *ck = P.ck, *c2 = P.c2, *fst = P.fst;
   const bool fast = b_r == 32;
   const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
   uint64_t lo_key, hi_key;
@@ -1182,6 +1266,278 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   // the rounding pass at the device tau: always for in-place calls, else only after a fallback
   return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
                    cursor_out, counters, err, rws, s, dthr, aliased ? nullptr : &h->fallback);
+}
+
+
+// ---------------------------------------------------------------------------
+// Batched adaptive round-and-log: many independent tensors (configs[2]: the
+// 161 ResNet-50 intermediates), each with its own budget, tau and log, in a
+// fixed number of launches instead of ~12 per tensor:
+//
+//   rl_batch_kernel (candidate pass) -> adapt_hist_batch -> adapt_select_batch
+//   -> adapt_filter_batch -> [exact fallback: adapt_fb_init_batch, 6 x
+//   adapt_fb_pass_batch, rl_batch_kernel gated per tensor]
+//
+// Same per-tensor algorithm and state as vt_round_log_adaptive (the kernel
+// bodies are shared); each tensor gets a share of the tail grids in
+// proportion to its expected candidate count, and the per-tensor "last CTA"
+// steps count that share.  The tables travel as __grid_constant__ kernel
+// parameters, so a batch is graph-capturable with no descriptor upload.
+// ---------------------------------------------------------------------------
+namespace vt {
+
+struct AdSeg {
+  const double* x;
+  uint8_t* ws;        // the tensor's adaptive state (adapt_layout_rl(n, 0))
+  uint64_t* log;
+  int64_t* flags;     // int32 error bits at flags[0], log entries at flags[2]
+  double* tau_out;
+  int64_t n, budget, log_cap, global_base;
+  uint64_t L_key;
+  int32_t s0, blk0;   // top-digit shift; first CTA of the tensor in the tail grids
+};
+
+// the batch's fallback roster: which tensors run the exact selection
+struct FbRoster {
+  int32_t count;
+  int32_t pad[63];
+  int32_t list[kMaxBatch];
+};
+
+struct AdBatch {
+  Grid g0;
+  double lo, hi;
+  uint64_t lo_key, hi_key;
+  FbRoster* fb;
+  int32_t nseg, nblk, iters, pad;
+  AdSeg seg[kMaxBatch];
+};
+
+__device__ __forceinline__ int ad_find(const AdBatch& b, int64_t blk) {
+  int lo = 0, hi = b.nseg - 1;  // last tensor with blk0 <= blk
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.seg[mid].blk0 <= blk) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t ad_nblk(const AdBatch& b, int j) {
+  return (j + 1 < b.nseg ? b.seg[j + 1].blk0 : b.nblk) - b.seg[j].blk0;
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_hist_batch_kernel(const __grid_constant__ AdBatch b) {
+  const int j = ad_find(b, blockIdx.x);
+  const AdSeg& sg = b.seg[j];
+  const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
+  if (blockIdx.x == 0 && threadIdx.x == 0) b.fb->count = 0;  // the previous batch's fallback kernels are done
+  adapt_hist_body(sg.x, b.g0, p.cw, p.ck, p.cap, sg.budget, sg.L_key, b.hi_key, sg.s0, p.h, p.ahist, p.fst, true,
+                  (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_select_batch_kernel(const __grid_constant__ AdBatch b) {
+  const int j = ad_find(b, blockIdx.x);
+  const AdSeg& sg = b.seg[j];
+  const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
+  adapt_select_body(p.ck, sg.L_key, b.hi_key, sg.s0, p.h, p.c2, b.lo, b.hi, b.iters, p.dthr, sg.tau_out, p.key,
+                    (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_filter_batch_kernel(const __grid_constant__ AdBatch b) {
+  const int j = ad_find(b, blockIdx.x);
+  const AdSeg& sg = b.seg[j];
+  const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
+  adapt_filter_body(p.cw, p.ck, p.h, p.dthr, sg.log, sg.log_cap, sg.global_base, nullptr, nullptr, sg.flags + 2,
+                    p.fst, ad_nblk(b, j));
+}
+
+// exact fallback, one CTA per tensor: fresh selection state and a roster
+// entry where needed (the later fallback kernels visit only the roster)
+__global__ void adapt_fb_init_batch_kernel(const __grid_constant__ AdBatch b) {
+  const AdSeg& sg = b.seg[blockIdx.x];
+  const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
+  if (!p.h->fallback) return;
+  for (int i = threadIdx.x; i < kBudMaxLevels * kBudBins; i += blockDim.x) p.bhist[i] = 0u;
+  if (threadIdx.x == 0) {
+    bud_init_body(p.st, b.lo_key, b.hi_key, p.key);
+    b.fb->list[atomicAdd(&b.fb->count, 1)] = (int32_t)blockIdx.x;
+  }
+}
+
+// one selection pass of every tensor still running the exact fallback; the
+// whole grid streams each such tensor in turn, its last CTA takes the step
+__global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_batch_kernel(const __grid_constant__ AdBatch b) {
+  __shared__ uint32_t sh[kBudBins];
+  const int nfb = *(volatile int32_t*)&b.fb->count;
+  for (int k = 0; k < nfb; ++k) {
+    const AdSeg& sg = b.seg[b.fb->list[k]];
+    const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
+    if (!p.h->fallback || p.st->status != 0) continue;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.h->above_lo = 0;
+    int32_t* err = reinterpret_cast<int32_t*>(sg.flags);
+    bud_pass_body(sg.x, sg.n, b.g0, p.st, p.bhist, p.bcand, err, sh, blockIdx.x, gridDim.x);
+    if (last_cta(&p.h->arrived, gridDim.x)) {
+      if (threadIdx.x == 0) p.h->arrived = 0u;
+      bud_step_body(p.st, p.bhist, p.bcand, sg.budget, p.key, sh);
+      __syncthreads();
+      if (threadIdx.x == 0 && p.st->status != 0) bisect_to(*p.key, b.lo, b.hi, b.iters, p.dthr, sg.tau_out);
+    }
+    __syncthreads();
+  }
+}
+}  // namespace vt
+
+namespace {
+size_t batch_rl_bytes(const int64_t* n, int nseg) {
+  int64_t worst = 0;  // the largest chunk's tickets: chunks run one after another on one stream
+  for (int c = 0; c < nseg; c += kMaxBatch) {
+    int64_t t = 0;
+    for (int j = c; j < std::min(nseg, c + kMaxBatch); ++j) t += rl_batch_tickets(n[j]);
+    worst = std::max(worst, t);
+  }
+  return al256(sizeof(FbRoster)) + al256(rl_batch_workspace(worst));
+}
+}  // namespace
+
+extern "C" size_t vt_round_log_adaptive_batch_workspace(const int64_t* n, int nseg) {
+  if (!n || nseg <= 0) return 0;
+  size_t total = batch_rl_bytes(n, nseg);
+  for (int j = 0; j < nseg; ++j) total += adapt_layout_rl(std::max<int64_t>(n[j], 0), 0).total;
+  return total;
+}
+
+extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int nseg, int b_r, int iters,
+                                           int out_kind, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (!segs || nseg <= 0 || b_r < 10 || b_r > 32 || iters < 0 || !ws || reinterpret_cast<uintptr_t>(ws) % 256 ||
+      (out_kind != VT_OUT_F32 && out_kind != VT_OUT_F64)) {
+    vt_set_error("vt_round_log_adaptive_batch: bad argument");
+    return VT_EINVAL;
+  }
+  std::vector<int64_t> ns((size_t)nseg);
+  const size_t ybytes = out_kind == VT_OUT_F64 ? 8 : 4;
+  for (int j = 0; j < nseg; ++j) {
+    const vt_adaptive_segment& sg = segs[j];
+    ns[(size_t)j] = sg.n;
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(sg.x), ya = reinterpret_cast<uintptr_t>(sg.out);
+    if (sg.n <= 0 || !sg.x || !sg.out || !sg.log || !sg.tau_out || !sg.flags || sg.budget < 0 ||
+        sg.log_cap < 0 || (xa & 31) || (ya & (out_kind == VT_OUT_F64 ? 31 : 15))) {
+      vt_set_error("vt_round_log_adaptive_batch: bad segment (n > 0, x 32-byte aligned, output aligned)");
+      return VT_EINVAL;
+    }
+    if (ya < xa + (uintptr_t)sg.n * 8 && xa < ya + (uintptr_t)sg.n * ybytes) {
+      vt_set_error("vt_round_log_adaptive_batch: in-place segments are not batched (use vt_round_log_adaptive)");
+      return VT_EINVAL;
+    }
+  }
+  if (ws_bytes < vt_round_log_adaptive_batch_workspace(ns.data(), nseg)) {
+    vt_set_error("vt_round_log_adaptive_batch: workspace too small");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  FbRoster* roster = reinterpret_cast<FbRoster*>(w);
+  void* rl_hdr = w + al256(sizeof(FbRoster));
+  uint8_t* seg_ws = w + batch_rl_bytes(ns.data(), nseg);
+  const bool fast = b_r == 32;
+  const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
+  uint64_t lo_key, hi_key;
+  memcpy(&lo_key, &lo, 8);
+  memcpy(&hi_key, &hi, 8);
+  const Grid g0 = make_grid(b_r, 0.0);
+  int rc = 0;
+  for (int c0 = 0; c0 < nseg; c0 += kMaxBatch) {
+    const int m = std::min(nseg - c0, kMaxBatch);
+    RLBatch cand{}, fb{};
+    AdBatch ab{};
+    cand.g = fb.g = g0;
+    cand.hdr = fb.hdr = rl_hdr;
+    cand.nseg = fb.nseg = ab.nseg = m;
+    ab.g0 = g0;
+    ab.lo = lo;
+    ab.hi = hi;
+    ab.lo_key = lo_key;
+    ab.hi_key = hi_key;
+    ab.iters = iters;
+    ab.fb = roster;
+    fb.any = &roster->count;
+    int64_t tick = 0, blk = 0;
+    for (int i = 0; i < m; ++i) {
+      const vt_adaptive_segment& sg = segs[c0 + i];
+      const int64_t n = sg.n, budget = sg.budget;
+      const AdaptLayout lay = adapt_layout_rl(n, 0);
+      const AdPtrs p = adapt_ptrs(seg_ws, lay);
+      // candidate threshold and top-digit width: as vt_round_log_adaptive
+      const double want = (double)kCandFactor * (double)(budget + 1) + 1024.0;
+      double L = hi * (1.0 - want / (double)n);
+      if (!(L > lo)) L = lo;
+      uint64_t L_key;
+      memcpy(&L_key, &L, 8);
+      const uint64_t W = hi_key - L_key;
+      const int wbits = W > 1 ? 64 - __builtin_clzll(W - 1) : 1;
+      const Grid gL = make_grid(b_r, L);
+      int32_t* err = reinterpret_cast<int32_t*>(sg.flags);
+      RLSeg& rc_ = cand.seg[i];
+      rc_.x = sg.x;
+      rc_.out = sg.out;
+      rc_.sparse = p.cw;
+      rc_.cursor_out = &p.h->ccount;
+      rc_.counters = &p.h->scratch;
+      rc_.err = err;
+      rc_.n = n;
+      rc_.cap = p.cap;
+      rc_.global_base = 0;
+      rc_.tick0 = tick;
+      rc_.thr = gL.thr;
+      rc_.thr_sub = gL.thr_sub;
+      rc_.thr32 = (int32_t)std::min<int64_t>(std::max<int64_t>(gL.thr, 0), INT32_MAX);
+      RLSeg& rf = fb.seg[i];
+      rf = rc_;
+      rf.sparse = sg.log;
+      rf.cursor_out = nullptr;
+      rf.counters = sg.flags + 2;
+      rf.cap = sg.log_cap;
+      rf.global_base = sg.global_base;
+      rf.dthr = p.dthr;
+      rf.gate = &p.h->fallback;
+      tick += rl_batch_tickets(n);
+      AdSeg& a = ab.seg[i];
+      a.x = sg.x;
+      a.ws = seg_ws;
+      a.log = sg.log;
+      a.flags = sg.flags;
+      a.tau_out = sg.tau_out;
+      a.n = n;
+      a.budget = budget;
+      a.log_cap = sg.log_cap;
+      a.global_base = sg.global_base;
+      a.L_key = L_key;
+      a.s0 = std::max(0, wbits - 13);
+      a.blk0 = (int32_t)blk;
+      blk += std::max<int64_t>(1, std::min<int64_t>((int64_t)(want + kFChunk - 1) / kFChunk, 148 * 4));
+      seg_ws += lay.total;
+    }
+    cand.total = fb.total = tick;
+    ab.nblk = (int32_t)blk;
+    // 1. rounding pass over every tensor: y + ordered candidate words
+    if ((rc = rl_stream_batch(cand, fast, out_kind, s))) return rc;
+    // 2-4. per tensor: digit histogram, exact selection + bisection, ordered filter
+    adapt_hist_batch_kernel<<<(unsigned)blk, kAdThreads, 0, s>>>(ab);
+    if ((rc = vt_check_launch("adapt_hist_batch_kernel"))) return rc;
+    adapt_select_batch_kernel<<<(unsigned)blk, kAdThreads, 0, s>>>(ab);
+    if ((rc = vt_check_launch("adapt_select_batch_kernel"))) return rc;
+    adapt_filter_batch_kernel<<<(unsigned)blk, kAdThreads, 0, s>>>(ab);
+    if ((rc = vt_check_launch("adapt_filter_batch_kernel"))) return rc;
+    // exact fallback for the tensors whose candidates could not decide (no-ops otherwise)
+    adapt_fb_init_batch_kernel<<<(unsigned)m, 256, 0, s>>>(ab);
+    if ((rc = vt_check_launch("adapt_fb_init_batch_kernel"))) return rc;
+    for (int p = 0; p <= kBudMaxLevels; ++p) {
+      adapt_fb_pass_batch_kernel<<<148 * 4, kAdThreads, 0, s>>>(ab);
+      if ((rc = vt_check_launch("adapt_fb_pass_batch_kernel"))) return rc;
+    }
+    if ((rc = rl_stream_batch(fb, fast, out_kind, s))) return rc;
+  }
+  return 0;
 }
 
 namespace {

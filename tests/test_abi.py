@@ -82,6 +82,7 @@ BAD_CALLS = [
     ("vt_tau_budget_key", (None, 10, 32, -1, 0.1, 0.2, None, None, None, None, 0, None)),
     ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
                                None)),
+    ("vt_round_log_adaptive_batch", (None, 0, 32, 30, 1, None, 0, None)),
     ("vt_straddle_min", (None, None, -1, 32, None, None, None, None, None)),
     ("vt_min_f64", (None, -1, None, None, None)),
     ("vt_sha256_leaves", (None, 0, 4096, None, None)),
@@ -108,3 +109,27 @@ def test_every_compute_entry_point_is_covered():
                  "vt_tau_kth_hist_bins"}
     covered = {c[0] for c in BAD_CALLS}
     assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}
+
+
+def test_adaptive_batch_validates_segments_on_the_host():
+    """Segments are checked before any launch: empty, misaligned, in-place."""
+    import ctypes as C
+    from paper_2403_09603_b200 import _lib
+    lib = _lib.lib()
+    ns = (C.c_int64 * 3)(1000, 1 << 20, 7)
+    total = lib.vt_round_log_adaptive_batch_workspace(ns, 3)
+    assert total >= sum(lib.vt_round_log_adaptive_workspace(n) - lib.vt_round_log_workspace(n) for n in ns) > 0
+    fake = 1 << 40  # never dereferenced: validation fails first
+
+    def seg(**kw):
+        d = dict(x=fake, n=1000, budget=5, out=fake + (1 << 30), log=fake + (2 << 30), log_cap=6, global_base=0,
+                 tau_out=fake + (3 << 30), flags=fake + (4 << 30))
+        d.update(kw)
+        return _lib.AdaptiveSegment(**d)
+
+    for bad, what in [(seg(n=0), "bad segment"), (seg(x=fake + 8), "bad segment"),
+                      (seg(out=fake + 64, n=1000), "in-place")]:
+        arr = (_lib.AdaptiveSegment * 1)(bad)
+        assert lib.vt_round_log_adaptive_batch(C.cast(arr, C.c_void_p), 1, 32, 30, 1, fake, 1 << 40, None) == \
+            _lib.VT_EINVAL
+        assert what in lib.vt_last_error().decode()

@@ -207,7 +207,9 @@ struct FusedSmem {
   uint32_t rpos[kMaskSlots][kRows];            // log warp: row start inside the super-tile
   int64_t sbase[kMaskSlots];                   // log warp: global log position of the super-tile
   int64_t slot_id[kMaskSlots];
+  int32_t slot_seg[kMaskSlots];   // batched kernel: tensor of slot_id[]
   int64_t ids[4];
+  int32_t sids[4];                // batched kernel: tensor of ids[]
   uint32_t slot_cnt[kMaskSlots];  // (warps arrived << 24) + logged entries, by the compute warps
   uint64_t full[kFStages], empty[kFStages], mfull[kMaskSlots], ofull[kMaskSlots];
   uint32_t epoch;
@@ -634,16 +636,6 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
 // ticket (atomicMax), so only the tickets of skipped tensors are ever jumped.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ int find_seg(const RLBatch& b, int64_t s) {
-  int lo = 0, hi = b.nseg - 1;  // last tensor with tick0 <= s
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (b.seg[mid].tick0 <= s) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 // the fields rlf_write_rows / st_first / st_ntiles read, for tensor j
 __device__ __forceinline__ RLFArgs seg_view(const RLBatch& b, int j) {
   RLFArgs v;
@@ -685,15 +677,17 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
   if (warp == kProdWarp) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-      // the next ticket of a tensor that runs (skips gated-off tensors whole)
+      // the next ticket of a tensor that runs (skips gated-off tensors whole);
+      // a CTA's tickets ascend, so its tensor index only moves forward
+      int jc = 0;
       auto draw = [&]() -> int64_t {
         while (true) {
           const int64_t s = (int64_t)atomicAdd(&hdr->ticket, 1u);
           if (s >= b.total) return -1;
-          const int j = find_seg(b, s);
-          const int32_t* gate = b.seg[j].gate;
+          while (jc + 1 < b.nseg && b.seg[jc + 1].tick0 <= s) ++jc;
+          const int32_t* gate = b.seg[jc].gate;
           if (!gate || *gate != 0) return s;
-          const int64_t next = j + 1 < b.nseg ? b.seg[j + 1].tick0 : b.total;
+          const int64_t next = jc + 1 < b.nseg ? b.seg[jc + 1].tick0 : b.total;
           atomicMax(&hdr->ticket, (uint32_t)next);
         }
       };
@@ -704,8 +698,8 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
         int nt = 1;
         int64_t t0 = 0, full_tiles = 0;
         const double* x = nullptr;
+        const int j = jc;  // the tensor of s (draw() left jc there)
         if (s >= 0) {
-          const int j = find_seg(b, s);
           const RLFArgs v = seg_view(b, j);
           const int64_t ls = s - b.seg[j].tick0;
           nt = st_ntiles(v, ls);
@@ -717,7 +711,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
         for (int i = 0; i < nt; ++i, ++q) {
           const int st = (int)(q % kFStages);
           mbar_wait(S.empty + st, (uint32_t)(((q / kFStages) & 1) ^ 1));
-          if (i == 0) S.ids[k & 3] = s;
+          if (i == 0) {
+            S.ids[k & 3] = s;
+            S.sids[k & 3] = j;
+          }
           if (i == nt - 1 && s >= 0) nxt = draw();
           const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
@@ -739,7 +736,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       mbar_wait(S.mfull + slot, (uint32_t)((k / kMaskSlots) & 1));
       const int64_t s = S.slot_id[slot];
       if (s < 0) break;
-      const int j = find_seg(b, s);
+      const int j = S.slot_seg[slot];
       const RLSeg& sg = b.seg[j];
       const RLFArgs v = seg_view(b, j);
       const int64_t ls = s - sg.tick0;
@@ -768,13 +765,13 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
     const uint32_t lt = lanemask_lt();
     const uint32_t epoch = S.epoch;
     int64_t h1 = -1, h2 = -1, h3 = -1;  // tickets of ordinals k-1, k-2, k-3
+    int j1 = 0, j2 = 0, j3 = 0;         // and their tensors
     int64_t q = 0;
-    auto write_rows = [&](int64_t kk, int64_t s) {
-      const int j = find_seg(b, s);
+    auto write_rows = [&](int64_t kk, int64_t s, int j) {
       rlf_write_rows(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
     };
     for (int64_t k = 0;; ++k) {
-      if (k >= kMaskSlots) write_rows(k - kMaskSlots, h3);
+      if (k >= kMaskSlots) write_rows(k - kMaskSlots, h3, j3);
       const int slot = (int)(k % kMaskSlots);
       int64_t s = -1, t0 = 0, ls = 0;
       int nt = 1, j = 0;
@@ -789,7 +786,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
             ++q;
             break;
           }
-          j = find_seg(b, s);
+          j = S.sids[k & 3];
           ls = s - b.seg[j].tick0;
           const RLFArgs v = seg_view(b, j);
           nt = st_ntiles(v, ls);
@@ -834,18 +831,24 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
             S.slot_cnt[slot] = 0u;
           }
         }
-        if (warp == 0) S.slot_id[slot] = s;
+        if (warp == 0) {
+          S.slot_id[slot] = s;
+          S.slot_seg[slot] = j;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(S.mfull + slot);
       if (s < 0) {
-        if (k >= 2) write_rows(k - 2, h2);
-        if (k >= 1) write_rows(k - 1, h1);
+        if (k >= 2) write_rows(k - 2, h2, j2);
+        if (k >= 1) write_rows(k - 1, h1, j1);
         break;
       }
       h3 = h2;
       h2 = h1;
       h1 = s;
+      j3 = j2;
+      j2 = j1;
+      j1 = j;
     }
   }
 

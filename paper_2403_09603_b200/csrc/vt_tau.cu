@@ -35,6 +35,14 @@ struct SelectState {
   int64_t found;
 };
 
+// One isolated FP64 (a candidate's x): no L1 allocation, and the smallest
+// L2 prefetch size, so each gather costs its own sector rather than a line.
+__device__ __forceinline__ double ldg_sector(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // FP64 bit pattern of p for one element; err gets rnd's error bits.
 __device__ __forceinline__ uint64_t dist_key(double x, const Grid& g, uint32_t& err) {
   const uint64_t bits = (uint64_t)__double_as_longlong(x);
@@ -665,7 +673,8 @@ namespace vt {
 // ---------------------------------------------------------------------------
 
 constexpr int kCandFactor = 3;
-constexpr int kAdBins = 1 << 13;
+constexpr int kAdBits = 11;  // digit width of the candidate selection
+constexpr int kAdBins = 1 << kAdBits;
 constexpr int kAdThreads = 256;
 constexpr int kFChunk = 2048;  // candidates per filter ticket
 
@@ -737,7 +746,7 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
       for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
       double xv[kGU];
 #pragma unroll
-      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? __ldg(x + (w[u] >> 1)) : 0.0;
+      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(x + (w[u] >> 1)) : 0.0;
 #pragma unroll
       for (int u = 0; u < kGU; ++u) {
         key[u] = dist_key(xv[u], g, err);
@@ -849,7 +858,7 @@ __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ c
   int64_t rank = h->rank;
   uint64_t low = 0, lmask = 0;
   for (int top = s0; top > 0;) {
-    const int bits = top < 13 ? top : 13;
+    const int bits = top < kAdBits ? top : kAdBits;
     top -= bits;
     for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0;
     __syncthreads();
@@ -1215,7 +1224,7 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   memcpy(&L_key, &L, 8);
   const uint64_t W = hi_key - L_key;  // key offsets 0 .. W - 1 above L
   const int wbits = W > 1 ? 64 - __builtin_clzll(W - 1) : 1;
-  const int s0 = std::max(0, wbits - 13);
+  const int s0 = std::max(0, wbits - kAdBits);
   const Grid gL = make_grid(b_r, L);
   const int thrL = (int)std::min<int64_t>(std::max<int64_t>(gL.thr, 0), INT32_MAX);
   const Grid g0 = make_grid(b_r, 0.0);
@@ -1512,7 +1521,7 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
       a.log_cap = sg.log_cap;
       a.global_base = sg.global_base;
       a.L_key = L_key;
-      a.s0 = std::max(0, wbits - 13);
+      a.s0 = std::max(0, wbits - kAdBits);
       a.blk0 = (int32_t)blk;
       blk += std::max<int64_t>(1, std::min<int64_t>((int64_t)(want + kFChunk - 1) / kFChunk, 148 * 4));
       seg_ws += lay.total;

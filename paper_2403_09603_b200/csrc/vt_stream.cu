@@ -776,6 +776,12 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       int64_t s = -1, t0 = 0, ls = 0;
       int nt = 1, j = 0;
       uint32_t wcnt = 0;
+      // the ordinal's tensor constants, loaded once per super-tile
+      Grid g = b.g;
+      int thr32 = 0;
+      uint32_t c8 = 0, w8 = 0;
+      int64_t full_tiles = 0;
+      const RLSeg* sgp = b.seg;
 #pragma unroll 1
       for (int i = 0; i < nt; ++i, ++q) {
         const int st = (int)(q % kFStages);
@@ -787,25 +793,25 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
             break;
           }
           j = S.sids[k & 3];
-          ls = s - b.seg[j].tick0;
+          sgp = b.seg + j;
+          ls = s - sgp->tick0;
           const RLFArgs v = seg_view(b, j);
           nt = st_ntiles(v, ls);
           t0 = st_first(v, ls);
+          thr32 = sgp->thr32;
+          g.thr = sgp->thr;
+          g.thr_sub = sgp->thr_sub;
+          if (sgp->dthr) {
+            g.thr = sgp->dthr->thr;
+            g.thr_sub = sgp->dthr->thr_sub;
+            thr32 = sgp->dthr->thr32;
+          }
+          c8 = ((uint32_t)thr32 + 1u) << 3;
+          w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
+          full_tiles = sgp->n / kSTile;
         }
-        const RLSeg& sg = b.seg[j];
+        const RLSeg& sg = *sgp;
         uint32_t err = 0;
-        Grid g = b.g;
-        int thr32 = sg.thr32;
-        g.thr = sg.thr;
-        g.thr_sub = sg.thr_sub;
-        if (sg.dthr) {
-          g.thr = sg.dthr->thr;
-          g.thr_sub = sg.dthr->thr_sub;
-          thr32 = sg.dthr->thr32;
-        }
-        const uint32_t c8 = ((uint32_t)thr32 + 1u) << 3;
-        const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
-        const int64_t full_tiles = sg.n / kSTile;
         const int64_t t = t0 + i;
         const int64_t tbase = t * kSTile;
         void* o = tile_out<OUT>(sg.out, tbase);

@@ -676,7 +676,7 @@ constexpr int kCandFactor = 3;
 constexpr int kAdBits = 11;  // digit width of the candidate selection
 constexpr int kAdBins = 1 << kAdBits;
 constexpr int kAdThreads = 256;
-constexpr int kFChunk = 2048;  // candidates per filter ticket
+constexpr int kFChunk = 8192;  // candidates per filter ticket
 
 struct AdaptHdr {
   int32_t fallback;    // 1: the exact path runs (written by adapt_hist_kernel every call)
@@ -835,21 +835,28 @@ __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ c
   const uint64_t digit = h->digit;
   const uint64_t lo1 = L_key + 1;
   const int lane = threadIdx.x & 31;
-  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += nblk * kAdThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    uint64_t key = 0;
-    bool in = false;
-    if (i < M) {
-      key = ck[i];
-      in = key <= hi_key && key >= lo1 && ((key - lo1) >> s0) == digit;
+  constexpr int kSU = 4;  // independent key loads in flight per thread
+  const int64_t stride = nblk * kAdThreads;
+  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += kSU * stride) {
+    uint64_t key[kSU];
+#pragma unroll
+    for (int u = 0; u < kSU; ++u) {
+      const int64_t i = i0 + u * stride + threadIdx.x;
+      key[u] = i < M ? ck[i] : 0ull;
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      unsigned long long pos = 0;
-      if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key - lo1;
+#pragma unroll
+    for (int u = 0; u < kSU; ++u) {
+      const int64_t i = i0 + u * stride + threadIdx.x;
+      const bool in = i < M && key[u] <= hi_key && key[u] >= lo1 && ((key[u] - lo1) >> s0) == digit;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader)
+          pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key[u] - lo1;
+      }
     }
   }
   if (!last_cta(&h->arrived, (uint32_t)nblk)) return;
@@ -909,8 +916,10 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
                                                   AdaptHdr* h, const DevThr* dthr, uint64_t* sparse, int64_t cap,
                                                   int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
                                                   int64_t* counters, uint64_t* status, int64_t nblk) {
-  constexpr int kPer = kFChunk / kAdThreads;  // 8 candidates per thread
-  __shared__ uint32_t s_warp[kAdThreads / 32];
+  constexpr int kPer = kFChunk / kAdThreads;  // 32 candidates per thread
+  constexpr int kAdWarps = kAdThreads / 32;
+  static_assert(kPer == 32, "one keep bit per candidate in a 32-bit mask");
+  __shared__ uint32_t s_warp[kAdWarps];
   __shared__ int64_t s_t, s_base;
   __shared__ uint32_t s_epoch;
   if (h->fallback) return;
@@ -928,14 +937,21 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
     const int64_t t = s_t;
     __syncthreads();
     if (t >= nchunks) break;
+    // kPer consecutive candidates per thread (16-byte loads); one look-back
+    // per kFChunk candidates
     const int64_t c0 = t * kFChunk + (int64_t)tid * kPer;
-    uint32_t keep = 0, cnt = 0;
+    uint32_t keep = 0;
+    if (c0 + kPer <= M) {
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const bool kp = c0 + k < M && ck[c0 + k] > tau_key;
-      keep |= kp ? (1u << k) : 0u;
-      cnt += kp ? 1u : 0u;
+      for (int v = 0; v < kPer / 2; ++v) {
+        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(ck + c0 + 2 * v);
+        keep |= (kk.x > tau_key ? 1u : 0u) << (2 * v);
+        keep |= (kk.y > tau_key ? 1u : 0u) << (2 * v + 1);
+      }
+    } else {
+      for (int k = 0; k < kPer && c0 + k < M; ++k) keep |= (ck[c0 + k] > tau_key ? 1u : 0u) << k;
     }
+    const uint32_t cnt = __popc(keep);
     uint32_t inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -946,7 +962,7 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
     __syncthreads();
     uint32_t wpre = 0, agg = 0;
 #pragma unroll
-    for (int w = 0; w < kAdThreads / 32; ++w) {
+    for (int w = 0; w < kAdWarps; ++w) {
       wpre += (w < warp) ? s_warp[w] : 0u;
       agg += s_warp[w];
     }
@@ -989,12 +1005,27 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
     }
     __syncthreads();
     int64_t pos = s_base + wpre + (inc - cnt);
+    // the kept words: each half's needed 16-byte pairs of cw are requested
+    // before its first store (two memory round trips, not one per kept word)
+    const bool whole = c0 + kPer <= M;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (keep & (1u << k)) {
-        const uint64_t w = cw[c0 + k];
-        if (pos < cap) sparse[pos] = ((uint64_t)(global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
-        ++pos;
+    for (int half = 0; half < 2; ++half) {
+      ulonglong2 wv[kPer / 4];
+#pragma unroll
+      for (int v = 0; v < kPer / 4; ++v) {
+        const int k = half * (kPer / 2) + 2 * v;
+        if ((keep >> k) & 3u)
+          wv[v] = whole ? *reinterpret_cast<const ulonglong2*>(cw + c0 + k)
+                        : make_ulonglong2(cw[c0 + k], (keep >> (k + 1)) & 1u ? cw[c0 + k + 1] : 0ull);
+      }
+#pragma unroll
+      for (int v = 0; v < kPer / 2; ++v) {
+        const int k = half * (kPer / 2) + v;
+        if ((keep >> k) & 1u) {
+          const uint64_t w = (v & 1) ? wv[v >> 1].y : wv[v >> 1].x;
+          if (pos < cap) sparse[pos] = ((uint64_t)(global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+          ++pos;
+        }
       }
     }
   }
@@ -1523,7 +1554,10 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
       a.L_key = L_key;
       a.s0 = std::max(0, wbits - kAdBits);
       a.blk0 = (int32_t)blk;
-      blk += std::max<int64_t>(1, std::min<int64_t>((int64_t)(want + kFChunk - 1) / kFChunk, 148 * 4));
+      // a tail CTA per 8192 expected candidates: each has several gathers /
+      // filter tickets in flight, so the chain of dependent steps per CTA
+      // (ticket, load, look-back, store, arrival) is paid ~2 waves deep
+      blk += std::max<int64_t>(1, std::min<int64_t>((int64_t)(want + 8191) / 8192, 148 * 4));
       seg_ws += lay.total;
     }
     cand.total = fb.total = tick;

@@ -265,17 +265,34 @@ class _HostPipe:
         for e in self.ev_xfree + self.ev_yfree:
             e.record(torch.cuda.current_stream(device))
 
-    def run(self, x_h: torch.Tensor, y_h: torch.Tensor, kernel) -> None:
+    def _load(self, x_h: torch.Tensor, i: int) -> None:
+        n = x_h.numel()
+        lo = i * self.chunk
+        hi = min(n, lo + self.chunk)
+        k = i & 1
+        with torch.cuda.stream(self.s_in):
+            self.s_in.wait_event(self.ev_xfree[k])
+            self.xbuf[k][: hi - lo].copy_(x_h[lo:hi], non_blocking=True)
+            self.ev_loaded[k].record(self.s_in)
+
+    def preload(self, x_h: torch.Tensor) -> int:
+        """Start the H2D copies of the first two chunks now (both staging
+        buffers), e.g. while the host waits on earlier work; run() then skips
+        them.  Returns the number of chunks preloaded."""
+        k = min(2, (x_h.numel() + self.chunk - 1) // self.chunk)
+        for i in range(k):
+            self._load(x_h, i)
+        return k
+
+    def run(self, x_h: torch.Tensor, y_h: torch.Tensor, kernel, preloaded: int = 0) -> None:
         n = x_h.numel()
         for i, lo in enumerate(range(0, n, self.chunk)):
             hi = min(n, lo + self.chunk)
             k = i & 1
             xb = self.xbuf[k][: hi - lo]
             yb = self.ybuf[k][: hi - lo]
-            with torch.cuda.stream(self.s_in):
-                self.s_in.wait_event(self.ev_xfree[k])
-                xb.copy_(x_h[lo:hi], non_blocking=True)
-                self.ev_loaded[k].record(self.s_in)
+            if i >= preloaded:
+                self._load(x_h, i)
             with torch.cuda.stream(self.s_run):
                 self.s_run.wait_event(self.ev_loaded[k])
                 self.s_run.wait_event(self.ev_yfree[k])
@@ -307,10 +324,15 @@ def round_and_log_replay_host(xt_h: torch.Tensor, xa_h: torch.Tensor, b_r: int, 
     _check_b(b_r)
     dev = D.require_cuda()
     n = xt_h.numel()
-    key = (dev.index, chunk)
-    pipe = _PIPES.get(key)
-    if pipe is None:
-        pipe = _PIPES[key] = _HostPipe(chunk, dev)
+    # one pipeline per side: the auditor's first H2D chunks stream into their
+    # own staging buffers while the host waits for the trainer's log length
+    pipes = []
+    for side in ("trainer", "auditor"):
+        key = (dev.index, chunk, side)
+        if key not in _PIPES:
+            _PIPES[key] = _HostPipe(chunk, dev)
+        pipes.append(_PIPES[key])
+    pipe, pipe_a = pipes
     words = D.workspace(8 * max(n // 4, 1024), "host_log").view(torch.int64)
     n_chunks = (n + chunk - 1) // chunk
     cursors = torch.zeros(n_chunks + 1, dtype=torch.int64, device=dev)
@@ -329,7 +351,8 @@ def round_and_log_replay_host(xt_h: torch.Tensor, xa_h: torch.Tensor, b_r: int, 
 
     torch.cuda.current_stream(dev).synchronize()
     pipe.run(xt_h, yt_h, rl)
-    err, cnt = fl.read()  # syncs: the auditor needs the log length
+    pre = pipe_a.preload(xa_h)  # PCIe stays busy across the host wait below
+    err, cnt = fl.read()  # syncs the trainer's streams only: the auditor needs the log length
     D.raise_fpround(err)
     count = cnt[0]
     if count > cap or count > log_h.numel():
@@ -344,7 +367,7 @@ def round_and_log_replay_host(xt_h: torch.Tensor, xa_h: torch.Tensor, b_r: int, 
                   int(global_base + lo), _lib.OUT_F32, D.ptr(yb), fl_a.cnt_ptr, fl_a.err_ptr,
                   D.ptr(ws), ws.numel(), D.stream_ptr())
 
-    pipe.run(xa_h, ya_h, rp)
+    pipe_a.run(xa_h, ya_h, rp, preloaded=pre)
     err_a, cnt_a = fl_a.read()
     if err_a & _lib.ERR_BAD_SPARSE:
         raise SparseLogError("sparse log is not strictly ascending")

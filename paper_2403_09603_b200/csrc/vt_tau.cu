@@ -17,9 +17,12 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "vt_common.cuh"
 
 namespace vt {
+namespace cg = cooperative_groups;
 
 constexpr int kPasses = 5;
 __host__ __device__ constexpr int pass_shift(int p) { return p == 0 ? 49 : p == 1 ? 35 : p == 2 ? 21 : p == 3 ? 7 : 0; }
@@ -740,21 +743,22 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
   const int64_t stride = nblk * kAdThreads;
   for (int64_t i0 = blk * kAdThreads + threadIdx.x; i0 < M; i0 += kGU * stride) {
     uint64_t key[kGU];
+    double xv[kGU];
     if (gather) {
       uint64_t w[kGU];
 #pragma unroll
       for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
-      double xv[kGU];
 #pragma unroll
       for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(x + (w[u] >> 1)) : 0.0;
+    } else {  // in place: adapt_keys_kernel staged the candidates' x values in ck
 #pragma unroll
-      for (int u = 0; u < kGU; ++u) {
-        key[u] = dist_key(xv[u], g, err);
-        if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];
-      }
-    } else {
+      for (int u = 0; u < kGU; ++u)
+        xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)ck[i0 + u * stride]) : 0.0;
+    }
 #pragma unroll
-      for (int u = 0; u < kGU; ++u) key[u] = (i0 + u * stride < M) ? ck[i0 + u * stride] : 0ull;
+    for (int u = 0; u < kGU; ++u) {
+      key[u] = dist_key(xv[u], g, err);
+      if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];
     }
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
@@ -1051,19 +1055,31 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t
 // In-place calls: one streaming read of x appends the keys above L
 // (unordered, warp-aggregated); the rounding pass then runs at the selected
 // tau and writes the ordered log itself.
+template <bool FAST>
 __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                                uint64_t L_key, uint64_t lo_key,
-                                                                uint64_t* __restrict__ ck, int64_t cap, AdaptHdr* h,
-                                                                int32_t* errp) {
+                                                                uint64_t L_key, uint64_t lo_key, int64_t thr_L,
+                                                                int64_t thr_lo, uint64_t* __restrict__ ck,
+                                                                int64_t cap, AdaptHdr* h, int32_t* errp) {
   // keys are staged per CTA and appended with one global atomic per flush:
   // a global atomic per warp ballot serialises on the counter's L2 slice
-  constexpr int kBuf = 2048;  // one step adds at most 1024
+  constexpr int kSteps = 4;                 // x 1024 elements per CTA iteration, loads issued up front
+  constexpr int kIter = 1024 * kSteps;
+  constexpr int kBuf = kIter + 1024;        // one iteration adds at most kIter
   __shared__ uint64_t sbuf[kBuf];
   __shared__ uint32_t scount;
   __shared__ unsigned long long sbase;
   uint32_t err = 0, above_lo = 0;
   const int lane = threadIdx.x & 31;
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+  // b_r = 32 (thresholds in [2^27, 2^28] here): candidate <=> (low32 << 3) - c8 < w8
+  auto cw8 = [](int64_t thr, uint32_t& c8, uint32_t& w8) {
+    const uint32_t t = (uint32_t)(thr < 0 ? 0 : (thr > (1 << 28) ? (1 << 28) : thr));
+    c8 = (t + 1u) << 3;
+    w8 = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
+  };
+  uint32_t c8L, w8L, c8lo, w8lo;
+  cw8(thr_L, c8L, w8L);
+  cw8(thr_lo, c8lo, w8lo);
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
   auto flush = [&]() {
@@ -1076,31 +1092,88 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
     if (threadIdx.x == 0) scount = 0;
     __syncthreads();
   };
-  for (int64_t base = (int64_t)blockIdx.x * 1024; base < n; base += (int64_t)gridDim.x * 1024) {
-    const int64_t i0 = base + 4 * threadIdx.x;
-    D4 xv;
-    if (vec && i0 + 3 < n) {
-      xv = ldg_stream4(x + i0);
-    } else {
+  for (int64_t base = (int64_t)blockIdx.x * kIter; base < n; base += (int64_t)gridDim.x * kIter) {
+    D4 xv[kSteps];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) xv.v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
-    }
+    for (int st = 0; st < kSteps; ++st) {
+      const int64_t i0 = base + st * 1024 + 4 * threadIdx.x;
+      if (vec && i0 + 3 < n) {
+        xv[st] = ldg_stream4(x + i0);
+      } else {
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const uint64_t key = (i0 + v < n) ? dist_key(xv.v[v], g, err) : 0ull;
-      const bool in = key > L_key;
-      above_lo += key > lo_key ? 1u : 0u;
-      const uint32_t m = __ballot_sync(0xffffffffu, in);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        uint32_t pos = 0;
-        if (lane == leader) pos = atomicAdd(&scount, (uint32_t)__popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (in) sbuf[pos + __popc(m & ((1u << lane) - 1u))] = key;
+        for (int v = 0; v < 4; ++v) xv[st].v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
       }
     }
+    // normal range (the common case): p > t  <=>  d > floor(t * 2^52) on the
+    // integer distance d of round_dir, so no key is formed unless the element
+    // is a candidate; |x| < 2^-126 (and, for b_r = 32, anything outside the
+    // FP32 normal range) takes the FP64 key of dist_key, off the main path
+    constexpr int kE = kSteps * 4;
+    uint32_t cm = 0, ab = 0, slowm = 0;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
+      if (FAST) {
+        // d > thr  <=>  thr < low29 < 2^29 - thr: one shifted unsigned compare
+        // (the rl kernel's test); +-0 gives low29 = 0, never a candidate, so
+        // only nonzero values outside the FP32 normal range take the key path
+        const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
+        const uint32_t s3 = lo32 << 3;
+        cm |= ((s3 - c8L) < w8L ? 1u : 0u) << e;
+        ab |= ((s3 - c8lo) < w8lo ? 1u : 0u) << e;
+        slowm |= (outside_normal32(ahi) && (ahi | lo32) != 0u ? 1u : 0u) << e;
+      } else {
+        const uint64_t mag = bits & kMag;
+        const uint64_t low = mag & g.low_mask;
+        const uint64_t hb = mag >> g.drop;
+        const bool up = (low > g.half) || ((low == g.half) && (hb & 1ull));
+        const uint64_t rmag = (hb + (up ? 1ull : 0ull)) << g.drop;
+        err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                    : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
+        const int64_t d = (int64_t)(up ? (g.one - low) : low);
+        cm |= (d > thr_L ? 1u : 0u) << e;
+        ab |= (d > thr_lo ? 1u : 0u) << e;
+        slowm |= (mag < kNormalMin ? 1u : 0u) << e;
+      }
+    }
+    if (slowm) {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        if ((slowm >> e) & 1u) {
+          const uint64_t key = dist_key(xv[e >> 2].v[e & 3], g, err);
+          cm = (cm & ~(1u << e)) | ((key > L_key ? 1u : 0u) << e);
+          ab = (ab & ~(1u << e)) | ((key > lo_key ? 1u : 0u) << e);
+        }
+      }
+    }
+    if (base + kIter > n) {  // the ragged last iteration: drop elements >= n
+      uint32_t vm = 0;
+#pragma unroll
+      for (int e = 0; e < kE; ++e) vm |= (base + (e >> 2) * 1024 + 4 * threadIdx.x + (e & 3) < n ? 1u : 0u) << e;
+      cm &= vm;
+      ab &= vm;
+    }
+    above_lo += __popc(ab);
+    // warp-aggregated append of the (rare) candidates' keys
+    const uint32_t c = __popc(cm);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (tot) {
+      uint32_t wb = 0;
+      if (lane == 31) wb = atomicAdd(&scount, tot);
+      uint32_t pos = __shfl_sync(0xffffffffu, wb, 31) + inc - c;
+      // the candidate's x itself: adapt_hist_kernel turns it into its key
+#pragma unroll
+      for (int e = 0; e < kE; ++e)
+        if ((cm >> e) & 1u) sbuf[pos++] = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
+    }
     __syncthreads();
-    if (scount >= kBuf - 1024) flush();
+    if (scount > (uint32_t)(kBuf - kIter)) flush();
   }
   if (scount) flush();
   report_err(errp, err);
@@ -1109,32 +1182,60 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
     atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), (unsigned long long)above_lo);
 }
 
-// Exact fallback, gated on h->fallback (the kernels return at once in the
-// common case): the multi-pass budget selection over x, each pass followed
-// by the selection step in its last CTA, the final step running the FP64
-// bisection.
-__global__ void adapt_fb_init_kernel(const AdaptHdr* h, BudState* st, uint32_t* hist, uint64_t lo_key,
-                                     uint64_t hi_key, uint64_t* key_out) {
-  if (!h->fallback) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kBudMaxLevels * kBudBins; i += gridDim.x * blockDim.x)
-    hist[i] = 0u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) bud_init_body(st, lo_key, hi_key, key_out);
+// Exact fallback, gated on h->fallback: the multi-pass budget selection over
+// x as ONE cooperative launch (grid-wide syncs between a pass and the
+// selection step after it; the final step runs the FP64 bisection).  In the
+// common case the whole grid returns at once: one near-empty launch per call
+// instead of seven.
+__device__ void fb_selection(const double* __restrict__ x, int64_t n, const Grid& g, AdaptHdr* h, BudState* st,
+                             uint32_t* hist, uint64_t* cand, int64_t budget, uint64_t lo_key, uint64_t hi_key,
+                             double lower, double upper, int iters, uint64_t* key_out, DevThr* dthr,
+                             double* tau_out, int32_t* errp, uint32_t* sh) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = gtid; i < (int64_t)kBudMaxLevels * kBudBins; i += (int64_t)gridDim.x * blockDim.x) hist[i] = 0u;
+  if (gtid == 0) {
+    bud_init_body(st, lo_key, hi_key, key_out);
+    h->above_lo = 0;
+  }
+  grid.sync();
+  for (int p = 0; p <= kBudMaxLevels; ++p) {
+    if (*(volatile int*)&st->status != 0) break;  // grid-uniform: read after a grid sync
+    bud_pass_body(x, n, g, st, hist, cand, errp, sh, blockIdx.x, gridDim.x);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      bud_step_body(st, hist, cand, budget, key_out, sh);
+      __syncthreads();
+      if (threadIdx.x == 0 && st->status != 0) bisect_to(*key_out, lower, upper, iters, dthr, tau_out);
+    }
+    grid.sync();
+  }
 }
 
-__global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                                   AdaptHdr* h, BudState* st, uint32_t* hist,
-                                                                   uint64_t* cand, int64_t budget, double lower,
-                                                                   double upper, int iters, uint64_t* key_out,
-                                                                   DevThr* dthr, double* tau_out, int32_t* errp) {
+__global__ void __launch_bounds__(kAdThreads) adapt_fb_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                              AdaptHdr* h, BudState* st, uint32_t* hist,
+                                                              uint64_t* cand, int64_t budget, uint64_t lo_key,
+                                                              uint64_t hi_key, double lower, double upper, int iters,
+                                                              uint64_t* key_out, DevThr* dthr, double* tau_out,
+                                                              int32_t* errp) {
   __shared__ uint32_t sh[kBudBins];
-  if (!h->fallback || st->status != 0) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) h->above_lo = 0;
-  bud_pass_body(x, n, g, st, hist, cand, errp, sh, blockIdx.x, gridDim.x);
-  if (!last_cta(&h->arrived, gridDim.x)) return;
-  if (threadIdx.x == 0) h->arrived = 0u;
-  bud_step_body(st, hist, cand, budget, key_out, sh);
-  __syncthreads();
-  if (threadIdx.x == 0 && st->status != 0) bisect_to(*key_out, lower, upper, iters, dthr, tau_out);
+  if (!h->fallback) return;
+  fb_selection(x, n, g, h, st, hist, cand, budget, lo_key, hi_key, lower, upper, iters, key_out, dthr, tau_out, errp,
+               sh);
+}
+
+// Cooperative grid for the fallback kernels: every CTA co-resident.
+template <typename K>
+int coop_grid(K kernel) {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kAdThreads, 0);
+    grid = std::max(1, std::min(per, 2) * sms);
+  }
+  return grid;
 }
 }  // namespace vt
 
@@ -1270,8 +1371,13 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   if (aliased) {
     // 1'. keys above L (unordered), 2-3. selection among them, bisection
     if (cudaMemsetAsync(&h->ccount, 0, sizeof(int64_t), s) != cudaSuccess) return vt_check_launch("memset");
-    const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 148 * 8));
-    adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, ck, lay.cap, h, err);
+    const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
+    if (fast)
+      adapt_keys_kernel<true><<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
+                                                        lay.cap, h, err);
+    else
+      adapt_keys_kernel<false><<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
+                                                         lay.cap, h, err);
     if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
     adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,
                                                 false);
@@ -1294,14 +1400,18 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
         cw, ck, h, dthr, sparse, sparse_cap, global_base, cursor_in, cursor_out, counters, fst);
     if ((rc = vt_check_launch("adapt_filter_kernel"))) return rc;
   }
-  // fallback (no-ops unless the candidates could not decide): exact selection over x, then a full pass
-  adapt_fb_init_kernel<<<(kBudMaxLevels * kBudBins + 255) / 256, 256, 0, s>>>(h, st, bhist, lo_key, hi_key, key);
-  if ((rc = vt_check_launch("adapt_fb_init_kernel"))) return rc;
-  const unsigned fb_blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, 148 * 8));
-  for (int p = 0; p <= kBudMaxLevels; ++p) {
-    adapt_fb_pass_kernel<<<fb_blocks, kAdThreads, 0, s>>>(x, n, g0, h, st, bhist, bcand, budget, lo, hi, iters, key,
-                                                          dthr, tau_out, err);
-    if ((rc = vt_check_launch("adapt_fb_pass_kernel"))) return rc;
+  // fallback (a no-op unless the candidates could not decide): exact selection over x, then a full pass
+  {
+    const double* xa = x;
+    int64_t na = n, ba = budget;
+    Grid ga = g0;
+    uint64_t lk = lo_key, hk = hi_key;
+    double la = lo, ua = hi;
+    int ia = iters;
+    void* args[] = {&xa, &na, &ga, &h, &st, &bhist, &bcand, &ba, &lk, &hk, &la, &ua, &ia, &key, &dthr, &tau_out, &err};
+    cudaLaunchCooperativeKernel((const void*)adapt_fb_kernel, dim3(coop_grid(adapt_fb_kernel)), dim3(kAdThreads),
+                                args, 0, s);
+    if ((rc = vt_check_launch("adapt_fb_kernel"))) return rc;
   }
   // the rounding pass at the device tau: always for in-place calls, else only after a fallback
   return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
@@ -1315,8 +1425,8 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
 // fixed number of launches instead of ~12 per tensor:
 //
 //   rl_batch_kernel (candidate pass) -> adapt_hist_batch -> adapt_select_batch
-//   -> adapt_filter_batch -> [exact fallback: adapt_fb_init_batch, 6 x
-//   adapt_fb_pass_batch, rl_batch_kernel gated per tensor]
+//   -> adapt_filter_batch -> [exact fallback: adapt_fb_roster, one
+//   cooperative adapt_fb_batch, rl_batch_kernel gated per tensor]
 //
 // Same per-tensor algorithm and state as vt_round_log_adaptive (the kernel
 // bodies are shared); each tensor gets a share of the tail grids in
@@ -1392,38 +1502,23 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_batch_kernel(const __
                     p.fst, ad_nblk(b, j));
 }
 
-// exact fallback, one CTA per tensor: fresh selection state and a roster
-// entry where needed (the later fallback kernels visit only the roster)
-__global__ void adapt_fb_init_batch_kernel(const __grid_constant__ AdBatch b) {
+// exact fallback: one CTA per tensor adds the tensors that need it to a
+// roster; one cooperative launch then runs the exact selection of every
+// rostered tensor in turn (returning at once when the roster is empty)
+__global__ void adapt_fb_roster_kernel(const __grid_constant__ AdBatch b) {
   const AdSeg& sg = b.seg[blockIdx.x];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
-  if (!p.h->fallback) return;
-  for (int i = threadIdx.x; i < kBudMaxLevels * kBudBins; i += blockDim.x) p.bhist[i] = 0u;
-  if (threadIdx.x == 0) {
-    bud_init_body(p.st, b.lo_key, b.hi_key, p.key);
-    b.fb->list[atomicAdd(&b.fb->count, 1)] = (int32_t)blockIdx.x;
-  }
+  if (threadIdx.x == 0 && p.h->fallback) b.fb->list[atomicAdd(&b.fb->count, 1)] = (int32_t)blockIdx.x;
 }
 
-// one selection pass of every tensor still running the exact fallback; the
-// whole grid streams each such tensor in turn, its last CTA takes the step
-__global__ void __launch_bounds__(kAdThreads, 4) adapt_fb_pass_batch_kernel(const __grid_constant__ AdBatch b) {
+__global__ void __launch_bounds__(kAdThreads) adapt_fb_batch_kernel(const __grid_constant__ AdBatch b) {
   __shared__ uint32_t sh[kBudBins];
   const int nfb = *(volatile int32_t*)&b.fb->count;
   for (int k = 0; k < nfb; ++k) {
     const AdSeg& sg = b.seg[b.fb->list[k]];
     const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
-    if (!p.h->fallback || p.st->status != 0) continue;
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.h->above_lo = 0;
-    int32_t* err = reinterpret_cast<int32_t*>(sg.flags);
-    bud_pass_body(sg.x, sg.n, b.g0, p.st, p.bhist, p.bcand, err, sh, blockIdx.x, gridDim.x);
-    if (last_cta(&p.h->arrived, gridDim.x)) {
-      if (threadIdx.x == 0) p.h->arrived = 0u;
-      bud_step_body(p.st, p.bhist, p.bcand, sg.budget, p.key, sh);
-      __syncthreads();
-      if (threadIdx.x == 0 && p.st->status != 0) bisect_to(*p.key, b.lo, b.hi, b.iters, p.dthr, sg.tau_out);
-    }
-    __syncthreads();
+    fb_selection(sg.x, sg.n, b.g0, p.h, p.st, p.bhist, p.bcand, sg.budget, b.lo_key, b.hi_key, b.lo, b.hi, b.iters,
+                 p.key, p.dthr, sg.tau_out, reinterpret_cast<int32_t*>(sg.flags), sh);
   }
 }
 }  // namespace vt
@@ -1572,11 +1667,13 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
     adapt_filter_batch_kernel<<<(unsigned)blk, kAdThreads, 0, s>>>(ab);
     if ((rc = vt_check_launch("adapt_filter_batch_kernel"))) return rc;
     // exact fallback for the tensors whose candidates could not decide (no-ops otherwise)
-    adapt_fb_init_batch_kernel<<<(unsigned)m, 256, 0, s>>>(ab);
-    if ((rc = vt_check_launch("adapt_fb_init_batch_kernel"))) return rc;
-    for (int p = 0; p <= kBudMaxLevels; ++p) {
-      adapt_fb_pass_batch_kernel<<<148 * 4, kAdThreads, 0, s>>>(ab);
-      if ((rc = vt_check_launch("adapt_fb_pass_batch_kernel"))) return rc;
+    adapt_fb_roster_kernel<<<(unsigned)m, 32, 0, s>>>(ab);
+    if ((rc = vt_check_launch("adapt_fb_roster_kernel"))) return rc;
+    {
+      void* args[] = {&ab};
+      cudaLaunchCooperativeKernel((const void*)adapt_fb_batch_kernel, dim3(coop_grid(adapt_fb_batch_kernel)),
+                                  dim3(kAdThreads), args, 0, s);
+      if ((rc = vt_check_launch("adapt_fb_batch_kernel"))) return rc;
     }
     if ((rc = rl_stream_batch(fb, fast, out_kind, s))) return rc;
   }

@@ -78,8 +78,10 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
 class Flags:
     """Device int32 error word + int64 counters for one call."""
 
-    def __init__(self, n_counters: int = 4):
-        self.buf = torch.zeros(2 + n_counters, dtype=torch.int64, device="cuda")
+    def __init__(self, n_counters: int = 4, buf: torch.Tensor | None = None):
+        # buf: a caller-owned, zeroed int64 slot of 2 + n_counters words (e.g. a
+        # row of a per-step arena, so a step allocates nothing)
+        self.buf = buf if buf is not None else torch.zeros(2 + n_counters, dtype=torch.int64, device="cuda")
         self.err_ptr = self.buf.data_ptr()
         self.cnt_ptr = self.buf.data_ptr() + 16
 

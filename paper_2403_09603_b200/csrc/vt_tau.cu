@@ -1055,7 +1055,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t
 // In-place calls: one streaming read of x appends the keys above L
 // (unordered, warp-aggregated); the rounding pass then runs at the selected
 // tau and writes the ordered log itself.
-template <bool FAST>
 __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __restrict__ x, int64_t n, Grid g,
                                                                 uint64_t L_key, uint64_t lo_key, int64_t thr_L,
                                                                 int64_t thr_lo, uint64_t* __restrict__ ck,
@@ -1071,15 +1070,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
   uint32_t err = 0, above_lo = 0;
   const int lane = threadIdx.x & 31;
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
-  // b_r = 32 (thresholds in [2^27, 2^28] here): candidate <=> (low32 << 3) - c8 < w8
-  auto cw8 = [](int64_t thr, uint32_t& c8, uint32_t& w8) {
-    const uint32_t t = (uint32_t)(thr < 0 ? 0 : (thr > (1 << 28) ? (1 << 28) : thr));
-    c8 = (t + 1u) << 3;
-    w8 = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
-  };
-  uint32_t c8L, w8L, c8lo, w8lo;
-  cw8(thr_L, c8L, w8L);
-  cw8(thr_lo, c8lo, w8lo);
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
   auto flush = [&]() {
@@ -1092,37 +1082,28 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
     if (threadIdx.x == 0) scount = 0;
     __syncthreads();
   };
+  // whole iterations take unguarded 256-bit loads; the ragged tail (or an
+  // unaligned x) loads element by element, zero past n
+  const int64_t nfull = vec ? (n / kIter) * kIter : 0;
   for (int64_t base = (int64_t)blockIdx.x * kIter; base < n; base += (int64_t)gridDim.x * kIter) {
     D4 xv[kSteps];
+    if (base < nfull) {
 #pragma unroll
-    for (int st = 0; st < kSteps; ++st) {
-      const int64_t i0 = base + st * 1024 + 4 * threadIdx.x;
-      if (vec && i0 + 3 < n) {
-        xv[st] = ldg_stream4(x + i0);
-      } else {
+      for (int st = 0; st < kSteps; ++st) xv[st] = ldg_stream4(x + base + st * 1024 + 4 * threadIdx.x);
+    } else {
+#pragma unroll
+      for (int st = 0; st < kSteps; ++st) {
+        const int64_t i0 = base + st * 1024 + 4 * threadIdx.x;
 #pragma unroll
         for (int v = 0; v < 4; ++v) xv[st].v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
       }
     }
-    // normal range (the common case): p > t  <=>  d > floor(t * 2^52) on the
-    // integer distance d of round_dir, so no key is formed unless the element
-    // is a candidate; |x| < 2^-126 (and, for b_r = 32, anything outside the
-    // FP32 normal range) takes the FP64 key of dist_key, off the main path
     constexpr int kE = kSteps * 4;
-    uint32_t cm = 0, ab = 0, slowm = 0;
+    {  // general b_r: the test on the 64-bit distance of round_dir (b_r = 32: adapt_keys32_kernel)
+      uint32_t cm = 0, ab = 0, slowm = 0;
 #pragma unroll
-    for (int e = 0; e < kE; ++e) {
-      const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
-      if (FAST) {
-        // d > thr  <=>  thr < low29 < 2^29 - thr: one shifted unsigned compare
-        // (the rl kernel's test); +-0 gives low29 = 0, never a candidate, so
-        // only nonzero values outside the FP32 normal range take the key path
-        const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
-        const uint32_t s3 = lo32 << 3;
-        cm |= ((s3 - c8L) < w8L ? 1u : 0u) << e;
-        ab |= ((s3 - c8lo) < w8lo ? 1u : 0u) << e;
-        slowm |= (outside_normal32(ahi) && (ahi | lo32) != 0u ? 1u : 0u) << e;
-      } else {
+      for (int e = 0; e < kE; ++e) {
+        const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
         const uint64_t mag = bits & kMag;
         const uint64_t low = mag & g.low_mask;
         const uint64_t hb = mag >> g.drop;
@@ -1135,47 +1116,137 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
         ab |= (d > thr_lo ? 1u : 0u) << e;
         slowm |= (mag < kNormalMin ? 1u : 0u) << e;
       }
-    }
-    if (slowm) {
+      if (slowm) {
 #pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        if ((slowm >> e) & 1u) {
-          const uint64_t key = dist_key(xv[e >> 2].v[e & 3], g, err);
-          cm = (cm & ~(1u << e)) | ((key > L_key ? 1u : 0u) << e);
-          ab = (ab & ~(1u << e)) | ((key > lo_key ? 1u : 0u) << e);
+        for (int e = 0; e < kE; ++e) {
+          if ((slowm >> e) & 1u) {
+            const uint64_t key = dist_key(xv[e >> 2].v[e & 3], g, err);
+            cm = (cm & ~(1u << e)) | ((key > L_key ? 1u : 0u) << e);
+            ab = (ab & ~(1u << e)) | ((key > lo_key ? 1u : 0u) << e);
+          }
         }
       }
-    }
-    if (base + kIter > n) {  // the ragged last iteration: drop elements >= n
-      uint32_t vm = 0;
+      if (base + kIter > n) {  // the ragged last iteration: drop elements >= n
+        uint32_t vm = 0;
 #pragma unroll
-      for (int e = 0; e < kE; ++e) vm |= (base + (e >> 2) * 1024 + 4 * threadIdx.x + (e & 3) < n ? 1u : 0u) << e;
-      cm &= vm;
-      ab &= vm;
-    }
-    above_lo += __popc(ab);
-    // warp-aggregated append of the (rare) candidates' keys
-    const uint32_t c = __popc(cm);
-    uint32_t inc = c;
+        for (int e = 0; e < kE; ++e) vm |= (base + (e >> 2) * 1024 + 4 * threadIdx.x + (e & 3) < n ? 1u : 0u) << e;
+        cm &= vm;
+        ab &= vm;
+      }
+      above_lo += __popc(ab);
+      // warp-aggregated append of the candidates' x values
+      const uint32_t c = __popc(cm);
+      uint32_t inc = c;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-    if (tot) {
-      uint32_t wb = 0;
-      if (lane == 31) wb = atomicAdd(&scount, tot);
-      uint32_t pos = __shfl_sync(0xffffffffu, wb, 31) + inc - c;
-      // the candidate's x itself: adapt_hist_kernel turns it into its key
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+      if (tot) {
+        uint32_t wb = 0;
+        if (lane == 31) wb = atomicAdd(&scount, tot);
+        uint32_t pos = __shfl_sync(0xffffffffu, wb, 31) + inc - c;
+        // the candidate's x itself: adapt_hist_kernel turns it into its key
 #pragma unroll
-      for (int e = 0; e < kE; ++e)
-        if ((cm >> e) & 1u) sbuf[pos++] = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
+        for (int e = 0; e < kE; ++e)
+          if ((cm >> e) & 1u) sbuf[pos++] = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
+      }
     }
     __syncthreads();
     if (scount > (uint32_t)(kBuf - kIter)) flush();
   }
   if (scount) flush();
+  report_err(errp, err);
+  for (int o = 16; o > 0; o >>= 1) above_lo += __shfl_xor_sync(0xffffffffu, above_lo, o);
+  if (lane == 0 && above_lo)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), (unsigned long long)above_lo);
+}
+
+// b_r = 32 form of adapt_keys_kernel: per element one shifted unsigned
+// compare on the low word (the rl kernel's test, thr < low29 < 2^29 - thr);
+// each warp appends its candidates' x values to its own shared-memory run
+// (ballot rank, no atomics, no block barriers) and flushes the run with one
+// global atomic when it fills.  +-0 (and the zeros loaded past n) have
+// low29 = 0 and are never counted; only nonzero values outside the FP32
+// normal range take the FP64 key of dist_key (rare path).
+__global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* __restrict__ x, int64_t n, Grid g,
+                                                                  uint64_t L_key, uint64_t lo_key, uint32_t c8L,
+                                                                  uint32_t w8L, uint32_t c8lo, uint32_t w8lo,
+                                                                  uint64_t* __restrict__ ck, int64_t cap,
+                                                                  AdaptHdr* h, int32_t* errp) {
+  constexpr int kSteps = 4;  // x 1024 elements per CTA iteration, loads issued up front
+  constexpr int kIter = 1024 * kSteps;
+  constexpr int kE = kSteps * 4;
+  constexpr int kRun = 640;  // entries per warp run; one iteration adds at most 32 * kE = 512
+  __shared__ uint64_t sbuf[kAdThreads / 32][kRun];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* run = sbuf[warp];
+  const uint32_t lt = lanemask_lt();
+  uint32_t err = 0, above_lo = 0, cnt = 0;
+  auto flush = [&]() {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(&h->ccount), (unsigned long long)cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncwarp();
+    for (uint32_t i = lane; i < cnt; i += 32)
+      if ((int64_t)(base + i) < cap) ck[base + i] = run[i];
+    __syncwarp();
+    cnt = 0;
+  };
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+  const int64_t nfull = vec ? (n / kIter) * kIter : 0;
+  for (int64_t base = (int64_t)blockIdx.x * kIter; base < n; base += (int64_t)gridDim.x * kIter) {
+    D4 xv[kSteps];
+    if (base < nfull) {
+#pragma unroll
+      for (int st = 0; st < kSteps; ++st) xv[st] = ldg_stream4(x + base + st * 1024 + 4 * threadIdx.x);
+    } else {
+#pragma unroll
+      for (int st = 0; st < kSteps; ++st) {
+        const int64_t i0 = base + st * 1024 + 4 * threadIdx.x;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) xv[st].v[v] = (i0 + v < n) ? x[i0 + v] : 0.0;
+      }
+    }
+    bool badw = false;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
+      const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
+      const uint32_t s3 = lo32 << 3;
+      const bool bad = outside_normal32(ahi) && (ahi | lo32) != 0u;
+      const bool in = (s3 - c8L) < w8L && !bad;
+      above_lo += ((s3 - c8lo) < w8lo && !bad) ? 1u : 0u;
+      badw |= bad;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        if (in) run[cnt + __popc(m & lt)] = bits;
+        cnt += __popc(m);
+      }
+    }
+    if (__any_sync(0xffffffffu, badw)) {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        const double xe = xv[e >> 2].v[e & 3];
+        const uint64_t bits = (uint64_t)__double_as_longlong(xe);
+        const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
+        bool in = false;
+        if (outside_normal32(ahi) && (ahi | lo32) != 0u) {
+          const uint64_t key = dist_key(xe, g, err);
+          above_lo += key > lo_key ? 1u : 0u;
+          in = key > L_key;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        if (m) {
+          if (in) run[cnt + __popc(m & lt)] = bits;
+          cnt += __popc(m);
+        }
+      }
+    }
+    if (cnt > (uint32_t)(kRun - 32 * kE)) flush();
+  }
+  if (cnt) flush();
   report_err(errp, err);
   for (int o = 16; o > 0; o >>= 1) above_lo += __shfl_xor_sync(0xffffffffu, above_lo, o);
   if (lane == 0 && above_lo)
@@ -1372,11 +1443,20 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
     // 1'. keys above L (unordered), 2-3. selection among them, bisection
     if (cudaMemsetAsync(&h->ccount, 0, sizeof(int64_t), s) != cudaSuccess) return vt_check_launch("memset");
     const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
-    if (fast)
-      adapt_keys_kernel<true><<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
-                                                        lay.cap, h, err);
-    else
-      adapt_keys_kernel<false><<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
+    if (fast) {
+      // candidate <=> (low32 << 3) - c8 < w8 (thresholds in [2^27, 2^28] here)
+      auto cw8 = [](int64_t thr, uint32_t& c8, uint32_t& w8) {
+        const uint32_t t = (uint32_t)(thr < 0 ? 0 : (thr > (1 << 28) ? (1 << 28) : thr));
+        c8 = (t + 1u) << 3;
+        w8 = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
+      };
+      uint32_t c8L, w8L, c8lo, w8lo;
+      cw8(gL.thr, c8L, w8L);
+      cw8(make_grid(b_r, lo).thr, c8lo, w8lo);
+      adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, c8L, w8L, c8lo, w8lo, ck, lay.cap, h,
+                                                    err);
+    } else
+      adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
                                                          lay.cap, h, err);
     if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
     adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,

@@ -8,7 +8,10 @@ training proceeds on the b_r grid exactly as the reference trainer does
 (protocol.py:259-285: forward stages, loss gradient, backward stages).
 
 Nothing here synchronises with the host during the step: taus, counts and
-logs stay on the device until ``collect()``.
+logs stay on the device until ``collect()``, which reads the whole step's
+taus and counts in one copy.  Result slots (tau, error/count words) and log
+buffers are reused from step to step, so a steady-state step allocates
+nothing (a device allocation inside a step can stall the stream).
 """
 
 from __future__ import annotations
@@ -17,6 +20,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from . import _device as D
 from . import ops
 
 
@@ -27,6 +31,7 @@ class HookRecord:
     numel: int
     budget: int
     pending: object  # ops.PendingAdaptive
+    slot: int = 0    # row of the hooks' result arena
 
 
 @dataclass
@@ -40,6 +45,9 @@ class RoundAndLogHooks:
 
     def __post_init__(self):
         self._handles = []
+        self._flags = torch.zeros((0, 6), dtype=torch.int64, device="cuda")  # per call: err, -, counters
+        self._taus = torch.zeros(0, dtype=torch.float64, device="cuda")
+        self._logs: list[torch.Tensor] = []  # per call index: log buffer, reused while large enough
         for name, mod in self.model.named_modules():
             if any(True for _ in mod.children()):
                 continue  # leaf modules only
@@ -55,11 +63,24 @@ class RoundAndLogHooks:
         d = t.detach()
         inplace = d.is_contiguous() and d.data_ptr() % 32 == 0
         flat = d.view(-1) if inplace else d.reshape(-1).clone()
+        k = len(self.records)
+        if k >= self._flags.shape[0]:  # first steps only: grow the result slots
+            grow = max(64, 2 * self._flags.shape[0])
+            self._flags = torch.cat([self._flags, torch.zeros((grow, 6), dtype=torch.int64, device="cuda")])
+            self._taus = torch.cat([self._taus, torch.zeros(grow, dtype=torch.float64, device="cuda")])
+            for r in self.records:  # keep pending results pointing at live slots
+                r.pending.flags = D.Flags(buf=self._flags[r.slot])
+                r.pending.tau = self._taus[r.slot:r.slot + 1]
+        if k >= len(self._logs):
+            self._logs.append(torch.empty(0, dtype=torch.int64, device="cuda"))
+        if self._logs[k].numel() < budget + 1:
+            self._logs[k] = torch.empty(budget + 1, dtype=torch.int64, device="cuda")
         # in place: every tile's FP64 input is staged in shared memory before
         # its rounded values are stored back to the same addresses
         p = ops.round_and_log_adaptive(flat, self.b_r, budget, iters=self.iters, out_dtype=torch.float64,
-                                       out=flat, check=False, tag=f"hooks_{kind}")
-        self.records.append(HookRecord(name, kind, n, budget, p))
+                                       out=flat, log_out=self._logs[k][: budget + 1], check=False,
+                                       tag=f"hooks_{kind}", tau_out=self._taus[k:k + 1], flags_out=self._flags[k])
+        self.records.append(HookRecord(name, kind, n, budget, p, k))
         return t if inplace else flat.view(t.shape)
 
     def _fwd_hook(self, name):
@@ -79,19 +100,26 @@ class RoundAndLogHooks:
         return hook
 
     def collect(self) -> dict:
-        """Synchronise once: per-tensor taus and log sizes of the step."""
-        taus, counts = [], []
-        for r in self.records:
-            _, log, tau = r.pending.finish()
-            taus.append(tau)
-            counts.append(log.count)
-            assert log.count <= r.budget
-        out = {"tensors": len(self.records), "elements": sum(r.numel for r in self.records),
-               "logged": sum(counts), "fwd": sum(1 for r in self.records if r.kind == "fwd"),
-               "bwd": sum(1 for r in self.records if r.kind == "bwd"),
-               "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None}
+        """Synchronise once: per-tensor taus and log sizes of the step (one
+        copy of the step's result slots), then clear the slots for the next
+        step.  Raises the reference's errors like PendingAdaptive.finish."""
+        m = len(self.records)
+        fl = self._flags[:m].cpu().tolist()
+        taus = self._taus[:m].cpu().tolist()
+        records = list(self.records)
+        self._flags[:m].zero_()  # the slots start the next step cleared, whatever is raised below
         self.records.clear()
-        return out
+        counts = []
+        for r, f in zip(records, fl):
+            D.raise_fpround(int(f[0]) & 0xFFFFFFFF)
+            if f[2] > r.budget + 1:
+                raise ops.LogOverflow(f"sparse log needs {f[2]} words, capacity {r.budget + 1}")
+            counts.append(int(f[2]))
+            assert f[2] <= r.budget
+        return {"tensors": m, "elements": sum(r.numel for r in records),
+                "logged": sum(counts), "fwd": sum(1 for r in records if r.kind == "fwd"),
+                "bwd": sum(1 for r in records if r.kind == "bwd"),
+                "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None}
 
     def remove(self):
         for h in self._handles:

@@ -138,13 +138,16 @@ class PendingAdaptive:
 
 def round_and_log_adaptive(x: torch.Tensor, b_r: int, budget: int, *, iters: int = 30,
                            out_dtype=torch.float32, global_base: int = 0, out: torch.Tensor | None = None,
-                           log_out: torch.Tensor | None = None, check: bool = True, tag: str = "adaptive"):
+                           log_out: torch.Tensor | None = None, check: bool = True, tag: str = "adaptive",
+                           tau_out: torch.Tensor | None = None, flags_out: torch.Tensor | None = None):
     """Per-tensor adaptive threshold + round-and-log, all on the device.
 
     tau = protocol.search_tau_budget(x, b_r, budget, iters) (bit-identical:
     same selection, same FP64 bisection run by one device thread), then the
     sparse round-and-log at tau.  No host synchronisation unless check=True,
-    so a whole model's worth of tensors can be queued or graph-captured."""
+    so a whole model's worth of tensors can be queued or graph-captured.
+    tau_out (float64[1]) and flags_out (zeroed int64[6]) let a caller supply
+    the per-call result slots, so repeated calls allocate nothing."""
     _check_b(b_r)
     D.require_cuda()
     shape = tuple(x.shape) if x.dim() else (1,)
@@ -153,9 +156,9 @@ def round_and_log_adaptive(x: torch.Tensor, b_r: int, budget: int, *, iters: int
     kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
     y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
     words = log_out if log_out is not None else torch.empty(max(budget + 1, 1), dtype=torch.int64, device=t.device)
-    tau = torch.empty(1, dtype=torch.float64, device=t.device)
+    tau = tau_out if tau_out is not None else torch.empty(1, dtype=torch.float64, device=t.device)
     ws = D.workspace(int(_lib.lib().vt_round_log_adaptive_workspace(n)), tag)
-    f = D.Flags()
+    f = D.Flags(buf=flags_out)
     if n:
         _lib.call("vt_round_log_adaptive", D.ptr(t), n, b_r, int(budget), int(iters), kind, D.ptr(y), D.ptr(words),
                   words.numel(), int(global_base), None, None, D.ptr(tau), f.cnt_ptr, f.err_ptr, D.ptr(ws),

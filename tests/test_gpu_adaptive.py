@@ -99,3 +99,29 @@ def test_in_place_fp64(oracle):
     assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
                           oracle.sparse_from_codes(oracle.direction_array(x, 32, t_or)))
     assert np.array_equal(bits(xt.cpu().numpy()), bits(oracle.rnd_array(x, 32)))
+
+
+@pytest.mark.parametrize("b_r,kind", [(32, "zeros"), (32, "tiny"), (32, "ragged"), (26, "normal"), (10, "tiny")])
+def test_in_place_key_pass(oracle, b_r, kind):
+    """The in-place key pass (adapt_keys32_kernel for b_r = 32, the general
+    kernel otherwise): exact zeros (never candidates on the fast test),
+    values below 2^-126 and beyond FP32 (the FP64 key path), and sizes that
+    end inside a CTA iteration."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(17 + b_r)
+    n = {"ragged": 4096 * 37 + 1234}.get(kind, 250_001)
+    x = rng.normal(0.0, 1.0, n)
+    if kind == "zeros":
+        x[rng.random(n) < 0.4] = 0.0
+        x[rng.random(n) < 0.01] = -0.0
+    elif kind == "tiny":
+        x = x * np.exp2(rng.integers(-160, 20, n))
+    xt = torch.from_numpy(x.copy()).cuda()
+    B = int(0.005 * n)
+    y, log, tau = ops.round_and_log_adaptive(xt, b_r, B, out_dtype=torch.float64, out=xt)
+    t_or = oracle.search_tau_budget(x, b_r, B)
+    assert tau == t_or, (tau.hex(), t_or.hex())
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
+                          oracle.sparse_from_codes(oracle.direction_array(x, b_r, t_or)))
+    assert np.array_equal(bits(xt.cpu().numpy()), bits(oracle.rnd_array(x, b_r)))

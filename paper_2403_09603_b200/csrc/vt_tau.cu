@@ -661,18 +661,17 @@ namespace vt {
 //      kCandFactor x budget elements have p > L when the dropped mantissa
 //      bits are uniform): y (final: rnd does not depend on tau) plus the
 //      ascending candidate words (local index << 1 | up);
-//   2. adapt_hist_kernel: gather each candidate's key (FP64 bits of p) from
-//      x, histogram its top digit above L; the last CTA picks the digit of
-//      the (budget+1)-th largest key;
-//   3. adapt_select_kernel: compact the keys of that digit; the last CTA
-//      finishes the exact selection in shared memory and runs the FP64
-//      bisection (protocol.py:494-506 skeleton) -> tau;
-//   4. adapt_filter_kernel: the log is exactly the candidates with p > tau,
-//      kept in order by a ticketed decoupled look-back.
+//   2. the candidates' keys (FP64 bits of p, gathered from x) and the
+//      histogram of their top digit above L -> the digit of the
+//      (budget+1)-th largest key;
+//   3. the keys of that digit, their exact selection and the FP64 bisection
+//      (protocol.py:494-506 skeleton) -> tau;
+//   4. the log is exactly the candidates with p > tau, in order.
+// A single call runs 2-4 as one cooperative launch (adapt_tail_kernel); a
+// batch (adapt_*_batch_kernel) gives each tensor a share of three grids.
 // If fewer than budget+1 candidates exist (v <= L) or they overflow the
-// buffer, the exact selection over x (the multi-pass radix select above) and
-// a second rl_fused at the device tau run instead; in the common case those
-// kernels return at once.
+// buffer, the exact selection over x (the multi-pass radix select above,
+// fb_selection) and a second rounding pass at the device tau run instead.
 // ---------------------------------------------------------------------------
 
 constexpr int kCandFactor = 3;
@@ -682,7 +681,7 @@ constexpr int kAdThreads = 256;
 constexpr int kFChunk = 8192;  // candidates per filter ticket
 
 struct AdaptHdr {
-  int32_t fallback;    // 1: the exact path runs (written by adapt_hist_kernel every call)
+  int32_t fallback;    // 1: the exact path runs (written by the tail / hist kernels every call)
   uint32_t arrived;    // CTAs done (hist, select kernels; reset by the last one)
   int64_t ccount;      // candidates (cursor_out of the rounding pass)
   int64_t scratch;     // the rounding pass's counters[0] (unused)
@@ -692,7 +691,7 @@ struct AdaptHdr {
   uint64_t bin_count;  // keys in that digit
   int32_t done;        // 1: decided at the top digit (v > tau_hi)
   int32_t pad;
-  uint64_t cand2;      // keys compacted by adapt_select_kernel
+  uint64_t cand2;      // keys of the selected digit (compacted)
   uint32_t f_epoch, f_ticket, f_done, f_pad;
   uint64_t above_lo;   // in-place calls: keys > lo_key (decides v <= tau_lo without a fallback)
 };
@@ -798,15 +797,6 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
   }
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_hist_kernel(const double* __restrict__ x, Grid g,
-                                                                const uint64_t* __restrict__ cw,
-                                                                uint64_t* __restrict__ ck, int64_t cap,
-                                                                int64_t budget, uint64_t L_key, uint64_t hi_key,
-                                                                int s0, AdaptHdr* h, uint32_t* __restrict__ hist,
-                                                                uint64_t* __restrict__ fstatus, bool gather) {
-  adapt_hist_body(x, g, cw, ck, cap, budget, L_key, hi_key, s0, h, hist, fstatus, gather, blockIdx.x, gridDim.x);
-}
-
 // One FP64 bisection thread: the search_tau skeleton on the selected key.
 __device__ void bisect_to(uint64_t key, double lower, double upper, int iters, DevThr* out, double* tau_out) {
   const double v = __longlong_as_double((long long)key);
@@ -894,15 +884,6 @@ __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ c
     h->arrived = 0;
     h->above_lo = 0;
   }
-}
-
-__global__ void __launch_bounds__(kAdThreads) adapt_select_kernel(const uint64_t* __restrict__ ck, uint64_t L_key,
-                                                                  uint64_t hi_key, int s0, AdaptHdr* h,
-                                                                  uint64_t* __restrict__ cand2, double lower,
-                                                                  double upper, int iters, DevThr* dthr,
-                                                                  double* tau_out, uint64_t* key_out) {
-  adapt_select_body(ck, L_key, hi_key, s0, h, cand2, lower, upper, iters, dthr, tau_out, key_out, blockIdx.x,
-                    gridDim.x);
 }
 
 // The log: candidates with p > tau, in order.  Persistent CTAs draw chunk
@@ -1043,15 +1024,6 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
   }
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_filter_kernel(const uint64_t* __restrict__ cw,
-                                                                  const uint64_t* __restrict__ ck, AdaptHdr* h,
-                                                                  const DevThr* dthr, uint64_t* sparse, int64_t cap,
-                                                                  int64_t global_base, const int64_t* cursor_in,
-                                                                  int64_t* cursor_out, int64_t* counters,
-                                                                  uint64_t* status) {
-  adapt_filter_body(cw, ck, h, dthr, sparse, cap, global_base, cursor_in, cursor_out, counters, status, gridDim.x);
-}
-
 // In-place calls: one streaming read of x appends the keys above L
 // (unordered, warp-aggregated); the rounding pass then runs at the selected
 // tau and writes the ordered log itself.
@@ -1147,7 +1119,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
         uint32_t wb = 0;
         if (lane == 31) wb = atomicAdd(&scount, tot);
         uint32_t pos = __shfl_sync(0xffffffffu, wb, 31) + inc - c;
-        // the candidate's x itself: adapt_hist_kernel turns it into its key
+        // the candidate's x itself: the tail kernel turns it into its key
 #pragma unroll
         for (int e = 0; e < kE; ++e)
           if ((cm >> e) & 1u) sbuf[pos++] = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
@@ -1283,16 +1255,229 @@ __device__ void fb_selection(const double* __restrict__ x, int64_t n, const Grid
   }
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_fb_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                              AdaptHdr* h, BudState* st, uint32_t* hist,
-                                                              uint64_t* cand, int64_t budget, uint64_t lo_key,
-                                                              uint64_t hi_key, double lower, double upper, int iters,
-                                                              uint64_t* key_out, DevThr* dthr, double* tau_out,
-                                                              int32_t* errp) {
+// ---------------------------------------------------------------------------
+// The single-call tail as ONE cooperative launch (grid-wide syncs between
+// phases instead of kernel boundaries and last-CTA hand-offs):
+//   0. can the candidates decide?  (else: in-place "v <= tau_lo", or the
+//      exact multi-pass fallback, fb_selection, in this same launch)
+//   1. every candidate's key (gathered from x, or from the x value the
+//      in-place key pass staged) and the top-digit histogram above L
+//   2. every CTA selects the digit of the (budget+1)-th largest key from the
+//      global histogram; the keys of that digit are compacted
+//   3. CTA 0: exact selection among them and the FP64 bisection -> tau
+//   4. out of place: the log = candidates with key > tau, in order (per-CTA
+//      contiguous ranges, counts exchanged through a grid sync)
+// ---------------------------------------------------------------------------
+struct TailArgs {
+  const double* x;
+  Grid g0;
+  const uint64_t* cw;
+  uint64_t* ck;
+  uint64_t* c2;
+  uint32_t* ahist;
+  AdaptHdr* h;
+  int64_t cap, budget, n;
+  uint64_t L_key, lo_key, hi_key;
+  int s0, iters;
+  double lower, upper;
+  DevThr* dthr;
+  double* tau_out;
+  uint64_t* key;
+  BudState* st;
+  uint32_t* bhist;
+  uint64_t* bcand;
+  int32_t* err;
+  // out of place: the ordered filter into the log (sparse == nullptr: in place)
+  uint64_t* sparse;
+  int64_t sparse_cap, global_base;
+  const int64_t* cursor_in;
+  int64_t* cursor_out;
+  int64_t* counters;
+};
+
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* s_acc) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (threadIdx.x == 0) *s_acc = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(s_acc, v);
+  __syncthreads();
+  return *s_acc;
+}
+
+__global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a) {
   __shared__ uint32_t sh[kBudBins];
-  if (!h->fallback) return;
-  fb_selection(x, n, g, h, st, hist, cand, budget, lo_key, hi_key, lower, upper, iters, key_out, dthr, tau_out, errp,
-               sh);
+  __shared__ unsigned long long s_acc;
+  __shared__ uint32_t s_warp[kAdThreads / 32];
+  cg::grid_group grid = cg::this_grid();
+  AdaptHdr* h = a.h;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t blk = blockIdx.x, nblk = gridDim.x;
+  const bool gather = a.sparse != nullptr;
+  const int64_t M = h->ccount;
+  const int64_t budget = a.budget;
+  // 0. grid-uniform decision (every CTA reads the same words)
+  if (M > a.cap || M < budget + 1) {
+    const bool low = !gather && M <= a.cap && (int64_t)h->above_lo <= budget;
+    grid.sync();  // every CTA has read above_lo
+    if (low) {  // at most budget keys above tau_lo: v <= tau_lo fixes the bisection
+      if (blk == 0 && tid == 0) {
+        h->fallback = 0;
+        h->above_lo = 0;
+        *a.key = a.lo_key;
+        bisect_to(a.lo_key, a.lower, a.upper, a.iters, a.dthr, a.tau_out);
+      }
+      return;
+    }
+    if (blk == 0 && tid == 0) h->fallback = 1;
+    fb_selection(a.x, a.n, a.g0, h, a.st, a.bhist, a.bcand, budget, a.lo_key, a.hi_key, a.lower, a.upper, a.iters,
+                 a.key, a.dthr, a.tau_out, a.err, sh);
+    return;
+  }
+  // 1. keys and the top-digit histogram
+  for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
+  __syncthreads();
+  uint32_t err = 0;
+  unsigned long long above = 0;
+  {
+    constexpr int kGU = 8;
+    const int64_t stride = nblk * kAdThreads;
+    for (int64_t i0 = blk * kAdThreads + tid; i0 < M; i0 += kGU * stride) {
+      double xv[kGU];
+      if (gather) {
+        uint64_t w[kGU];
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? a.cw[i0 + u * stride] : 0ull;
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(a.x + (w[u] >> 1)) : 0.0;
+      } else {
+#pragma unroll
+        for (int u = 0; u < kGU; ++u)
+          xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)a.ck[i0 + u * stride]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        if (i0 + u * stride >= M) break;
+        const uint64_t key = dist_key(xv[u], a.g0, err);
+        a.ck[i0 + u * stride] = key;
+        if (key > a.hi_key) ++above;
+        else if (key > a.L_key) atomicAdd(&sh[(uint32_t)((key - a.L_key - 1) >> a.s0)], 1u);
+      }
+    }
+  }
+  above = block_sum(above, &s_acc);
+  for (int i = tid; i < kAdBins; i += kAdThreads)
+    if (sh[i]) atomicAdd(&a.ahist[i], sh[i]);
+  if (tid == 0 && above) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above), above);
+  grid.sync();
+  // 2. the digit (every CTA, same answer), then its keys
+  const int64_t above_hi = (int64_t)h->above;
+  const bool past_hi = above_hi > budget;  // v > tau_hi
+  int bin = 0;
+  int64_t rank = 0;
+  const uint64_t lo1 = a.L_key + 1;
+  if (!past_hi) {
+    int64_t above_bin;
+    stage_hist(a.ahist, sh, kAdBins);
+    select_digit(sh, kAdBins, budget - above_hi, bin, above_bin);
+    rank = budget - above_hi - above_bin;
+    const uint64_t digit = (uint64_t)bin;
+    const int64_t stride = nblk * kAdThreads;
+    for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += stride) {  // warp-uniform bounds: a ballot follows
+      const int64_t i = i0 + tid;
+      const uint64_t key = i < M ? a.ck[i] : 0ull;
+      const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader)
+          pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (in) a.c2[pos + __popc(m & lanemask_lt())] = key - lo1;
+      }
+    }
+  }
+  grid.sync();
+  // 3. CTA 0: exact selection + bisection; every CTA clears its share of the
+  // histogram (all CTAs read it before the sync above)
+  for (int64_t i = blk * kAdThreads + tid; i < kAdBins; i += nblk * kAdThreads) a.ahist[i] = 0u;
+  if (blk == 0) {
+    uint64_t key = 0x7ff0000000000000ull;
+    if (!past_hi) {
+      const int64_t m = (int64_t)h->cand2;
+      uint64_t low = 0, lmask = 0;
+      for (int top = a.s0; top > 0;) {
+        const int bits = top < kAdBits ? top : kAdBits;
+        top -= bits;
+        for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < m; i += kAdThreads) {
+          const uint64_t o = a.c2[i];
+          if ((o & lmask) == low) atomicAdd(&sh[(uint32_t)(o >> top) & ((1u << bits) - 1u)], 1u);
+        }
+        __syncthreads();
+        int b2;
+        int64_t ab2;
+        select_digit(sh, 1 << bits, rank, b2, ab2);
+        low |= (uint64_t)b2 << top;
+        lmask |= ((1ull << bits) - 1ull) << top;
+        rank -= ab2;
+        __syncthreads();
+      }
+      key = lo1 + (((uint64_t)bin << a.s0) | low);
+    }
+    if (tid == 0) {
+      *a.key = key;
+      bisect_to(key, a.lower, a.upper, a.iters, a.dthr, a.tau_out);
+      h->above = 0;
+      h->cand2 = 0;
+      h->above_lo = 0;
+      h->fallback = 0;
+    }
+  }
+  report_err(a.err, err);
+  if (!gather) return;
+  grid.sync();
+  // 4. the log: candidates with key > tau, in order
+  const uint64_t tau_key = (uint64_t)__double_as_longlong(a.dthr->tau);
+  const int64_t per = ((M + nblk - 1) / nblk + kAdThreads - 1) / kAdThreads * kAdThreads;
+  const int64_t r0 = blk * per, r1 = r0 + per < M ? r0 + per : M;
+  unsigned long long cnt = 0;
+  for (int64_t i = r0 + tid; i < r1; i += kAdThreads) cnt += a.ck[i] > tau_key ? 1u : 0u;
+  cnt = block_sum(cnt, &s_acc);
+  uint64_t* bcnt = a.c2;  // the digit keys are done with: per-CTA counts
+  if (tid == 0) bcnt[blk] = cnt;
+  grid.sync();
+  unsigned long long pre = 0;
+  for (int64_t b = tid; b < blk; b += kAdThreads) pre += bcnt[b];
+  pre = block_sum(pre, &s_acc);
+  const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
+  int64_t pos = cur + (int64_t)pre;
+  for (int64_t c0 = r0; c0 < r1; c0 += kAdThreads) {
+    const int64_t i = c0 + tid;
+    const bool keep = i < r1 && a.ck[i] > tau_key;
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kAdThreads / 32; ++w) {
+      wpre += w < warp ? s_warp[w] : 0u;
+      tot += s_warp[w];
+    }
+    if (keep) {
+      const int64_t p = pos + wpre + __popc(m & lanemask_lt());
+      const uint64_t w = a.cw[i];
+      if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+    }
+    pos += tot;
+    __syncthreads();
+  }
+  if (blk == nblk - 1 && tid == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(pos - cur));
+    if (a.cursor_out) *a.cursor_out = pos;
+  }
 }
 
 // Cooperative grid for the fallback kernels: every CTA co-resident.
@@ -1317,7 +1502,7 @@ namespace vt {
 // Everything that outlives a call (the headers, the self-cleaning histogram,
 // the round-and-log epoch header) sits at offsets independent of n, because
 // one workspace serves calls of any size; the filter status words are
-// cleared by adapt_hist_kernel for the chunks a call uses.
+// cleared by the batched histogram kernel for the chunks a call uses.
 struct AdaptLayout {
   size_t tau, rl, hist, cw, ck, c2, fst, total;
   int64_t cap;
@@ -1379,9 +1564,6 @@ __host__ __device__ inline AdPtrs adapt_ptrs(uint8_t* w, const AdaptLayout& lay)
 
 namespace {
 AdaptLayout adapt_layout(int64_t n) { return adapt_layout_rl(n, vt_round_log_workspace(n)); }
-int adapt_grid(int64_t work, int per) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((work + per - 1) / per, 148 * 4));
-}
 }  // namespace
 
 extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) { return adapt_layout(n).total; }
@@ -1412,7 +1594,7 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   uint64_t* bcand = P.bcand;
   void* rws = w + lay.rl;
   uint32_t* ahist = P.ahist;
-  uint64_t *cw = P.cw, *ck = P.ck, *c2 = P.c2, *fst = P.fst;
+  uint64_t *cw = P.cw, *ck = P.ck, *c2 = P.c2;
   const bool fast = b_r == 32;
   const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
   uint64_t lo_key, hi_key;
@@ -1438,9 +1620,8 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(out);
   const bool aliased = ybytes && ya < xa + (uintptr_t)n * 8 && xa < ya + (uintptr_t)n * ybytes;
   int rc = 0;
-  const int gc = adapt_grid(lay.cap, kAdThreads * 8);
   if (aliased) {
-    // 1'. keys above L (unordered), 2-3. selection among them, bisection
+    // 1'. the candidates' x values (unordered) from one read of x
     if (cudaMemsetAsync(&h->ccount, 0, sizeof(int64_t), s) != cudaSuccess) return vt_check_launch("memset");
     const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
     if (fast) {
@@ -1455,43 +1636,59 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
       cw8(make_grid(b_r, lo).thr, c8lo, w8lo);
       adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, c8L, w8L, c8lo, w8lo, ck, lay.cap, h,
                                                     err);
-    } else
+    } else {
       adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
-                                                         lay.cap, h, err);
+                                                  lay.cap, h, err);
+    }
     if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
-    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,
-                                                false);
-    if ((rc = vt_check_launch("adapt_hist_kernel"))) return rc;
-    adapt_select_kernel<<<gc, kAdThreads, 0, s>>>(ck, L_key, hi_key, s0, h, c2, lo, hi, iters, dthr, tau_out, key);
-    if ((rc = vt_check_launch("adapt_select_kernel"))) return rc;
   } else {
     // 1. rounding pass: y + candidate words (local index << 1 | up) with p > L
     rc = rl_stream(x, n, gL, thrL, fast, out_kind, out, cw, lay.cap, 0, nullptr, &h->ccount, &h->scratch, err,
                    rws, s);
     if (rc) return rc;
-    // 2-3. exact selection of the (budget+1)-th largest p among the candidates, bisection
-    adapt_hist_kernel<<<gc, kAdThreads, 0, s>>>(x, g0, cw, ck, lay.cap, budget, L_key, hi_key, s0, h, ahist, fst,
-                                                true);
-    if ((rc = vt_check_launch("adapt_hist_kernel"))) return rc;
-    adapt_select_kernel<<<gc, kAdThreads, 0, s>>>(ck, L_key, hi_key, s0, h, c2, lo, hi, iters, dthr, tau_out, key);
-    if ((rc = vt_check_launch("adapt_select_kernel"))) return rc;
-    // 4. the log = candidates with p > tau, in order
-    adapt_filter_kernel<<<adapt_grid(lay.cap, kFChunk), kAdThreads, 0, s>>>(
-        cw, ck, h, dthr, sparse, sparse_cap, global_base, cursor_in, cursor_out, counters, fst);
-    if ((rc = vt_check_launch("adapt_filter_kernel"))) return rc;
   }
-  // fallback (a no-op unless the candidates could not decide): exact selection over x, then a full pass
+  // 2-4. one cooperative launch: selection of the (budget+1)-th largest p
+  // among the candidates, bisection, and (out of place) the ordered log; or
+  // the exact fallback when the candidates cannot decide
   {
-    const double* xa = x;
-    int64_t na = n, ba = budget;
-    Grid ga = g0;
-    uint64_t lk = lo_key, hk = hi_key;
-    double la = lo, ua = hi;
-    int ia = iters;
-    void* args[] = {&xa, &na, &ga, &h, &st, &bhist, &bcand, &ba, &lk, &hk, &la, &ua, &ia, &key, &dthr, &tau_out, &err};
-    cudaLaunchCooperativeKernel((const void*)adapt_fb_kernel, dim3(coop_grid(adapt_fb_kernel)), dim3(kAdThreads),
-                                args, 0, s);
-    if ((rc = vt_check_launch("adapt_fb_kernel"))) return rc;
+    TailArgs ta{};
+    ta.x = x;
+    ta.g0 = g0;
+    ta.cw = cw;
+    ta.ck = ck;
+    ta.c2 = c2;
+    ta.ahist = ahist;
+    ta.h = h;
+    ta.cap = lay.cap;
+    ta.budget = budget;
+    ta.n = n;
+    ta.L_key = L_key;
+    ta.lo_key = lo_key;
+    ta.hi_key = hi_key;
+    ta.s0 = s0;
+    ta.iters = iters;
+    ta.lower = lo;
+    ta.upper = hi;
+    ta.dthr = dthr;
+    ta.tau_out = tau_out;
+    ta.key = key;
+    ta.st = st;
+    ta.bhist = bhist;
+    ta.bcand = bcand;
+    ta.err = err;
+    if (!aliased) {
+      ta.sparse = sparse;
+      ta.sparse_cap = sparse_cap;
+      ta.global_base = global_base;
+      ta.cursor_in = cursor_in;
+      ta.cursor_out = cursor_out;
+      ta.counters = counters;
+    }
+    const int gmax = coop_grid(adapt_tail_kernel);
+    const int grid = (int)std::min<int64_t>(gmax, std::max<int64_t>(64, (int64_t)(want / 2048)));
+    void* args[] = {&ta};
+    cudaLaunchCooperativeKernel((const void*)adapt_tail_kernel, dim3(grid), dim3(kAdThreads), args, 0, s);
+    if ((rc = vt_check_launch("adapt_tail_kernel"))) return rc;
   }
   // the rounding pass at the device tau: always for in-place calls, else only after a fallback
   return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,

@@ -125,3 +125,38 @@ def test_in_place_key_pass(oracle, b_r, kind):
     assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
                           oracle.sparse_from_codes(oracle.direction_array(x, b_r, t_or)))
     assert np.array_equal(bits(xt.cpu().numpy()), bits(oracle.rnd_array(x, b_r)))
+
+
+@pytest.mark.parametrize("case", ["on_grid", "midpoints", "huge_budget", "low"])
+def test_in_place_tail_decisions(oracle, case):
+    """Every decision of the cooperative tail, in place: too few candidates
+    (mostly on-grid data -> exact fallback), too many (exact midpoints, a 40%
+    budget), and v <= tau_lo settled from the key pass's count alone."""
+    import torch
+    from paper_2403_09603_b200 import ops, workloads
+    rng = np.random.default_rng(23)
+    n = 300_000
+    B = int(0.005 * n)
+    if case == "on_grid":
+        x = np.where(rng.random(n) < 0.9, np.round(rng.normal(0, 100, n)), rng.normal(0, 1, n))
+    elif case == "midpoints":
+        x = workloads.config0_x(n, 8)
+    elif case == "huge_budget":
+        x = rng.normal(0, 1, n)
+        B = int(0.4 * n)
+    else:  # nearly everything on the grid, the rest far from the midpoint: p <= tau_lo for all
+        x = np.round(rng.normal(0, 100, n))
+        k = rng.random(n) < 0.002
+        x[k] += 0.25
+    xt = torch.from_numpy(x.copy()).cuda()
+    y, log, tau = ops.round_and_log_adaptive(xt, 32, B, out_dtype=torch.float64, out=xt)
+    t_or = oracle.search_tau_budget(x, 32, B)
+    assert tau == t_or, (tau.hex(), t_or.hex())
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
+                          oracle.sparse_from_codes(oracle.direction_array(x, 32, t_or)))
+    assert np.array_equal(bits(xt.cpu().numpy()), bits(oracle.rnd_array(x, 32)))
+    # the workspace is clean afterwards: a plain call on fresh data still matches
+    z = rng.normal(0, 1, 50_000)
+    zt = torch.from_numpy(z.copy()).cuda()
+    _, log2, tau2 = ops.round_and_log_adaptive(zt, 32, 250, out_dtype=torch.float64, out=zt)
+    assert tau2 == oracle.search_tau_budget(z, 32, 250)

@@ -1,0 +1,72 @@
+"""The multi-GPU path of paper_2403_09603_b200/dist.py on a real NCCL
+communicator (one rank: this pool's boxes have one GPU, and NCCL does not
+put two ranks on one device).  The collectives -- the count all-gather, the
+Merkle block-root all-gather, the corrections all-reduce -- run through
+NCCL here; their multi-rank arithmetic is covered by the world-size-2 gloo
+tests (tests/test_dist_gloo.py).  Results must equal the single-device
+operators bit for bit."""
+
+from __future__ import annotations
+
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    import torch
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield dist.group.WORLD
+    dist.destroy_process_group()
+
+
+def test_sharded_round_and_log_replay_nccl(nccl_group):
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    from paper_2403_09603_b200 import ops, workloads
+    n = (1 << 20) + 777
+    xt, xa = workloads.config1_pair_torch(n, seed=4, device=torch.device("cuda"))
+    lo, hi = vdist.shard_range(n, 0, 1)
+    assert (lo, hi) == (0, n)
+    base = 5 * n
+    y, slog = vdist.round_and_log_sharded(xt, 32, workloads.TAU_CONFIG0, base, group=nccl_group)
+    y1, log1 = ops.round_and_log(xt, 32, workloads.TAU_CONFIG0, global_base=base)
+    assert torch.equal(y.view(torch.int32), y1.view(torch.int32))
+    assert torch.equal(slog.local.words, log1.words)
+    assert slog.offset == 0 and slog.total == log1.count and slog.counts.tolist() == [log1.count]
+    ya, corr = vdist.replay_sharded(xa, 32, slog, base, group=nccl_group)
+    ya1, corr1 = ops.replay(xa, 32, log1, global_base=base)
+    assert torch.equal(ya.view(torch.int32), ya1.view(torch.int32)) and corr == corr1
+    assert torch.equal(ya.view(torch.int32), y.view(torch.int32))
+
+
+def test_sharded_budget_search_nccl(nccl_group, oracle):
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    x = np.random.default_rng(12).normal(0.0, 3.0, 400_003)
+    B = int(0.005 * x.size)
+    tau = vdist.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, B, group=nccl_group)
+    assert tau == oracle.search_tau_budget(x, 32, B)
+
+
+def test_merkle_sharded_nccl(nccl_group):
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    from paper_2403_09603_b200 import merkle
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    w = torch.randn(3 * (1 << 20) + 12345, dtype=torch.float32, device="cuda", generator=g) * 0.02
+    b = w.view(torch.uint8)
+    n_leaves = (b.numel() + 4095) // 4096
+    lv, top = vdist.merkle_sharded(b, n_leaves, group=nccl_group, k=8)
+    ref = merkle.merkle_chunked(w)
+    assert bytes(top[-1][0].cpu().numpy()) == ref.root

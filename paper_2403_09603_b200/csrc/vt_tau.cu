@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
   __shared__ uint64_t sbuf[kBuf];
   __shared__ uint32_t scount;
   __shared__ unsigned long long sbase;
-  uint32_t err = 0, above_lo = 0;
+  uint32_t err = 0;
   const int lane = threadIdx.x & 31;
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
   if (threadIdx.x == 0) scount = 0;
@@ -1105,7 +1105,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
         cm &= vm;
         ab &= vm;
       }
-      above_lo += __popc(ab);
       // warp-aggregated append of the candidates' x values
       const uint32_t c = __popc(cm);
       uint32_t inc = c;
@@ -1130,9 +1129,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
   }
   if (scount) flush();
   report_err(errp, err);
-  for (int o = 16; o > 0; o >>= 1) above_lo += __shfl_xor_sync(0xffffffffu, above_lo, o);
-  if (lane == 0 && above_lo)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), (unsigned long long)above_lo);
 }
 
 // b_r = 32 form of adapt_keys_kernel: per element one shifted unsigned
@@ -1143,8 +1139,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
 // low29 = 0 and are never counted; only nonzero values outside the FP32
 // normal range take the FP64 key of dist_key (rare path).
 __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                                  uint64_t L_key, uint64_t lo_key, uint32_t c8L,
-                                                                  uint32_t w8L, uint32_t c8lo, uint32_t w8lo,
+                                                                  uint64_t L_key, uint32_t c8L, uint32_t w8L,
                                                                   uint64_t* __restrict__ ck, int64_t cap,
                                                                   AdaptHdr* h, int32_t* errp) {
   constexpr int kSteps = 4;  // x 1024 elements per CTA iteration, loads issued up front
@@ -1155,7 +1150,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* run = sbuf[warp];
   const uint32_t lt = lanemask_lt();
-  uint32_t err = 0, above_lo = 0, cnt = 0;
+  uint32_t err = 0, cnt = 0;
   auto flush = [&]() {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(&h->ccount), (unsigned long long)cnt);
@@ -1186,11 +1181,11 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
     for (int e = 0; e < kE; ++e) {
       const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
       const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
-      const uint32_t s3 = lo32 << 3;
-      const bool bad = outside_normal32(ahi) && (ahi | lo32) != 0u;
-      const bool in = (s3 - c8L) < w8L && !bad;
-      above_lo += ((s3 - c8lo) < w8lo && !bad) ? 1u : 0u;
-      badw |= bad;
+      // outside the FP32 normal range: never a fast candidate; the FP64 key
+      // path decides it unless ahi == 0 (+-0 and FP64 subnormals: p ~ 0)
+      const bool o = outside_normal32(ahi);
+      const bool in = ((lo32 << 3) - c8L) < w8L && !o;
+      badw |= o && ahi != 0u;
       const uint32_t m = __ballot_sync(0xffffffffu, in);
       if (m) {
         if (in) run[cnt + __popc(m & lt)] = bits;
@@ -1204,11 +1199,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
         const uint64_t bits = (uint64_t)__double_as_longlong(xe);
         const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
         bool in = false;
-        if (outside_normal32(ahi) && (ahi | lo32) != 0u) {
-          const uint64_t key = dist_key(xe, g, err);
-          above_lo += key > lo_key ? 1u : 0u;
-          in = key > L_key;
-        }
+        if (outside_normal32(ahi) && ahi != 0u) in = dist_key(xe, g, err) > L_key;
         const uint32_t m = __ballot_sync(0xffffffffu, in);
         if (m) {
           if (in) run[cnt + __popc(m & lt)] = bits;
@@ -1220,9 +1211,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
   }
   if (cnt) flush();
   report_err(errp, err);
-  for (int o = 16; o > 0; o >>= 1) above_lo += __shfl_xor_sync(0xffffffffu, above_lo, o);
-  if (lane == 0 && above_lo)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), (unsigned long long)above_lo);
 }
 
 // Exact fallback, gated on h->fallback: the multi-pass budget selection over
@@ -1318,6 +1306,25 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
   const int64_t budget = a.budget;
   // 0. grid-uniform decision (every CTA reads the same words)
   if (M > a.cap || M < budget + 1) {
+    if (!gather && M <= a.cap) {
+      // in place, too few candidates: count the keys above tau_lo (one pass
+      // over x, which the rounding pass has not overwritten yet)
+      uint32_t e2 = 0;
+      unsigned long long c = 0;
+      const int64_t n4 = a.n / 4 * 4;
+      for (int64_t i = (blk * kAdThreads + tid) * 4; i < a.n; i += nblk * kAdThreads * 4) {
+        if (i < n4) {
+          const D4 xv = ldg_stream4(a.x + i);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) c += dist_key(xv.v[v], a.g0, e2) > a.lo_key ? 1u : 0u;
+        } else {
+          for (int64_t j = i; j < a.n; ++j) c += dist_key(a.x[j], a.g0, e2) > a.lo_key ? 1u : 0u;
+        }
+      }
+      c = block_sum(c, &s_acc);
+      if (tid == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above_lo), c);
+      grid.sync();
+    }
     const bool low = !gather && M <= a.cap && (int64_t)h->above_lo <= budget;
     grid.sync();  // every CTA has read above_lo
     if (low) {  // at most budget keys above tau_lo: v <= tau_lo fixes the bisection
@@ -1631,11 +1638,9 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
         c8 = (t + 1u) << 3;
         w8 = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
       };
-      uint32_t c8L, w8L, c8lo, w8lo;
+      uint32_t c8L, w8L;
       cw8(gL.thr, c8L, w8L);
-      cw8(make_grid(b_r, lo).thr, c8lo, w8lo);
-      adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, c8L, w8L, c8lo, w8lo, ck, lay.cap, h,
-                                                    err);
+      adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, c8L, w8L, ck, lay.cap, h, err);
     } else {
       adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
                                                   lay.cap, h, err);

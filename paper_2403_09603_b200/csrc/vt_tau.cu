@@ -679,6 +679,7 @@ constexpr int kAdBits = 11;  // digit width of the candidate selection
 constexpr int kAdBins = 1 << kAdBits;
 constexpr int kAdThreads = 256;
 constexpr int kFChunk = 8192;  // candidates per filter ticket
+constexpr int kSmallSel = 2048;  // digit keys selected by direct counting (in 16 KB of shared memory)
 
 struct AdaptHdr {
   int32_t fallback;    // 1: the exact path runs (written by the tail / hist kernels every call)
@@ -1197,7 +1198,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
       for (int e = 0; e < kE; ++e) {
         const double xe = xv[e >> 2].v[e & 3];
         const uint64_t bits = (uint64_t)__double_as_longlong(xe);
-        const uint32_t lo32 = (uint32_t)bits, ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
+        const uint32_t ahi = (uint32_t)(bits >> 32) & 0x7fffffffu;
         bool in = false;
         if (outside_normal32(ahi) && ahi != 0u) in = dist_key(xe, g, err) > L_key;
         const uint32_t m = __ballot_sync(0xffffffffu, in);
@@ -1294,7 +1295,7 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
 }
 
 __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a) {
-  __shared__ uint32_t sh[kBudBins];
+  __shared__ __align__(16) uint32_t sh[kBudBins];
   __shared__ unsigned long long s_acc;
   __shared__ uint32_t s_warp[kAdThreads / 32];
   cg::grid_group grid = cg::this_grid();
@@ -1411,7 +1412,27 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
   for (int64_t i = blk * kAdThreads + tid; i < kAdBins; i += nblk * kAdThreads) a.ahist[i] = 0u;
   if (blk == 0) {
     uint64_t key = 0x7ff0000000000000ull;
-    if (!past_hi) {
+    if (!past_hi && (int64_t)h->cand2 <= kSmallSel) {
+      // few keys in the digit: the rank-th largest by direct counting in
+      // shared memory (one pass of m^2 / 256 compares per thread)
+      const int m = (int)h->cand2;
+      uint64_t* sk = reinterpret_cast<uint64_t*>(sh);
+      __shared__ unsigned long long s_pick;
+      for (int i = tid; i < m; i += kAdThreads) sk[i] = a.c2[i];
+      __syncthreads();
+      for (int i = tid; i < m; i += kAdThreads) {
+        const uint64_t ki = sk[i];
+        int gt = 0, eq = 0;
+        for (int j = 0; j < m; ++j) {
+          const uint64_t kj = sk[j];
+          gt += kj > ki ? 1 : 0;
+          eq += kj == ki ? 1 : 0;
+        }
+        if (gt <= rank && rank < gt + eq) s_pick = ki;  // equal keys write the same value
+      }
+      __syncthreads();
+      key = lo1 + (uint64_t)s_pick;  // the offsets carry the digit bits
+    } else if (!past_hi) {
       const int64_t m = (int64_t)h->cand2;
       uint64_t low = 0, lmask = 0;
       for (int top = a.s0; top > 0;) {

@@ -160,3 +160,30 @@ def test_in_place_tail_decisions(oracle, case):
     zt = torch.from_numpy(z.copy()).cuda()
     _, log2, tau2 = ops.round_and_log_adaptive(zt, 32, 250, out_dtype=torch.float64, out=zt)
     assert tau2 == oracle.search_tau_budget(z, 32, 250)
+
+
+@pytest.mark.parametrize("in_place", [False, True])
+def test_hot_digit_tail(oracle, in_place):
+    """More than 2048 keys in the selected digit, all tied: the tail's
+    multi-level exact selection (not the direct count) with the (B+1)-th
+    largest key inside a run of equal keys."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(29)
+    n = 1_000_000
+    x = rng.normal(0.0, 1.0, n)
+    hot = rng.random(n) < 0.03
+    b = x.view(np.uint64).copy()
+    b[hot] = (b[hot] & ~np.uint64(0x1FFFFFFF)) | np.uint64((1 << 28) - 5)  # same low 29 bits: equal p
+    x = b.view(np.float64)
+    B = int(0.005 * n)
+    xt = torch.from_numpy(x.copy()).cuda()
+    kw = dict(out_dtype=torch.float64, out=xt) if in_place else {}
+    y, log, tau = ops.round_and_log_adaptive(xt, 32, B, **kw)
+    t_or = oracle.search_tau_budget(x, 32, B)
+    assert tau == t_or, (tau.hex(), t_or.hex())
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64),
+                          oracle.sparse_from_codes(oracle.direction_array(x, 32, t_or)))
+    r = oracle.rnd_array(x, 32)
+    got = (xt if in_place else y).cpu().numpy()
+    assert np.array_equal(bits(got), bits(r if got.dtype == np.float64 else r.astype(np.float32)))

@@ -810,11 +810,34 @@ __device__ void bisect_to(uint64_t key, double lower, double upper, int iters, D
   *tau_out = upper;
 }
 
+// The rank-th largest (0-based from the top) of m offsets by direct counting
+// in shared memory (sk: m uint64 slots), one CTA: for few keys this beats the
+// digit-by-digit histogram selection.  Equal keys give the same answer.
+__device__ uint64_t select_by_count(const uint64_t* __restrict__ src, int m, int64_t rank, uint64_t* sk) {
+  __shared__ unsigned long long s_pick;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) sk[i] = src[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint64_t ki = sk[i];
+    int gt = 0, eq = 0;
+    for (int j = 0; j < m; ++j) {
+      const uint64_t kj = sk[j];
+      gt += kj > ki ? 1 : 0;
+      eq += kj == ki ? 1 : 0;
+    }
+    if (gt <= rank && rank < gt + eq) s_pick = ki;
+  }
+  __syncthreads();
+  const uint64_t v = s_pick;
+  __syncthreads();
+  return v;
+}
+
 __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ ck, uint64_t L_key, uint64_t hi_key,
                                                   int s0, AdaptHdr* h, uint64_t* __restrict__ cand2, double lower,
                                                   double upper, int iters, DevThr* dthr, double* tau_out,
                                                   uint64_t* key_out, int64_t blk, int64_t nblk) {
-  __shared__ uint32_t sh[kAdBins];
+  __shared__ __align__(16) uint32_t sh[kAdBins];
   if (h->fallback) return;
   if (h->done) {  // 1: more than budget keys above tau_hi (v > tau_hi); 2: v <= tau_lo
     if (blk == 0 && threadIdx.x == 0) {
@@ -858,6 +881,18 @@ __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ c
   // last CTA: exact selection of the rank-th largest among the digit's keys
   const int64_t m = (int64_t)h->cand2;
   int64_t rank = h->rank;
+  if (m <= kAdBins / 2) {  // the digit's offsets fit the histogram's shared memory
+    const uint64_t off = select_by_count(cand2, (int)m, rank, reinterpret_cast<uint64_t*>(sh));
+    if (threadIdx.x == 0) {
+      const uint64_t key = lo1 + off;
+      *key_out = key;
+      bisect_to(key, lower, upper, iters, dthr, tau_out);
+      h->cand2 = 0;
+      h->arrived = 0;
+      h->above_lo = 0;
+    }
+    return;
+  }
   uint64_t low = 0, lmask = 0;
   for (int top = s0; top > 0;) {
     const int bits = top < kAdBits ? top : kAdBits;
@@ -1413,25 +1448,8 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
   if (blk == 0) {
     uint64_t key = 0x7ff0000000000000ull;
     if (!past_hi && (int64_t)h->cand2 <= kSmallSel) {
-      // few keys in the digit: the rank-th largest by direct counting in
-      // shared memory (one pass of m^2 / 256 compares per thread)
-      const int m = (int)h->cand2;
-      uint64_t* sk = reinterpret_cast<uint64_t*>(sh);
-      __shared__ unsigned long long s_pick;
-      for (int i = tid; i < m; i += kAdThreads) sk[i] = a.c2[i];
-      __syncthreads();
-      for (int i = tid; i < m; i += kAdThreads) {
-        const uint64_t ki = sk[i];
-        int gt = 0, eq = 0;
-        for (int j = 0; j < m; ++j) {
-          const uint64_t kj = sk[j];
-          gt += kj > ki ? 1 : 0;
-          eq += kj == ki ? 1 : 0;
-        }
-        if (gt <= rank && rank < gt + eq) s_pick = ki;  // equal keys write the same value
-      }
-      __syncthreads();
-      key = lo1 + (uint64_t)s_pick;  // the offsets carry the digit bits
+      // few keys in the digit: direct counting (the offsets carry the digit bits)
+      key = lo1 + select_by_count(a.c2, (int)h->cand2, rank, reinterpret_cast<uint64_t*>(sh));
     } else if (!past_hi) {
       const int64_t m = (int64_t)h->cand2;
       uint64_t low = 0, lmask = 0;

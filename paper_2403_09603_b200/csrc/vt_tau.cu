@@ -714,18 +714,15 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
                                                 const uint64_t* __restrict__ cw, uint64_t* __restrict__ ck,
                                                 int64_t cap, int64_t budget, uint64_t L_key, uint64_t hi_key, int s0,
                                                 AdaptHdr* h, uint32_t* __restrict__ hist,
-                                                uint64_t* __restrict__ fstatus, bool gather, int64_t blk,
+                                                uint64_t* __restrict__ fstatus, int64_t blk,
                                                 int64_t nblk) {
   __shared__ uint32_t sh[kAdBins];
   __shared__ unsigned long long s_above;
   const int64_t M = h->ccount;
   if (M > cap || M < budget + 1) {  // v <= L, or too many candidates: the exact path decides
     if (blk == 0 && threadIdx.x == 0) {
-      // unless at most budget keys exceed tau_lo at all (in-place calls count
-      // them): then v <= tau_lo and the bisection result is fixed
-      const bool low = !gather && M <= cap && (int64_t)h->above_lo <= budget;
-      h->fallback = low ? 0 : 1;
-      h->done = low ? 2 : 0;
+      h->fallback = 1;
+      h->done = 0;
     }
     return;
   }
@@ -744,17 +741,11 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
   for (int64_t i0 = blk * kAdThreads + threadIdx.x; i0 < M; i0 += kGU * stride) {
     uint64_t key[kGU];
     double xv[kGU];
-    if (gather) {
-      uint64_t w[kGU];
+    uint64_t w[kGU];
 #pragma unroll
-      for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
+    for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
 #pragma unroll
-      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(x + (w[u] >> 1)) : 0.0;
-    } else {  // in place: adapt_keys_kernel staged the candidates' x values in ck
-#pragma unroll
-      for (int u = 0; u < kGU; ++u)
-        xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)ck[i0 + u * stride]) : 0.0;
-    }
+    for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(x + (w[u] >> 1)) : 0.0;
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
       key[u] = dist_key(xv[u], g, err);
@@ -1064,9 +1055,9 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
 // (unordered, warp-aggregated); the rounding pass then runs at the selected
 // tau and writes the ordered log itself.
 __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __restrict__ x, int64_t n, Grid g,
-                                                                uint64_t L_key, uint64_t lo_key, int64_t thr_L,
-                                                                int64_t thr_lo, uint64_t* __restrict__ ck,
-                                                                int64_t cap, AdaptHdr* h, int32_t* errp) {
+                                                                uint64_t L_key, int64_t thr_L,
+                                                                uint64_t* __restrict__ ck, int64_t cap, AdaptHdr* h,
+                                                                int32_t* errp) {
   // keys are staged per CTA and appended with one global atomic per flush:
   // a global atomic per warp ballot serialises on the counter's L2 slice
   constexpr int kSteps = 4;                 // x 1024 elements per CTA iteration, loads issued up front
@@ -1108,7 +1099,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
     }
     constexpr int kE = kSteps * 4;
     {  // general b_r: the test on the 64-bit distance of round_dir (b_r = 32: adapt_keys32_kernel)
-      uint32_t cm = 0, ab = 0, slowm = 0;
+      uint32_t cm = 0, slowm = 0;
 #pragma unroll
       for (int e = 0; e < kE; ++e) {
         const uint64_t bits = (uint64_t)__double_as_longlong(xv[e >> 2].v[e & 3]);
@@ -1121,7 +1112,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
                                     : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
         const int64_t d = (int64_t)(up ? (g.one - low) : low);
         cm |= (d > thr_L ? 1u : 0u) << e;
-        ab |= (d > thr_lo ? 1u : 0u) << e;
         slowm |= (mag < kNormalMin ? 1u : 0u) << e;
       }
       if (slowm) {
@@ -1130,7 +1120,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
           if ((slowm >> e) & 1u) {
             const uint64_t key = dist_key(xv[e >> 2].v[e & 3], g, err);
             cm = (cm & ~(1u << e)) | ((key > L_key ? 1u : 0u) << e);
-            ab = (ab & ~(1u << e)) | ((key > lo_key ? 1u : 0u) << e);
           }
         }
       }
@@ -1139,7 +1128,6 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys_kernel(const double* __
 #pragma unroll
         for (int e = 0; e < kE; ++e) vm |= (base + (e >> 2) * 1024 + 4 * threadIdx.x + (e & 3) < n ? 1u : 0u) << e;
         cm &= vm;
-        ab &= vm;
       }
       // warp-aggregated append of the candidates' x values
       const uint32_t c = __popc(cm);
@@ -1681,8 +1669,7 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
       cw8(gL.thr, c8L, w8L);
       adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, c8L, w8L, ck, lay.cap, h, err);
     } else {
-      adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, lo_key, gL.thr, make_grid(b_r, lo).thr, ck,
-                                                  lay.cap, h, err);
+      adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, gL.thr, ck, lay.cap, h, err);
     }
     if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
   } else {
@@ -1803,7 +1790,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_batch_kernel(const __gr
   const AdSeg& sg = b.seg[j];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
   if (blockIdx.x == 0 && threadIdx.x == 0) b.fb->count = 0;  // the previous batch's fallback kernels are done
-  adapt_hist_body(sg.x, b.g0, p.cw, p.ck, p.cap, sg.budget, sg.L_key, b.hi_key, sg.s0, p.h, p.ahist, p.fst, true,
+  adapt_hist_body(sg.x, b.g0, p.cw, p.ck, p.cap, sg.budget, sg.L_key, b.hi_key, sg.s0, p.h, p.ahist, p.fst,
                   (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
 }
 

@@ -1350,7 +1350,8 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
       grid.sync();
     }
     const bool low = !gather && M <= a.cap && (int64_t)h->above_lo <= budget;
-    grid.sync();  // every CTA has read above_lo
+    grid.sync();  // every CTA has read above_lo (and the candidate count)
+    if (blk == 0 && tid == 0) h->ccount = 0;  // the next in-place key pass appends from 0
     if (low) {  // at most budget keys above tau_lo: v <= tau_lo fixes the bisection
       if (blk == 0 && tid == 0) {
         h->fallback = 0;
@@ -1401,6 +1402,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
     if (sh[i]) atomicAdd(&a.ahist[i], sh[i]);
   if (tid == 0 && above) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above), above);
   grid.sync();
+  if (blk == 0 && tid == 0) h->ccount = 0;  // read by every CTA at entry; the next in-place key pass appends from 0
   // 2. the digit (every CTA, same answer), then its keys
   const int64_t above_hi = (int64_t)h->above;
   const bool past_hi = above_hi > budget;  // v > tau_hi
@@ -1656,7 +1658,7 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   int rc = 0;
   if (aliased) {
     // 1'. the candidates' x values (unordered) from one read of x
-    if (cudaMemsetAsync(&h->ccount, 0, sizeof(int64_t), s) != cudaSuccess) return vt_check_launch("memset");
+    // h->ccount is 0 here: zero-filled workspace, reset by every tail
     const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
     if (fast) {
       // candidate <=> (low32 << 3) - c8 < w8 (thresholds in [2^27, 2^28] here)

@@ -1317,13 +1317,186 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
   return *s_acc;
 }
 
+// Phases of the tail for one tensor, run by its nblk CTAs (blk = this CTA's
+// index among them): the whole grid for a single call, the tensor's share of
+// the grid in a batch.  Grid-wide syncs separate the phases.
+struct TailSel {
+  int bin;
+  int64_t rank;
+  bool past_hi;  // more than budget keys above tau_hi: v > tau_hi
+};
+
+// 1. every candidate's key (gathered from x, or the x value the in-place key
+// pass staged) and the histogram of its top digit above L
+__device__ void tail_hist(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk, uint32_t* sh,
+                          unsigned long long* s_acc, uint32_t& err) {
+  const int tid = threadIdx.x;
+  const bool gather = a.sparse != nullptr;
+  for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
+  __syncthreads();
+  unsigned long long above = 0;
+  constexpr int kGU = 8;
+  const int64_t stride = nblk * kAdThreads;
+  for (int64_t i0 = blk * kAdThreads + tid; i0 < M; i0 += kGU * stride) {
+    double xv[kGU];
+    if (gather) {
+      uint64_t w[kGU];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? a.cw[i0 + u * stride] : 0ull;
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(a.x + (w[u] >> 1)) : 0.0;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kGU; ++u)
+        xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)a.ck[i0 + u * stride]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      if (i0 + u * stride >= M) break;
+      const uint64_t key = dist_key(xv[u], a.g0, err);
+      a.ck[i0 + u * stride] = key;
+      if (key > a.hi_key) ++above;
+      else if (key > a.L_key) atomicAdd(&sh[(uint32_t)((key - a.L_key - 1) >> a.s0)], 1u);
+    }
+  }
+  above = block_sum(above, s_acc);
+  for (int i = tid; i < kAdBins; i += kAdThreads)
+    if (sh[i]) atomicAdd(&a.ahist[i], sh[i]);
+  if (tid == 0 && above) atomicAdd(reinterpret_cast<unsigned long long*>(&a.h->above), above);
+}
+
+// 2. the digit of the (budget+1)-th largest key (every CTA of the tensor
+// computes the same one from the global histogram), then its keys compacted
+__device__ TailSel tail_digit(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk, uint32_t* sh) {
+  TailSel t{0, 0, false};
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t above_hi = (int64_t)a.h->above;
+  t.past_hi = above_hi > a.budget;
+  if (t.past_hi) return t;
+  int64_t above_bin;
+  stage_hist(a.ahist, sh, kAdBins);
+  select_digit(sh, kAdBins, a.budget - above_hi, t.bin, above_bin);
+  t.rank = a.budget - above_hi - above_bin;
+  const uint64_t digit = (uint64_t)t.bin, lo1 = a.L_key + 1;
+  const int64_t stride = nblk * kAdThreads;
+  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += stride) {  // warp-uniform bounds: a ballot follows
+    const int64_t i = i0 + tid;
+    const uint64_t key = i < M ? a.ck[i] : 0ull;
+    const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if (lane == leader)
+        pos = atomicAdd(reinterpret_cast<unsigned long long*>(&a.h->cand2), (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (in) a.c2[pos + __popc(m & lanemask_lt())] = key - lo1;
+    }
+  }
+  return t;
+}
+
+// 3. one CTA: exact selection among the digit's keys and the FP64 bisection;
+// the tensor's state is left clean for its next call
+__device__ void tail_exact(const TailArgs& a, const TailSel& t, uint32_t* sh) {
+  const int tid = threadIdx.x;
+  AdaptHdr* h = a.h;
+  const uint64_t lo1 = a.L_key + 1;
+  uint64_t key = 0x7ff0000000000000ull;
+  if (!t.past_hi && (int64_t)h->cand2 <= kSmallSel) {
+    // few keys in the digit: direct counting (the offsets carry the digit bits)
+    key = lo1 + select_by_count(a.c2, (int)h->cand2, t.rank, reinterpret_cast<uint64_t*>(sh));
+  } else if (!t.past_hi) {
+    const int64_t m = (int64_t)h->cand2;
+    int64_t rank = t.rank;
+    uint64_t low = 0, lmask = 0;
+    for (int top = a.s0; top > 0;) {
+      const int bits = top < kAdBits ? top : kAdBits;
+      top -= bits;
+      for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
+      __syncthreads();
+      for (int64_t i = tid; i < m; i += kAdThreads) {
+        const uint64_t o = a.c2[i];
+        if ((o & lmask) == low) atomicAdd(&sh[(uint32_t)(o >> top) & ((1u << bits) - 1u)], 1u);
+      }
+      __syncthreads();
+      int b2;
+      int64_t ab2;
+      select_digit(sh, 1 << bits, rank, b2, ab2);
+      low |= (uint64_t)b2 << top;
+      lmask |= ((1ull << bits) - 1ull) << top;
+      rank -= ab2;
+      __syncthreads();
+    }
+    key = lo1 + (((uint64_t)t.bin << a.s0) | low);
+  }
+  if (tid == 0) {
+    *a.key = key;
+    bisect_to(key, a.lower, a.upper, a.iters, a.dthr, a.tau_out);
+    h->above = 0;
+    h->cand2 = 0;
+    h->above_lo = 0;
+    h->fallback = 0;
+  }
+}
+
+// 4a. per-CTA count of the candidates with key > tau in its contiguous range
+__device__ void tail_filter_count(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk,
+                                  unsigned long long* s_acc) {
+  const uint64_t tau_key = (uint64_t)__double_as_longlong(a.dthr->tau);
+  const int64_t per = ((M + nblk - 1) / nblk + kAdThreads - 1) / kAdThreads * kAdThreads;
+  const int64_t r0 = blk * per, r1 = r0 + per < M ? r0 + per : M;
+  unsigned long long cnt = 0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kAdThreads) cnt += a.ck[i] > tau_key ? 1u : 0u;
+  cnt = block_sum(cnt, s_acc);
+  if (threadIdx.x == 0) a.c2[blk] = cnt;  // the digit keys are done with: per-CTA counts
+}
+
+// 4b. the log words of that range at the prefix of the earlier CTAs' counts
+__device__ void tail_filter_write(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk,
+                                  unsigned long long* s_acc, uint32_t* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t tau_key = (uint64_t)__double_as_longlong(a.dthr->tau);
+  const int64_t per = ((M + nblk - 1) / nblk + kAdThreads - 1) / kAdThreads * kAdThreads;
+  const int64_t r0 = blk * per, r1 = r0 + per < M ? r0 + per : M;
+  unsigned long long pre = 0;
+  for (int64_t b = tid; b < blk; b += kAdThreads) pre += a.c2[b];
+  pre = block_sum(pre, s_acc);
+  const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
+  int64_t pos = cur + (int64_t)pre;
+  for (int64_t c0 = r0; c0 < r1; c0 += kAdThreads) {
+    const int64_t i = c0 + tid;
+    const bool keep = i < r1 && a.ck[i] > tau_key;
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kAdThreads / 32; ++w) {
+      wpre += w < warp ? s_warp[w] : 0u;
+      tot += s_warp[w];
+    }
+    if (keep) {
+      const int64_t p = pos + wpre + __popc(m & lanemask_lt());
+      const uint64_t w = a.cw[i];
+      if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+    }
+    pos += tot;
+    __syncthreads();
+  }
+  if (blk == nblk - 1 && tid == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(pos - cur));
+    if (a.cursor_out) *a.cursor_out = pos;
+  }
+}
+
 __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a) {
   __shared__ __align__(16) uint32_t sh[kBudBins];
   __shared__ unsigned long long s_acc;
   __shared__ uint32_t s_warp[kAdThreads / 32];
   cg::grid_group grid = cg::this_grid();
   AdaptHdr* h = a.h;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int64_t blk = blockIdx.x, nblk = gridDim.x;
   const bool gather = a.sparse != nullptr;
   const int64_t M = h->ccount;
@@ -1366,154 +1539,21 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
                  a.key, a.dthr, a.tau_out, a.err, sh);
     return;
   }
-  // 1. keys and the top-digit histogram
-  for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
-  __syncthreads();
   uint32_t err = 0;
-  unsigned long long above = 0;
-  {
-    constexpr int kGU = 8;
-    const int64_t stride = nblk * kAdThreads;
-    for (int64_t i0 = blk * kAdThreads + tid; i0 < M; i0 += kGU * stride) {
-      double xv[kGU];
-      if (gather) {
-        uint64_t w[kGU];
-#pragma unroll
-        for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? a.cw[i0 + u * stride] : 0ull;
-#pragma unroll
-        for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(a.x + (w[u] >> 1)) : 0.0;
-      } else {
-#pragma unroll
-        for (int u = 0; u < kGU; ++u)
-          xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)a.ck[i0 + u * stride]) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kGU; ++u) {
-        if (i0 + u * stride >= M) break;
-        const uint64_t key = dist_key(xv[u], a.g0, err);
-        a.ck[i0 + u * stride] = key;
-        if (key > a.hi_key) ++above;
-        else if (key > a.L_key) atomicAdd(&sh[(uint32_t)((key - a.L_key - 1) >> a.s0)], 1u);
-      }
-    }
-  }
-  above = block_sum(above, &s_acc);
-  for (int i = tid; i < kAdBins; i += kAdThreads)
-    if (sh[i]) atomicAdd(&a.ahist[i], sh[i]);
-  if (tid == 0 && above) atomicAdd(reinterpret_cast<unsigned long long*>(&h->above), above);
+  tail_hist(a, M, blk, nblk, sh, &s_acc, err);
   grid.sync();
   if (blk == 0 && tid == 0) h->ccount = 0;  // read by every CTA at entry; the next in-place key pass appends from 0
-  // 2. the digit (every CTA, same answer), then its keys
-  const int64_t above_hi = (int64_t)h->above;
-  const bool past_hi = above_hi > budget;  // v > tau_hi
-  int bin = 0;
-  int64_t rank = 0;
-  const uint64_t lo1 = a.L_key + 1;
-  if (!past_hi) {
-    int64_t above_bin;
-    stage_hist(a.ahist, sh, kAdBins);
-    select_digit(sh, kAdBins, budget - above_hi, bin, above_bin);
-    rank = budget - above_hi - above_bin;
-    const uint64_t digit = (uint64_t)bin;
-    const int64_t stride = nblk * kAdThreads;
-    for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += stride) {  // warp-uniform bounds: a ballot follows
-      const int64_t i = i0 + tid;
-      const uint64_t key = i < M ? a.ck[i] : 0ull;
-      const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
-      const uint32_t m = __ballot_sync(0xffffffffu, in);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        unsigned long long pos = 0;
-        if (lane == leader)
-          pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (in) a.c2[pos + __popc(m & lanemask_lt())] = key - lo1;
-      }
-    }
-  }
+  const TailSel t = tail_digit(a, M, blk, nblk, sh);
   grid.sync();
-  // 3. CTA 0: exact selection + bisection; every CTA clears its share of the
-  // histogram (all CTAs read it before the sync above)
+  // every CTA clears its share of the histogram (all read it before the sync)
   for (int64_t i = blk * kAdThreads + tid; i < kAdBins; i += nblk * kAdThreads) a.ahist[i] = 0u;
-  if (blk == 0) {
-    uint64_t key = 0x7ff0000000000000ull;
-    if (!past_hi && (int64_t)h->cand2 <= kSmallSel) {
-      // few keys in the digit: direct counting (the offsets carry the digit bits)
-      key = lo1 + select_by_count(a.c2, (int)h->cand2, rank, reinterpret_cast<uint64_t*>(sh));
-    } else if (!past_hi) {
-      const int64_t m = (int64_t)h->cand2;
-      uint64_t low = 0, lmask = 0;
-      for (int top = a.s0; top > 0;) {
-        const int bits = top < kAdBits ? top : kAdBits;
-        top -= bits;
-        for (int i = tid; i < kAdBins; i += kAdThreads) sh[i] = 0;
-        __syncthreads();
-        for (int64_t i = tid; i < m; i += kAdThreads) {
-          const uint64_t o = a.c2[i];
-          if ((o & lmask) == low) atomicAdd(&sh[(uint32_t)(o >> top) & ((1u << bits) - 1u)], 1u);
-        }
-        __syncthreads();
-        int b2;
-        int64_t ab2;
-        select_digit(sh, 1 << bits, rank, b2, ab2);
-        low |= (uint64_t)b2 << top;
-        lmask |= ((1ull << bits) - 1ull) << top;
-        rank -= ab2;
-        __syncthreads();
-      }
-      key = lo1 + (((uint64_t)bin << a.s0) | low);
-    }
-    if (tid == 0) {
-      *a.key = key;
-      bisect_to(key, a.lower, a.upper, a.iters, a.dthr, a.tau_out);
-      h->above = 0;
-      h->cand2 = 0;
-      h->above_lo = 0;
-      h->fallback = 0;
-    }
-  }
+  if (blk == 0) tail_exact(a, t, sh);
   report_err(a.err, err);
   if (!gather) return;
   grid.sync();
-  // 4. the log: candidates with key > tau, in order
-  const uint64_t tau_key = (uint64_t)__double_as_longlong(a.dthr->tau);
-  const int64_t per = ((M + nblk - 1) / nblk + kAdThreads - 1) / kAdThreads * kAdThreads;
-  const int64_t r0 = blk * per, r1 = r0 + per < M ? r0 + per : M;
-  unsigned long long cnt = 0;
-  for (int64_t i = r0 + tid; i < r1; i += kAdThreads) cnt += a.ck[i] > tau_key ? 1u : 0u;
-  cnt = block_sum(cnt, &s_acc);
-  uint64_t* bcnt = a.c2;  // the digit keys are done with: per-CTA counts
-  if (tid == 0) bcnt[blk] = cnt;
+  tail_filter_count(a, M, blk, nblk, &s_acc);
   grid.sync();
-  unsigned long long pre = 0;
-  for (int64_t b = tid; b < blk; b += kAdThreads) pre += bcnt[b];
-  pre = block_sum(pre, &s_acc);
-  const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
-  int64_t pos = cur + (int64_t)pre;
-  for (int64_t c0 = r0; c0 < r1; c0 += kAdThreads) {
-    const int64_t i = c0 + tid;
-    const bool keep = i < r1 && a.ck[i] > tau_key;
-    const uint32_t m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_warp[warp] = __popc(m);
-    __syncthreads();
-    uint32_t wpre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kAdThreads / 32; ++w) {
-      wpre += w < warp ? s_warp[w] : 0u;
-      tot += s_warp[w];
-    }
-    if (keep) {
-      const int64_t p = pos + wpre + __popc(m & lanemask_lt());
-      const uint64_t w = a.cw[i];
-      if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
-    }
-    pos += tot;
-    __syncthreads();
-  }
-  if (blk == nblk - 1 && tid == 0) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(pos - cur));
-    if (a.cursor_out) *a.cursor_out = pos;
-  }
+  tail_filter_write(a, M, blk, nblk, &s_acc, s_warp);
 }
 
 // Cooperative grid for the fallback kernels: every CTA co-resident.

@@ -35,3 +35,61 @@ def test_hooks_tiny_gpt2(oracle):
     for p in model.parameters():
         assert p.grad is not None and torch.isfinite(p.grad).all()
     hk.remove()
+
+
+def test_hooks_arena_growth_and_reuse(oracle):
+    """More hooked tensors than the first result arena (64 slots): the slots
+    grow during the first step while earlier calls are still pending, and a
+    second step reuses them; per-tensor taus equal the oracle's search and
+    every rounded output is on the grid."""
+    import torch
+    from paper_2403_09603_b200 import hooks, ops
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(*[torch.nn.Linear(48, 48, dtype=torch.float64) for _ in range(45)]).cuda()
+    x = torch.randn(64, 48, dtype=torch.float64, device="cuda")
+    seen = []
+    orig = ops.round_and_log_adaptive
+
+    def spy(t, b_r, budget, **kw):
+        seen.append((t.detach().clone().cpu().numpy(), b_r, budget))
+        return orig(t, b_r, budget, **kw)
+
+    ops.round_and_log_adaptive = spy
+    try:
+        hk = hooks.RoundAndLogHooks(model)
+        infos = []
+        for step in range(2):
+            seen.clear()
+            model(x).sum().backward()
+            taus = hk._taus[:len(hk.records)].cpu().tolist()
+            counts = [int(c) for c in hk._flags[:len(hk.records), 2].cpu().tolist()]
+            infos.append(hk.collect())
+            assert infos[-1]["tensors"] == len(seen) > 64
+            for (a, b_r, budget), tau, cnt in zip(seen, taus, counts):
+                t_or = oracle.search_tau_budget(a.reshape(-1), b_r, budget)
+                assert tau == t_or
+                assert cnt == int(np.count_nonzero(oracle.direction_array(a.reshape(-1), b_r, t_or) != 1))
+        assert infos[0]["tensors"] == infos[1]["tensors"]
+        hk.remove()
+    finally:
+        ops.round_and_log_adaptive = orig
+
+
+def test_hooks_error_then_clean_step():
+    """A non-finite activation raises the reference's error at collect();
+    the next step starts from cleared slots."""
+    import torch
+    from paper_2403_09603_b200 import hooks
+    model = torch.nn.Sequential(torch.nn.Linear(16, 16, dtype=torch.float64),
+                                torch.nn.Linear(16, 16, dtype=torch.float64)).cuda()
+    hk = hooks.RoundAndLogHooks(model)
+    x = torch.randn(8, 16, dtype=torch.float64, device="cuda")
+    bad = x.clone()
+    bad[0, 0] = float("inf")
+    model(bad)
+    with pytest.raises(ValueError, match="non-finite value"):
+        hk.collect()
+    model(x).sum().backward()
+    info = hk.collect()
+    assert info["tensors"] > 0
+    hk.remove()

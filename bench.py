@@ -284,6 +284,7 @@ def run_ours(args) -> None:
         line["sweep"] = sweep(args.sweep)
     if args.extras and world == 1:
         line["extras"] = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
+                          "vtrl_codec_2^26": vtrl_codec(26),
                           "configs[2]_resnet50_budget": config2(),
                           "configs[3]_gpt2_fp64_step": config3_gpt2(),
                           "configs[4]_merkle_1.5B": config4_merkle()}
@@ -422,6 +423,65 @@ def sweep(log2s) -> dict:
         del x, y, words, ya, lw, log, graphs
         torch.cuda.empty_cache()
     return out
+
+
+def vtrl_codec(lg: int = 26) -> dict:
+    """the reference's own log format end to end on the device --
+    the fused round-and-log writing the packed `.vtrl` payload (5 base-3 codes
+    per byte, roundlog.py:43-53) instead of sparse words, and the replay
+    decoding it (roundlog.py:73-82 + fpround.rev_array).  Algorithmic bytes per
+    element: 8 (x) + 4 (FP32 y) + 0.2 (payload).  Graph-timed."""
+    import torch
+
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, workloads
+    peak, _ = peaks()
+    n = 1 << lg
+    x, xa = workloads.config1_pair_torch(n, seed=1)
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    ya = torch.empty_like(y)
+    packed = torch.empty(n // 5 + 1, dtype=torch.uint8, device="cuda")
+    edge = torch.empty(16, dtype=torch.uint8, device="cuda")
+    f, fa = D.Flags(), D.Flags()
+    ws = D.workspace(int(_lib.lib().vt_round_log_workspace(n)), "vtrl_bench")
+
+    def rl():
+        _lib.call("vt_round_log", D.ptr(x), n, 32, workloads.TAU_CONFIG0, _lib.OUT_F32, D.ptr(y), None, 0, 0,
+                  None, None, None, D.ptr(packed), 0, D.ptr(edge), f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(),
+                  D.stream_ptr())
+
+    rl()
+    torch.cuda.synchronize()
+    nfull, rem = divmod(n, 5)
+    if rem:  # the writer's pending codes (LogWriter.close pads with 1s)
+        tail = edge[:rem].tolist() + [1] * (5 - rem)
+        packed[nfull] = sum(c * 3 ** k for k, c in enumerate(tail))
+    nbytes = nfull + (1 if rem else 0)
+
+    def rp():
+        _lib.call("vt_replay", D.ptr(xa), n, 32, _lib.LOG_PACKED, D.ptr(packed), nbytes, 0, _lib.OUT_F32,
+                  D.ptr(ya), fa.cnt_ptr, fa.err_ptr, None, 0, D.stream_ptr())
+
+    rp()
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(y.view(torch.int32), ya.view(torch.int32))) and f.read()[0] == 0 and fa.read()[0] == 0
+    graphs = []
+    for fn in (rl, rp):
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_):
+            fn()
+        torch.cuda.current_stream().wait_stream(s_)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        graphs.append(g)
+    ms, ms2 = _time(graphs[0].replay, 10), _time(graphs[1].replay, 10)
+    b = n * (8 + 4 + 0.2)
+    return {"n": n, "round_log_packed_gbs": round(b / ms / 1e6, 1), "round_log_packed_frac": round(b / ms / 1e6 / peak, 4),
+            "replay_packed_gbs": round(b / ms2 / 1e6, 1), "replay_packed_frac": round(b / ms2 / 1e6 / peak, 4),
+            "auditor_equals_trainer_bitwise": ok,
+            "kernels": "round_log_kernel<PACKED> (codes packed 5 per byte in the same pass), replay_kernel<PACKED>"}
 
 
 def config2() -> dict:

@@ -357,14 +357,20 @@ __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a)
     const int r0 = (int)(pos0 - 5 * b0);
     const int lim = (int)std::min<int64_t>(kTile, a.n - tile_base);
     for (int e = lim + threadIdx.x; e < kTile; e += kThreads) cs[e] = 1;  // past the end
-    for (int e = threadIdx.x; e < lim; e += kThreads) {
-      const int q = (r0 + e) / 5;
-      const int dpos = r0 + e - 5 * q;
+    // one thread per payload byte: its five base-3 digits by constant
+    // divisions (roundlog.py:73-82), stored at the elements they code
+    const int nb = (r0 + lim + 4) / 5;  // bytes covering elements [0, lim)
+    for (int q = threadIdx.x; q < nb; q += kThreads) {
       const int64_t bi = b0 + q;
       const uint32_t b = (bi < a.log_len) ? (uint32_t)__ldg(p + bi) : 255u;
       if (b > 242u) err |= VT_ERR_BAD_LOG_BYTE;
-      const uint32_t p3 = dpos == 0 ? 1u : dpos == 1 ? 3u : dpos == 2 ? 9u : dpos == 3 ? 27u : 81u;
-      cs[e] = (uint8_t)((b / p3) % 3u);
+      uint32_t t = b;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int e = 5 * q + k - r0;
+        if (e >= 0 && e < lim) cs[e] = (uint8_t)(t % 3u);
+        t /= 3u;
+      }
     }
     __syncthreads();
   }

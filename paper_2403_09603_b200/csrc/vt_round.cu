@@ -338,7 +338,6 @@ struct ReplayArgs {
 // goes through the persistent rp_fused_kernel (vt_stream.cu).
 template <int OUT, int LOGK, bool FAST>
 __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a) {
-  __shared__ __align__(16) uint8_t cs[kTile];
   __shared__ uint32_t s_warp[kWarps];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -350,31 +349,25 @@ __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a)
   load_slots(a.x, a.n, wbase, lane, xv);
   uint32_t err = 0;
 
+  // packed: a 256-entry table of each payload byte's five base-3 digits (3
+  // bits each, roundlog.py:73-82); every thread then reads the one or two
+  // payload bytes its 4 consecutive elements fall in -- no staging pass
+  __shared__ uint16_t lut[256];
+  int64_t qt = 0;
+  int rt = 0;
   if (LOGK == VT_LOG_PACKED) {
-    const uint8_t* p = static_cast<const uint8_t*>(a.log);
-    const int64_t pos0 = a.log_base + tile_base;
-    const int64_t b0 = pos0 / 5;
-    const int r0 = (int)(pos0 - 5 * b0);
-    const int lim = (int)std::min<int64_t>(kTile, a.n - tile_base);
-    for (int e = lim + threadIdx.x; e < kTile; e += kThreads) cs[e] = 1;  // past the end
-    // one thread per payload byte: its five base-3 digits by constant
-    // divisions (roundlog.py:73-82), stored at the elements they code
-    const int nb = (r0 + lim + 4) / 5;  // bytes covering elements [0, lim)
-    for (int q = threadIdx.x; q < nb; q += kThreads) {
-      const int64_t bi = b0 + q;
-      const uint32_t b = (bi < a.log_len) ? (uint32_t)__ldg(p + bi) : 255u;
-      if (b > 242u) err |= VT_ERR_BAD_LOG_BYTE;
-      uint32_t t = b;
+    uint32_t t = threadIdx.x, v = 0;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const int e = 5 * q + k - r0;
-        if (e >= 0 && e < lim) cs[e] = (uint8_t)(t % 3u);
-        t /= 3u;
-      }
+    for (int k = 0; k < 5; ++k) {
+      v |= (t % 3u) << (3 * k);
+      t /= 3u;
     }
+    lut[threadIdx.x] = (uint16_t)v;
+    const int64_t pos_tile = a.log_base + tile_base;  // stream position of the tile's first element
+    qt = pos_tile / 5;
+    rt = (int)(pos_tile - 5 * qt);
     __syncthreads();
   }
-
   uint32_t flips = 0;
 #pragma unroll
   for (int j = 0; j < kSlots; ++j) {
@@ -391,10 +384,26 @@ __global__ void __launch_bounds__(kThreads, 4) replay_kernel(const ReplayArgs a)
         for (int v = 0; v < 4; ++v) code[v] = (i0 + v < a.n) ? cg[i0 + v] : 1u;
       }
     } else {
-      const int e0 = warp * kWarpElems + j * 128 + lane * 4;
-      const uint32_t c4 = *reinterpret_cast<const uint32_t*>(cs + e0);
+      const uint8_t* p = static_cast<const uint8_t*>(a.log);
+      const int rel = rt + warp * kWarpElems + j * 128 + lane * 4;  // < 2^16: 32-bit divisions by 5
+      const int q0 = rel / 5, d0 = rel - 5 * q0;
+      const int64_t bi0 = qt + q0;
+      const int nv = (int)std::min<int64_t>(4, a.n - i0);  // valid elements of the four
+      uint32_t b0 = 1u, b1 = 1u;  // bytes of the valid elements (past the end: unused)
+      if (nv > 0) {
+        b0 = (bi0 < a.log_len) ? (uint32_t)__ldg(p + bi0) : 255u;
+        if (b0 > 242u) err |= VT_ERR_BAD_LOG_BYTE;
+        if (d0 + nv > 5) {
+          b1 = (bi0 + 1 < a.log_len) ? (uint32_t)__ldg(p + bi0 + 1) : 255u;
+          if (b1 > 242u) err |= VT_ERR_BAD_LOG_BYTE;
+        }
+      }
+      const uint32_t l0 = lut[b0 & 0xffu], l1 = lut[b1 & 0xffu];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) code[v] = (c4 >> (8 * v)) & 0xffu;
+      for (int v = 0; v < 4; ++v) {
+        const int d = d0 + v;
+        code[v] = v < nv ? (((d < 5 ? l0 : l1) >> (3 * (d < 5 ? d : d - 5))) & 7u) : 1u;
+      }
     }
     if (FAST) {
       float y[4];

@@ -691,22 +691,33 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
           atomicMax(&hdr->ticket, (uint32_t)next);
         }
       };
-      int64_t s = draw();
+      // a ticket's tensor and tiles, looked up once it is drawn (off the path
+      // from a free ring slot to the next copy)
+      struct TicketInfo {
+        int64_t s, t0, full_tiles;
+        const double* x;
+        int nt, j;
+      };
+      auto lookup = [&](int64_t s) {
+        TicketInfo ti{s, 0, 0, nullptr, 1, jc};  // draw() left jc at the tensor of s
+        if (s >= 0) {
+          const RLFArgs v = seg_view(b, jc);
+          const int64_t ls = s - b.seg[jc].tick0;
+          ti.nt = st_ntiles(v, ls);
+          ti.t0 = st_first(v, ls);
+          ti.full_tiles = v.n / kSTile;
+          ti.x = v.x;
+        }
+        return ti;
+      };
+      TicketInfo cur = lookup(draw());
       int64_t q = 0;  // ring sequence number
       for (int64_t k = 0;; ++k) {
-        int64_t nxt = -1;
-        int nt = 1;
-        int64_t t0 = 0, full_tiles = 0;
-        const double* x = nullptr;
-        const int j = jc;  // the tensor of s (draw() left jc there)
-        if (s >= 0) {
-          const RLFArgs v = seg_view(b, j);
-          const int64_t ls = s - b.seg[j].tick0;
-          nt = st_ntiles(v, ls);
-          t0 = st_first(v, ls);
-          full_tiles = v.n / kSTile;
-          x = v.x;
-        }
+        const int64_t s = cur.s;
+        const int nt = cur.nt, j = cur.j;
+        const int64_t t0 = cur.t0, full_tiles = cur.full_tiles;
+        const double* x = cur.x;
+        TicketInfo nxt{-1, 0, 0, nullptr, 1, 0};
 #pragma unroll 1
         for (int i = 0; i < nt; ++i, ++q) {
           const int st = (int)(q % kFStages);
@@ -715,7 +726,6 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
             S.ids[k & 3] = s;
             S.sids[k & 3] = j;
           }
-          if (i == nt - 1 && s >= 0) nxt = draw();
           const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
             fence_proxy_async();
@@ -723,9 +733,12 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
           } else {
             mbar_arrive(S.full + st);
           }
+          // the next ticket after this tile's copy is in flight: draw() waits
+          // on its atomic and the tensor lookup, the TMA must not
+          if (i == nt - 1 && s >= 0) nxt = lookup(draw());
         }
         if (s < 0) break;
-        s = nxt;
+        cur = nxt;
       }
     }
     __syncwarp();

@@ -7,6 +7,12 @@ sparse log), and the rounded FP64 grid values replace the originals, so
 training proceeds on the b_r grid exactly as the reference trainer does
 (protocol.py:259-285: forward stages, loss gradient, backward stages).
 
+``ReplayHooks`` is the auditor side (protocol._AuditorChannel.process,
+protocol.py:212-216, on a torch model): the same hook points replay the
+trainer's per-tensor logs in place (``ops.replay``), so an auditor whose
+hardware computes slightly different FP64 values lands on the trainer's grid
+values bit for bit.
+
 Nothing here synchronises with the host during the step: taus, counts and
 logs stay on the device until ``collect()``, which reads the whole step's
 taus and counts in one copy.  Result slots (tau, error/count words) and log
@@ -21,6 +27,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _device as D
+from . import _lib
 from . import ops
 
 
@@ -99,10 +106,13 @@ class RoundAndLogHooks:
             return tuple(self._round(g, name, "bwd") if isinstance(g, torch.Tensor) else g for g in grad_input)
         return hook
 
-    def collect(self) -> dict:
+    def collect(self, keep_logs: bool = False) -> dict:
         """Synchronise once: per-tensor taus and log sizes of the step (one
         copy of the step's result slots), then clear the slots for the next
-        step.  Raises the reference's errors like PendingAdaptive.finish."""
+        step.  Raises the reference's errors like PendingAdaptive.finish.
+        keep_logs: also return the step's logs (``"logs"``: one (name, kind,
+        int64 words) per hooked tensor, in call order, copied out of the
+        reused buffers) -- what the trainer ships to an auditor."""
         m = len(self.records)
         fl = self._flags[:m].cpu().tolist()
         taus = self._taus[:m].cpu().tolist()
@@ -116,12 +126,104 @@ class RoundAndLogHooks:
                 raise ops.LogOverflow(f"sparse log needs {f[2]} words, capacity {r.budget + 1}")
             counts.append(int(f[2]))
             assert f[2] <= r.budget
-        return {"tensors": m, "elements": sum(r.numel for r in records),
-                "logged": sum(counts), "fwd": sum(1 for r in records if r.kind == "fwd"),
-                "bwd": sum(1 for r in records if r.kind == "bwd"),
-                "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None}
+        out = {"tensors": m, "elements": sum(r.numel for r in records),
+               "logged": sum(counts), "fwd": sum(1 for r in records if r.kind == "fwd"),
+               "bwd": sum(1 for r in records if r.kind == "bwd"),
+               "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None}
+        if keep_logs:
+            out["logs"] = [(r.name, r.kind, self._logs[r.slot][:c].clone()) for r, c in zip(records, counts)]
+        return out
 
     def remove(self):
         for h in self._handles:
             h.remove()
         self._handles.clear()
+
+
+@dataclass
+class ReplayHooks:
+    """Auditor side: at the trainer's hook points, in the trainer's call
+    order, round each tensor in place with the trainer's log forcing the
+    logged directions (``ops.replay``: rev_array, fpround.py:227-247).
+    ``logs`` is ``RoundAndLogHooks.collect(keep_logs=True)["logs"]`` of the
+    step being audited.  ``perturb`` (optional, tensor -> None, in place)
+    runs before each replay: a stand-in for the auditor's hardware computing
+    slightly different values."""
+
+    model: torch.nn.Module
+    logs: list
+    b_r: int = 32
+    perturb: object = None
+    enabled: bool = True
+
+    def __post_init__(self):
+        self._handles = []
+        self._k = 0
+        self._flags = torch.zeros((max(len(self.logs), 1), 6), dtype=torch.int64, device="cuda")
+        for name, mod in self.model.named_modules():
+            if any(True for _ in mod.children()):
+                continue
+            self._handles.append(mod.register_forward_hook(self._fwd_hook(name)))
+            self._handles.append(mod.register_full_backward_hook(self._bwd_hook(name)))
+
+    def _replay(self, t: torch.Tensor, name: str, kind: str) -> torch.Tensor:
+        if not (self.enabled and isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
+                and t.numel() > 0):
+            return t
+        k = self._k
+        if k >= len(self.logs) or self.logs[k][0] != name or self.logs[k][1] != kind:
+            want = self.logs[k][:2] if k < len(self.logs) else None
+            raise RuntimeError(f"audit out of step at hooked tensor {k}: trainer {want}, auditor {(name, kind)}")
+        self._k += 1
+        d = t.detach()
+        inplace = d.is_contiguous() and d.data_ptr() % 32 == 0
+        flat = d.view(-1) if inplace else d.reshape(-1).clone()
+        if self.perturb is not None:
+            self.perturb(flat)
+        f = D.Flags(buf=self._flags[k])
+        _lib_call_replay(flat, self.b_r, self.logs[k][2], f)
+        return t if inplace else flat.view(t.shape)
+
+    def _fwd_hook(self, name):
+        def hook(mod, inp, out):
+            if isinstance(out, torch.Tensor):
+                y = self._replay(out, name, "fwd")
+                return None if y is out else out + (y - out).detach()
+            return None
+        return hook
+
+    def _bwd_hook(self, name):
+        def hook(mod, grad_input, grad_output):
+            if not any(isinstance(g, torch.Tensor) for g in grad_input):
+                return None
+            return tuple(self._replay(g, name, "bwd") if isinstance(g, torch.Tensor) else g for g in grad_input)
+        return hook
+
+    def collect(self) -> dict:
+        """Synchronise once: per-tensor corrections (elements where the log
+        overrode plain rounding), errors raised as the reference does."""
+        m = self._k
+        fl = self._flags[:m].cpu().tolist()
+        self._flags[:m].zero_()
+        self._k = 0
+        for f in fl:
+            if int(f[0]) & _lib.ERR_BAD_SPARSE:
+                raise ops.SparseLogError("sparse log is not strictly ascending")
+            D.raise_fpround(int(f[0]) & 0xFFFFFFFF)
+        if m != len(self.logs):
+            raise RuntimeError(f"audit out of step: {m} hooked tensors, the trainer logged {len(self.logs)}")
+        return {"tensors": m, "corrections": [int(f[2]) for f in fl]}
+
+    def remove(self):
+        for h in self._handles:
+            h.remove()
+        self._handles.clear()
+
+
+def _lib_call_replay(flat: torch.Tensor, b_r: int, words: torch.Tensor, f) -> None:
+    """In-place FP64 replay of one tensor against its sparse log (the fused
+    replay stages each tile before writing it back)."""
+    ws = D.workspace(int(_lib.lib().vt_replay_workspace(flat.numel())), "replay_hooks")
+    w = words.contiguous()
+    _lib.call("vt_replay", D.ptr(flat), flat.numel(), b_r, _lib.LOG_SPARSE, D.ptr(w), w.numel(), 0,
+              _lib.OUT_F64, D.ptr(flat), f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())

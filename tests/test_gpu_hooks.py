@@ -93,3 +93,60 @@ def test_hooks_error_then_clean_step():
     info = hk.collect()
     assert info["tensors"] > 0
     hk.remove()
+
+
+def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
+    """Trainer: RoundAndLogHooks on a small FP64 GPT-2 step, logs kept.
+    Auditor: the same step on a copy of the model whose every hooked tensor
+    is perturbed (a stand-in for other hardware: 5% of the elements moved by
+    up to 2^-34 relative, inside the logged band) and then replayed with the
+    trainer's logs -- every hooked tensor, the loss and every gradient equal
+    the trainer's bit for bit, with corrections where plain rounding of the
+    perturbed values would have diverged (protocol._AuditorChannel on a
+    torch model)."""
+    import copy
+    import torch
+    from paper_2403_09603_b200 import hooks, workloads
+    torch.manual_seed(4)
+    model = workloads.gpt2_small_fp64(vocab=97, d=64, layers=2, heads=4, ctx=32)
+    model_a = copy.deepcopy(model)
+    idx = torch.randint(0, 97, (4, 32), device="cuda")
+
+    def run(m, hk_factory):
+        seen = []
+        hk = hk_factory(m)
+        hs = [mod.register_forward_hook(lambda mod, i, o: seen.append(o.detach().clone()))
+              for mod in m.modules() if not any(True for _ in mod.children())]
+        logits = m(idx)
+        loss = torch.nn.functional.cross_entropy(logits.view(-1, 97), idx.view(-1))
+        loss.backward()
+        for h in hs:
+            h.remove()
+        return hk, seen, loss.detach().clone(), [p.grad.clone() for p in m.parameters()]
+
+    hk_t, seen_t, loss_t, grads_t = run(model, lambda m: hooks.RoundAndLogHooks(m))
+    info = hk_t.collect(keep_logs=True)
+    hk_t.remove()
+    assert len(info["logs"]) == info["tensors"] and info["logged"] > 0
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+
+    def perturb(flat):
+        sel = torch.rand(flat.numel(), device="cuda", generator=g) < 0.05
+        # below the budget tau's margin to the midpoint ((1 - tau / 2^-24) ~ 0.005 of the half-ulp):
+        # an auditor deviation the trainer's log covers
+        rel = (torch.rand(flat.numel(), device="cuda", dtype=torch.float64, generator=g) * 2 - 1) * 2.0 ** -34
+        flat.add_(torch.where(sel, flat * rel, torch.zeros_like(flat)))
+
+    hk_a, seen_a, loss_a, grads_a = run(model_a, lambda m: hooks.ReplayHooks(m, info["logs"], perturb=perturb))
+    res = hk_a.collect()
+    hk_a.remove()
+    assert res["tensors"] == info["tensors"]
+    assert sum(res["corrections"]) > 0
+    assert len(seen_a) == len(seen_t)
+    for a, t in zip(seen_a, seen_t):
+        assert torch.equal(a.view(torch.int64), t.view(torch.int64))
+    assert torch.equal(loss_a.view(torch.int64), loss_t.view(torch.int64))
+    for a, t in zip(grads_a, grads_t):
+        assert torch.equal(a.view(torch.int64), t.view(torch.int64))

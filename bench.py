@@ -609,10 +609,22 @@ def config3_gpt2(steps: int = 3) -> dict:
         hk.collect()
 
     ms_hooked = _time(step_hooked, reps=steps, warm=1)
+    step()
+    logs = hk.collect(keep_logs=True)["logs"]
     hk.remove()
+    # the auditor's step: the same hook points replay a trainer step's logs in place
+    ha = hooks.ReplayHooks(model, logs)
+
+    def step_audited():
+        step()
+        ha.collect()
+
+    ms_audited = _time(step_audited, reps=steps, warm=1)
+    ha.remove()
     return {"model": "GPT-2 small FP64 (12x768, 12 heads, vocab 50257), random init", "batch": [8, 1024],
             "step_ms_plain": round(ms_plain, 2), "step_ms_round_and_log": round(ms_hooked, 2),
-            "trainer_overhead": round(ms_hooked / ms_plain, 4), "hooked_tensors": info["tensors"],
+            "trainer_overhead": round(ms_hooked / ms_plain, 4), "step_ms_replay": round(ms_audited, 2),
+            "auditor_overhead": round(ms_audited / ms_plain, 4), "hooked_tensors": info["tensors"],
             "hooked_fwd": info["fwd"], "hooked_bwd": info["bwd"], "hooked_elements": info["elements"],
             "logged_entries": info["logged"], "budget": "0.5% per tensor",
             "paper_trainer_overhead": "1.2-1.4x (PAPER.md:402, A40 / Titan XP / 2080 Ti)"}

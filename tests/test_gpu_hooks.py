@@ -150,3 +150,26 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
     assert torch.equal(loss_a.view(torch.int64), loss_t.view(torch.int64))
     for a, t in zip(grads_a, grads_t):
         assert torch.equal(a.view(torch.int64), t.view(torch.int64))
+
+
+def test_replay_hooks_out_of_step():
+    """An auditor whose hooked tensors do not follow the trainer's order (or
+    count) is refused, as protocol._run refuses an operation-count mismatch."""
+    import torch
+    from paper_2403_09603_b200 import hooks
+    model = torch.nn.Sequential(torch.nn.Linear(16, 16, dtype=torch.float64),
+                                torch.nn.Linear(16, 16, dtype=torch.float64)).cuda()
+    x = torch.randn(8, 16, dtype=torch.float64, device="cuda")
+    hk = hooks.RoundAndLogHooks(model)
+    model(x)  # forward only: two hooked outputs
+    logs = hk.collect(keep_logs=True)["logs"]
+    hk.remove()
+    ha = hooks.ReplayHooks(model, logs[::-1])  # wrong order
+    with pytest.raises(RuntimeError, match="out of step"):
+        model(x)
+    ha.remove()
+    ha = hooks.ReplayHooks(model, logs + logs)  # the trainer logged more
+    model(x)
+    with pytest.raises(RuntimeError, match="out of step"):
+        ha.collect()
+    ha.remove()

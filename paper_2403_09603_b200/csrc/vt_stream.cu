@@ -185,6 +185,7 @@ constexpr int kMaskSlots = 3;                    // super-tiles of masks in flig
 constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
 constexpr int kRow = 64;                         // staged entries per warp-tile (else from masks)
 constexpr int kRows = kSuper * kWarps;           // warp-tiles per super-tile
+static_assert(kRows == 32, "the log warp scans a super-tile's rows one per lane");
 constexpr int kFCompute = kSThreads;             // 8 compute warps
 constexpr int kFThreads = kFCompute + 64;        // + log warp + producer warp
 constexpr int kLogWarp = kWarps;                 // warp 8

@@ -212,6 +212,9 @@ def round_and_log_adaptive_batch(xs, b_r: int, budgets, *, iters: int = 30, out_
     budgets = [int(b) for b in budgets]
     if len(budgets) != m:
         raise ValueError("one budget per tensor")
+    for name, seq in (("global_bases", global_bases), ("outs", outs), ("log_outs", log_outs)):
+        if seq is not None and len(seq) != m:
+            raise ValueError(f"{name}: one entry per tensor")
     kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
     flat = [D.aligned_f64(x.reshape(-1)) for x in xs]
     ys = list(outs) if outs is not None else [torch.empty(t.numel(), dtype=out_dtype, device=dev) for t in flat]

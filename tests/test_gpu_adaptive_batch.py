@@ -143,3 +143,9 @@ def test_batch_errors():
         ops.round_and_log_adaptive_batch([a], 32, [50], out_dtype=torch.float64, outs=[a])
     with pytest.raises(ValueError, match="one budget per tensor"):
         ops.round_and_log_adaptive_batch([a, b], 32, [50])
+    with pytest.raises(ValueError, match="global_bases: one entry per tensor"):
+        ops.round_and_log_adaptive_batch([a, c], 32, [50, 100], global_bases=[0])
+    small = torch.empty(3, dtype=torch.int64, device="cuda")
+    with pytest.raises(ops.LogOverflow):
+        ops.round_and_log_adaptive_batch([torch.randn(100_000, dtype=torch.float64, device="cuda")], 32, [500],
+                                         log_outs=[small])

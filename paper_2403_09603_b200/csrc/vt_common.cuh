@@ -345,6 +345,28 @@ int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind
 // and the look-back words at the same offsets; its log is its own.
 constexpr int kMaxBatch = 224;
 
+// FP64 bit pattern of p for one element; err gets rnd's error bits.
+__device__ __forceinline__ uint64_t dist_key(double x, const Grid& g, uint32_t& err) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const uint64_t mag = bits & kMag;
+  if (mag >= kNormalMin) {
+    const uint64_t low = mag & g.low_mask;
+    const uint64_t base = mag >> g.drop;
+    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
+    const uint64_t rmag = (base + (up ? 1ull : 0ull)) << g.drop;
+    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
+                                : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
+    const uint64_t d = up ? (g.one - low) : low;  // |x - r| = d * 2^(E-52), scale = 2^E
+    return (uint64_t)__double_as_longlong(__dmul_rn(__ull2double_rn(d), 0x1p-52));
+  }
+  const double r = __dmul_rn(rint(__dmul_rn(x, g.sub_up)), g.sub_dn);
+  return (uint64_t)__double_as_longlong(__dmul_rn(fabs(__dsub_rn(x, r)), 0x1p126));
+}
+
+// rl_batch_kernel<..., KEYS>: a candidate whose x was not staged (its row
+// overflowed the staging slots); the adaptive histogram gathers it
+constexpr uint64_t kKeyMissing = ~0ull;
+
 struct RLSeg {
   const double* x;
   void* out;
@@ -354,6 +376,7 @@ struct RLSeg {
   int32_t* err;
   const DevThr* dthr;   // nullable: thresholds from the device instead of thr / thr_sub / thr32
   const int32_t* gate;  // nullable: the tensor is skipped while *gate == 0
+  uint64_t* keys;       // KEYS launches: x bits of each logged element (or kKeyMissing), at its log position
   int64_t n, cap, global_base, tick0;
   int64_t thr;
   double thr_sub;
@@ -375,7 +398,7 @@ __host__ __device__ inline int64_t rl_batch_tickets(int64_t n) {
 }
 // the batch's look-back words come after a 64-byte header
 inline size_t rl_batch_workspace(int64_t total_tickets) { return (size_t)(64 + total_tickets * 8 + 256); }
-int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st);
+int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st, bool keys = false);
 
 }  // namespace vt
 

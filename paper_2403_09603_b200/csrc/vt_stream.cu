@@ -184,6 +184,10 @@ constexpr int kSuper = 4;                        // tiles per super-tile / statu
 constexpr int kMaskSlots = 3;                    // super-tiles of masks in flight
 constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
 constexpr int kRow = 64;                         // staged entries per warp-tile (else from masks)
+// KEYS launches reuse a row's 128 bytes as kRowK {key, entry} pairs: 8-byte
+// keys first, then the 16-bit entries
+constexpr int kRowK = 12;
+static_assert(kRowK * 10 <= kRow * 2, "keyed staging must fit a row");
 constexpr int kRows = kSuper * kWarps;           // warp-tiles per super-tile
 static_assert(kRows == 32, "the log warp scans a super-tile's rows one per lane");
 constexpr int kFCompute = kSThreads;             // 8 compute warps
@@ -236,6 +240,7 @@ struct RLFArgs {
   int32_t* err;
   const DevThr* dthr;
   const int32_t* gate;  // nullable: the kernel returns at once when *gate == 0
+  uint64_t* keys;       // KEYS launches only
 };
 
 // Ticket s -> its first tile and tile count: n4 super-tiles of kSuper tiles,
@@ -261,7 +266,7 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
 // One tile, compute warp: round, store, ballot.  `gx` non-null = partial
 // tile read straight from global memory (elements >= lim are zero, which is
 // on the grid and never logged).
-template <int OUT, bool FAST, bool FULL>
+template <int OUT, bool FAST, bool FULL, bool KEYS = false>
 __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_t w8, int thr32, const double* src,
                                          void* o, int lim, uint4* mslot, uint16_t* row, uint32_t sbase, int warp,
                                          int lane, uint32_t lt, uint32_t& err) {
@@ -317,8 +322,21 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
     const uint32_t r0 = wcnt + __popc(L0 & lt) + __popc(L1 & lt);
     const uint32_t r1 = r0 + (l0 ? 1u : 0u);
     const uint32_t v0 = ((sbase + (uint32_t)e0) << 1) | (u0 ? 1u : 0u);
-    if (l0 && r0 < (uint32_t)kRow) row[r0] = (uint16_t)v0;
-    if (l1 && r1 < (uint32_t)kRow) row[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+    if (KEYS) {  // also each entry's x (the adaptive selection then needs no gather of x)
+      double* rk = reinterpret_cast<double*>(row);
+      uint16_t* re = row + 4 * kRowK;
+      if (l0 && r0 < (uint32_t)kRowK) {
+        re[r0] = (uint16_t)v0;
+        rk[r0] = xv.x;
+      }
+      if (l1 && r1 < (uint32_t)kRowK) {
+        re[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+        rk[r1] = xv.y;
+      }
+    } else {
+      if (l0 && r0 < (uint32_t)kRow) row[r0] = (uint16_t)v0;
+      if (l1 && r1 < (uint32_t)kRow) row[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+    }
     wcnt += __popc(L0) + __popc(L1);
   }
   return wcnt;
@@ -371,7 +389,7 @@ __device__ __forceinline__ int64_t lookback128(uint64_t* status, int64_t s, uint
 // words come from the ballot masks, one 64-element group per step.
 // `dst` = the row's first log position, `lim` = positions still in capacity.
 __device__ __noinline__ void rlf_row_from_masks(const FusedSmem& S, int slot, int q, uint64_t gw, uint64_t* dst,
-                                                int64_t lim, int lane, uint32_t lt) {
+                                                int64_t lim, int lane, uint32_t lt, uint64_t* kdst = nullptr) {
   const int tile = q / kWarps, w = q % kWarps;
   uint32_t r = 0;
   for (int j = 0; j < kSSlots; ++j) {
@@ -382,6 +400,10 @@ __device__ __noinline__ void rlf_row_from_masks(const FusedSmem& S, int slot, in
     if (l0 && (int64_t)r0 < lim) dst[r0] = gw + (e0 << 1) + ((m.z >> lane) & 1u);
     const uint32_t r1 = r0 + (l0 ? 1u : 0u);
     if (l1 && (int64_t)r1 < lim) dst[r1] = gw + ((e0 + 1) << 1) + ((m.w >> lane) & 1u);
+    if (kdst) {
+      if (l0 && (int64_t)r0 < lim) kdst[r0] = kKeyMissing;
+      if (l1 && (int64_t)r1 < lim) kdst[r1] = kKeyMissing;
+    }
     r += __popc(m.x) + __popc(m.y);
   }
 }
@@ -389,6 +411,7 @@ __device__ __noinline__ void rlf_row_from_masks(const FusedSmem& S, int slot, in
 // Compute warp: once the log warp has placed ordinal k (super-tile s) of this
 // CTA (ofull), write this warp's four rows of it -- staged entries by
 // coalesced stores, an overflowing row from its ballot masks.
+template <bool KEYS = false>
 __device__ __forceinline__ void rlf_write_rows(const RLFArgs& a, FusedSmem& S, int64_t k, int64_t s, int warp,
                                                int lane, uint32_t lt) {
   const int slot = (int)(k % kMaskSlots);
@@ -405,6 +428,20 @@ __device__ __forceinline__ void rlf_write_rows(const RLFArgs& a, FusedSmem& S, i
     if (i >= nt) break;
     const uint32_t cq = S.cnts[slot][q];
     const uint32_t pq = S.rpos[slot][q];
+    if (KEYS) {
+      uint64_t* kd = a.keys + off;
+      if (cq <= (uint32_t)kRowK) {
+        const uint64_t* rk = reinterpret_cast<const uint64_t*>(S.rows[slot][q]);
+        const uint16_t* re = S.rows[slot][q] + 4 * kRowK;
+        if ((uint32_t)lane < cq && (int64_t)(pq + lane) < lim) {
+          dst[pq + lane] = gw + re[lane];
+          kd[pq + lane] = rk[lane];
+        }
+      } else {
+        rlf_row_from_masks(S, slot, q, gw, dst + pq, lim - (int64_t)pq, lane, lt, kd + pq);
+      }
+      continue;
+    }
     if (cq <= (uint32_t)kRow) {
       const uint16_t* row = S.rows[slot][q];
       if ((uint32_t)lane < cq && (int64_t)(pq + lane) < lim) dst[pq + lane] = gw + row[lane];
@@ -649,10 +686,11 @@ __device__ __forceinline__ RLFArgs seg_view(const RLBatch& b, int j) {
   v.sparse = sg.sparse;
   v.cap = sg.cap;
   v.global_base = sg.global_base;
+  v.keys = sg.keys;
   return v;
 }
 
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool KEYS>
 __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_constant__ RLBatch b) {
   extern __shared__ __align__(128) uint8_t smraw[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
@@ -782,7 +820,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
     int j1 = 0, j2 = 0, j3 = 0;         // and their tensors
     int64_t q = 0;
     auto write_rows = [&](int64_t kk, int64_t s, int j) {
-      rlf_write_rows(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
+      rlf_write_rows<KEYS>(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
     };
     for (int64_t k = 0;; ++k) {
       if (k >= kMaskSlots) write_rows(k - kMaskSlots, h3, j3);
@@ -832,10 +870,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
         uint16_t* row = S.rows[slot][i * kWarps + warp];
         const uint32_t tc =
             (t < full_tiles)
-                ? rlf_tile<OUT, FAST, true>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
-                                            (uint32_t)(i * kSTile), warp, lane, lt, err)
-                : rlf_tile<OUT, FAST, false>(g, c8, w8, thr32, sg.x + tbase, o, (int)(sg.n - tbase),
-                                             S.masks[slot][i], row, (uint32_t)(i * kSTile), warp, lane, lt, err);
+                ? rlf_tile<OUT, FAST, true, KEYS>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
+                                                  (uint32_t)(i * kSTile), warp, lane, lt, err)
+                : rlf_tile<OUT, FAST, false, KEYS>(g, c8, w8, thr32, sg.x + tbase, o, (int)(sg.n - tbase),
+                                                   S.masks[slot][i], row, (uint32_t)(i * kSTile), warp, lane, lt, err);
         if (lane == 0) S.cnts[slot][i * kWarps + warp] = tc;
         wcnt += tc;
         report_err(sg.err, err);
@@ -1261,11 +1299,11 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
                                 : launch_rlf<VT_OUT_NONE, false>(f, st);
 }
 
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool KEYS>
 static int launch_rlb(const RLBatch& b, cudaStream_t st) {
   static_assert(sizeof(RLBatch) <= 32000, "batch table must fit the kernel parameter space");
   const size_t smem = sizeof(FusedSmem);
-  auto k = rl_batch_kernel<OUT, FAST>;
+  auto k = rl_batch_kernel<OUT, FAST, KEYS>;
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1280,15 +1318,20 @@ static int launch_rlb(const RLBatch& b, cudaStream_t st) {
   return vt_check_launch("rl_batch_kernel");
 }
 
-int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st) {
+template <bool KEYS>
+static int rl_stream_batch_t(const RLBatch& b, bool fast, int out_kind, cudaStream_t st) {
   if (fast) {
-    return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, true>(b, st)
-         : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, true>(b, st)
-                                  : launch_rlb<VT_OUT_NONE, true>(b, st);
+    return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, true, KEYS>(b, st)
+         : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, true, KEYS>(b, st)
+                                  : launch_rlb<VT_OUT_NONE, true, KEYS>(b, st);
   }
-  return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, false>(b, st)
-       : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, false>(b, st)
-                                : launch_rlb<VT_OUT_NONE, false>(b, st);
+  return out_kind == VT_OUT_F32 ? launch_rlb<VT_OUT_F32, false, KEYS>(b, st)
+       : out_kind == VT_OUT_F64 ? launch_rlb<VT_OUT_F64, false, KEYS>(b, st)
+                                : launch_rlb<VT_OUT_NONE, false, KEYS>(b, st);
+}
+
+int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st, bool keys) {
+  return keys ? rl_stream_batch_t<true>(b, fast, out_kind, st) : rl_stream_batch_t<false>(b, fast, out_kind, st);
 }
 
 template <int OUT, bool FAST>

@@ -46,24 +46,6 @@ __device__ __forceinline__ double ldg_sector(const double* p) {
   return v;
 }
 
-// FP64 bit pattern of p for one element; err gets rnd's error bits.
-__device__ __forceinline__ uint64_t dist_key(double x, const Grid& g, uint32_t& err) {
-  const uint64_t bits = (uint64_t)__double_as_longlong(x);
-  const uint64_t mag = bits & kMag;
-  if (mag >= kNormalMin) {
-    const uint64_t low = mag & g.low_mask;
-    const uint64_t base = mag >> g.drop;
-    const bool up = (low > g.half) || ((low == g.half) && (base & 1ull));
-    const uint64_t rmag = (base + (up ? 1ull : 0ull)) << g.drop;
-    err |= (mag >= kExpAllOnes) ? (uint32_t)VT_ERR_NONFINITE
-                                : ((rmag > g.gmax_bits) ? (uint32_t)VT_ERR_RANGE : 0u);
-    const uint64_t d = up ? (g.one - low) : low;  // |x - r| = d * 2^(E-52), scale = 2^E
-    return (uint64_t)__double_as_longlong(__dmul_rn(__ull2double_rn(d), 0x1p-52));
-  }
-  const double r = __dmul_rn(rint(__dmul_rn(x, g.sub_up)), g.sub_dn);
-  return (uint64_t)__double_as_longlong(__dmul_rn(fabs(__dsub_rn(x, r)), 0x1p126));
-}
-
 template <int PASS>
 __global__ void __launch_bounds__(kHistThreads) tau_hist_kernel(const double* __restrict__ x, int64_t n,
                                                                 Grid g, const SelectState* st,
@@ -734,22 +716,22 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
   if (threadIdx.x == 0) s_above = 0;
   __syncthreads();
   uint32_t err = 0, above = 0;
-  // kGU independent gathers in flight per thread: the candidates sit ~1/67
-  // apart in x, so every one is its own DRAM line and latency-bound
-  constexpr int kGU = 8;
+  constexpr int kGU = 8;  // independent loads in flight per thread
   const int64_t stride = nblk * kAdThreads;
   for (int64_t i0 = blk * kAdThreads + threadIdx.x; i0 < M; i0 += kGU * stride) {
     uint64_t key[kGU];
-    double xv[kGU];
     uint64_t w[kGU];
+    // the rounding pass staged the candidates' x bits in ck; gather only the
+    // rows it could not stage, and leave the keys in ck
 #pragma unroll
-    for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? cw[i0 + u * stride] : 0ull;
-#pragma unroll
-    for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(x + (w[u] >> 1)) : 0.0;
+    for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? ck[i0 + u * stride] : 0ull;
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
-      key[u] = dist_key(xv[u], g, err);
-      if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];
+      // a NaN x equal to the marker is gathered again: the same value
+      const double xu = w[u] == kKeyMissing ? ldg_sector(x + (cw[i0 + u * stride] >> 1))
+                                             : __longlong_as_double((long long)w[u]);
+      key[u] = dist_key(xu, g, err);
+      if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];  // the selection and the filter read keys
     }
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
@@ -1966,6 +1948,7 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
       rc_.x = sg.x;
       rc_.out = sg.out;
       rc_.sparse = p.cw;
+      rc_.keys = p.ck;  // the rounding pass stages each candidate's key
       rc_.cursor_out = &p.h->ccount;
       rc_.counters = &p.h->scratch;
       rc_.err = err;
@@ -1985,6 +1968,7 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
       rf.global_base = sg.global_base;
       rf.dthr = p.dthr;
       rf.gate = &p.h->fallback;
+      rf.keys = nullptr;
       tick += rl_batch_tickets(n);
       AdSeg& a = ab.seg[i];
       a.x = sg.x;
@@ -2008,7 +1992,7 @@ extern "C" int vt_round_log_adaptive_batch(const vt_adaptive_segment* segs, int 
     cand.total = fb.total = tick;
     ab.nblk = (int32_t)blk;
     // 1. rounding pass over every tensor: y + ordered candidate words
-    if ((rc = rl_stream_batch(cand, fast, out_kind, s))) return rc;
+    if ((rc = rl_stream_batch(cand, fast, out_kind, s, /*keys=*/true))) return rc;
     // 2-4. per tensor: digit histogram, exact selection + bisection, ordered filter
     adapt_hist_batch_kernel<<<(unsigned)blk, kAdThreads, 0, s>>>(ab);
     if ((rc = vt_check_launch("adapt_hist_batch_kernel"))) return rc;

@@ -149,3 +149,19 @@ def test_batch_errors():
     with pytest.raises(ops.LogOverflow):
         ops.round_and_log_adaptive_batch([torch.randn(100_000, dtype=torch.float64, device="cuda")], 32, [500],
                                          log_outs=[small])
+
+
+@pytest.mark.parametrize("frac", [0.02, 0.1])
+def test_batch_dense_candidates(oracle, frac):
+    """Budgets of 2 % and 10 %: at the candidate threshold many 256-element
+    rows hold more candidates than the rounding pass stages keys for (12),
+    so those keys are gathered from x by the histogram pass; mixed with
+    staged rows the result still equals the oracle."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(int(frac * 1000))
+    xs = [rng.normal(0.0, 1.0, n) for n in (300_001, 65_536, 9_999)]
+    xs.append(rng.normal(0.0, 1.0, 100_000) * np.exp2(rng.integers(-140, -120, 100_000)))  # FP32-subnormal zone
+    budgets = [int(frac * x.size) for x in xs]
+    res = ops.round_and_log_adaptive_batch([torch.from_numpy(x).cuda() for x in xs], 32, budgets)
+    _check_all(oracle, xs, res, 32, budgets)

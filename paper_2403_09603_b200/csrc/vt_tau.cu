@@ -690,11 +690,19 @@ __device__ __forceinline__ bool last_cta(uint32_t* arrived, uint32_t count) {
   return s_last != 0;
 }
 
+// A candidate's digit code: 0xfffe below L (never, for keys the rounding
+// pass logged), the top digit of key - L - 1 for keys in (L, hi], 0xffff
+// above hi.  ad_ord maps codes to the key order: -1, digit, kAdBins.
+__device__ __forceinline__ uint16_t ad_code(uint64_t key, uint64_t L_key, uint64_t hi_key, int s0) {
+  return key > hi_key ? (uint16_t)0xffffu : key > L_key ? (uint16_t)((key - L_key - 1) >> s0) : (uint16_t)0xfffeu;
+}
+__device__ __forceinline__ int ad_ord(uint32_t c) { return c == 0xfffeu ? -1 : c == 0xffffu ? kAdBins : (int)c; }
+
 // blk / nblk: this CTA's index among the CTAs working on the tensor (the
 // whole grid for a single call, the tensor's share of a batched grid)
 __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, const Grid& g,
                                                 const uint64_t* __restrict__ cw, uint64_t* __restrict__ ck,
-                                                int64_t cap, int64_t budget, uint64_t L_key, uint64_t hi_key, int s0,
+                                                uint16_t* __restrict__ cd, int64_t cap, int64_t budget, uint64_t L_key, uint64_t hi_key, int s0,
                                                 AdaptHdr* h, uint32_t* __restrict__ hist,
                                                 uint64_t* __restrict__ fstatus, int64_t blk,
                                                 int64_t nblk) {
@@ -722,7 +730,8 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
     uint64_t key[kGU];
     uint64_t w[kGU];
     // the rounding pass staged the candidates' x bits in ck; gather only the
-    // rows it could not stage, and leave the keys in ck
+    // rows it could not stage.  The selection and the filter read the 2-byte
+    // digit codes and compute a key only where the code cannot decide.
 #pragma unroll
     for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? ck[i0 + u * stride] : 0ull;
 #pragma unroll
@@ -731,7 +740,10 @@ __device__ __forceinline__ void adapt_hist_body(const double* __restrict__ x, co
       const double xu = w[u] == kKeyMissing ? ldg_sector(x + (cw[i0 + u * stride] >> 1))
                                              : __longlong_as_double((long long)w[u]);
       key[u] = dist_key(xu, g, err);
-      if (i0 + u * stride < M) ck[i0 + u * stride] = key[u];  // the selection and the filter read keys
+      if (i0 + u * stride < M) {
+        if (w[u] == kKeyMissing) ck[i0 + u * stride] = (uint64_t)__double_as_longlong(xu);
+        cd[i0 + u * stride] = ad_code(key[u], L_key, hi_key, s0);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
@@ -806,7 +818,8 @@ __device__ uint64_t select_by_count(const uint64_t* __restrict__ src, int m, int
   return v;
 }
 
-__device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ ck, uint64_t L_key, uint64_t hi_key,
+__device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ ck, const uint16_t* __restrict__ cd,
+                                                  const Grid& g, uint64_t L_key, uint64_t hi_key,
                                                   int s0, AdaptHdr* h, uint64_t* __restrict__ cand2, double lower,
                                                   double upper, int iters, DevThr* dthr, double* tau_out,
                                                   uint64_t* key_out, int64_t blk, int64_t nblk) {
@@ -826,27 +839,32 @@ __device__ __forceinline__ void adapt_select_body(const uint64_t* __restrict__ c
   const uint64_t digit = h->digit;
   const uint64_t lo1 = L_key + 1;
   const int lane = threadIdx.x & 31;
-  constexpr int kSU = 4;  // independent key loads in flight per thread
+  constexpr int kSU = 8;  // independent code loads in flight per thread
   const int64_t stride = nblk * kAdThreads;
   for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += kSU * stride) {
-    uint64_t key[kSU];
+    uint32_t code[kSU];
 #pragma unroll
     for (int u = 0; u < kSU; ++u) {
       const int64_t i = i0 + u * stride + threadIdx.x;
-      key[u] = i < M ? ck[i] : 0ull;
+      code[u] = i < M ? cd[i] : 0xfffeu;
     }
 #pragma unroll
     for (int u = 0; u < kSU; ++u) {
       const int64_t i = i0 + u * stride + threadIdx.x;
-      const bool in = i < M && key[u] <= hi_key && key[u] >= lo1 && ((key[u] - lo1) >> s0) == digit;
+      const bool in = code[u] == (uint32_t)digit;
       const uint32_t m = __ballot_sync(0xffffffffu, in);
       if (m) {
+        uint64_t key = 0;
+        if (in) {
+          uint32_t e = 0;  // reported by the histogram pass
+          key = dist_key(__longlong_as_double((long long)ck[i]), g, e);
+        }
         const int leader = __ffs(m) - 1;
         unsigned long long pos = 0;
         if (lane == leader)
           pos = atomicAdd(reinterpret_cast<unsigned long long*>(&h->cand2), (unsigned long long)__popc(m));
         pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key[u] - lo1;
+        if (in) cand2[pos + __popc(m & ((1u << lane) - 1u))] = key - lo1;
       }
     }
   }
@@ -907,6 +925,8 @@ __device__ __forceinline__ uint64_t lbw(uint32_t e, uint64_t f, uint64_t v) {
 }
 
 __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ cw, const uint64_t* __restrict__ ck,
+                                                  const uint16_t* __restrict__ cd, const Grid& g, uint64_t L_key,
+                                                  uint64_t hi_key, int s0,
                                                   AdaptHdr* h, const DevThr* dthr, uint64_t* sparse, int64_t cap,
                                                   int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
                                                   int64_t* counters, uint64_t* status, int64_t nblk) {
@@ -921,6 +941,14 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
   const int64_t M = h->ccount;
   const int64_t nchunks = (M + kFChunk - 1) / kFChunk;
   const uint64_t tau_key = (uint64_t)__double_as_longlong(dthr->tau);
+  const int tau_ord = ad_ord(ad_code(tau_key, L_key, hi_key, s0));
+  // keep <=> key > tau: decided by the codes except in tau's own digit
+  auto keep_bit = [&](uint32_t c, int64_t i) -> uint32_t {
+    const int o = ad_ord(c);
+    if (o != tau_ord) return o > tau_ord ? 1u : 0u;
+    uint32_t e = 0;
+    return dist_key(__longlong_as_double((long long)ck[i]), g, e) > tau_key ? 1u : 0u;
+  };
   const int64_t cur = cursor_in ? *cursor_in : 0;
   if (tid == 0) s_epoch = ((*(volatile uint32_t*)&h->f_epoch) + 1u) & (uint32_t)kLBEpoch;
   __syncthreads();
@@ -936,14 +964,18 @@ __device__ __forceinline__ void adapt_filter_body(const uint64_t* __restrict__ c
     const int64_t c0 = t * kFChunk + (int64_t)tid * kPer;
     uint32_t keep = 0;
     if (c0 + kPer <= M) {
+      uint4 cc[kPer / 8];  // 32 codes, 64 bytes
+#pragma unroll
+      for (int v = 0; v < kPer / 8; ++v) cc[v] = *reinterpret_cast<const uint4*>(cd + c0 + 8 * v);
 #pragma unroll
       for (int v = 0; v < kPer / 2; ++v) {
-        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(ck + c0 + 2 * v);
-        keep |= (kk.x > tau_key ? 1u : 0u) << (2 * v);
-        keep |= (kk.y > tau_key ? 1u : 0u) << (2 * v + 1);
+        const uint4& q = cc[v >> 2];
+        const uint32_t pr = (v & 3) == 0 ? q.x : (v & 3) == 1 ? q.y : (v & 3) == 2 ? q.z : q.w;
+        keep |= keep_bit(pr & 0xffffu, c0 + 2 * v) << (2 * v);
+        keep |= keep_bit(pr >> 16, c0 + 2 * v + 1) << (2 * v + 1);
       }
     } else {
-      for (int k = 0; k < kPer && c0 + k < M; ++k) keep |= (ck[c0 + k] > tau_key ? 1u : 0u) << k;
+      for (int k = 0; k < kPer && c0 + k < M; ++k) keep |= keep_bit(cd[c0 + k], c0 + k) << k;
     }
     const uint32_t cnt = __popc(keep);
     uint32_t inc = cnt;
@@ -1562,7 +1594,7 @@ namespace vt {
 // one workspace serves calls of any size; the filter status words are
 // cleared by the batched histogram kernel for the chunks a call uses.
 struct AdaptLayout {
-  size_t tau, rl, hist, cw, ck, c2, fst, total;
+  size_t tau, rl, hist, cw, ck, c2, cd, fst, total;
   int64_t cap;
 };
 __host__ __device__ inline size_t al256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -1586,6 +1618,8 @@ __host__ __device__ inline AdaptLayout adapt_layout_rl(int64_t n, size_t rl_byte
   o += al256((size_t)L.cap * 8);
   L.c2 = o;
   o += al256((size_t)L.cap * 8);
+  L.cd = o;
+  o += al256((size_t)L.cap * 2);
   L.total = o;
   return L;
 }
@@ -1597,6 +1631,7 @@ struct AdPtrs {
   BudState* st;
   uint32_t *bhist, *ahist;
   uint64_t *bcand, *cw, *ck, *c2, *fst;
+  uint16_t* cd;  // batched calls: each candidate's digit code (ad_code)
   int64_t cap;
 };
 
@@ -1613,6 +1648,7 @@ __host__ __device__ inline AdPtrs adapt_ptrs(uint8_t* w, const AdaptLayout& lay)
   p.cw = reinterpret_cast<uint64_t*>(w + lay.cw);
   p.ck = reinterpret_cast<uint64_t*>(w + lay.ck);
   p.c2 = reinterpret_cast<uint64_t*>(w + lay.c2);
+  p.cd = reinterpret_cast<uint16_t*>(w + lay.cd);
   p.fst = reinterpret_cast<uint64_t*>(w + lay.fst);
   p.cap = lay.cap;
   return p;
@@ -1814,7 +1850,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_hist_batch_kernel(const __gr
   const AdSeg& sg = b.seg[j];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
   if (blockIdx.x == 0 && threadIdx.x == 0) b.fb->count = 0;  // the previous batch's fallback kernels are done
-  adapt_hist_body(sg.x, b.g0, p.cw, p.ck, p.cap, sg.budget, sg.L_key, b.hi_key, sg.s0, p.h, p.ahist, p.fst,
+  adapt_hist_body(sg.x, b.g0, p.cw, p.ck, p.cd, p.cap, sg.budget, sg.L_key, b.hi_key, sg.s0, p.h, p.ahist, p.fst,
                   (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
 }
 
@@ -1822,7 +1858,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_batch_kernel(const __
   const int j = ad_find(b, blockIdx.x);
   const AdSeg& sg = b.seg[j];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
-  adapt_select_body(p.ck, sg.L_key, b.hi_key, sg.s0, p.h, p.c2, b.lo, b.hi, b.iters, p.dthr, sg.tau_out, p.key,
+  adapt_select_body(p.ck, p.cd, b.g0, sg.L_key, b.hi_key, sg.s0, p.h, p.c2, b.lo, b.hi, b.iters, p.dthr, sg.tau_out, p.key,
                     (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
 }
 
@@ -1830,7 +1866,7 @@ __global__ void __launch_bounds__(kAdThreads) adapt_filter_batch_kernel(const __
   const int j = ad_find(b, blockIdx.x);
   const AdSeg& sg = b.seg[j];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));
-  adapt_filter_body(p.cw, p.ck, p.h, p.dthr, sg.log, sg.log_cap, sg.global_base, nullptr, nullptr, sg.flags + 2,
+  adapt_filter_body(p.cw, p.ck, p.cd, b.g0, sg.L_key, b.hi_key, sg.s0, p.h, p.dthr, sg.log, sg.log_cap, sg.global_base, nullptr, nullptr, sg.flags + 2,
                     p.fst, ad_nblk(b, j));
 }
 

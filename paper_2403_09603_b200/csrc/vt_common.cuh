@@ -334,7 +334,7 @@ size_t rp_stream_workspace(int64_t n);
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr,
-              const int32_t* gate = nullptr);
+              const int32_t* gate = nullptr, uint64_t* keys = nullptr);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 

@@ -453,7 +453,7 @@ __device__ __forceinline__ void rlf_write_rows(const RLFArgs& a, FusedSmem& S, i
   }
 }
 
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool KEYS = false>
 __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(smraw);
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     for (int64_t k = 0;; ++k) {
       // this warp's rows of ordinal k - 3 leave slot k % kMaskSlots before it is reused
       if (warp == 0 && lane == 0 && k < 14) TL(4 + 4 * (int)k);
-      if (k >= kMaskSlots) rlf_write_rows(a, S, k - kMaskSlots, h3, warp, lane, lt);
+      if (k >= kMaskSlots) rlf_write_rows<KEYS>(a, S, k - kMaskSlots, h3, warp, lane, lt);
       if (warp == 0 && lane == 0 && k < 14) TL(6 + 4 * (int)k);
       const int slot = (int)(k % kMaskSlots);
       int64_t s = -1, t0 = 0;
@@ -586,9 +586,9 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
           uint16_t* row = S.rows[slot][i * kWarps + warp];
           const uint32_t tc =
               (t < full_tiles)
-                  ? rlf_tile<OUT, FAST, true>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
+                  ? rlf_tile<OUT, FAST, true, KEYS>(g, c8, w8, thr32, S.ring[st], o, kSTile, S.masks[slot][i], row,
                                               (uint32_t)(i * kSTile), warp, lane, lt, err)
-                  : rlf_tile<OUT, FAST, false>(g, c8, w8, thr32, a.x + tbase, o, (int)(a.n - tbase),
+                  : rlf_tile<OUT, FAST, false, KEYS>(g, c8, w8, thr32, a.x + tbase, o, (int)(a.n - tbase),
                                                S.masks[slot][i], row, (uint32_t)(i * kSTile), warp, lane, lt, err);
           if (lane == 0) S.cnts[slot][i * kWarps + warp] = tc;
           wcnt += tc;
@@ -617,9 +617,9 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       }
       if (warp == 0 && lane == 0 && s < 0) TL(60);
       if (s < 0) {  // drain ordinals k - 2, k - 1
-        if (k >= 2) rlf_write_rows(a, S, k - 2, h2, warp, lane, lt);
+        if (k >= 2) rlf_write_rows<KEYS>(a, S, k - 2, h2, warp, lane, lt);
         if (warp == 0 && lane == 0) TL(61);
-        if (k >= 1) rlf_write_rows(a, S, k - 1, h1, warp, lane, lt);
+        if (k >= 1) rlf_write_rows<KEYS>(a, S, k - 1, h1, warp, lane, lt);
         if (warp == 0 && lane == 0) TL(62);
         break;
       }
@@ -1260,11 +1260,11 @@ size_t rp_stream_workspace(int64_t n) {
   return 64;  // ticket header
 }
 
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool KEYS = false>
 static int launch_rlf(RLFArgs a, cudaStream_t st) {
   const size_t smem = sizeof(FusedSmem);
   static_assert(sizeof(FusedSmem) <= 74 * 1024, "three fused CTAs per SM");
-  auto k = rl_fused_kernel<OUT, FAST>;
+  auto k = rl_fused_kernel<OUT, FAST, KEYS>;
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1284,11 +1284,20 @@ static int launch_rlf(RLFArgs a, cudaStream_t st) {
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr,
-              const int32_t* gate) {
+              const int32_t* gate, uint64_t* keys) {
   uint8_t* w = static_cast<uint8_t*>(ws);
   RLFArgs f{x, n, g, thr32, out, stream_tiles(n), 0, 0, reinterpret_cast<FusedHeader*>(w),
             reinterpret_cast<uint64_t*>(w + 64), sparse, cap, global_base, cursor_in, cursor_out, counters, err,
-            dthr, gate};
+            dthr, gate, keys};
+  if (keys) {  // the adaptive candidate pass (b_r = 32 or not)
+    if (fast)
+      return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, true, true>(f, st)
+           : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, true, true>(f, st)
+                                    : launch_rlf<VT_OUT_NONE, true, true>(f, st);
+    return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, false, true>(f, st)
+         : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, false, true>(f, st)
+                                  : launch_rlf<VT_OUT_NONE, false, true>(f, st);
+  }
   if (fast) {
     return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, true>(f, st)
          : out_kind == VT_OUT_F64 ? launch_rlf<VT_OUT_F64, true>(f, st)

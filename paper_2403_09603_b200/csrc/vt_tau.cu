@@ -1352,17 +1352,19 @@ __device__ void tail_hist(const TailArgs& a, int64_t M, int64_t blk, int64_t nbl
   constexpr int kGU = 8;
   const int64_t stride = nblk * kAdThreads;
   for (int64_t i0 = blk * kAdThreads + tid; i0 < M; i0 += kGU * stride) {
+    // ck holds each candidate's x: from the key pass (in place) or staged by
+    // the rounding pass (out of place), which marks the rows it could not
+    // stage -- those are gathered from x (a NaN equal to the marker too: the
+    // same value)
     double xv[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u)
+      xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)a.ck[i0 + u * stride]) : 0.0;
     if (gather) {
-      uint64_t w[kGU];
-#pragma unroll
-      for (int u = 0; u < kGU; ++u) w[u] = (i0 + u * stride < M) ? a.cw[i0 + u * stride] : 0ull;
-#pragma unroll
-      for (int u = 0; u < kGU; ++u) xv[u] = (i0 + u * stride < M) ? ldg_sector(a.x + (w[u] >> 1)) : 0.0;
-    } else {
 #pragma unroll
       for (int u = 0; u < kGU; ++u)
-        xv[u] = (i0 + u * stride < M) ? __longlong_as_double((long long)a.ck[i0 + u * stride]) : 0.0;
+        if (i0 + u * stride < M && __double_as_longlong(xv[u]) == (long long)kKeyMissing)
+          xv[u] = ldg_sector(a.x + (a.cw[i0 + u * stride] >> 1));
     }
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
@@ -1734,8 +1736,9 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
     if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
   } else {
     // 1. rounding pass: y + candidate words (local index << 1 | up) with p > L
+    // (and each candidate's x at its position in ck: the tail reads it there)
     rc = rl_stream(x, n, gL, thrL, fast, out_kind, out, cw, lay.cap, 0, nullptr, &h->ccount, &h->scratch, err,
-                   rws, s);
+                   rws, s, nullptr, nullptr, ck);
     if (rc) return rc;
   }
   // 2-4. one cooperative launch: selection of the (budget+1)-th largest p

@@ -187,3 +187,22 @@ def test_hot_digit_tail(oracle, in_place):
     r = oracle.rnd_array(x, 32)
     got = (xt if in_place else y).cpu().numpy()
     assert np.array_equal(bits(got), bits(r if got.dtype == np.float64 else r.astype(np.float32)))
+
+
+@pytest.mark.parametrize("frac", [0.02, 0.1])
+def test_out_of_place_dense_candidates(oracle, frac):
+    """Out of place, the rounding pass stages each candidate's x for the
+    tail; rows with more candidates than it stages (budgets of 2 % / 10 %)
+    are gathered from x.  tau, log and y equal the oracle's."""
+    import torch
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(int(1000 * frac) + 7)
+    for x in (rng.normal(0.0, 1.0, 300_001),
+              rng.normal(0.0, 1.0, 100_000) * np.exp2(rng.integers(-140, -120, 100_000))):
+        B = int(frac * x.size)
+        y, log, tau = ops.round_and_log_adaptive(torch.from_numpy(x).cuda(), 32, B)
+        t_or = oracle.search_tau_budget(x, 32, B)
+        assert tau == t_or
+        want = oracle.sparse_from_codes(oracle.direction_array(x, 32, t_or))
+        assert np.array_equal(log.words.cpu().numpy().view(np.uint64), want)
+        assert np.array_equal(y.cpu().numpy().view(np.uint32), oracle.rnd_array(x, 32).astype(np.float32).view(np.uint32))

@@ -31,6 +31,7 @@
  *   vt_tau_kth_key    <- protocol.search_tau predicate       protocol.py:494-506 (budget form,
  *   vt_tau_kth_begin/hist/select: the same, one pass at a time (sharded tensors)
  *   vt_tau_budget_key    SURVEY.md Appendix A.4)
+ *   vt_tau_budget     <- the same budget search incl. the bisection, one read of x
  *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
@@ -169,6 +170,22 @@ int vt_tau_kth_select(int pass, uint64_t *key_out, void *ws, size_t ws_bytes, vt
 int vt_tau_budget_key(const double *x, int64_t n, int b_r, int64_t budget, double tau_lo,
                       double tau_hi, uint64_t *key_out, int32_t *status_out, int32_t *err,
                       void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * Budget search with no host round trip (protocol.search_tau_budget, the
+ * north-star form of protocol.search_tau, pkg/src/vtrain/protocol.py:494-506,
+ * SURVEY.md A.4): ONE streaming read of x collects the values of the
+ * candidates above a threshold below the expected tau, then one cooperative
+ * launch selects the (budget+1)-th largest p among them exactly and runs the
+ * 30-step FP64 bisection on the device (the exact multi-pass selection over x
+ * runs in the same launch when the candidates cannot decide).  *tau_out
+ * (device double) = the returned upper bound; *key_out (device, optional) =
+ * FP64 bits of v' (v clamped as for vt_tau_budget_key).  x 32-byte aligned;
+ * workspace vt_tau_budget_workspace(n) bytes, 256-byte aligned, zero-filled
+ * before first use, one stream at a time.
+ */
+size_t vt_tau_budget_workspace(int64_t n);
+int vt_tau_budget(const double *x, int64_t n, int b_r, int64_t budget, int iters, double *tau_out,
+                  uint64_t *key_out, int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
 /*
  * Per-tensor adaptive round-and-log with no host round trip: budget select
  * (vt_tau_budget_key), the 30-step search_tau-skeleton bisection on the

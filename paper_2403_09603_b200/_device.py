@@ -8,12 +8,16 @@ tensors are zero-copy when contiguous and 32-byte aligned.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
 from . import _lib
 
 _WS: dict[tuple, torch.Tensor] = {}
+_RETIRED: list[torch.Tensor] = []
+_WS_LOCK = threading.Lock()
 
 
 def require_cuda() -> torch.device:
@@ -63,16 +67,42 @@ def back(t: torch.Tensor, host: bool, shape: tuple):
 
 
 def workspace(nbytes: int, tag: str) -> torch.Tensor:
-    """Per (device, tag) scratch buffer, grown on demand.  Operators that may
-    run concurrently on different streams use different tags.  Zero-filled
-    once at allocation (vt_round_log keeps an epoch header and epoch-tagged
-    status words in it that must start out zero)."""
-    key = (torch.cuda.current_device(), tag)
-    ws = _WS.get(key)
-    if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
-        _WS[key] = ws
-    return ws
+    """Scratch buffer per (device, current stream, tag), grown on demand.
+
+    Keyed by stream so the public operators are reentrant across streams and
+    host threads: the ticketed kernels keep a ticket counter,
+    an epoch and epoch-tagged look-back words in their workspace, and two
+    grids drawing from one counter at once would corrupt each other.  Calls
+    on ONE stream may share a workspace because the stream serialises them.
+    Zero-filled once at allocation (the epoch scheme needs a zero start).
+    A grown-out-of buffer is retired, not freed: a CUDA graph captured with
+    the old pointer (or queued work) may still use it."""
+    key = (torch.cuda.current_device(), stream_ptr(), tag)
+    with _WS_LOCK:
+        ws = _WS.get(key)
+        if ws is None or ws.numel() < nbytes:
+            if ws is not None:
+                _RETIRED.append(ws)
+            ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+            _WS[key] = ws
+        return ws
+
+
+def check_out(t: torch.Tensor | None, n: int, dtype: torch.dtype, device: torch.device, name: str = "out") -> None:
+    """Caller-supplied output buffers go to the C ABI as raw pointers: require
+    the element count, dtype, contiguity and device before the call."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if t.numel() < n:
+        raise ValueError(f"{name} holds {t.numel()} elements, needs {n}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
 
 
 class Flags:

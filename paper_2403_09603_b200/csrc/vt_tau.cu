@@ -1664,6 +1664,96 @@ AdaptLayout adapt_layout(int64_t n) { return adapt_layout_rl(n, vt_round_log_wor
 
 extern "C" size_t vt_round_log_adaptive_workspace(int64_t n) { return adapt_layout(n).total; }
 
+namespace vt {
+// The candidate plan of one adaptive call: threshold L below the expected
+// tau (about kCandFactor x (budget + 1) elements above it when p is uniform
+// on [0, hi], as the dropped bits of real data are) and the top-digit shift
+// of the key offsets above L.
+struct AdPlan {
+  double lo, hi, L, want;
+  uint64_t lo_key, hi_key, L_key;
+  int s0, thrL;
+  Grid gL, g0;
+};
+
+AdPlan adapt_plan(int64_t n, int b_r, int64_t budget) {
+  AdPlan P;
+  P.lo = 0x1p-25;
+  P.hi = ldexp(1.0, 8 - b_r);
+  memcpy(&P.lo_key, &P.lo, 8);
+  memcpy(&P.hi_key, &P.hi, 8);
+  P.want = (double)kCandFactor * (double)(budget + 1) + 1024.0;
+  P.L = P.hi * (1.0 - P.want / (double)n);
+  if (!(P.L > P.lo)) P.L = P.lo;
+  memcpy(&P.L_key, &P.L, 8);
+  const uint64_t W = P.hi_key - P.L_key;  // key offsets 0 .. W - 1 above L
+  const int wbits = W > 1 ? 64 - __builtin_clzll(W - 1) : 1;
+  P.s0 = std::max(0, wbits - kAdBits);
+  P.gL = make_grid(b_r, P.L);
+  P.thrL = (int)std::min<int64_t>(std::max<int64_t>(P.gL.thr, 0), INT32_MAX);
+  P.g0 = make_grid(b_r, 0.0);
+  return P;
+}
+
+// One streaming read of x: the x values of every candidate (p > L), unordered,
+// appended to ck (h->ccount is 0 on entry: zero-filled workspace, reset by
+// every tail).
+int adapt_key_pass(const double* x, int64_t n, int b_r, const AdPlan& P, uint64_t* ck, int64_t cap, AdaptHdr* h,
+                   int32_t* err, cudaStream_t s) {
+  const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
+  if (b_r == 32) {
+    // candidate <=> (low32 << 3) - c8 < w8 (thresholds in [2^27, 2^28] here)
+    const uint32_t t = (uint32_t)(P.gL.thr < 0 ? 0 : (P.gL.thr > (1 << 28) ? (1 << 28) : P.gL.thr));
+    const uint32_t c8L = (t + 1u) << 3;
+    const uint32_t w8L = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
+    adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, P.g0, P.L_key, c8L, w8L, ck, cap, h, err);
+  } else {
+    adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, P.g0, P.L_key, P.gL.thr, ck, cap, h, err);
+  }
+  return vt_check_launch("adapt_keys_kernel");
+}
+
+TailArgs tail_args(const double* x, int64_t n, int64_t budget, int iters, const AdPlan& P, const AdPtrs& A,
+                   double* tau_out, int32_t* err) {
+  TailArgs ta{};
+  ta.x = x;
+  ta.g0 = P.g0;
+  ta.cw = A.cw;
+  ta.ck = A.ck;
+  ta.c2 = A.c2;
+  ta.ahist = A.ahist;
+  ta.h = A.h;
+  ta.cap = A.cap;
+  ta.budget = budget;
+  ta.n = n;
+  ta.L_key = P.L_key;
+  ta.lo_key = P.lo_key;
+  ta.hi_key = P.hi_key;
+  ta.s0 = P.s0;
+  ta.iters = iters;
+  ta.lower = P.lo;
+  ta.upper = P.hi;
+  ta.dthr = A.dthr;
+  ta.tau_out = tau_out;
+  ta.key = A.key;
+  ta.st = A.st;
+  ta.bhist = A.bhist;
+  ta.bcand = A.bcand;
+  ta.err = err;
+  return ta;
+}
+
+int launch_tail(TailArgs& ta, double want, cudaStream_t s) {
+  const int gmax = coop_grid(adapt_tail_kernel);
+  const int grid = (int)std::min<int64_t>(gmax, std::max<int64_t>(64, (int64_t)(want / 2048)));
+  void* args[] = {&ta};
+  cudaLaunchCooperativeKernel((const void*)adapt_tail_kernel, dim3(grid), dim3(kAdThreads), args, 0, s);
+  return vt_check_launch("adapt_tail_kernel");
+}
+
+__global__ void copy_key_kernel(const uint64_t* key, uint64_t* out) { *out = *key; }
+}  // namespace vt
+
 extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_t budget, int iters, int out_kind,
                                      void* out, uint64_t* sparse, int64_t sparse_cap, int64_t global_base,
                                      const int64_t* cursor_in, int64_t* cursor_out, double* tau_out,
@@ -1681,34 +1771,10 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
   const AdaptLayout lay = adapt_layout(n);
-  const AdPtrs P = adapt_ptrs(w, lay);
-  DevThr* dthr = P.dthr;
-  uint64_t* key = P.key;
-  AdaptHdr* h = P.h;
-  BudState* st = P.st;
-  uint32_t* bhist = P.bhist;
-  uint64_t* bcand = P.bcand;
+  const AdPtrs A = adapt_ptrs(w, lay);
   void* rws = w + lay.rl;
-  uint32_t* ahist = P.ahist;
-  uint64_t *cw = P.cw, *ck = P.ck, *c2 = P.c2;
   const bool fast = b_r == 32;
-  const double lo = 0x1p-25, hi = ldexp(1.0, 8 - b_r);
-  uint64_t lo_key, hi_key;
-  memcpy(&lo_key, &lo, 8);
-  memcpy(&hi_key, &hi, 8);
-  // candidate threshold: about kCandFactor x (budget + 1) elements above it
-  // when p is uniform on [0, hi] (the dropped bits of real data are)
-  const double want = (double)kCandFactor * (double)(budget + 1) + 1024.0;
-  double L = hi * (1.0 - want / (double)n);
-  if (!(L > lo)) L = lo;
-  uint64_t L_key;
-  memcpy(&L_key, &L, 8);
-  const uint64_t W = hi_key - L_key;  // key offsets 0 .. W - 1 above L
-  const int wbits = W > 1 ? 64 - __builtin_clzll(W - 1) : 1;
-  const int s0 = std::max(0, wbits - kAdBits);
-  const Grid gL = make_grid(b_r, L);
-  const int thrL = (int)std::min<int64_t>(std::max<int64_t>(gL.thr, 0), INT32_MAX);
-  const Grid g0 = make_grid(b_r, 0.0);
+  const AdPlan P = adapt_plan(n, b_r, budget);
 
   // In place (y overwrites x) the candidates' keys could not be gathered
   // after the rounding pass: their keys come from a read of x first.
@@ -1718,58 +1784,19 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
   int rc = 0;
   if (aliased) {
     // 1'. the candidates' x values (unordered) from one read of x
-    // h->ccount is 0 here: zero-filled workspace, reset by every tail
-    const unsigned kb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 148 * 8));
-    if (fast) {
-      // candidate <=> (low32 << 3) - c8 < w8 (thresholds in [2^27, 2^28] here)
-      auto cw8 = [](int64_t thr, uint32_t& c8, uint32_t& w8) {
-        const uint32_t t = (uint32_t)(thr < 0 ? 0 : (thr > (1 << 28) ? (1 << 28) : thr));
-        c8 = (t + 1u) << 3;
-        w8 = (t >= (1u << 28)) ? 0u : ((0x20000000u - 2u * t - 1u) << 3);
-      };
-      uint32_t c8L, w8L;
-      cw8(gL.thr, c8L, w8L);
-      adapt_keys32_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, c8L, w8L, ck, lay.cap, h, err);
-    } else {
-      adapt_keys_kernel<<<kb, kAdThreads, 0, s>>>(x, n, g0, L_key, gL.thr, ck, lay.cap, h, err);
-    }
-    if ((rc = vt_check_launch("adapt_keys_kernel"))) return rc;
+    if ((rc = adapt_key_pass(x, n, b_r, P, A.ck, lay.cap, A.h, err, s))) return rc;
   } else {
     // 1. rounding pass: y + candidate words (local index << 1 | up) with p > L
     // (and each candidate's x at its position in ck: the tail reads it there)
-    rc = rl_stream(x, n, gL, thrL, fast, out_kind, out, cw, lay.cap, 0, nullptr, &h->ccount, &h->scratch, err,
-                   rws, s, nullptr, nullptr, ck);
+    rc = rl_stream(x, n, P.gL, P.thrL, fast, out_kind, out, A.cw, lay.cap, 0, nullptr, &A.h->ccount, &A.h->scratch,
+                   err, rws, s, nullptr, nullptr, A.ck);
     if (rc) return rc;
   }
   // 2-4. one cooperative launch: selection of the (budget+1)-th largest p
   // among the candidates, bisection, and (out of place) the ordered log; or
   // the exact fallback when the candidates cannot decide
   {
-    TailArgs ta{};
-    ta.x = x;
-    ta.g0 = g0;
-    ta.cw = cw;
-    ta.ck = ck;
-    ta.c2 = c2;
-    ta.ahist = ahist;
-    ta.h = h;
-    ta.cap = lay.cap;
-    ta.budget = budget;
-    ta.n = n;
-    ta.L_key = L_key;
-    ta.lo_key = lo_key;
-    ta.hi_key = hi_key;
-    ta.s0 = s0;
-    ta.iters = iters;
-    ta.lower = lo;
-    ta.upper = hi;
-    ta.dthr = dthr;
-    ta.tau_out = tau_out;
-    ta.key = key;
-    ta.st = st;
-    ta.bhist = bhist;
-    ta.bcand = bcand;
-    ta.err = err;
+    TailArgs ta = tail_args(x, n, budget, iters, P, A, tau_out, err);
     if (!aliased) {
       ta.sparse = sparse;
       ta.sparse_cap = sparse_cap;
@@ -1778,15 +1805,40 @@ extern "C" int vt_round_log_adaptive(const double* x, int64_t n, int b_r, int64_
       ta.cursor_out = cursor_out;
       ta.counters = counters;
     }
-    const int gmax = coop_grid(adapt_tail_kernel);
-    const int grid = (int)std::min<int64_t>(gmax, std::max<int64_t>(64, (int64_t)(want / 2048)));
-    void* args[] = {&ta};
-    cudaLaunchCooperativeKernel((const void*)adapt_tail_kernel, dim3(grid), dim3(kAdThreads), args, 0, s);
-    if ((rc = vt_check_launch("adapt_tail_kernel"))) return rc;
+    if ((rc = launch_tail(ta, P.want, s))) return rc;
   }
   // the rounding pass at the device tau: always for in-place calls, else only after a fallback
-  return rl_stream(x, n, make_grid(b_r, lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
-                   cursor_out, counters, err, rws, s, dthr, aliased ? nullptr : &h->fallback);
+  return rl_stream(x, n, make_grid(b_r, P.lo), 0, fast, out_kind, out, sparse, sparse_cap, global_base, cursor_in,
+                   cursor_out, counters, err, rws, s, A.dthr, aliased ? nullptr : &A.h->fallback);
+}
+
+// The standalone budget search (protocol.search_tau_budget): the in-place
+// path's single read of x for the candidates' values, then the tail's
+// selection + FP64 bisection (the exact multi-pass fallback inside the same
+// cooperative launch when the candidates cannot decide).  No rounding pass.
+extern "C" size_t vt_tau_budget_workspace(int64_t n) { return adapt_layout_rl(n > 0 ? n : 1, 0).total; }
+
+extern "C" int vt_tau_budget(const double* x, int64_t n, int b_r, int64_t budget, int iters, double* tau_out,
+                             uint64_t* key_out, int32_t* err, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (n <= 0 || b_r < 10 || b_r > 32 || budget < 0 || iters < 0 || !tau_out || !ws ||
+      ws_bytes < vt_tau_budget_workspace(n) || reinterpret_cast<uintptr_t>(ws) % 256 ||
+      (reinterpret_cast<uintptr_t>(x) & 31)) {
+    vt_set_error("vt_tau_budget: bad argument (n > 0, 32-byte aligned x, 256-byte aligned workspace)");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const AdaptLayout lay = adapt_layout_rl(n, 0);
+  const AdPtrs A = adapt_ptrs(static_cast<uint8_t*>(ws), lay);
+  const AdPlan P = adapt_plan(n, b_r, budget);
+  int rc = adapt_key_pass(x, n, b_r, P, A.ck, lay.cap, A.h, err, s);
+  if (rc) return rc;
+  TailArgs ta = tail_args(x, n, budget, iters, P, A, tau_out, err);  // sparse == nullptr: select only
+  if ((rc = launch_tail(ta, P.want, s))) return rc;
+  if (key_out) {
+    copy_key_kernel<<<1, 1, 0, s>>>(A.key, key_out);
+    return vt_check_launch("copy_key_kernel");
+  }
+  return 0;
 }
 
 

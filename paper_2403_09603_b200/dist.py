@@ -15,10 +15,11 @@ path shards naturally:
   pass histogram summed over the ranks (``ncclAllReduce``, 64 KiB) before
   every rank makes the same selection (``search_tau_budget_sharded``).
 * Merkle: leaves are grouped in blocks of 2^K; each rank hashes a
-  contiguous run of blocks and builds levels 0..K locally, all ranks
-  all-gather the block roots and build the top levels redundantly.  Every
-  node of ``merkle.build`` over the full leaf list is reproduced (the
-  promotion rule only acts at the right edge, which is the last rank's).
+  contiguous run of blocks and builds levels 0..K locally (fewer when the
+  whole tree fits one block), all ranks all-gather the block roots and build
+  the top levels redundantly.  Every level of ``merkle.build`` over the full
+  leaf list is reproduced, and no more (``assemble_levels``; the promotion
+  rule only acts at the right edge, which is the last rank's).
 
 The combination logic is pure host arithmetic over tensors (``*_plan`` /
 ``combine_*``) so it is unit-tested with the gloo backend on CPU; the
@@ -210,16 +211,25 @@ def leaf_block_range(n_leaves: int, rank: int, world: int, k: int = BLOCK_LEAVES
     return min(b_lo << k, n_leaves), min(b_hi << k, n_leaves)
 
 
-def local_levels(leaves: torch.Tensor, k: int, hash_level) -> list[torch.Tensor]:
-    """Levels 0..k over a run of whole 2^k blocks (the last may be partial,
-    in which case it is the global right edge and promotion applies)."""
+def local_depth(n_leaves_total: int, k: int = BLOCK_LEAVES_LOG2) -> int:
+    """Index of the highest level every rank builds locally: k, or the root's
+    level when the whole tree fits in one 2^k block (merkle.build stops at one
+    node, merkle.py:63-72)."""
+    if n_leaves_total <= 1:
+        return 0
+    return min(k, (n_leaves_total - 1).bit_length())
+
+
+def local_levels(leaves: torch.Tensor, depth: int, hash_level) -> list[torch.Tensor]:
+    """Levels 0..depth over a run of whole 2^k blocks (depth <= k).  A run
+    that shrinks to one node before ``depth`` is the global right edge (the
+    last, partial block), where merkle.build promotes the node unchanged, so
+    the node repeats up to ``depth``; an empty run gives empty levels."""
     levels = [leaves]
     cur = leaves
-    for _ in range(k):
-        if cur.shape[0] <= 1 and len(levels) > 1:
-            levels.append(cur)
-            continue
-        cur = hash_level(cur)
+    for _ in range(depth):
+        if cur.shape[0] > 1:
+            cur = hash_level(cur)
         levels.append(cur)
     return levels
 
@@ -234,26 +244,51 @@ def combine_top(block_roots: torch.Tensor, hash_level) -> list[torch.Tensor]:
     return levels
 
 
+def assemble_levels(per_rank_local: list[list], top: list) -> list:
+    """The full ``merkle.build`` level list from every rank's local levels (in
+    rank order) and the top levels: global level L <= depth is the rank-order
+    concatenation of local level L; top[0] repeats level depth (the block
+    roots), so the levels above are top[1:].  Works on lists of 32-byte
+    digests or on [m, 32] uint8 tensors."""
+    depth = len(per_rank_local[0]) - 1
+    out = []
+    for L in range(depth + 1):
+        parts = [lv[L] for lv in per_rank_local]
+        if isinstance(parts[0], torch.Tensor):
+            out.append(torch.cat(parts))
+        else:
+            out.append([d for p in parts for d in p])
+    return out + list(top[1:])
+
+
 def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes: int = 4096,
                    k: int = BLOCK_LEAVES_LOG2, group=None, hash_leaves=None, hash_level=None):
-    """Per-rank lower levels (0..k) + all-gathered block roots + top levels.
+    """Per-rank lower levels (0..depth) + all-gathered block roots + top levels.
 
-    Returns (local_levels, top_levels).  Global level L (L <= k) of the full
-    tree is the rank-order concatenation of every rank's local level L
-    (ranks own whole blocks); levels above k are the top levels.
+    Returns (local_levels, top_levels).  Every rank returns depth + 1 local
+    levels (``local_depth``: k, or fewer when the tree fits one block; empty
+    tensors on a rank that owns no leaves).  Global level L <= depth of the
+    full tree is the rank-order concatenation of every rank's local level L
+    (ranks own whole blocks); top_levels[0] are the block roots (= global
+    level depth) and the levels above it follow (``assemble_levels``).
     """
     if hash_leaves is None or hash_level is None:
         from . import merkle as mk
         hash_leaves = hash_leaves or (lambda b: mk.sha256_leaves(b, leaf_bytes))
         hash_level = hash_level or _device_level
     world = dist.get_world_size(group)
-    leaves = hash_leaves(w_local_bytes)
-    lv = local_levels(leaves, k, hash_level) if leaves.shape[0] else [leaves]
+    depth = local_depth(n_leaves_total, k)
+    leaves = hash_leaves(w_local_bytes) if w_local_bytes.numel() else None
+    if leaves is None or leaves.shape[0] == 0:
+        dev = w_local_bytes.device
+        lv = [torch.zeros((0, 32), dtype=torch.uint8, device=dev) for _ in range(depth + 1)]
+    else:
+        lv = local_levels(leaves, depth, hash_level)
     # each rank contributes its block roots; ranks own whole blocks, so the
     # number of roots per rank is known from the plan
     n_blocks = [(hi - lo + (1 << k) - 1) >> k
                 for lo, hi in (leaf_block_range(n_leaves_total, r, world, k) for r in range(world))]
-    mine = lv[-1] if leaves.shape[0] else leaves.new_zeros((0, 32))
+    mine = lv[-1]
     width = max(n_blocks)
     pad = torch.zeros((width, 32), dtype=torch.uint8, device=mine.device)
     pad[: mine.shape[0]] = mine

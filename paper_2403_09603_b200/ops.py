@@ -57,41 +57,80 @@ class PendingRound:
     words: torch.Tensor
     flags: D.Flags
 
-    def finish(self) -> tuple[torch.Tensor, SparseLog]:
-        err, cnt = self.flags.read()
+    def finish(self, err: int | None = None, cnt: list | None = None) -> tuple[torch.Tensor, SparseLog]:
+        if err is None:
+            err, cnt = self.flags.read()
         D.raise_fpround(err)
         if cnt[0] > self.words.numel():
             raise LogOverflow(f"sparse log needs {cnt[0]} words, capacity {self.words.numel()}")
         return self.y, SparseLog(self.words[: cnt[0]], cnt[0])
 
 
+def default_log_capacity(n: int) -> int:
+    """Default sparse-log capacity (words) when the caller passes no log_out:
+    1/8 of the elements (configs 0/1 log ~10%), at least 64 Ki words, at most
+    n.  With check=True a call whose log needs more is re-run once with the
+    exact size; with check=False finish() raises LogOverflow -- pass log_out
+    (up to n words) for inputs that may log more than 1/8."""
+    return max(1, min(n, max(n // 8, 1 << 16)))
+
+
+def _out_kind(out_dtype) -> int:
+    if out_dtype == torch.float32:
+        return _lib.OUT_F32
+    if out_dtype == torch.float64:
+        return _lib.OUT_F64
+    raise ValueError(f"out_dtype must be torch.float32 or torch.float64, got {out_dtype}")
+
+
 def round_and_log(x: torch.Tensor, b_r: int, tau: float, *, out_dtype=torch.float32,
                   global_base: int = 0, out: torch.Tensor | None = None,
                   log_out: torch.Tensor | None = None, codes_out: torch.Tensor | None = None,
-                  check: bool = True):
-    """Fused rnd + direction + stream compaction (one kernel launch)."""
+                  check: bool = True, workspace: torch.Tensor | None = None):
+    """Fused rnd + direction + stream compaction (one kernel launch).
+
+    Reentrant across streams and host threads: the call's scratch state lives
+    in a workspace keyed by the current stream (or the caller's
+    ``workspace``, a zero-initialised uint8 CUDA tensor of at least
+    ``vt_round_log_workspace(n)`` bytes used by one stream at a time)."""
     _check_b(b_r)
     D.require_cuda()
     shape = tuple(x.shape) if x.dim() else (1,)
     t = D.aligned_f64(x.reshape(-1))
     n = t.numel()
-    kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
+    kind = _out_kind(out_dtype)
+    D.check_out(out, n, out_dtype, t.device, "out")
+    D.check_out(log_out, 0, torch.int64, t.device, "log_out")
+    D.check_out(codes_out, n, torch.uint8, t.device, "codes_out")
     y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
-    words = log_out if log_out is not None else torch.empty(max(n, 1), dtype=torch.int64, device=t.device)
-    ws = D.workspace(int(_lib.lib().vt_round_log_workspace(n)), "round_log")
+    words = log_out if log_out is not None else torch.empty(default_log_capacity(n), dtype=torch.int64,
+                                                            device=t.device)
+    need = int(_lib.lib().vt_round_log_workspace(n))
+    ws = workspace if workspace is not None else D.workspace(need, "round_log")
+    D.check_out(ws, need, torch.uint8, t.device, "workspace")
     f = D.Flags()
     if n:
         _lib.call("vt_round_log", D.ptr(t), n, b_r, float(tau), kind, D.ptr(y),
                   D.ptr(words), words.numel(), int(global_base), None, None, D.ptr(codes_out),
                   None, 0, None, f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
     pending = PendingRound(y.reshape(shape) if out is None else y, words, f)
-    return pending.finish() if check else pending
+    if not check:
+        return pending
+    err, cnt = f.read()
+    if log_out is None and err == 0 and cnt[0] > words.numel():
+        # more entries than the default capacity: once more with the exact size
+        words = torch.empty(cnt[0], dtype=torch.int64, device=t.device)
+        return round_and_log(x, b_r, tau, out_dtype=out_dtype, global_base=global_base, out=out,
+                             log_out=words, codes_out=codes_out, check=True, workspace=workspace)
+    return pending.finish(err, cnt)
 
 
 def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtype=torch.float32,
            global_base: int = 0, out: torch.Tensor | None = None, strict: bool = True,
-           check: bool = True):
-    """Fused rev with a sparse log; returns (y, corrections)."""
+           check: bool = True, workspace: torch.Tensor | None = None):
+    """Fused rev with a sparse log; returns (y, corrections).  Reentrant
+    across streams (workspace keyed by the current stream, or the caller's
+    zeroed ``workspace`` of ``vt_replay_workspace(n)`` bytes)."""
     _check_b(b_r)
     D.require_cuda()
     words = log.words if isinstance(log, SparseLog) else log
@@ -99,9 +138,14 @@ def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtyp
     shape = tuple(x.shape) if x.dim() else (1,)
     t = D.aligned_f64(x.reshape(-1))
     n = t.numel()
-    kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
+    kind = _out_kind(out_dtype)
+    D.check_out(out, n, out_dtype, t.device, "out")
+    if words.dtype != torch.int64 or words.device != t.device:
+        raise ValueError("log words must be an int64 tensor on the input's device")
     y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
-    ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "replay")
+    need = int(_lib.lib().vt_replay_workspace(n))
+    ws = workspace if workspace is not None else D.workspace(need, "replay")
+    D.check_out(ws, need, torch.uint8, t.device, "workspace")
     f = D.Flags()
     if n:
         _lib.call("vt_replay", D.ptr(t), n, b_r, _lib.LOG_SPARSE, D.ptr(words), words.numel(),
@@ -139,7 +183,8 @@ class PendingAdaptive:
 def round_and_log_adaptive(x: torch.Tensor, b_r: int, budget: int, *, iters: int = 30,
                            out_dtype=torch.float32, global_base: int = 0, out: torch.Tensor | None = None,
                            log_out: torch.Tensor | None = None, check: bool = True, tag: str = "adaptive",
-                           tau_out: torch.Tensor | None = None, flags_out: torch.Tensor | None = None):
+                           tau_out: torch.Tensor | None = None, flags_out: torch.Tensor | None = None,
+                           workspace: torch.Tensor | None = None):
     """Per-tensor adaptive threshold + round-and-log, all on the device.
 
     tau = protocol.search_tau_budget(x, b_r, budget, iters) (bit-identical:
@@ -153,11 +198,17 @@ def round_and_log_adaptive(x: torch.Tensor, b_r: int, budget: int, *, iters: int
     shape = tuple(x.shape) if x.dim() else (1,)
     t = D.aligned_f64(x.reshape(-1))
     n = t.numel()
-    kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
+    kind = _out_kind(out_dtype)
+    D.check_out(out, n, out_dtype, t.device, "out")
+    D.check_out(log_out, 0, torch.int64, t.device, "log_out")
+    D.check_out(tau_out, 1, torch.float64, t.device, "tau_out")
+    D.check_out(flags_out, 6, torch.int64, t.device, "flags_out")
     y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
     words = log_out if log_out is not None else torch.empty(max(budget + 1, 1), dtype=torch.int64, device=t.device)
     tau = tau_out if tau_out is not None else torch.empty(1, dtype=torch.float64, device=t.device)
-    ws = D.workspace(int(_lib.lib().vt_round_log_adaptive_workspace(n)), tag)
+    need = int(_lib.lib().vt_round_log_adaptive_workspace(n))
+    ws = workspace if workspace is not None else D.workspace(need, tag)
+    D.check_out(ws, need, torch.uint8, t.device, "workspace")
     f = D.Flags(buf=flags_out)
     if n:
         _lib.call("vt_round_log_adaptive", D.ptr(t), n, b_r, int(budget), int(iters), kind, D.ptr(y), D.ptr(words),
@@ -215,8 +266,13 @@ def round_and_log_adaptive_batch(xs, b_r: int, budgets, *, iters: int = 30, out_
     for name, seq in (("global_bases", global_bases), ("outs", outs), ("log_outs", log_outs)):
         if seq is not None and len(seq) != m:
             raise ValueError(f"{name}: one entry per tensor")
-    kind = _lib.OUT_F32 if out_dtype == torch.float32 else _lib.OUT_F64
+    kind = _out_kind(out_dtype)
     flat = [D.aligned_f64(x.reshape(-1)) for x in xs]
+    for i in range(m):
+        if outs is not None:
+            D.check_out(outs[i], flat[i].numel(), out_dtype, dev, f"outs[{i}]")
+        if log_outs is not None:
+            D.check_out(log_outs[i], 0, torch.int64, dev, f"log_outs[{i}]")
     ys = list(outs) if outs is not None else [torch.empty(t.numel(), dtype=out_dtype, device=dev) for t in flat]
     words = list(log_outs) if log_outs is not None else [
         torch.empty(max(b + 1, 1), dtype=torch.int64, device=dev) for b in budgets]
@@ -236,9 +292,10 @@ def round_and_log_adaptive_batch(xs, b_r: int, budgets, *, iters: int = 30, out_
         # per-tensor state sits at offsets set by the batch's sizes: a new
         # size signature starts from a zeroed workspace
         sig = (ws.data_ptr(), tuple(ns))
-        if _BATCH_SIG.get((torch.cuda.current_device(), tag)) != sig:
+        key = (torch.cuda.current_device(), D.stream_ptr(), tag)
+        if _BATCH_SIG.get(key) != sig:
             ws.zero_()
-            _BATCH_SIG[(torch.cuda.current_device(), tag)] = sig
+            _BATCH_SIG[key] = sig
         _lib.call("vt_round_log_adaptive_batch", C.cast(segs, C.c_void_p), len(live), b_r, int(iters), kind,
                   D.ptr(ws), ws.numel(), D.stream_ptr())
     for i in range(m):
@@ -334,12 +391,13 @@ def round_and_log_replay_host(xt_h: torch.Tensor, xa_h: torch.Tensor, b_r: int, 
     # own staging buffers while the host waits for the trainer's log length
     pipes = []
     for side in ("trainer", "auditor"):
-        key = (dev.index, chunk, side)
+        key = (dev.index, D.stream_ptr(), chunk, side)  # per calling stream: reentrant like the operators
         if key not in _PIPES:
             _PIPES[key] = _HostPipe(chunk, dev)
         pipes.append(_PIPES[key])
     pipe, pipe_a = pipes
-    words = D.workspace(8 * max(n // 4, 1024), "host_log").view(torch.int64)
+    # the device log holds as many words as the caller's host log can take
+    words = D.workspace(8 * max(min(int(log_h.numel()), n), 1024), "host_log").view(torch.int64)
     n_chunks = (n + chunk - 1) // chunk
     cursors = torch.zeros(n_chunks + 1, dtype=torch.int64, device=dev)
     ws_rl = [D.workspace(int(_lib.lib().vt_round_log_workspace(chunk)), f"hp_rl{k}") for k in range(2)]

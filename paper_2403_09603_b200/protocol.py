@@ -190,32 +190,28 @@ def kth_largest_distance(x, b_r: int, rank: int) -> float:
     return float(np.array([key.item()], dtype=np.int64).view(np.float64)[0])
 
 
-def budget_key(x, b_r: int, budget: int) -> float:
-    """v' = the (budget+1)-th largest p, clamped for a bisection strictly inside
-    tau_bounds(b_r) (two-pass device select; exact 5-pass select as fallback)."""
+def _budget_select(x, b_r: int, budget: int, iters: int) -> tuple[float, float]:
+    """(tau, v'): ``vt_tau_budget`` -- one streaming read of x for the
+    candidates above a threshold below the expected tau, then the exact
+    selection of the (budget+1)-th largest p among them and the FP64
+    bisection on the device (exact multi-pass fallback in the same launch)."""
     _check_b(b_r)
     lower, upper = tau_bounds(b_r)
     t, _, _ = D.to_device_f64(x)
     n = t.numel()
-    if budget >= n:
-        return lower
-    ws = D.workspace(int(_lib.lib().vt_tau_workspace(n)), "tau")
-    out = torch.zeros(2, dtype=torch.int64, device=t.device)  # [key, status]
+    if n == 0 or budget >= n:  # every tau is feasible: v' = tau_lo
+        return _bisect(lower, lower, upper, iters), lower
+    ws = D.workspace(int(_lib.lib().vt_tau_budget_workspace(n)), "tau_budget")
+    out = torch.empty(2, dtype=torch.float64, device=t.device)  # [tau, key bits]
     f = D.Flags()
-    _lib.call("vt_tau_budget_key", D.ptr(t), n, b_r, int(budget), lower, upper, D.ptr(out),
-              out.data_ptr() + 8, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
-    key, status = out.tolist()
+    _lib.call("vt_tau_budget", D.ptr(t), n, b_r, int(budget), int(iters), D.ptr(out), out.data_ptr() + 8,
+              f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
+    tau, key = out.tolist()
     D.raise_fpround(f.read()[0])
-    if (status & 0xFFFFFFFF) != 1:
-        return kth_largest_distance(x, b_r, int(budget))
-    return float(np.array([key], dtype=np.int64).view(np.float64)[0])
+    return tau, key
 
 
-def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
-    """Per-tensor adaptive threshold: the search_tau skeleton with predicate
-    count(p > tau) <= budget, feasible -> upper = tau, returns ``upper``."""
-    lower, upper = tau_bounds(b_r)
-    v = budget_key(x, b_r, int(budget))
+def _bisect(v: float, lower: float, upper: float, iters: int) -> float:
     for _ in range(iters):
         tau = (lower + upper) / 2.0
         if v <= tau:
@@ -223,6 +219,19 @@ def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
         else:
             lower = tau
     return upper
+
+
+def budget_key(x, b_r: int, budget: int) -> float:
+    """v' = the (budget+1)-th largest p, clamped for a bisection strictly inside
+    tau_bounds(b_r): tau_lo if v <= tau_lo, +inf if v > tau_hi, else v."""
+    return _budget_select(x, b_r, int(budget), 30)[1]
+
+
+def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
+    """Per-tensor adaptive threshold: the search_tau skeleton with predicate
+    count(p > tau) <= budget, feasible -> upper = tau, returns ``upper``
+    (bisection on the device, bit-identical to the host FP64 loop)."""
+    return _budget_select(x, b_r, int(budget), int(iters))[0]
 
 
 __all__ = ["AuditFailure", "GpuAuditorChannel", "GpuPlainChannel", "GpuTrainerChannel",

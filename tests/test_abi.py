@@ -80,6 +80,7 @@ BAD_CALLS = [
     ("vt_log_histogram", (None, -1, None, None, None)),
     ("vt_tau_kth_key", (None, -1, 32, 0, None, None, None, 0, None)),
     ("vt_tau_budget_key", (None, 10, 32, -1, 0.1, 0.2, None, None, None, None, 0, None)),
+    ("vt_tau_budget", (None, 10, 32, -1, 30, None, None, None, None, 0, None)),
     ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
                                None)),
     ("vt_round_log_adaptive_batch", (None, 0, 32, 30, 1, None, 0, None)),
@@ -133,3 +134,26 @@ def test_adaptive_batch_validates_segments_on_the_host():
         assert lib.vt_round_log_adaptive_batch(C.cast(arr, C.c_void_p), 1, 32, 30, 1, fake, 1 << 40, None) == \
             _lib.VT_EINVAL
         assert what in lib.vt_last_error().decode()
+
+
+def test_out_buffer_validation_host_logic():
+    """Caller buffers reach the C ABI as raw pointers; check_out rejects a wrong
+    dtype, a short or strided buffer and the wrong device before any call."""
+    import torch
+    from paper_2403_09603_b200 import _device as D
+    cpu = torch.device("cpu")
+    D.check_out(None, 10, torch.float32, cpu)
+    D.check_out(torch.empty(10), 10, torch.float32, cpu)
+    D.check_out(torch.empty(12), 10, torch.float32, cpu)
+    for t, dev in ((torch.empty(10, dtype=torch.float64), cpu), (torch.empty(9), cpu),
+                   (torch.empty(20)[::2], cpu), (torch.empty(10), torch.device("meta")), ([0.0] * 10, cpu)):
+        with pytest.raises(ValueError):
+            D.check_out(t, 10, torch.float32, dev)
+
+
+def test_default_log_capacity_bound():
+    from paper_2403_09603_b200 import ops
+    assert ops.default_log_capacity(0) == 1
+    assert ops.default_log_capacity(1000) == 1000
+    assert ops.default_log_capacity(1 << 20) == 1 << 17
+    assert ops.default_log_capacity(1 << 30) == 1 << 27  # 1 GiB of words at 2^30, not 8 GiB

@@ -69,27 +69,29 @@ def _worker(rank: int, world: int, port: int, q) -> None:
             placed[off:off + len(w)] = np.array(w, dtype=np.uint64)
         ok_log = bool(np.array_equal(placed, full)) and int(counts.sum()) == full.size
 
-        # --- Merkle: whole 2^k-leaf blocks per rank, all-gathered block roots
-        k = 3
-        w32 = np.random.default_rng(9).normal(0, 0.02, size=123_457).astype(np.float32)
-        data = w32.tobytes()
-        leaf_bytes = 4096
-        nl = (len(data) + leaf_bytes - 1) // leaf_bytes
-        l0, l1 = vd.leaf_block_range(nl, rank, world, k)
-        mine = torch.frombuffer(bytearray(data[l0 * leaf_bytes: min(len(data), l1 * leaf_bytes)]),
-                                dtype=torch.uint8)
-        lv, top = vd.merkle_sharded(mine, nl, leaf_bytes, k, hash_leaves=lambda b: _sha_leaves(b, leaf_bytes),
-                                    hash_level=_sha_level)
-        ref = O.merkle_levels(O.chunk_leaves(data, leaf_bytes))
-        all_lv = [None] * world
-        dist.all_gather_object(all_lv, [[bytes(r) for r in t.numpy()] for t in lv])
+        # --- Merkle: whole 2^k-leaf blocks per rank, all-gathered block roots;
+        # the assembled level list equals merkle.build's, level for level
         ok_tree = True
-        for L in range(min(k + 1, len(ref))):
-            got = [d for r in range(world) if L < len(all_lv[r]) for d in all_lv[r][L]]
-            ok_tree &= got == ref[L]
-        tops = [[bytes(r) for r in t.numpy()] for t in top]
-        ok_tree &= tops == ref[k:] if len(ref) > k else True
+        for n_floats, k in ((123_457, 3), (100 * 1024, 12), (1024, 3), (9 * 1024 + 5, 3), (17 * 1024, 2)):
+            w32 = np.random.default_rng(9).normal(0, 0.02, size=n_floats).astype(np.float32)
+            data = w32.tobytes()
+            leaf_bytes = 4096
+            nl = (len(data) + leaf_bytes - 1) // leaf_bytes
+            l0, l1 = vd.leaf_block_range(nl, rank, world, k)
+            raw = data[l0 * leaf_bytes: min(len(data), l1 * leaf_bytes)]
+            mine = torch.frombuffer(bytearray(raw), dtype=torch.uint8) if raw else torch.zeros(0, dtype=torch.uint8)
+            lv, top = vd.merkle_sharded(mine, nl, leaf_bytes, k,
+                                        hash_leaves=lambda b: _sha_leaves(b, leaf_bytes), hash_level=_sha_level)
+            ref = O.merkle_levels(O.chunk_leaves(data, leaf_bytes))
+            all_lv = [None] * world
+            dist.all_gather_object(all_lv, [[bytes(r) for r in t.numpy()] for t in lv])
+            tops = [[bytes(r) for r in t.numpy()] for t in top]
+            ok_tree &= vd.assemble_levels(all_lv, tops) == ref
+            ok_tree &= len(lv) == vd.local_depth(nl, k) + 1
         q.put((rank, ok_log, ok_tree, (lo, hi)))
+    except Exception as e:  # surface the error instead of leaving the parent waiting
+        q.put((rank, False, repr(e), (0, 0)))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -104,10 +106,10 @@ def test_sharded_log_and_merkle_gloo(world):
         p.start()
     for p in procs:
         p.join(timeout=240)
-    res = sorted(q.get() for _ in range(world))
+    res = sorted((q.get() for _ in range(world)), key=lambda r: r[0])
     for rank, ok_log, ok_tree, rng in res:
         assert ok_log, (rank, rng)
-        assert ok_tree, rank
+        assert ok_tree is True, (rank, ok_tree)
     assert res[0][3][1] == res[1][3][0] and res[0][3][0] == 0
 
 

@@ -492,15 +492,10 @@ def config2() -> dict:
     import torch
 
     from paper_2403_09603_b200 import ops, protocol, workloads
-    shapes = workloads.resnet50_tensors()
-    sig = workloads.config2_sigmas(len(shapes))
-    g = torch.Generator(device="cuda")
-    g.manual_seed(2)
-    xs = [torch.randn(int(np.prod(s)), dtype=torch.float64, device="cuda", generator=g) * float(sig[i])
-          for i, (_, s) in enumerate(shapes)]
+    xs = workloads.config2_tensors_torch()
     total = sum(x.numel() for x in xs)
     ys = torch.empty(total, dtype=torch.float32, device="cuda")
-    budgets = [int(0.005 * x.numel()) for x in xs]
+    budgets = workloads.config2_budgets([x.numel() for x in xs])
     words = torch.empty(sum(budgets) + len(xs), dtype=torch.int64, device="cuda")
     state = {}
 
@@ -635,11 +630,9 @@ def config4_merkle() -> dict:
     import torch
 
     from paper_2403_09603_b200 import _device as D
-    from paper_2403_09603_b200 import _lib, merkle
-    g = torch.Generator(device="cuda")
-    g.manual_seed(4)
-    n = 1_500_000_000
-    w = torch.randn(n, device="cuda", generator=g) * 0.02
+    from paper_2403_09603_b200 import _lib, merkle, workloads
+    n = workloads.CONFIG4_PARAMS
+    w = workloads.config4_weights_torch(n)
     ms = _time(lambda: merkle.merkle_chunked(w), reps=3, warm=1)
     t = merkle.merkle_chunked(w)
     sizes = [int(l.shape[0]) for l in t.levels_device]

@@ -314,6 +314,36 @@ def search_tau_budget(x, b_r: int, budget: int, iters: int = 30) -> float:
     return hi
 
 
+def kth_largest(p, k: int) -> float:
+    """The (k+1)-th largest value of p (k 0-based from the top), by
+    np.partition: the order statistic the budget predicate reduces to,
+    count(p > tau) <= k  <=>  kth_largest(p, k) <= tau."""
+    a = np.asarray(p, dtype=np.float64).reshape(-1)
+    return float(np.partition(a, a.size - 1 - k)[a.size - 1 - k])
+
+
+def bisect_budget(v, b_r: int, iters: int = 30) -> float:
+    """The search_tau skeleton (protocol.py:494-506 bounds and midpoint) on the
+    order-statistic predicate v <= tau; v None = no element can exceed the
+    budget (n <= budget): every tau is feasible.  Returns ``upper``."""
+    lo, hi = tau_bounds(b_r)
+    for _ in range(iters):
+        t = (lo + hi) / 2.0
+        if v is None or v <= t:
+            hi = t
+        else:
+            lo = t
+    return hi
+
+
+def search_tau_budget_kth(x, b_r: int, budget: int, iters: int = 30) -> float:
+    """search_tau_budget through the order statistic (one np.partition instead
+    of ``iters`` counting passes); equal to it bit for bit
+    (tests/test_oracle_golden.py checks the two against each other)."""
+    p = normalized_distance(x, b_r).reshape(-1)
+    return bisect_budget(kth_largest(p, budget) if p.size > budget else None, b_r, iters)
+
+
 # --------------------------------------------------------------------------
 # Merkle  (reference: pkg/src/vtrain/merkle.py)
 # --------------------------------------------------------------------------

@@ -129,7 +129,9 @@ class RoundAndLogHooks:
         out = {"tensors": m, "elements": sum(r.numel for r in records),
                "logged": sum(counts), "fwd": sum(1 for r in records if r.kind == "fwd"),
                "bwd": sum(1 for r in records if r.kind == "bwd"),
-               "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None}
+               "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None,
+               "taus": taus, "counts": counts,
+               "calls": [(r.name, r.kind, r.numel, r.budget) for r in records]}
         if keep_logs:
             out["logs"] = [(r.name, r.kind, self._logs[r.slot][:c].clone()) for r, c in zip(records, counts)]
         return out

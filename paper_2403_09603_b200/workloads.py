@@ -158,6 +158,36 @@ def config2_sigmas(n_tensors: int, seed: int = 2) -> np.ndarray:
     return 10.0 ** np.random.default_rng(seed).uniform(-3.0, 1.0, size=n_tensors)
 
 
+def config2_tensors_torch(device="cuda") -> list:
+    """The 161 configs[2] FP64 tensors exactly as bench.py times them: shapes of
+    ``resnet50_tensors`` (flattened), x ~ N(0, sigma_t) drawn in order from one
+    torch generator seeded 2 on ``device``."""
+    import torch
+    shapes = resnet50_tensors()
+    sig = config2_sigmas(len(shapes))
+    g = torch.Generator(device=device)
+    g.manual_seed(2)
+    return [torch.randn(int(np.prod(s)), dtype=torch.float64, device=device, generator=g) * float(sig[i])
+            for i, (_, s) in enumerate(shapes)]
+
+
+def config2_budgets(sizes) -> list[int]:
+    """B_t = floor(0.005 n_t)."""
+    return [int(0.005 * int(n)) for n in sizes]
+
+
+CONFIG4_PARAMS = 1_500_000_000
+
+
+def config4_weights_torch(n: int = CONFIG4_PARAMS, device="cuda"):
+    """configs[4]: n FP32 weights ~ N(0, 0.02) from a torch generator seeded 4
+    (the bench's exact bits)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(4)
+    return torch.randn(n, device=device, generator=g) * 0.02
+
+
 def _torch_bracket(v):
     import torch
     f = v.float()

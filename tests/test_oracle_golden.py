@@ -207,3 +207,52 @@ def test_oracle_replays_reference_channel_traces(oracle, name):
     assert hashlib.sha256(oracle.vtrl_bytes(codes_all, m["b_r"])).hexdigest() == m["vtrl_sha"]
     if name == "trend":
         assert sum(m["corrections"]) == 77
+
+
+def test_order_statistic_budget_search_equals_counting_search(oracle):
+    """search_tau_budget_kth (np.partition, used at full BASELINE sizes) is the
+    counting bisection of search_tau_budget, bit for bit, incl. budget >= n,
+    budget 0, ties and magnitudes across the FP32 range."""
+    from paper_2403_09603_b200 import workloads
+    rng = np.random.default_rng(123)
+    cases = [rng.normal(0, 10.0 ** s, size=n) for s, n in ((-3, 5000), (0, 20_001), (1, 777))]
+    cases += [workloads.config0_x(30_000, 5), np.full(4096, 1.0 + 0.4 * 2.0 ** -23),
+              (rng.integers(1 << 23, 1 << 24, size=3000) + 0.5) * 2.0 ** -23, np.zeros(0)]
+    for b_r in (32, 26):
+        for x in cases:
+            for B in sorted({0, 1, 17, int(0.005 * x.size), x.size // 3, x.size, x.size + 5}):
+                assert oracle.search_tau_budget_kth(x, b_r, B) == oracle.search_tau_budget(x, b_r, B), (b_r, x.size, B)
+
+
+def test_parallel_oracle_driver(oracle):
+    """vt_parallel (the chunked, all-cores driver of the full-size GPU parity
+    tests) agrees with the sequential oracle, and detects a flipped bit."""
+    import vt_parallel as P
+    from paper_2403_09603_b200 import workloads
+    n = 300_007
+    xt, xa = workloads.config1_pair(n, 77)
+    tau = workloads.TAU_CONFIG0
+    codes = oracle.direction_array(xt, 32, tau)
+    words = oracle.sparse_from_codes(codes, base=1000)
+    yt = oracle.rnd_array(xt, 32).astype(np.float32)
+    ya = oracle.rev_array(xa, 32, codes).astype(np.float32)
+    r = P.check_round_and_log(xt, 32, tau, words, yt, xa, ya, base=1000, chunk=1 << 15, procs=4)
+    assert r["n_log"] == r["words"] == words.size
+    assert r["log_mismatches"] == r["yt_mismatches"] == r["ya_mismatches"] == 0
+    assert r["corrections"] == int(np.count_nonzero(ya != oracle.rnd_array(xa, 32).astype(np.float32)))
+    ya2 = ya.copy()
+    ya2[123_456] = np.nextafter(ya2[123_456], np.float32(np.inf))
+    words2 = words.copy()
+    words2[5] ^= np.uint64(1)
+    r2 = P.check_round_and_log(xt, 32, tau, words2, yt, xa, ya2, base=1000, chunk=1 << 15, procs=4)
+    assert r2["ya_mismatches"] == 1 and r2["ya_first_bad"] == 123_456 and r2["log_mismatches"] == 1
+    # exact top-k over chunks == the sequential order-statistic search
+    xs = [np.random.default_rng(s).normal(0, 10.0 ** (s - 3), size=m) for s, m in ((1, 100_000), (2, 5), (3, 70_001))]
+    Bs = [500, 5, 350]
+    assert P.search_tau_budget_many(xs, 32, Bs, chunk=1 << 14, procs=4) == \
+        [oracle.search_tau_budget(x, 32, B) for x, B in zip(xs, Bs)]
+    # Merkle levels over all cores == merkle.build over the chunked leaves
+    w = np.random.default_rng(4).normal(0, 0.02, size=1_000_003).astype(np.float32)
+    lv = P.merkle_levels_bytes(w, 4096, procs=4)
+    ref = oracle.merkle_levels(oracle.chunk_leaves(w.tobytes(), 4096))
+    assert [b"".join(level) for level in ref] == lv

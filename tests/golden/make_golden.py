@@ -364,7 +364,37 @@ def golden_channel_traces() -> None:
     (HERE / "channel_traces.json").write_text(json.dumps(meta))
 
 
+def golden_live_runs() -> None:
+    """Appendix C of SURVEY.md, frozen from the real reference here: full
+    ``train`` + ``audit`` runs (trainer profile of the config, auditor
+    ``pairwise``) of every shipped config -- root, audit root, .vtrl digest,
+    entry count, direction histogram, total corrections.  The GPU test
+    tests/test_gpu_protocol_live.py runs ``protocol._run`` unmodified with the
+    GPU channels and must reproduce them."""
+    from vtrain.cli import load_config
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name in ("tiny", "mlp", "logreg", "trend"):
+            cfg = load_config(Path("/root/reference/pkg/configs") / f"{name}.json")
+            log = Path(td) / f"{name}.vtrl"
+            t = pr.train(cfg, log)
+            a = pr.audit(cfg, "pairwise", log)
+            r = rl.LogReader(log)
+            out[name] = {"root": t.root.hex(), "audit_root": a.root.hex(), "vtrl_sha": sha(log.read_bytes()),
+                         "entries": int(t.entries_logged), "histogram": {str(k): int(v) for k, v in r.histogram().items()},
+                         "corrections": int(a.total_corrections), "steps": len(t.per_step),
+                         "b_r": cfg.b_r, "trainer_profile": cfg.trainer_profile,
+                         "cpu_train_s_here": round(t.seconds, 3), "cpu_audit_s_here": round(a.seconds, 3)}
+    (HERE / "live_runs.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
+    import sys as _sys
+    if "--live-only" in _sys.argv:
+        golden_live_runs()
+        raise SystemExit(0)
+    golden_live_runs()
     golden_channel_traces()
     golden_fpround()
     golden_errors()

@@ -122,16 +122,79 @@ def dist_env():
     return world, rank, local
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> None:
+    """``--gpus N`` without a launcher: re-execute this command under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1,
+    NCCL_DEBUG=INFO for the INIT lines that show the communicator's nranks)
+    and exit with its status.  Under the driver's torchrun (WORLD_SIZE set)
+    this does nothing."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def _graph(fn, stream):
+    """Capture fn (already warmed on ``stream``) into a CUDA graph on that stream."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
+
+
+def run_harness_check(args) -> None:
+    """CPU self-test of the launcher path (no GPU, no kernels; tests only):
+    gloo ranks, the barrier + max-over-ranks timing and rank 0's single JSON
+    line with n_gpus = world size.  Its value is not a measurement."""
+    import torch
+    import torch.distributed as dist
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    for _ in range(args.warmup + args.steps):
+        torch.ones(1024).sum()
+    ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
+    t = torch.tensor([ms], dtype=torch.float64)
+    ranks = torch.tensor([1], dtype=torch.int64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ranks)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world,
+                          "ranks_reporting": int(ranks.item()), "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(float(t.item()), 4), "harness_check": True}), flush=True)
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
-    from paper_2403_09603_b200 import _lib, ops, workloads
+    from paper_2403_09603_b200 import ops, workloads
     from paper_2403_09603_b200 import dist as vdist
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # under a launcher (WORLD_SIZE set, even 1) the NCCL path runs: process
+    # group, count all-gather captured in the step's graph, max over ranks
+    ddp = "WORLD_SIZE" in os.environ
+    if ddp:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     n = 1 << args.log2n
@@ -141,90 +204,95 @@ def run_ours(args) -> None:
     y_t = torch.empty(n, dtype=torch.float32, device=dev)
     y_a = torch.empty(n, dtype=torch.float32, device=dev)
     words = torch.empty(n // 4, dtype=torch.int64, device=dev)
+    counts = torch.empty(max(world, 1), dtype=torch.int64, device=dev)
+    stream = torch.cuda.Stream(dev)  # every operator runs (and is captured) on this stream
+    stream.wait_stream(torch.cuda.current_stream(dev))
 
-    # the auditor receives the log with its length (as a file carries it);
-    # take it from one untimed trainer pass
-    p0 = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
-    _, log0 = p0.finish()
+    with torch.cuda.stream(stream):
+        # the auditor receives the log with its length (as a file carries it);
+        # take it from one untimed trainer pass
+        p0 = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+        _, log0 = p0.finish()
     count = log0.count
     log_words = words[:count]
+    state = {}
 
     def trainer():
-        return ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+        state["p"] = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+
+    def exchange():
+        if ddp:  # the exchange step: all-gather of per-rank log counts (device-resident)
+            vdist._all_gather_flat(counts, state["p"].flags.buf[2:3])
 
     def auditor():
-        return ops.replay(xa, 32, log_words, out=y_a, global_base=base, check=False)[1]
+        state["fa"] = ops.replay(xa, 32, log_words, out=y_a, global_base=base, check=False)[1]
 
-    def exchange(p):
-        if world > 1:  # the exchange step: all-gather of per-rank log counts
-            vdist.all_gather_counts(p.flags.buf[2:3])
+    def step():
+        trainer()
+        exchange()
+        auditor()
 
-    for _ in range(args.warmup):
-        p = trainer()
-        exchange(p)
-        fl = auditor()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
     torch.cuda.synchronize()
     # verify once (outside the timed region): auditor output == trainer output, no errors
-    err_t, cnt_t = p.flags.read()
-    err_a, cnt_a = fl.read()
+    err_t, cnt_t = state["p"].flags.read()
+    err_a, cnt_a = state["fa"].read()
     assert err_t == 0 and err_a == 0 and cnt_t[0] == count, (err_t, err_a, cnt_t, count)
     ok_equal = bool(torch.equal(y_t.view(torch.int32), y_a.view(torch.int32)))
 
-    # Each operator is captured once into a CUDA graph (its kernels + flag
-    # resets); the timed loop replays the graphs, so host launch latency does
-    # not leak into the device timeline.
+    # The step (both operators and, at N > 1, the NCCL count all-gather between
+    # them) is captured once into CUDA graphs on `stream`; the timed loop
+    # replays them, so host launch latency does not leak into the timeline.
     graphs = None
     if not args.no_graph:
-        g_t, g_a = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream(dev)
-        s.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(s):
-            trainer()
-            auditor()
-        torch.cuda.current_stream(dev).wait_stream(s)
-        torch.cuda.synchronize()
-        with torch.cuda.graph(g_t):
-            pg = trainer()
-        with torch.cuda.graph(g_a):
-            flg = auditor()
-        g_t.replay()
-        g_a.replay()
-        torch.cuda.synchronize()
-        assert pg.flags.read()[1][0] == count and flg.read()[0] == 0
-        graphs = (g_t, g_a, pg)
+        try:
+            g_t = _graph(lambda: (trainer(), exchange()), stream)
+            pg = state["p"]
+            g_a = _graph(auditor, stream)
+            flg = state["fa"]
+            with torch.cuda.stream(stream):
+                g_t.replay()
+                g_a.replay()
+            torch.cuda.synchronize()
+            assert pg.flags.read()[1][0] == count and flg.read()[0] == 0
+            graphs = (g_t, g_a)
+        except Exception as e:  # e.g. a communicator that cannot be captured: eager steps
+            print(f"[bench] graph capture failed, timing eager steps: {e!r}", file=sys.stderr)
+            torch.cuda.synchronize()
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
+    if ddp:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(local) as clk, torch.cuda.stream(stream):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
+        t0.record(stream)
         for i in range(args.steps):
-            starts[i].record()
+            starts[i].record(stream)
             if graphs:
                 graphs[0].replay()
-                mids[i].record()
-                exchange(graphs[2])
+                mids[i].record(stream)
                 graphs[1].replay()
             else:
-                p = trainer()
-                mids[i].record()
-                exchange(p)
+                trainer()
+                exchange()
+                mids[i].record(stream)
                 auditor()
-            ends[i].record()
-        t1.record()
+            ends[i].record(stream)
+        t1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
+    if ddp:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
     rl_ms = statistics.mean(starts[i].elapsed_time(mids[i]) for i in range(args.steps))
     rp_ms = statistics.mean(mids[i].elapsed_time(ends[i]) for i in range(args.steps))
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
+    if ddp:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -234,16 +302,37 @@ def run_ours(args) -> None:
     rl_bytes = n * (8 + 4 + 8 * f)
     rp_bytes = n * (8 + 4 + 8 * f)
     peak, peak_src = peaks()
+    del xt, xa
+    torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, n, tau, base, dev, world)
 
+    strong = None
+    if args.extras or ddp:
+        strong = strong_scaling(args, world, rank, dev)
+
+    extras = None
+    if args.extras and world == 1:
+        extras = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
+                  "vtrl_codec_2^26": vtrl_codec(26),
+                  "configs[2]_resnet50_budget": config2(),
+                  "configs[3]_gpt2_fp64_step": config3_gpt2(),
+                  "configs[4]_merkle_1.5B": config4_merkle(),
+                  "budget_search_standalone": budget_search(),
+                  "f2_reference_loop_trend": f2_trend()}
+
+    cpu = cpu_extra = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args)
+        if args.extras:
+            cpu_extra = cpu_legs()
+    if ddp:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
         return
-    cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(args)
     rl_ach = rl_bytes / (rl_ms * 1e-3) / 1e9
     rp_ach = rp_bytes / (rp_ms * 1e-3) / 1e9
     line = {
@@ -264,7 +353,8 @@ def run_ours(args) -> None:
                    "n_per_gpu": n, "logged_fraction": round(f, 6), "parallelism": f"dp{world} (contiguous shards)",
                    "l2": "no flush: every step streams 2 x 512 MiB of FP64 (>= 4x the 126 MB L2)",
                    "auditor_equals_trainer_bitwise": ok_equal,
-                   "launch": "cuda graphs (one per operator)" if graphs else "eager"},
+                   "launch": ("cuda graphs (trainer + count all-gather, auditor)" if ddp else
+                              "cuda graphs (one per operator)") if graphs else "eager"},
         "roofline": {"bound": "hbm",
                      "kernel": "round-and-log op: rl_fused_kernel (single pass: TMA-pipelined rnd + direction + "
                                "ballot staging, in-kernel decoupled look-back, final log words)",
@@ -280,21 +370,15 @@ def run_ours(args) -> None:
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    if strong is not None:
+        line["strong_scaling"] = strong
     if args.sweep:
         line["sweep"] = sweep(args.sweep)
-    if args.extras and world == 1:
-        line["extras"] = {"configs[4]_size_sweep": sweep([20, 24, 26, 28, 30, 32]),
-                          "vtrl_codec_2^26": vtrl_codec(26),
-                          "configs[2]_resnet50_budget": config2(),
-                          "configs[3]_gpt2_fp64_step": config3_gpt2(),
-                          "configs[4]_merkle_1.5B": config4_merkle()}
-        if not args.no_cpu:
-            cores = len(os.sched_getaffinity(0))
-            line["extras"]["configs[4]_merkle_1.5B"]["cpu_baseline"] = cpu_merkle(1 << 16, cores)
-            line["extras"]["configs[2]_resnet50_budget"]["cpu_baseline"] = cpu_adaptive(1 << 22)
+    if extras is not None:
+        if cpu_extra is not None:
+            extras["cpu_legs"] = cpu_extra
+        line["extras"] = extras
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 def run_e2e(args, n, tau, base, dev, world: int = 1):
@@ -643,123 +727,304 @@ def config4_merkle() -> dict:
     blocks, reps = 148 * 32, 64
     pk_ms = _time(lambda: _lib.call("vt_sha256_peak_bench", D.ptr(sink), blocks, reps, D.stream_ptr()), reps=3)
     peak_cps = blocks * 128 * reps / (pk_ms * 1e-3)
+    # independent denominator: the SHF/LOP3/IADD3 mix on register-only chains
+    mix_blocks, mix_reps = 148 * 16, 4096
+    mix_ms = _time(lambda: _lib.call("vt_int_mix_peak_bench", D.ptr(sink), mix_blocks, mix_reps, D.stream_ptr()),
+                   reps=3)
+    mix_ops = mix_blocks * 256 * mix_reps * int(_lib.lib().vt_int_mix_ops_per_thread_rep()) / (mix_ms * 1e-3)
     cps = comps / (ms * 1e-3)
     return {"params": n, "leaves": int(leaves), "hashed_internal_nodes": int(nodes), "levels": len(sizes),
             "ms": round(ms, 3), "hashed_gbs": round(n * 4 / ms / 1e6, 1),
             "compressions_per_s": round(cps / 1e9, 3), "unit_cps": "G compressions/s",
             "int_ops_per_s": round(cps * 1400 / 1e12, 2), "unit_ops": "T int ops/s (analytic 1400 / compression)",
-            "sha256_compute_ceiling_cps": round(peak_cps / 1e9, 3),
-            "frac_of_sha256_int_peak": round(cps / peak_cps, 4),
-            "peak_note": "ceiling = the same compress() on register-resident messages (vt_sha256_peak_bench)",
+            "int_mix_peak_ops_per_s": round(mix_ops / 1e12, 2),
+            "frac_of_sha256_int_peak": round(cps * 1400 / mix_ops, 4),
+            "peak_note": "denominator = int_mix_peak_kernel: register-only SHF/LOP3/IADD3 chains in the SHA-256 op "
+                         "mix (6:4:4), not compress(); numerator = compressions/s x 1400 analytic ops",
+            "sha256_compress_ceiling_cps": round(peak_cps / 1e9, 3),
+            "frac_of_compress_ceiling": round(cps / peak_cps, 4),
             "root": t.root_hex[:16]}
 
 
-# ---------------------------------------------------------------------------
-# CPU: the reference algorithm (oracle port) on the host cores
-# ---------------------------------------------------------------------------
+def budget_search() -> dict:
+    """The standalone budget search (protocol.search_tau_budget ->
+    vt_tau_budget: one read of x + the cooperative selection / bisection) at
+    2^26 and 2^30 N(0,1) elements, 0.5% budget; algorithmic bytes = 8 per
+    element (one read of x).  The sharded form's exact 5-pass select
+    (dist.kth_largest_distance_sharded, one rank) is timed beside it."""
+    import torch
 
-def _cpu_chunk(args):
-    lo, hi, seed = args
-    sys.path.insert(0, str(REPO / "oracle"))
-    import numpy as np
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, protocol
+    from paper_2403_09603_b200 import dist as vdist
+    peak, _ = peaks()
+    out = {}
+    for lg in (26, 30):
+        n = 1 << lg
+        g = torch.Generator(device="cuda")
+        g.manual_seed(lg)
+        x = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+        B = int(0.005 * n)
+        ws = D.workspace(int(_lib.lib().vt_tau_budget_workspace(n)), "bench_tau")
+        res = torch.empty(2, dtype=torch.float64, device="cuda")
+        fl = D.Flags()
 
-    import vt_oracle as O
-    from paper_2403_09603_b200 import workloads
-    n = hi - lo
-    xt, xa = workloads.config1_pair(n, seed)
-    tau = workloads.TAU_CONFIG0
-    t0 = time.perf_counter()
-    # trainer channel (protocol.py:198-202): direction + rnd + pack
-    codes = O.direction_array(xt, 32, tau)
-    O.rnd_array(xt, 32)
-    O.pack_groups(np.concatenate([codes, np.ones((-codes.size) % 5, np.uint8)]))
-    # auditor channel (protocol.py:212-216): rev + rnd for the correction count
-    ya = O.rev_array(xa, 32, codes)
-    int(np.count_nonzero(ya != O.rnd_array(xa, 32)))
-    dt = time.perf_counter() - t0
-    return n, int(np.count_nonzero(codes != 1)), dt
+        def run():
+            _lib.call("vt_tau_budget", D.ptr(x), n, 32, B, 30, D.ptr(res), res.data_ptr() + 8, fl.err_ptr, D.ptr(ws),
+                      ws.numel(), D.stream_ptr())
 
-
-def cpu_measure(total: int, chunk: int, procs: int):
-    import multiprocessing as mp
-    jobs = [(i * chunk, min(total, (i + 1) * chunk), 100 + i) for i in range((total + chunk - 1) // chunk)]
-    t0 = time.perf_counter()
-    if procs > 1:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_cpu_chunk, jobs)
-    else:
-        res = [_cpu_chunk(j) for j in jobs]
-    wall = time.perf_counter() - t0
-    n = sum(r[0] for r in res)
-    logged = sum(r[1] for r in res)
-    compute = sum(r[2] for r in res)
-    f = logged / n
-    # input generation is excluded: the timed region is the reference calls,
-    # spread perfectly over the processes (compute / procs)
-    eff = compute / max(1, min(procs, len(jobs)))
-    gbs = n * (8 + 4 + 8 * f) * 2 / eff / 1e9
-    return {"gbs": gbs, "n": n, "wall_s": wall, "compute_s": compute, "eff_s": eff, "f": f}
+        ms = _time(run, reps=10)
+        tau = float(res[0].item())
+        assert tau == protocol.search_tau_budget(x, 32, B)
+        ms5 = _time(lambda: vdist.ShardedKth(x, 32).local_hist(0), reps=5)  # one of the 5 exact passes
+        out[f"2^{lg}"] = {"ms": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1), "frac": round(8 * n / ms / 1e6 / peak, 4),
+                          "tau_over_2^-24": round(tau / 2.0 ** -24, 6),
+                          "sharded_exact_select_pass_ms": round(ms5, 4),
+                          "sharded_exact_select_5_passes_ms_est": round(5 * ms5, 4)}
+        del x, ws
+        torch.cuda.empty_cache()
+    out["kernels"] = "adapt_keys32_kernel (candidate values, one read of x) + adapt_tail_kernel (cooperative selection, " \
+                     "device FP64 bisection)"
+    return out
 
 
-def _cpu_leaf_chunk(args):
-    lo, hi, leaf = args
+def f2_trend() -> dict:
+    """the reference's own loop (vtrain.protocol._run, unmodified,
+    from baseline/_ref) on the shipped ``trend`` config, trainer then auditor,
+    with the reference's NumPy channels and with the GPU channels in the seam;
+    wall time of each run and of the channel calls inside it (a timing proxy
+    around process()).  Roots / .vtrl / corrections must agree."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "vtrain" / "protocol.py").exists():
+        return {"skipped": "reference not installed (tools/install_reference.sh)"}
     import hashlib
+    import tempfile
+    sys.path.insert(0, str(ref))
+    from vtrain import cli
+    from vtrain import protocol as pr
+    from vtrain import roundlog as rrl
 
+    from paper_2403_09603_b200 import protocol as gp
+    from paper_2403_09603_b200 import roundlog
+
+    class Timed:
+        def __init__(self, inner):
+            self.inner, self.s, self.calls = inner, 0.0, 0
+
+        def process(self, values, tau):
+            t0 = time.perf_counter()
+            r = self.inner.process(values, tau)
+            self.s += time.perf_counter() - t0
+            self.calls += 1
+            return r
+
+    cfg = cli.load_config(ref / "vtrain_configs" / "trend.json")
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for side, W, R, T, A in (("reference_numpy", rrl.LogWriter, rrl.LogReader, pr._TrainerChannel,
+                                  pr._AuditorChannel),
+                                 ("gpu", roundlog.LogWriter, roundlog.LogReader, gp.GpuTrainerChannel,
+                                  gp.GpuAuditorChannel)):
+            log = Path(td) / f"{side}.vtrl"
+            w = W(log, cfg.b_r)
+            tc = Timed(T(w, cfg.b_r))
+            t0 = time.perf_counter()
+            tree_t, *_ = pr._run(cfg, pr.get_profile(cfg.trainer_profile), tc, False)
+            w.close()
+            t1 = time.perf_counter()
+            ac = Timed(A(R(log), cfg.b_r))
+            tree_a, _, _, per_step, _, _ = pr._run(cfg, pr.get_profile("pairwise"), ac, False)
+            t2 = time.perf_counter()
+            out[side] = {"train_s": round(t1 - t0, 3), "audit_s": round(t2 - t1, 3),
+                         "train_channel_s": round(tc.s, 3), "audit_channel_s": round(ac.s, 3), "calls": tc.calls,
+                         "root": tree_t.root.hex()[:16], "audit_root": tree_a.root.hex()[:16],
+                         "vtrl_sha": hashlib.sha256(log.read_bytes()).hexdigest()[:16],
+                         "corrections": int(sum(s.forward_corrections + s.backward_corrections for s in per_step))}
+    r, g = out["reference_numpy"], out["gpu"]
+    out["same_results"] = all(r[k] == g[k] for k in ("root", "audit_root", "vtrl_sha", "corrections"))
+    out["speedup_train_audit"] = round((r["train_s"] + r["audit_s"]) / (g["train_s"] + g["audit_s"]), 3)
+    out["speedup_channels"] = round((r["train_channel_s"] + r["audit_channel_s"]) /
+                                    (g["train_channel_s"] + g["audit_channel_s"]), 3)
+    return out
+
+
+def strong_scaling(args, world: int, rank: int, dev) -> dict:
+    """Strong-scaling legs (fixed total work over the N ranks),
+    device-timed with a barrier on both sides, max over ranks:
+      * the 2^32 size-sweep point: round-and-log + count all-gather + replay
+        over contiguous shards (dist.shard_range; global indices);
+      * configs[4]: the 1.5e9-parameter Merkle tree, whole 2^12-leaf blocks
+        per rank + block-root all-gather + top levels (dist.merkle_sharded);
+        its root is checked equal to the single-GPU root;
+      * configs[2]: the 161 ResNet-50 tensors LPT-assigned to ranks, each rank
+        one batched adaptive call; taus checked against the single-GPU batch."""
     import numpy as np
-    w = np.random.default_rng(lo).normal(0.0, 0.02, size=(hi - lo) * leaf // 4).astype("<f4").tobytes()
-    t0 = time.perf_counter()
-    out = [hashlib.sha256(w[i:i + leaf]).digest() for i in range(0, len(w), leaf)]
-    return out, time.perf_counter() - t0
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_09603_b200 import merkle, ops, workloads
+    from paper_2403_09603_b200 import dist as vdist
+
+    def tmax(ms: float) -> float:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if dist.is_initialized():
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, reps: int) -> float:
+        fn()
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+        return tmax(s.elapsed_time(e) / reps)
+
+    out = {"n_gpus": world, "scaling": "strong"}
+    peak, _ = peaks()
+    # --- 2^32 round-and-log + replay, sharded
+    total = 1 << 32
+    lo, hi = vdist.shard_range(total, rank, world)
+    n = hi - lo
+    x = workloads.config0_x_torch_bernoulli(n, seed=32 + rank, device=dev)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    ya = torch.empty(n, dtype=torch.float32, device=dev)
+    words = torch.empty(n // 8 + 4096, dtype=torch.int64, device=dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    tau = workloads.TAU_CONFIG0
+    st = {}
+
+    def rl():
+        st["p"] = ops.round_and_log(x, 32, tau, out=y, log_out=words, global_base=lo, check=False)
+        if dist.is_initialized():
+            vdist._all_gather_flat(counts, st["p"].flags.buf[2:3])
+
+    rl()
+    _, log = st["p"].finish()
+    lw = words[:log.count]
+
+    def rp():
+        ops.replay(x, 32, lw, out=ya, global_base=lo, check=False)
+
+    ms_rl, ms_rp = timed(rl, 4), timed(rp, 4)
+    logged = torch.tensor([log.count], dtype=torch.int64, device=dev)
+    if dist.is_initialized():
+        dist.all_reduce(logged)
+    f = int(logged.item()) / total
+    b = total * (8 + 4 + 8 * f)
+    out["round_log_replay_2^32"] = {"round_log_ms": round(ms_rl, 3), "replay_ms": round(ms_rp, 3),
+                                     "round_log_gbs": round(b / ms_rl / 1e6, 1), "replay_gbs": round(b / ms_rp / 1e6, 1),
+                                     "pair_gbs": round(2 * b / (ms_rl + ms_rp) / 1e6, 1),
+                                     "frac_per_gpu": round(2 * b / (ms_rl + ms_rp) / 1e6 / peak / world, 4),
+                                     "logged_fraction": round(f, 5)}
+    del x, y, ya, words, lw, log, st
+    torch.cuda.empty_cache()
+    # --- configs[4] Merkle, sharded by whole 2^12-leaf blocks
+    nparam = workloads.CONFIG4_PARAMS
+    n_leaves = (nparam * 4 + 4095) // 4096
+    l0, l1 = vdist.leaf_block_range(n_leaves, rank, world)
+    p0, p1 = l0 * 1024, min(nparam, l1 * 1024)
+    w = workloads.config4_weights_torch(nparam, device=dev, lo=p0, hi=p1) if p1 > p0 else \
+        torch.empty(0, device=dev)
+    wb = w.view(torch.uint8)
+    res = {}
+
+    def mk():
+        res["lv"], res["top"] = vdist.merkle_sharded(wb, n_leaves)
+
+    ms_m = timed(mk, 3)
+    root = bytes(res["top"][-1][0].cpu().numpy())
+    del w, wb, res
+    torch.cuda.empty_cache()
+    same = None
+    if rank == 0:  # the single-GPU tree over the whole checkpoint (untimed)
+        wall = workloads.config4_weights_torch(nparam, device=dev)
+        same = merkle.merkle_chunked(wall).root == root
+        del wall
+        torch.cuda.empty_cache()
+    out["merkle_1.5B"] = {"ms": round(ms_m, 3), "hashed_gbs": round(nparam * 4 / ms_m / 1e6, 1),
+                          "root": root.hex()[:16], "root_equals_single_gpu": same}
+    # --- configs[2], LPT over ranks
+    xs = workloads.config2_tensors_torch(device=dev)
+    sizes = [t.numel() for t in xs]
+    budgets = workloads.config2_budgets(sizes)
+    owner = vdist.lpt_assign(sizes, world)
+    mine = [i for i in range(len(xs)) if owner[i] == rank]
+    mx = [xs[i] for i in mine]
+    mb = [budgets[i] for i in mine]
+    ys = [torch.empty(t.numel(), dtype=torch.float32, device=dev) for t in mx]
+    lws = [torch.empty(B + 1, dtype=torch.int64, device=dev) for B in mb]
+    r2 = {}
+
+    def c2():
+        r2["b"] = ops.round_and_log_adaptive_batch(mx, 32, mb, outs=ys, log_outs=lws, check=False)
+
+    ms_c2 = timed(c2, 3)
+    taus = torch.zeros(len(xs), dtype=torch.float64, device=dev)
+    if mine:
+        taus[torch.tensor(mine, device=dev)] = r2["b"].taus
+    if dist.is_initialized():
+        dist.all_reduce(taus)
+    same2 = None
+    if rank == 0 and dist.is_initialized():
+        full = ops.round_and_log_adaptive_batch(xs, 32, budgets, check=False)
+        same2 = bool(torch.equal(full.taus, taus))
+    out["configs[2]_lpt"] = {"ms": round(ms_c2, 3), "elements": int(sum(sizes)),
+                             "g_elements_per_s": round(sum(sizes) / ms_c2 / 1e6, 2),
+                             "max_rank_elements": int(max(np.bincount(owner, weights=sizes, minlength=world))),
+                             "taus_equal_single_gpu": same2}
+    del xs, mx, ys, lws, r2
+    torch.cuda.empty_cache()
+    return out
 
 
-def cpu_merkle(n_leaves: int, procs: int, leaf: int = 4096) -> dict:
-    """Reference Merkle path on the host: hashlib (OpenSSL) SHA-256 of each
-    4 KiB leaf over all cores, then merkle.build's levels (one process)."""
-    import multiprocessing as mp
-    sys.path.insert(0, str(REPO / "oracle"))
-    import vt_oracle as O
-    per = (n_leaves + procs - 1) // procs
-    jobs = [(i * per, min(n_leaves, (i + 1) * per), leaf) for i in range(procs) if i * per < n_leaves]
-    with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_leaf_chunk, jobs)
-    leaves = [d for r in res for d in r[0]]
-    hash_s = max(r[1] for r in res)
-    t0 = time.perf_counter()
-    O.merkle_levels(leaves)
-    build_s = time.perf_counter() - t0
-    return {"value": round(n_leaves * leaf / (hash_s + build_s) / 1e9, 3), "unit": "GB/s hashed",
-            "cores": procs, "kind": "port", "sample": f"{n_leaves} leaves of {leaf} B (hashlib over {procs} "
-                                                       f"processes, then the level build)"}
+# ---------------------------------------------------------------------------
+# CPU: the reference algorithm on the host cores (BASELINE.md §2)
+#
+# The reference's own functions (vtrain 0.1.0 from baseline/_ref, installed
+# by tools/install_reference.sh) when present -- kind "reference" -- else the
+# oracle port of them (oracle/vt_oracle.py) -- kind "port".  Inputs are
+# generated before the timed region and shared with a forked process pool
+# (copy-on-write, no pickling); every timing is same-run WALL clock around the
+# pool's map (the pool is started and warmed first), at P = 1 and P = all
+# host cores, with the core count and CPU model stated.
+# ---------------------------------------------------------------------------
+
+_CPU: dict = {}
 
 
-def cpu_adaptive(n: int) -> dict:
-    """Reference budget search + trainer channel on one host core: the
-    oracle's search_tau_budget (bisection on the exact order statistic) then
-    direction_array + rnd_array at that tau, on one N(0,1) tensor."""
-    import numpy as np
-    sys.path.insert(0, str(REPO / "oracle"))
-    import vt_oracle as O
-    x = np.random.default_rng(2).normal(0.0, 1.0, n)
-    t0 = time.perf_counter()
-    tau = O.search_tau_budget(x, 32, int(0.005 * n))
-    O.direction_array(x, 32, tau)
-    O.rnd_array(x, 32)
-    dt = time.perf_counter() - t0
-    return {"value": round(n / dt / 1e9, 4), "unit": "G elements/s", "cores": 1, "kind": "port",
-            "sample": f"one tensor of {n} elements"}
+class _Impl:
+    """direction_array / rnd_array / rev_array / exponent_scale_array / pack."""
+
+    def __init__(self):
+        ref = REPO / "baseline" / "_ref"
+        if (ref / "vtrain" / "fpround.py").exists():
+            sys.path.insert(0, str(ref))
+            from vtrain import fpround as F
+            from vtrain import roundlog as R
+            self.direction_array, self.rnd_array, self.rev_array = F.direction_array, F.rnd_array, F.rev_array
+            self.exponent_scale_array, self.pack = F.exponent_scale_array, R._pack_block
+            self.kind = "reference"
+            self.what = "vtrain 0.1.0 functions (baseline/_ref, unmodified)"
+        else:
+            sys.path.insert(0, str(REPO / "oracle"))
+            import vt_oracle as O
+            self.direction_array, self.rnd_array, self.rev_array = O.direction_array, O.rnd_array, O.rev_array
+            self.exponent_scale_array, self.pack = O.exponent_scale_array, O.pack_groups
+            self.kind = "port"
+            self.what = "oracle/vt_oracle.py (NumPy restatement of the reference functions)"
 
 
-def cpu_baseline(args):
-    cores = len(os.sched_getaffinity(0))
-    total = 1 << args.cpu_log2n
-    r = cpu_measure(total, 1 << 20, cores)
-    r1 = cpu_measure(1 << 22, 1 << 20, 1)
-    return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": cores, "kind": "port",
-            "value_1core": round(r1["gbs"], 4),
-            "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair (trainer channel: direction_array + "
-                      f"rnd_array + pack; auditor: rev_array + rnd_array count), chunks of 2^20 over "
-                      f"{cores} processes, wall {r['wall_s']:.1f}s",
-            "cpu_model": _cpu_model()}
+def _impl() -> _Impl:
+    if "impl" not in _CPU:
+        _CPU["impl"] = _Impl()
+    return _CPU["impl"]
 
 
 def _cpu_model() -> str:
@@ -772,18 +1037,201 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def _pool(procs: int):
+    import multiprocessing as mp
+    pool = mp.get_context("fork").Pool(procs)
+    pool.map(abs, range(4 * procs))  # workers up before any timing
+    return pool
+
+
+def _timed_map(fn, jobs, procs: int):
+    """(results, wall seconds): in process for P = 1, else a warmed pool."""
+    if procs <= 1:
+        t0 = time.perf_counter()
+        res = [fn(j) for j in jobs]
+        return res, time.perf_counter() - t0
+    with _pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(fn, jobs)
+        wall = time.perf_counter() - t0
+    return res, wall
+
+
+def _pair_job(job):
+    """The trainer channel (protocol.py:198-202: direction_array, write_array's
+    _pack_block, rnd_array) and the auditor channel (protocol.py:212-216:
+    rev_array, rnd_array for the correction count) on one chunk."""
+    import numpy as np
+    lo, hi = job
+    F = _impl()
+    xt, xa = _CPU["xt"][lo:hi], _CPU["xa"][lo:hi]
+    tau = _CPU["tau"]
+    codes = F.direction_array(xt, 32, tau)
+    F.pack(np.concatenate([codes, np.ones((-codes.size) % 5, np.uint8)]))
+    F.rnd_array(xt, 32)
+    ya = F.rev_array(xa, 32, codes)
+    corr = int(np.count_nonzero(ya != F.rnd_array(xa, 32)))
+    return hi - lo, int(np.count_nonzero(codes != 1)), corr
+
+
+def cpu_pair(total: int, procs: int, chunk: int = 1 << 22, seed: int = 100) -> dict:
+    """configs[1] pair over ``total`` elements: GB/s of the step's algorithmic
+    bytes (both channels, the GPU formula) over the same-run wall clock."""
+    from paper_2403_09603_b200 import workloads
+    xt, xa = workloads.config1_pair(total, seed)
+    _CPU.update(xt=xt, xa=xa, tau=workloads.TAU_CONFIG0)
+    jobs = [(lo, min(total, lo + chunk)) for lo in range(0, total, chunk)]
+    try:
+        res, wall = _timed_map(_pair_job, jobs, procs)
+    finally:
+        for k in ("xt", "xa"):
+            _CPU.pop(k, None)
+    n = sum(r[0] for r in res)
+    f = sum(r[1] for r in res) / n
+    return {"gbs": n * (8 + 4 + 8 * f) * 2 / wall / 1e9, "n": n, "wall_s": wall, "f": f, "procs": procs}
+
+
+def _budget_job(job):
+    """Budget search (the search_tau skeleton of protocol.py:494-506
+    with predicate count(p > tau) <= B on the exact p = |x - rnd(x)| /
+    max(scale, 2^-126), fpround.py:171-173) then the trainer channel at tau."""
+    import numpy as np
+    i = job
+    F = _impl()
+    x = _CPU["tensors"][i]
+    B = int(0.005 * x.size)
+    r = F.rnd_array(x, 32)
+    p = np.abs(x - r) / np.maximum(F.exponent_scale_array(x), 2.0 ** -126)
+    lo, hi = 2.0 ** -25, 2.0 ** -24
+    for _ in range(30):
+        t = (lo + hi) / 2.0
+        if int(np.count_nonzero(p > t)) <= B:
+            hi = t
+        else:
+            lo = t
+    codes = F.direction_array(x, 32, hi)
+    F.pack(np.concatenate([codes, np.ones((-codes.size) % 5, np.uint8)]))
+    F.rnd_array(x, 32)
+    return x.size, int(np.count_nonzero(codes != 1))
+
+
+def cpu_budget(sizes: list[int], procs: int, seed: int) -> dict:
+    """Per-tensor budget search + round-and-log over independent tensors
+    (one tensor per job), x ~ N(0, sigma_t), sigma_t log-uniform [1e-3, 10]."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    _CPU["tensors"] = [rng.standard_normal(int(n)) * 10.0 ** rng.uniform(-3, 1) for n in sizes]
+    try:
+        res, wall = _timed_map(_budget_job, list(range(len(sizes))), procs)
+    finally:
+        _CPU.pop("tensors", None)
+    n = sum(r[0] for r in res)
+    return {"elements": n, "wall_s": round(wall, 3), "g_elements_per_s": round(n / wall / 1e9, 5), "procs": procs}
+
+
+def _leaf_job(job):
+    import hashlib
+    lo, hi = job
+    raw, lb = _CPU["w"], 4096
+    return b"".join(hashlib.sha256(raw[i * lb:(i + 1) * lb]).digest() for i in range(lo, hi))
+
+
+def cpu_merkle(n_leaves: int, procs: int) -> dict:
+    """hashlib (OpenSSL, the reference's SHA-256, merkle.py:24-25) over 4 KiB
+    leaves of FP32 N(0, 0.02) weights on ``procs`` processes, then the level
+    build of merkle.build (merkle.py:55-72) in one process; wall clock."""
+    import hashlib
+
+    import numpy as np
+    _CPU["w"] = memoryview(np.random.default_rng(4).normal(0.0, 0.02, size=n_leaves * 1024).astype("<f4")).cast("B")
+    per = max(1, n_leaves // (4 * max(procs, 1)))
+    jobs = [(lo, min(n_leaves, lo + per)) for lo in range(0, n_leaves, per)]
+    try:
+        res, wall = _timed_map(_leaf_job, jobs, procs)
+    finally:
+        _CPU.pop("w", None)
+    leaves = b"".join(res)
+    t0 = time.perf_counter()
+    cur = [leaves[i:i + 32] for i in range(0, len(leaves), 32)]
+    while len(cur) > 1:
+        nxt = [hashlib.sha256(cur[i] + cur[i + 1]).digest() for i in range(0, len(cur) - 1, 2)]
+        if len(cur) % 2:
+            nxt.append(cur[-1])
+        cur = nxt
+    wall += time.perf_counter() - t0
+    return {"gbs_hashed": round(n_leaves * 4096 / wall / 1e9, 4), "wall_s": round(wall, 3), "procs": procs,
+            "leaves": n_leaves}
+
+
+def _cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(args) -> dict:
+    """The headline's cpu_baseline: the configs[1] pair at P = all (bounded
+    sample of 2^cpu_log2n elements) and P = 1 (2^22 elements)."""
+    cores = _cores()
+    F = _impl()
+    r = cpu_pair(1 << args.cpu_log2n, cores)
+    r1 = cpu_pair(1 << 22, 1)
+    return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": cores, "kind": F.kind,
+            "value_1core": round(r1["gbs"], 4),
+            "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair in 2^22 chunks over {cores} processes "
+                      f"(P=1: 2^22 elements in process); trainer channel: direction_array + _pack_block + rnd_array; "
+                      f"auditor: rev_array + rnd_array count; same-run wall clock {r['wall_s']:.2f}s / "
+                      f"{r1['wall_s']:.2f}s; {F.what}",
+            "cpu_model": _cpu_model()}
+
+
+def cpu_legs() -> dict:
+    """CPU rows for the other configs, P = 1 and P = all."""
+    import numpy as np
+
+    from paper_2403_09603_b200 import workloads
+    cores = _cores()
+    F = _impl()
+    out = {"cores": cores, "cpu_model": _cpu_model(), "kind": F.kind, "functions": F.what}
+    shapes = [int(np.prod(s)) for _, s in workloads.resnet50_tensors()]
+    sample = shapes[::8]  # every 8th of the 161 tensors (1/8 of the elements, all layer kinds)
+    c2 = cpu_budget(sample, cores, 2)
+    c2_1 = cpu_budget([1 << 22], 1, 2)
+    out["configs[2]_budget_round_log"] = {
+        "P_all": c2, "P_1": c2_1, "unit": "G elements/s",
+        "sample": f"{len(sample)} of the 161 ResNet-50 tensors (every 8th, {sum(sample)} elements), one tensor per "
+                  f"process; P=1: one 2^22-element tensor",
+        "sweep_s_extrapolated_P_all": round(1_052_589_312 / (c2["g_elements_per_s"] * 1e9), 2)}
+    # GPT-2 small, batch 8 x 1024: the hooked tensors' sizes (d = 768, 4d MLP)
+    d_act, mlp_act = 8 * 1024 * 768, 8 * 1024 * 3072
+    sample3 = [d_act] * 12 + [mlp_act] * 4
+    c3 = cpu_budget(sample3, cores, 3)
+    c3_1 = cpu_budget([d_act], 1, 3)
+    out["configs[3]_gpt2_hooked_trainer_channel"] = {
+        "P_all": c3, "P_1": c3_1, "unit": "G elements/s",
+        "sample": "16 hooked-tensor shapes of the GPT-2-small step (12 x 8x1024x768, 4 x 8x1024x3072), budget "
+                  "search + trainer channel each; P=1: one 8x1024x768 tensor",
+        "step_s_extrapolated_P_all": round(2.55e9 / (c3["g_elements_per_s"] * 1e9), 2)}
+    m_all = cpu_merkle(1 << 18, cores)
+    m_1 = cpu_merkle(1 << 15, 1)
+    out["configs[4]_merkle"] = {"P_all": m_all, "P_1": m_1, "unit": "GB/s hashed",
+                                "sample": "2^18 leaves (1 GiB) at P=all, 2^15 leaves at P=1; hashlib leaves + "
+                                          "merkle.build levels",
+                                "tree_s_extrapolated_P_all": round(6e9 / (m_all["gbs_hashed"] * 1e9), 2)}
+    return out
+
+
 def run_reference(args) -> None:
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
+    cores = _cores()
+    F = _impl()
     total = 1 << args.cpu_log2n
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_measure(1 << 20, 1 << 20, 1)
+    for _ in range(min(args.warmup, 1)):
+        cpu_pair(1 << 20, 1)
     vals = []
     t_all = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_measure(total, 1 << 20, cores))
+        vals.append(cpu_pair(total, cores))
     wall = time.perf_counter() - t_all
     gbs = statistics.mean(v["gbs"] for v in vals)
     ms = wall / args.steps * 1e3
@@ -797,8 +1245,8 @@ def run_reference(args) -> None:
                                f"b_r=32, tau=0x1.ff7ced916872bp-25",
                    "n_per_gpu": 1 << args.log2n, "parallelism": f"{cores} host processes",
                    "sample": f"each step times a bounded sample of 2^{args.cpu_log2n} elements of that pair"},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"2^{args.cpu_log2n} elements per step in 2^20 chunks",
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": F.kind,
+                         "sample": f"2^{args.cpu_log2n} elements per step in 2^22 chunks, wall clock; {F.what}",
                          "cpu_model": _cpu_model()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -819,10 +1267,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-extras", dest="extras", action="store_false",
-                    help="skip configs[2], configs[4] and the 2^20..2^32 size sweep (run by default at N=1)")
+                    help="skip the configs[2]/[3]/[4] extras, the size sweep and the strong-scaling legs at N=1")
+    ap.add_argument("--harness-check", action="store_true",
+                    help="CPU self-test of the multi-rank launcher (gloo, no kernels; tests only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    if args.impl == "reference":
+    maybe_spawn(args)
+    if args.harness_check:
+        run_harness_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -264,6 +264,15 @@ int vt_serialize_f32(const double *x, int64_t n, float *out, int64_t index_base,
 /* measurement support: blocks x 128 threads x reps compressions of
  * register-resident messages (compute-only SHA-256 ceiling of this chip) */
 int vt_sha256_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t stream);
+/*
+ * Integer-pipe peak independent of compress(): register-only chains of the
+ * SHA-256 op mix (6 SHF rotates + 4 LOP3 + 4 IADD3 per unit, SURVEY §8d OPS),
+ * blocks x 256 threads x reps iterations of vt_int_mix_ops_per_thread_rep()
+ * ops each; the denominator of the Merkle "fraction of SHA-256 int peak"
+ * (BASELINE.md §3).  sink: one device uint32 (written only to keep the work).
+ */
+int vt_int_mix_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t stream);
+int64_t vt_int_mix_ops_per_thread_rep(void);
 
 #ifdef __cplusplus
 }

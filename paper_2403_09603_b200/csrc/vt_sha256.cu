@@ -337,6 +337,64 @@ extern "C" int vt_sha256_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt
 }
 
 // ---------------------------------------------------------------------------
+// Integer-pipe peak, independent of compress(): register-only chains of the
+// SHA-256 op MIX (per unit: 6 SHF funnel-shift rotates, 4 LOP3, 4 IADD3 --
+// SURVEY.md §8(d) OPS) with no message schedule, no constants table, no
+// memory traffic and 4 independent chains per thread for ILP.  The bench
+// divides the Merkle kernel's analytic op rate (1,400 ops per compression)
+// by this rate.  Ops per launch = blocks * 256 * reps *
+// kMixChains * 14 (the SASS is checked by tests/test_abi.py).
+// ---------------------------------------------------------------------------
+namespace vt {
+constexpr int kMixChains = 4;
+__global__ void __launch_bounds__(256) int_mix_peak_kernel(uint32_t* sink, int reps, uint32_t seed) {
+  uint32_t a[kMixChains], b[kMixChains], c[kMixChains], d[kMixChains];
+#pragma unroll
+  for (int k = 0; k < kMixChains; ++k) {
+    a[k] = seed ^ (threadIdx.x * 0x9e3779b9u) ^ (k * 0x85ebca6bu);
+    b[k] = a[k] * 3u + blockIdx.x;
+    c[k] = b[k] ^ 0xc2b2ae35u;
+    d[k] = c[k] + 0x27d4eb2fu;
+  }
+#pragma unroll 1
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll
+    for (int k = 0; k < kMixChains; ++k) {
+      const uint32_t s1 = __funnelshift_r(a[k], a[k], 6) ^ __funnelshift_r(a[k], a[k], 11) ^
+                          __funnelshift_r(a[k], a[k], 25);                   // 3 SHF + 1 LOP3
+      const uint32_t s0 = __funnelshift_r(b[k], b[k], 2) ^ __funnelshift_r(b[k], b[k], 13) ^
+                          __funnelshift_r(b[k], b[k], 22);                   // 3 SHF + 1 LOP3
+      const uint32_t ch = (a[k] & c[k]) ^ (~a[k] & d[k]);                     // 1 LOP3
+      const uint32_t mj = (a[k] & b[k]) ^ (a[k] & c[k]) ^ (b[k] & c[k]);     // 1 LOP3
+      const uint32_t na = s1 + ch + d[k];                                     // IADD3
+      const uint32_t nb = s0 + mj + c[k];                                     // IADD3
+      const uint32_t nc = a[k] + b[k] + (uint32_t)r;                          // IADD3
+      const uint32_t nd = d[k] + s1 + s0;                                     // IADD3
+      a[k] = na;
+      b[k] = nb;
+      c[k] = nc;
+      d[k] = nd;
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < kMixChains; ++k) acc ^= a[k] ^ b[k] ^ c[k] ^ d[k];
+  if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the work alive
+}
+}  // namespace vt
+
+extern "C" int vt_int_mix_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt_stream_t stream) {
+  if (blocks <= 0 || reps <= 0 || !sink) {
+    vt_set_error("vt_int_mix_peak_bench: bad argument");
+    return VT_EINVAL;
+  }
+  vt::int_mix_peak_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps, 0x1234567u);
+  return vt_check_launch("int_mix_peak_kernel");
+}
+
+extern "C" int64_t vt_int_mix_ops_per_thread_rep(void) { return (int64_t)vt::kMixChains * 14; }
+
+// ---------------------------------------------------------------------------
 // Canonical checkpoint serialization (merkle.hash_weights, merkle.py:155-166):
 // FP64 -> FP32 round-to-nearest-even, little-endian (the device's own byte
 // order), overflow to +-inf exactly like numpy's astype('<f4'); the first

@@ -177,15 +177,26 @@ def config2_budgets(sizes) -> list[int]:
 
 
 CONFIG4_PARAMS = 1_500_000_000
+CONFIG4_BLOCK = 1 << 22  # parameters per generation block = 16 MiB = one 2^12-leaf Merkle block
 
 
-def config4_weights_torch(n: int = CONFIG4_PARAMS, device="cuda"):
-    """configs[4]: n FP32 weights ~ N(0, 0.02) from a torch generator seeded 4
-    (the bench's exact bits)."""
+def config4_weights_torch(n: int = CONFIG4_PARAMS, device="cuda", lo: int = 0, hi: int | None = None):
+    """configs[4]: FP32 weights ~ N(0, 0.02), parameters [lo, hi) of n.  Each
+    block of CONFIG4_BLOCK parameters has its own torch generator (seed
+    4 << 32 | block), so a rank that owns whole Merkle blocks (dist.
+    leaf_block_range, 4 KiB leaves) generates exactly its part of the same
+    checkpoint."""
     import torch
+    hi = n if hi is None else hi
+    if lo % CONFIG4_BLOCK or (hi != n and hi % CONFIG4_BLOCK):
+        raise ValueError("lo / hi must be block aligned")
+    out = torch.empty(hi - lo, device=device)
     g = torch.Generator(device=device)
-    g.manual_seed(4)
-    return torch.randn(n, device=device, generator=g) * 0.02
+    for b0 in range(lo, hi, CONFIG4_BLOCK):
+        b1 = min(hi, b0 + CONFIG4_BLOCK)
+        g.manual_seed((4 << 32) | (b0 // CONFIG4_BLOCK))
+        torch.randn(b1 - b0, device=device, generator=g, out=out[b0 - lo:b1 - lo])
+    return out.mul_(0.02)
 
 
 def _torch_bracket(v):

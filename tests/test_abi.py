@@ -90,6 +90,7 @@ BAD_CALLS = [
     ("vt_merkle_level", (None, 0, None, None)),
     ("vt_merkle_build", (None, 0, 4096, None, 0, None)),
     ("vt_sha256_peak_bench", (None, 0, 1, None)),
+    ("vt_int_mix_peak_bench", (None, 0, 1, None)),
     ("vt_serialize_f32", (None, -1, None, 0, None, None)),
     ("vt_tau_kth_begin", (-1, None, None, 0, None)),
     ("vt_tau_kth_hist", (None, 10, 32, 7, None, None, 0, None)),
@@ -107,7 +108,7 @@ def test_entry_points_reject_bad_arguments(name, args):
 
 def test_every_compute_entry_point_is_covered():
     host_only = {"vt_version", "vt_last_error", "vt_tile_elems", "vt_merkle_node_count", "vt_tau_kth_hist_offset",
-                 "vt_tau_kth_hist_bins"}
+                 "vt_tau_kth_hist_bins", "vt_int_mix_ops_per_thread_rep"}
     covered = {c[0] for c in BAD_CALLS}
     assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}
 
@@ -157,3 +158,23 @@ def test_default_log_capacity_bound():
     assert ops.default_log_capacity(1000) == 1000
     assert ops.default_log_capacity(1 << 20) == 1 << 17
     assert ops.default_log_capacity(1 << 30) == 1 << 27  # 1 GiB of words at 2^30, not 8 GiB
+
+
+def test_int_mix_peak_kernel_is_the_sha_op_mix():
+    """The Merkle roofline's denominator kernel: its loop body is the SHA-256
+    op mix (6 SHF : 4 LOP3 : 4 IADD3 per unit, 4 units per iteration) with no
+    memory instructions, so ops/s = blocks * 256 * reps * 56 / time."""
+    import subprocess
+    from paper_2403_09603_b200 import _lib
+    so = REPO / "paper_2403_09603_b200" / "libvtrain_b200.so"
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", "_ZN2vt19int_mix_peak_kernelEPjij", str(so)],
+                          capture_output=True, text=True).stdout
+    lines = [ln for ln in sass.splitlines() if re.search(r"/\*[0-9a-f]{4}\*/", ln)]
+    # the loop: from the first SHF to the backward branch
+    start = next(i for i, ln in enumerate(lines) if " SHF." in ln)
+    end = next(i for i, ln in enumerate(lines) if "BRA.U UP0" in ln or ("BRA" in ln and i > start))
+    body = lines[start:end]
+    count = lambda op: sum(1 for ln in body if re.search(rf"\b{op}\b", ln))  # noqa: E731
+    assert count("SHF.R.W.U32") == 24 and count("LOP3.LUT") == 16 and count("IADD3") == 16
+    assert not any(re.search(r"\b(LDG|STG|LDS|STS)\b", ln) for ln in body)
+    assert _lib.lib().vt_int_mix_ops_per_thread_rep() == 56

@@ -139,7 +139,6 @@ def maybe_spawn(args) -> None:
         return
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
     sys.exit(subprocess.call(cmd, env=env))
@@ -194,7 +193,6 @@ def run_ours(args) -> None:
     ddp = "WORLD_SIZE" in os.environ
     if ddp:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     n = 1 << args.log2n

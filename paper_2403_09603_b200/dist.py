@@ -52,8 +52,17 @@ def exclusive_offsets(counts: torch.Tensor) -> torch.Tensor:
     return torch.cumsum(counts, 0) - counts
 
 
+def _world(group=None) -> int:
+    """World size; 1 without an initialised process group (single process)."""
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
 def _all_gather_flat(out: torch.Tensor, mine: torch.Tensor, group=None) -> None:
-    """all_gather_into_tensor on NCCL; list form on backends without it (gloo)."""
+    """all_gather_into_tensor on NCCL; list form on backends without it (gloo);
+    a copy in a single process."""
+    if not dist.is_initialized():
+        out.copy_(mine.reshape(out.shape))
+        return
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, mine, group=group)
     else:
@@ -66,7 +75,7 @@ def _all_gather_flat(out: torch.Tensor, mine: torch.Tensor, group=None) -> None:
 
 def all_gather_counts(count: int | torch.Tensor, group=None, device=None) -> torch.Tensor:
     """All ranks' int64 counts (one tiny NCCL all-gather over NVLink)."""
-    world = dist.get_world_size(group)
+    world = _world(group)
     if isinstance(count, torch.Tensor):
         mine = count.reshape(1).to(torch.int64)
     else:
@@ -92,7 +101,7 @@ def round_and_log_sharded(x_local: torch.Tensor, b_r: int, tau: float, global_ba
     y, log = ops.round_and_log(x_local, b_r, tau, global_base=global_base, **kw)
     counts = all_gather_counts(log.count, group, device=x_local.device)
     offs = exclusive_offsets(counts)
-    rank = dist.get_rank(group)
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
     return y, ShardedLog(log, int(offs[rank]), int(counts.sum()), counts)
 
 
@@ -101,7 +110,8 @@ def replay_sharded(xa_local: torch.Tensor, b_r: int, slog: ShardedLog, global_ba
     from . import ops
     y, corr = ops.replay(xa_local, b_r, slog.local, global_base=global_base, **kw)
     t = torch.tensor([corr], dtype=torch.int64, device=xa_local.device)
-    dist.all_reduce(t, group=group)
+    if dist.is_initialized():
+        dist.all_reduce(t, group=group)
     return y, int(t.item())
 
 
@@ -166,7 +176,7 @@ class ShardedKth:
 def kth_largest_distance_sharded(x_local: torch.Tensor, b_r: int, rank: int, group=None) -> float:
     """(rank+1)-th largest p over the union of every rank's shard, exactly
     (rank 0-based from the top); 0.0 when the union has at most rank elements."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    world = _world(group)
     n = torch.tensor([x_local.numel()], dtype=torch.int64, device=x_local.device)
     if world > 1:
         dist.all_reduce(n, group=group)
@@ -276,7 +286,7 @@ def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes:
         from . import merkle as mk
         hash_leaves = hash_leaves or (lambda b: mk.sha256_leaves(b, leaf_bytes))
         hash_level = hash_level or _device_level
-    world = dist.get_world_size(group)
+    world = _world(group)
     depth = local_depth(n_leaves_total, k)
     leaves = hash_leaves(w_local_bytes) if w_local_bytes.numel() else None
     if leaves is None or leaves.shape[0] == 0:

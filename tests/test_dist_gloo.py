@@ -126,3 +126,19 @@ def test_shard_range_plan():
             rs = [vd.leaf_block_range(nl, r, world, 12) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == nl
             assert all(a1 == b0 for (_, a1), (b0, _) in zip(rs, rs[1:]))
+
+
+def test_sharded_paths_without_a_process_group():
+    """Single process (no torch.distributed init): the sharded functions are the
+    one-rank case -- the gathers are copies and the levels equal merkle.build."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    import vt_oracle as O
+    from paper_2403_09603_b200 import dist as vd
+    assert not dist.is_initialized()
+    assert vd.all_gather_counts(7).tolist() == [7]
+    data = np.random.default_rng(3).normal(0, 0.02, size=70_001).astype(np.float32).tobytes()
+    nl = (len(data) + 4095) // 4096
+    lv, top = vd.merkle_sharded(torch.frombuffer(bytearray(data), dtype=torch.uint8), nl, 4096, 3,
+                                hash_leaves=lambda b: _sha_leaves(b, 4096), hash_level=_sha_level)
+    got = vd.assemble_levels([[[bytes(r) for r in t.numpy()] for t in lv]], [[bytes(r) for r in t.numpy()] for t in top])
+    assert got == O.merkle_levels(O.chunk_leaves(data, 4096))

@@ -153,6 +153,21 @@ def _graph(fn, stream):
     return g
 
 
+def _capture(fn):
+    """Warm fn up on a side stream, then capture it on THAT stream: the
+    operators' workspaces are per stream, so the graph reuses the warmed one
+    (a workspace first allocated inside a capture would put its zero-fill in
+    the graph)."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    return _graph(fn, s)
+
+
 def run_harness_check(args) -> None:
     """CPU self-test of the launcher path (no GPU, no kernels; tests only):
     gloo ranks, the barrier + max-over-ranks timing and rank 0's single JSON
@@ -484,17 +499,7 @@ def sweep(log2s) -> dict:
         rl = lambda: ops.round_and_log(x, 32, workloads.TAU_CONFIG0, out=y, log_out=words, check=False)  # noqa: E731
         rp = lambda: ops.replay(x, 32, lw, out=ya, check=False)  # noqa: E731
         ms_e, ms2_e = _time(rl, reps), _time(rp, reps)
-        graphs = []
-        for fn in (rl, rp):
-            s_ = torch.cuda.Stream()
-            s_.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s_):
-                fn()
-            torch.cuda.current_stream().wait_stream(s_)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn()
-            graphs.append(g)
+        graphs = [_capture(fn) for fn in (rl, rp)]
         ms, ms2 = _time(graphs[0].replay, reps), _time(graphs[1].replay, reps)
         b = n * (8 + 4 + 8 * log.count / n)
         out[f"2^{lg}"] = {"round_log_gbs": round(b / ms / 1e6, 1), "round_log_frac": round(b / ms / 1e6 / peak, 4),
@@ -547,17 +552,7 @@ def vtrl_codec(lg: int = 26) -> dict:
     rp()
     torch.cuda.synchronize()
     ok = bool(torch.equal(y.view(torch.int32), ya.view(torch.int32))) and f.read()[0] == 0 and fa.read()[0] == 0
-    graphs = []
-    for fn in (rl, rp):
-        s_ = torch.cuda.Stream()
-        s_.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s_):
-            fn()
-        torch.cuda.current_stream().wait_stream(s_)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
-        graphs.append(g)
+    graphs = [_capture(fn) for fn in (rl, rp)]
     ms, ms2 = _time(graphs[0].replay, 10), _time(graphs[1].replay, 10)
     b = n * (8 + 4 + 0.2)
     return {"n": n, "round_log_packed_gbs": round(b / ms / 1e6, 1), "round_log_packed_frac": round(b / ms / 1e6 / peak, 4),
@@ -614,16 +609,7 @@ def config2() -> dict:
     def graphed(fn):
         fn()
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            fn()
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        with torch.cuda.graph(graph):
-            fn()
-        return graph
+        return _capture(fn)
 
     g_calls = graphed(run)
     ms_calls = _time(g_calls.replay, reps=5, warm=1)
@@ -725,20 +711,27 @@ def config4_merkle() -> dict:
     blocks, reps = 148 * 32, 64
     pk_ms = _time(lambda: _lib.call("vt_sha256_peak_bench", D.ptr(sink), blocks, reps, D.stream_ptr()), reps=3)
     peak_cps = blocks * 128 * reps / (pk_ms * 1e-3)
-    # independent denominator: the SHF/LOP3/IADD3 mix on register-only chains
-    mix_blocks, mix_reps = 148 * 16, 4096
-    mix_ms = _time(lambda: _lib.call("vt_int_mix_peak_bench", D.ptr(sink), mix_blocks, mix_reps, D.stream_ptr()),
-                   reps=3)
-    mix_ops = mix_blocks * 256 * mix_reps * int(_lib.lib().vt_int_mix_ops_per_thread_rep()) / (mix_ms * 1e-3)
+    # independent denominator: the SHF/LOP3/add mix on register-only chains,
+    # adds on the ALU pipe (IADD3) or on the FMA pipe (IMAD); the faster is the peak
+    mix_blocks, mix_reps = 148 * 8, 2048
+    per = mix_blocks * 256 * mix_reps * int(_lib.lib().vt_int_mix_ops_per_thread_rep())
+    mix = {}
+    for fma in (0, 1):
+        mix_ms = _time(lambda: _lib.call("vt_int_mix_peak_bench", D.ptr(sink), mix_blocks, mix_reps, fma,
+                                         D.stream_ptr()), reps=3)
+        mix["fma_adds" if fma else "iadd3_adds"] = per / (mix_ms * 1e-3)
+    mix_ops = max(mix.values())
     cps = comps / (ms * 1e-3)
     return {"params": n, "leaves": int(leaves), "hashed_internal_nodes": int(nodes), "levels": len(sizes),
             "ms": round(ms, 3), "hashed_gbs": round(n * 4 / ms / 1e6, 1),
             "compressions_per_s": round(cps / 1e9, 3), "unit_cps": "G compressions/s",
             "int_ops_per_s": round(cps * 1400 / 1e12, 2), "unit_ops": "T int ops/s (analytic 1400 / compression)",
             "int_mix_peak_ops_per_s": round(mix_ops / 1e12, 2),
+            "int_mix_variants_ops_per_s": {k: round(v / 1e12, 2) for k, v in mix.items()},
             "frac_of_sha256_int_peak": round(cps * 1400 / mix_ops, 4),
-            "peak_note": "denominator = int_mix_peak_kernel: register-only SHF/LOP3/IADD3 chains in the SHA-256 op "
-                         "mix (6:4:4), not compress(); numerator = compressions/s x 1400 analytic ops",
+            "peak_note": "denominator = int_mix_peak_kernel: register-only chains of the SHA-256 op mix (6 SHF : "
+                         "4 LOP3 : 4 three-input adds), not compress(); the faster of adds-as-IADD3 (ALU pipe) and "
+                         "adds-as-2xIMAD (FMA pipe); numerator = compressions/s x 1400 analytic ops",
             "sha256_compress_ceiling_cps": round(peak_cps / 1e9, 3),
             "frac_of_compress_ceiling": round(cps / peak_cps, 4),
             "root": t.root_hex[:16]}

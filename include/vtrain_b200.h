@@ -269,9 +269,11 @@ int vt_sha256_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t s
  * SHA-256 op mix (6 SHF rotates + 4 LOP3 + 4 IADD3 per unit, SURVEY §8d OPS),
  * blocks x 256 threads x reps iterations of vt_int_mix_ops_per_thread_rep()
  * ops each; the denominator of the Merkle "fraction of SHA-256 int peak"
- * (BASELINE.md §3).  sink: one device uint32 (written only to keep the work).
+ * (BASELINE.md §3).  fma_adds != 0: the three-input adds as two IMADs each on
+ * the FMA pipe (off the ALU pipe, as ptxas balances compress()); the peak of
+ * the mix is the faster variant.  sink: one device uint32 (keeps the work).
  */
-int vt_int_mix_peak_bench(uint32_t *sink, int64_t blocks, int reps, vt_stream_t stream);
+int vt_int_mix_peak_bench(uint32_t *sink, int64_t blocks, int reps, int fma_adds, vt_stream_t stream);
 int64_t vt_int_mix_ops_per_thread_rep(void);
 
 #ifdef __cplusplus

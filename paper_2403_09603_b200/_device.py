@@ -9,6 +9,7 @@ tensors are zero-copy when contiguous and 32-byte aligned.
 from __future__ import annotations
 
 import threading
+import warnings
 
 import numpy as np
 import torch
@@ -18,6 +19,7 @@ from . import _lib
 _WS: dict[tuple, torch.Tensor] = {}
 _RETIRED: list[torch.Tensor] = []
 _WS_LOCK = threading.Lock()
+_WARNED: set = set()
 
 
 def require_cuda() -> torch.device:
@@ -83,6 +85,11 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
         if ws is None or ws.numel() < nbytes:
             if ws is not None:
                 _RETIRED.append(ws)
+            if torch.cuda.is_current_stream_capturing() and key not in _WARNED:
+                _WARNED.add(key)
+                warnings.warn(f"paper_2403_09603_b200: workspace '{tag}' first allocated inside a CUDA graph capture; "
+                              "its zero-fill becomes part of the graph.  Warm up on the capture stream "
+                              "(torch.cuda.graph(g, stream=s)) or pass workspace=.", stacklevel=3)
             ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
             _WS[key] = ws
         return ws
@@ -126,3 +133,54 @@ def raise_fpround(err: int, neighbor_semantics: bool = False) -> None:
         raise ValueError("non-finite value")
     if err & (_lib.ERR_RANGE | _lib.ERR_RANGE_NEIGHBOR):
         raise ValueError("out of representable range")
+
+
+class HostStage:
+    """Pinned host <-> device staging for host-array calls of one channel
+    (protocol._run hands the channels NumPy arrays of a few thousand
+    elements): the call's input and zeroed flag words go over in ONE H2D copy,
+    every output (flags, side outputs, the FP64 result) comes back in ONE D2H
+    copy, and the host waits once -- instead of a pageable copy, a flag read
+    and a result read, each synchronising.
+
+    Layout (host and device alike, 256-byte aligned regions):
+        [ x: in_bytes | flags: 256 | out regions ... ]
+    H2D covers [0, flags_end); D2H covers [flags_off, end).  One stage per
+    channel object; calls on it are sequential (the channel is)."""
+
+    def __init__(self):
+        self.cap = 0
+        self.host = self.dev = None
+
+    @staticmethod
+    def _al(v: int) -> int:
+        return (v + 255) & ~255
+
+    def layout(self, in_bytes: int, out_sizes: list[int]) -> tuple[int, list[int], int]:
+        flags_off = self._al(in_bytes)
+        offs, o = [], flags_off + 256
+        for sz in out_sizes:
+            offs.append(o)
+            o = self._al(o + sz)
+        return flags_off, offs, o
+
+    def ensure(self, nbytes: int) -> None:
+        if nbytes > self.cap:
+            cap = max(nbytes, 2 * self.cap, 1 << 16)
+            self.host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self.dev = torch.empty(cap, dtype=torch.uint8, device=require_cuda())
+            self.host_np = self.host.numpy()
+            self.cap = cap
+
+    def h2d(self, end: int) -> None:
+        self.dev[:end].copy_(self.host[:end], non_blocking=True)
+
+    def d2h_wait(self, lo: int, hi: int) -> None:
+        self.host[lo:hi].copy_(self.dev[lo:hi], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def hview(self, off: int, n: int, dtype) -> np.ndarray:
+        return self.host_np[off:off + n * np.dtype(dtype).itemsize].view(dtype)
+
+    def dptr(self, off: int) -> int:
+        return self.dev.data_ptr() + off

@@ -71,7 +71,7 @@ EXPORTS: dict[str, tuple] = {
     "vt_merkle_node_count": (_i64, [_i64]),
     "vt_merkle_build": (_i32, [_p, _i64, _i64, _p, _i64, _p]),
     "vt_sha256_peak_bench": (_i32, [_p, _i64, _i32, _p]),
-    "vt_int_mix_peak_bench": (_i32, [_p, _i64, _i32, _p]),
+    "vt_int_mix_peak_bench": (_i32, [_p, _i64, _i32, _i32, _p]),
     "vt_int_mix_ops_per_thread_rep": (_i64, []),
     "vt_serialize_f32": (_i32, [_p, _i64, _p, _i64, _p, _p]),
 }

@@ -340,14 +340,25 @@ extern "C" int vt_sha256_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt
 // Integer-pipe peak, independent of compress(): register-only chains of the
 // SHA-256 op MIX (per unit: 6 SHF funnel-shift rotates, 4 LOP3, 4 IADD3 --
 // SURVEY.md §8(d) OPS) with no message schedule, no constants table, no
-// memory traffic and 4 independent chains per thread for ILP.  The bench
+// memory traffic and 8 independent chains per thread for ILP.  The bench
 // divides the Merkle kernel's analytic op rate (1,400 ops per compression)
 // by this rate.  Ops per launch = blocks * 256 * reps *
 // kMixChains * 14 (the SASS is checked by tests/test_abi.py).
 // ---------------------------------------------------------------------------
 namespace vt {
-constexpr int kMixChains = 4;
-__global__ void __launch_bounds__(256) int_mix_peak_kernel(uint32_t* sink, int reps, uint32_t seed) {
+constexpr int kMixChains = 8;
+// FMA_ADDS: every 3-input add as two IMADs by a runtime 1 on the FMA pipe
+// (how ptxas balances adds off the ALU pipe in compress()); otherwise IADD3
+// on the ALU pipe.  The bench takes the faster of the two as the peak of
+// the mix.
+template <bool FMA_ADDS>
+__device__ __forceinline__ uint32_t add3(uint32_t x, uint32_t y, uint32_t z, uint32_t one) {
+  if (FMA_ADDS) return x * one + (y * one + z);
+  return x + y + z;
+}
+
+template <bool FMA_ADDS>
+__global__ void __launch_bounds__(256) int_mix_peak_kernel(uint32_t* sink, int reps, uint32_t seed, uint32_t one) {
   uint32_t a[kMixChains], b[kMixChains], c[kMixChains], d[kMixChains];
 #pragma unroll
   for (int k = 0; k < kMixChains; ++k) {
@@ -356,24 +367,22 @@ __global__ void __launch_bounds__(256) int_mix_peak_kernel(uint32_t* sink, int r
     c[k] = b[k] ^ 0xc2b2ae35u;
     d[k] = c[k] + 0x27d4eb2fu;
   }
+  // each update overwrites one state word; per chain and iteration the SHA-256
+  // round's op mix: 6 SHF + 4 LOP3 + 4 three-input adds
 #pragma unroll 1
   for (int r = 0; r < reps; ++r) {
 #pragma unroll
     for (int k = 0; k < kMixChains; ++k) {
-      const uint32_t s1 = __funnelshift_r(a[k], a[k], 6) ^ __funnelshift_r(a[k], a[k], 11) ^
-                          __funnelshift_r(a[k], a[k], 25);                   // 3 SHF + 1 LOP3
-      const uint32_t s0 = __funnelshift_r(b[k], b[k], 2) ^ __funnelshift_r(b[k], b[k], 13) ^
-                          __funnelshift_r(b[k], b[k], 22);                   // 3 SHF + 1 LOP3
-      const uint32_t ch = (a[k] & c[k]) ^ (~a[k] & d[k]);                     // 1 LOP3
-      const uint32_t mj = (a[k] & b[k]) ^ (a[k] & c[k]) ^ (b[k] & c[k]);     // 1 LOP3
-      const uint32_t na = s1 + ch + d[k];                                     // IADD3
-      const uint32_t nb = s0 + mj + c[k];                                     // IADD3
-      const uint32_t nc = a[k] + b[k] + (uint32_t)r;                          // IADD3
-      const uint32_t nd = d[k] + s1 + s0;                                     // IADD3
-      a[k] = na;
-      b[k] = nb;
-      c[k] = nc;
-      d[k] = nd;
+      a[k] = add3<FMA_ADDS>(a[k],
+                            __funnelshift_r(b[k], b[k], 6) ^ __funnelshift_r(b[k], b[k], 11) ^
+                                __funnelshift_r(b[k], b[k], 25),
+                            (b[k] & c[k]) ^ (~b[k] & d[k]), one);
+      b[k] = add3<FMA_ADDS>(b[k],
+                            __funnelshift_r(c[k], c[k], 2) ^ __funnelshift_r(c[k], c[k], 13) ^
+                                __funnelshift_r(c[k], c[k], 22),
+                            (c[k] & d[k]) ^ (c[k] & a[k]) ^ (d[k] & a[k]), one);
+      c[k] = add3<FMA_ADDS>(c[k], d[k], a[k], one);
+      d[k] = add3<FMA_ADDS>(d[k], b[k], (uint32_t)r, one);
     }
   }
   uint32_t acc = 0;
@@ -383,12 +392,16 @@ __global__ void __launch_bounds__(256) int_mix_peak_kernel(uint32_t* sink, int r
 }
 }  // namespace vt
 
-extern "C" int vt_int_mix_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt_stream_t stream) {
+extern "C" int vt_int_mix_peak_bench(uint32_t* sink, int64_t blocks, int reps, int fma_adds, vt_stream_t stream) {
   if (blocks <= 0 || reps <= 0 || !sink) {
     vt_set_error("vt_int_mix_peak_bench: bad argument");
     return VT_EINVAL;
   }
-  vt::int_mix_peak_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps, 0x1234567u);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fma_adds)
+    vt::int_mix_peak_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(sink, reps, 0x1234567u, 1u);
+  else
+    vt::int_mix_peak_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(sink, reps, 0x1234567u, 1u);
   return vt_check_launch("int_mix_peak_kernel");
 }
 

@@ -45,6 +45,9 @@ class GpuTrainerChannel:
 
     def process(self, values, tau: float):
         if isinstance(self.writer, LogWriter):
+            if not isinstance(values, torch.Tensor):  # the reference loop's NumPy arrays: staged path
+                y, directed = self.writer.write_values_host(values, tau)
+                return y, int(directed), 0
             y, directed = self.writer.write_values(values, tau)
             return _host_like(values, y), int(directed), 0
         # foreign writer with the reference interface: hand it the codes
@@ -68,8 +71,40 @@ class GpuAuditorChannel:
     def __init__(self, reader, b_r: int):
         self.reader = reader
         self.b_r = b_r
+        self._stage = None
+
+    def _process_host(self, values, tau: float):
+        """NumPy input with a device-resident .vtrl payload: one H2D copy of
+        [x | zeroed flags], the fused packed replay, one D2H copy of
+        [flags | y], one host wait."""
+        a = np.asarray(values, dtype=np.float64)
+        shape = a.shape if a.shape else (1,)
+        n = a.size
+        payload, pos = self.reader.take_device(n)
+        if n == 0:
+            return np.zeros(shape, dtype=np.float64), 0, 0
+        st = self._stage
+        if st is None:
+            st = self._stage = D.HostStage()
+        fo, (oy,), end = st.layout(8 * n, [8 * n])
+        st.ensure(end)
+        np.copyto(st.hview(0, n, np.float64), a.reshape(-1))
+        st.hview(fo, 32, np.int64)[:] = 0
+        st.h2d(fo + 256)
+        _lib.call("vt_replay", st.dptr(0), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload), self.reader.payload_nbytes,
+                  pos, _lib.OUT_F64, st.dptr(oy), st.dptr(fo + 16), st.dptr(fo), None, 0, D.stream_ptr())
+        st.d2h_wait(fo, oy + 8 * n)
+        fl = st.hview(fo, 6, np.int64)
+        err = int(fl[0]) & 0xFFFFFFFF
+        if err & _lib.ERR_BAD_LOG_BYTE:
+            from .roundlog import LogFormatError
+            raise LogFormatError("corrupt log byte")
+        D.raise_fpround(err)
+        return st.hview(oy, n, np.float64).copy().reshape(shape), 0, int(fl[2])
 
     def process(self, values, tau: float):
+        if isinstance(self.reader, LogReader) and not isinstance(values, torch.Tensor):
+            return self._process_host(values, tau)
         t, _, shape = D.to_device_f64(values)
         n = t.numel()
         y = torch.empty_like(t)

@@ -90,7 +90,7 @@ BAD_CALLS = [
     ("vt_merkle_level", (None, 0, None, None)),
     ("vt_merkle_build", (None, 0, 4096, None, 0, None)),
     ("vt_sha256_peak_bench", (None, 0, 1, None)),
-    ("vt_int_mix_peak_bench", (None, 0, 1, None)),
+    ("vt_int_mix_peak_bench", (None, 0, 1, 0, None)),
     ("vt_serialize_f32", (None, -1, None, 0, None, None)),
     ("vt_tau_kth_begin", (-1, None, None, 0, None)),
     ("vt_tau_kth_hist", (None, 10, 32, 7, None, None, 0, None)),
@@ -162,19 +162,25 @@ def test_default_log_capacity_bound():
 
 def test_int_mix_peak_kernel_is_the_sha_op_mix():
     """The Merkle roofline's denominator kernel: its loop body is the SHA-256
-    op mix (6 SHF : 4 LOP3 : 4 IADD3 per unit, 4 units per iteration) with no
-    memory instructions, so ops/s = blocks * 256 * reps * 56 / time."""
+    op mix (6 SHF : 4 LOP3 : 4 three-input adds per unit, 8 units per
+    iteration) with no memory instructions; the adds are IADD3 on the ALU
+    pipe, or two IMADs each on the FMA pipe in the FMA_ADDS variant."""
     import subprocess
     from paper_2403_09603_b200 import _lib
     so = REPO / "paper_2403_09603_b200" / "libvtrain_b200.so"
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", "_ZN2vt19int_mix_peak_kernelEPjij", str(so)],
-                          capture_output=True, text=True).stdout
-    lines = [ln for ln in sass.splitlines() if re.search(r"/\*[0-9a-f]{4}\*/", ln)]
-    # the loop: from the first SHF to the backward branch
-    start = next(i for i, ln in enumerate(lines) if " SHF." in ln)
-    end = next(i for i, ln in enumerate(lines) if "BRA.U UP0" in ln or ("BRA" in ln and i > start))
-    body = lines[start:end]
-    count = lambda op: sum(1 for ln in body if re.search(rf"\b{op}\b", ln))  # noqa: E731
-    assert count("SHF.R.W.U32") == 24 and count("LOP3.LUT") == 16 and count("IADD3") == 16
-    assert not any(re.search(r"\b(LDG|STG|LDS|STS)\b", ln) for ln in body)
-    assert _lib.lib().vt_int_mix_ops_per_thread_rep() == 56
+    for fma, name in ((False, "_ZN2vt19int_mix_peak_kernelILb0EEEvPjijj"),
+                      (True, "_ZN2vt19int_mix_peak_kernelILb1EEEvPjijj")):
+        sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", name, str(so)],
+                              capture_output=True, text=True).stdout
+        lines = [ln for ln in sass.splitlines() if re.search(r"/\*[0-9a-f]{4}\*/", ln)]
+        start = next(i for i, ln in enumerate(lines) if " SHF." in ln)
+        end = next(i for i, ln in enumerate(lines) if i > start and "BRA" in ln)
+        body = lines[start:end]
+        count = lambda op: sum(1 for ln in body if re.search(rf"\b{op}\b", ln))  # noqa: E731
+        assert count("SHF.R.W.U32") == 48 and count("LOP3.LUT") == 32, name
+        if fma:
+            assert count("IADD3") == 0 and count("IMAD") >= 64, name
+        else:
+            assert count("IADD3") == 32, name
+        assert not any(re.search(r"\b(LDG|STG|LDS|STS)\b", ln) for ln in body)
+    assert _lib.lib().vt_int_mix_ops_per_thread_rep() == 8 * 14

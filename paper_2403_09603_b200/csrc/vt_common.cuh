@@ -392,9 +392,11 @@ struct RLBatch {
   RLSeg seg[kMaxBatch];
 };
 
+// tiles (of 2048 elements) per round-and-log ticket / look-back word
+constexpr int kRLSuper = 4;
 __host__ __device__ inline int64_t rl_batch_tickets(int64_t n) {
   const int64_t tiles = (n + 2047) / 2048;
-  return tiles / 4 + tiles % 4;
+  return tiles / kRLSuper + tiles % kRLSuper;
 }
 // the batch's look-back words come after a 64-byte header
 inline size_t rl_batch_workspace(int64_t total_tickets) { return (size_t)(64 + total_tickets * 8 + 256); }

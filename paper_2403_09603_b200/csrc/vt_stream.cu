@@ -180,7 +180,13 @@ extern "C" int vt_debug_timeline(uint64_t* host) {
 #define TLV(i, v)
 #endif
 
-constexpr int kSuper = 4;                        // tiles per super-tile / status word
+// A ticket ("super-tile") is kSuper tiles: the unit of the dynamic schedule
+// and of the look-back; kMaskSlots tickets of staged masks / rows give the
+// look-back ~3 ordinals (~20 us) of slack.  Measured and not kept: 2-tile
+// tickets with 6 slots (same slack in time, half the tail granularity):
+// 2^26 78% vs 81%, 2^28 85% vs 90% -- twice the look-backs and ordinal
+// overheads, and the tail spread (CTA speeds differ ~1.6x) barely moved.
+constexpr int kSuper = kRLSuper;                 // tiles per super-tile / status word
 constexpr int kMaskSlots = 3;                    // super-tiles of masks in flight
 constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
 constexpr int kRow = 64;                         // staged entries per warp-tile (else from masks)
@@ -189,7 +195,7 @@ constexpr int kRow = 64;                         // staged entries per warp-tile
 constexpr int kRowK = 12;
 static_assert(kRowK * 10 <= kRow * 2, "keyed staging must fit a row");
 constexpr int kRows = kSuper * kWarps;           // warp-tiles per super-tile
-static_assert(kRows == 32, "the log warp scans a super-tile's rows one per lane");
+static_assert(kRows <= 32, "the log warp scans a super-tile's rows one per lane");
 constexpr int kFCompute = kSThreads;             // 8 compute warps
 constexpr int kFThreads = kFCompute + 64;        // + log warp + producer warp
 constexpr int kLogWarp = kWarps;                 // warp 8
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       const int64_t s = S.slot_id[slot];
       if (s < 0) break;
       // lane = warp-tile (tile-major): exclusive position of each row inside the super-tile
-      const uint32_t c = (lane / kWarps < st_ntiles(a, s)) ? S.cnts[slot][lane] : 0u;
+      const uint32_t c = (lane < kRows && lane / kWarps < st_ntiles(a, s)) ? S.cnts[slot][lane] : 0u;
       uint32_t inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -529,7 +535,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
         if (lane >= o) inc += u;
       }
       const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
-      S.rpos[slot][lane] = inc - c;
+      if (lane < kRows) S.rpos[slot][lane] = inc - c;
       const int64_t excl = lookback128(a.status, s, agg, epoch, lane);
       if (lane == 0) {
         if (s == a.num_super - 1) {
@@ -554,12 +560,12 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     const uint32_t c8 = ((uint32_t)thr32 + 1u) << 3;
     const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
     const uint32_t epoch = S.epoch;
-    int64_t h1 = -1, h2 = -1, h3 = -1;  // super-tiles of ordinals k-1, k-2, k-3
-    int64_t q = 0;                      // ring sequence number
+    int64_t hist[kMaskSlots];  // super-tile of ordinal kk at hist[kk % kMaskSlots]
+    int64_t q = 0;             // ring sequence number
     for (int64_t k = 0;; ++k) {
-      // this warp's rows of ordinal k - 3 leave slot k % kMaskSlots before it is reused
+      // this warp's rows of ordinal k - kMaskSlots leave slot k % kMaskSlots before it is reused
       if (warp == 0 && lane == 0 && k < 14) TL(4 + 4 * (int)k);
-      if (k >= kMaskSlots) rlf_write_rows<KEYS>(a, S, k - kMaskSlots, h3, warp, lane, lt);
+      if (k >= kMaskSlots) rlf_write_rows<KEYS>(a, S, k - kMaskSlots, hist[k % kMaskSlots], warp, lane, lt);
       if (warp == 0 && lane == 0 && k < 14) TL(6 + 4 * (int)k);
       const int slot = (int)(k % kMaskSlots);
       int64_t s = -1, t0 = 0;
@@ -616,16 +622,15 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
         TLV(55, (uint64_t)s);
       }
       if (warp == 0 && lane == 0 && s < 0) TL(60);
-      if (s < 0) {  // drain ordinals k - 2, k - 1
-        if (k >= 2) rlf_write_rows<KEYS>(a, S, k - 2, h2, warp, lane, lt);
-        if (warp == 0 && lane == 0) TL(61);
-        if (k >= 1) rlf_write_rows<KEYS>(a, S, k - 1, h1, warp, lane, lt);
+      if (s < 0) {  // drain ordinals k - kMaskSlots + 1 .. k - 1
+        for (int64_t kk = k >= kMaskSlots - 1 ? k - kMaskSlots + 1 : 0; kk < k; ++kk) {
+          rlf_write_rows<KEYS>(a, S, kk, hist[kk % kMaskSlots], warp, lane, lt);
+          if (warp == 0 && lane == 0 && kk == k - 2) TL(61);
+        }
         if (warp == 0 && lane == 0) TL(62);
         break;
       }
-      h3 = h2;
-      h2 = h1;
-      h1 = s;
+      hist[k % kMaskSlots] = s;
     }
     report_err(a.err, err);
   }
@@ -792,7 +797,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       const RLSeg& sg = b.seg[j];
       const RLFArgs v = seg_view(b, j);
       const int64_t ls = s - sg.tick0;
-      const uint32_t c = (lane / kWarps < st_ntiles(v, ls)) ? S.cnts[slot][lane] : 0u;
+      const uint32_t c = (lane < kRows && lane / kWarps < st_ntiles(v, ls)) ? S.cnts[slot][lane] : 0u;
       uint32_t inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -800,7 +805,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
         if (lane >= o) inc += u;
       }
       const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
-      S.rpos[slot][lane] = inc - c;
+      if (lane < kRows) S.rpos[slot][lane] = inc - c;
       const int64_t excl = lookback128(status + sg.tick0, ls, agg, epoch, lane);
       if (lane == 0) {
         if (ls == v.num_super - 1) {
@@ -816,14 +821,14 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
   } else {  // compute warps
     const uint32_t lt = lanemask_lt();
     const uint32_t epoch = S.epoch;
-    int64_t h1 = -1, h2 = -1, h3 = -1;  // tickets of ordinals k-1, k-2, k-3
-    int j1 = 0, j2 = 0, j3 = 0;         // and their tensors
+    int64_t hist[kMaskSlots];  // ticket of ordinal kk at hist[kk % kMaskSlots]
+    int histj[kMaskSlots];     // and its tensor
     int64_t q = 0;
     auto write_rows = [&](int64_t kk, int64_t s, int j) {
       rlf_write_rows<KEYS>(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
     };
     for (int64_t k = 0;; ++k) {
-      if (k >= kMaskSlots) write_rows(k - kMaskSlots, h3, j3);
+      if (k >= kMaskSlots) write_rows(k - kMaskSlots, hist[k % kMaskSlots], histj[k % kMaskSlots]);
       const int slot = (int)(k % kMaskSlots);
       int64_t s = -1, t0 = 0, ls = 0;
       int nt = 1, j = 0;
@@ -897,16 +902,12 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(S.mfull + slot);
       if (s < 0) {
-        if (k >= 2) write_rows(k - 2, h2, j2);
-        if (k >= 1) write_rows(k - 1, h1, j1);
+        for (int64_t kk = k >= kMaskSlots - 1 ? k - kMaskSlots + 1 : 0; kk < k; ++kk)
+          write_rows(kk, hist[kk % kMaskSlots], histj[kk % kMaskSlots]);
         break;
       }
-      h3 = h2;
-      h2 = h1;
-      h1 = s;
-      j3 = j2;
-      j2 = j1;
-      j1 = j;
+      hist[k % kMaskSlots] = s;
+      histj[k % kMaskSlots] = j;
     }
   }
 
@@ -966,10 +967,11 @@ struct ReplaySmem {
   uint32_t red[kWarps];
 };
 
+constexpr int kRSuper = 4;  // tiles per replay ticket (no look-back: only the dynamic schedule)
 __device__ __forceinline__ int64_t rp_first(const RPArgs& a, int64_t s) {
-  return s < a.n4 ? s * kSuper : a.n4 * kSuper + (s - a.n4);
+  return s < a.n4 ? s * kRSuper : a.n4 * kRSuper + (s - a.n4);
 }
-__device__ __forceinline__ int rp_ntiles(const RPArgs& a, int64_t s) { return s < a.n4 ? kSuper : 1; }
+__device__ __forceinline__ int rp_ntiles(const RPArgs& a, int64_t s) { return s < a.n4 ? kRSuper : 1; }
 
 // named barrier over the 256 compute threads (barrier 0 is the whole CTA)
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
@@ -1357,8 +1359,8 @@ static int launch_rp(RPArgs a, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRThreads, smem);
     resident = std::max(1, per * sms);
   }
-  a.n4 = a.num_tiles / kSuper;
-  a.num_super = a.n4 + a.num_tiles % kSuper;
+  a.n4 = a.num_tiles / kRSuper;
+  a.num_super = a.n4 + a.num_tiles % kRSuper;
   const int grid = (int)std::min<int64_t>(a.num_super, resident);
   k<<<grid, kRThreads, smem, st>>>(a);
   return vt_check_launch("rp_fused_kernel");

@@ -12,6 +12,7 @@
 // block of constant content, so its schedule W[t] + K[t] is precomputed on
 // the host once per length and passed in the kernel parameters.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "vt_common.cuh"
@@ -48,16 +49,28 @@ struct PadWK {
 __device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
 __device__ __forceinline__ uint32_t bswap(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-#define VT_ROUND(a, b, c, d, e, f, g, h, wk)                                             \
-  {                                                                                     \
-    const uint32_t t1 = h + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + (wk); \
-    const uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));  \
-    d += t1;                                                                            \
-    h = t1 + t2;                                                                        \
+// Adds: on the ALU pipe (IADD3) or, with FMA_ADDS, as IMADs by a runtime 1 on
+// the FMA pipe.  The rotates and Ch/Maj/Sigma (SHF, LOP3) can only use the
+// ALU pipe, which a plain compress() saturates (ncu: ALU 97% active, FMA 5%);
+// moving the adds off it balances the two pipes.
+template <bool FMA_ADDS>
+__device__ __forceinline__ uint32_t vadd(uint32_t x, uint32_t y, uint32_t one) {
+  if (FMA_ADDS) return x * one + y;
+  return x + y;
+}
+
+#define VT_ROUND(a, b, c, d, e, f, g, h, wk)                                                              \
+  {                                                                                                      \
+    const uint32_t t1 = vadd<FMA>(h, vadd<FMA>(rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25),                  \
+                                               vadd<FMA>((e & f) ^ (~e & g), (wk), one), one), one);    \
+    const uint32_t t2 = vadd<FMA>(rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22), (a & b) ^ (a & c) ^ (b & c), one); \
+    d = vadd<FMA>(d, t1, one);                                                                           \
+    h = vadd<FMA>(t1, t2, one);                                                                          \
   }
 
 // One compression of a data block held in w[16] (consumed).
-__device__ __forceinline__ void compress(uint32_t (&s)[8], uint32_t (&w)[16]) {
+template <bool FMA>
+__device__ __forceinline__ void compress(uint32_t (&s)[8], uint32_t (&w)[16], uint32_t one) {
   uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
 #pragma unroll
   for (int t = 0; t < 64; t += 8) {
@@ -66,24 +79,26 @@ __device__ __forceinline__ void compress(uint32_t (&s)[8], uint32_t (&w)[16]) {
       for (int k = 0; k < 8; ++k) {
         const int j = (t + k) & 15;
         const uint32_t w15 = w[(j + 1) & 15], w2 = w[(j + 14) & 15];
-        w[j] += (rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10)) + w[(j + 9) & 15] +
-                (rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3));
+        w[j] = vadd<FMA>(w[j], vadd<FMA>(rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10),
+                                         vadd<FMA>(w[(j + 9) & 15], rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3), one),
+                                         one), one);
       }
     }
-    VT_ROUND(a, b, c, d, e, f, g, h, kK[t + 0] + w[(t + 0) & 15]);
-    VT_ROUND(h, a, b, c, d, e, f, g, kK[t + 1] + w[(t + 1) & 15]);
-    VT_ROUND(g, h, a, b, c, d, e, f, kK[t + 2] + w[(t + 2) & 15]);
-    VT_ROUND(f, g, h, a, b, c, d, e, kK[t + 3] + w[(t + 3) & 15]);
-    VT_ROUND(e, f, g, h, a, b, c, d, kK[t + 4] + w[(t + 4) & 15]);
-    VT_ROUND(d, e, f, g, h, a, b, c, kK[t + 5] + w[(t + 5) & 15]);
-    VT_ROUND(c, d, e, f, g, h, a, b, kK[t + 6] + w[(t + 6) & 15]);
-    VT_ROUND(b, c, d, e, f, g, h, a, kK[t + 7] + w[(t + 7) & 15]);
+    VT_ROUND(a, b, c, d, e, f, g, h, vadd<FMA>(kK[t + 0], w[(t + 0) & 15], one));
+    VT_ROUND(h, a, b, c, d, e, f, g, vadd<FMA>(kK[t + 1], w[(t + 1) & 15], one));
+    VT_ROUND(g, h, a, b, c, d, e, f, vadd<FMA>(kK[t + 2], w[(t + 2) & 15], one));
+    VT_ROUND(f, g, h, a, b, c, d, e, vadd<FMA>(kK[t + 3], w[(t + 3) & 15], one));
+    VT_ROUND(e, f, g, h, a, b, c, d, vadd<FMA>(kK[t + 4], w[(t + 4) & 15], one));
+    VT_ROUND(d, e, f, g, h, a, b, c, vadd<FMA>(kK[t + 5], w[(t + 5) & 15], one));
+    VT_ROUND(c, d, e, f, g, h, a, b, vadd<FMA>(kK[t + 6], w[(t + 6) & 15], one));
+    VT_ROUND(b, c, d, e, f, g, h, a, vadd<FMA>(kK[t + 7], w[(t + 7) & 15], one));
   }
   s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
 }
 
 // Compression of a constant block whose W+K schedule is precomputed.
-__device__ __forceinline__ void compress_wk(uint32_t (&s)[8], const PadWK& p) {
+template <bool FMA>
+__device__ __forceinline__ void compress_wk(uint32_t (&s)[8], const PadWK& p, uint32_t one) {
   uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
 #pragma unroll
   for (int t = 0; t < 64; t += 8) {
@@ -112,10 +127,13 @@ struct LeafArgs {
   int64_t n_leaves;
   uint8_t* out;
   PadWK pad;  // padding block for a full leaf when leaf_bytes % 64 == 0
+  uint32_t one;  // 1 (a runtime value: the FMA-pipe adds multiply by it)
 };
 
 // Generic tail: `rem` (< 64) trailing bytes at p, total message length len.
-__device__ __forceinline__ void finish_generic(uint32_t (&s)[8], const uint8_t* p, int rem, int64_t len) {
+template <bool FMA>
+__device__ __forceinline__ void finish_generic(uint32_t (&s)[8], const uint8_t* p, int rem, int64_t len,
+                                               uint32_t one) {
   uint32_t w[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) w[k] = 0u;
@@ -123,16 +141,18 @@ __device__ __forceinline__ void finish_generic(uint32_t (&s)[8], const uint8_t* 
   w[rem >> 2] |= 0x80u << (24 - 8 * (rem & 3));
   const uint64_t bitlen = (uint64_t)len * 8ull;
   if (rem >= 56) {
-    compress(s, w);
+    compress<FMA>(s, w, one);
 #pragma unroll
     for (int k = 0; k < 16; ++k) w[k] = 0u;
   }
   w[14] = (uint32_t)(bitlen >> 32);
   w[15] = (uint32_t)bitlen;
-  compress(s, w);
+  compress<FMA>(s, w, one);
 }
 
+template <bool FMA>
 __global__ void __launch_bounds__(128) sha256_leaves_kernel(const LeafArgs a) {
+  const uint32_t one = a.one;
   const int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (leaf >= a.n_leaves) return;
   const int64_t off = leaf * a.leaf_bytes;
@@ -162,13 +182,13 @@ __global__ void __launch_bounds__(128) sha256_leaves_kernel(const LeafArgs a) {
         w[k] = ((uint32_t)b[0] << 24) | ((uint32_t)b[1] << 16) | ((uint32_t)b[2] << 8) | b[3];
       }
     }
-    compress(s, w);
+    compress<FMA>(s, w, one);
   }
   const int rem = (int)(len - (nblk << 6));
   if (rem == 0 && len == a.leaf_bytes && (a.leaf_bytes & 63) == 0) {
-    compress_wk(s, a.pad);
+    compress_wk<FMA>(s, a.pad, one);
   } else {
-    finish_generic(s, p + (nblk << 6), rem, len);
+    finish_generic<FMA>(s, p + (nblk << 6), rem, len, one);
   }
   store_digest(a.out + leaf * 32, s);
 }
@@ -178,9 +198,12 @@ struct NodeArgs {
   int64_t n_in;
   uint8_t* out;
   PadWK pad;  // padding block of a 64-byte message
+  uint32_t one;
 };
 
+template <bool FMA>
 __global__ void __launch_bounds__(128) merkle_level_kernel(const NodeArgs a) {
+  const uint32_t one = a.one;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_out = (a.n_in + 1) >> 1;
   if (i >= n_out) return;
@@ -203,8 +226,8 @@ __global__ void __launch_bounds__(128) merkle_level_kernel(const NodeArgs a) {
   uint32_t s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = kIV[k];
-  compress(s, w);
-  compress_wk(s, a.pad);
+  compress<FMA>(s, w, one);
+  compress_wk<FMA>(s, a.pad, one);
   store_digest(a.out + 32 * i, s);
   (void)dst;
 }
@@ -229,6 +252,17 @@ PadWK make_pad(int64_t len) {
   return p;
 }
 
+// Which add placement the Merkle kernels use: FMA-pipe adds unless
+// VT_SHA_ALU_ADDS=1 (A/B switch for measurement).
+bool sha_fma_adds() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VT_SHA_ALU_ADDS");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 }  // namespace vt
 
 using namespace vt;
@@ -246,7 +280,12 @@ extern "C" int vt_sha256_leaves(const uint8_t* data, int64_t nbytes, int64_t lea
   a.n_leaves = (nbytes + leaf_bytes - 1) / leaf_bytes;
   a.out = digests;
   a.pad = make_pad(leaf_bytes);
-  sha256_leaves_kernel<<<(unsigned)((a.n_leaves + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  a.one = 1u;
+  const unsigned grid = (unsigned)((a.n_leaves + 127) / 128);
+  if (sha_fma_adds())
+    sha256_leaves_kernel<true><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  else
+    sha256_leaves_kernel<false><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return vt_check_launch("sha256_leaves_kernel");
 }
 
@@ -260,8 +299,13 @@ extern "C" int vt_merkle_level(const uint8_t* in, int64_t n_in, uint8_t* out, vt
   a.n_in = n_in;
   a.out = out;
   a.pad = make_pad(64);
+  a.one = 1u;
   const int64_t n_out = (n_in + 1) / 2;
-  merkle_level_kernel<<<(unsigned)((n_out + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  const unsigned grid = (unsigned)((n_out + 127) / 128);
+  if (sha_fma_adds())
+    merkle_level_kernel<true><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  else
+    merkle_level_kernel<false><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return vt_check_launch("merkle_level_kernel");
 }
 
@@ -307,7 +351,8 @@ extern "C" int vt_merkle_build(const uint8_t* data, int64_t nbytes, int64_t leaf
 // ---------------------------------------------------------------------------
 
 namespace vt {
-__global__ void __launch_bounds__(128) sha256_peak_kernel(uint32_t* sink, int reps) {
+template <bool FMA>
+__global__ void __launch_bounds__(128) sha256_peak_kernel(uint32_t* sink, int reps, uint32_t one) {
   uint32_t s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = kIV[k] ^ (threadIdx.x * 0x9e3779b9u + blockIdx.x);
@@ -318,7 +363,7 @@ __global__ void __launch_bounds__(128) sha256_peak_kernel(uint32_t* sink, int re
     uint32_t w[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) w[k] = m[k] ^ s[k & 7];
-    compress(s, w);
+    compress<FMA>(s, w, one);
   }
   uint32_t acc = 0;
 #pragma unroll
@@ -332,7 +377,10 @@ extern "C" int vt_sha256_peak_bench(uint32_t* sink, int64_t blocks, int reps, vt
     vt_set_error("vt_sha256_peak_bench: bad argument");
     return VT_EINVAL;
   }
-  vt::sha256_peak_kernel<<<(unsigned)blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps);
+  if (vt::sha_fma_adds())
+    vt::sha256_peak_kernel<true><<<(unsigned)blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps, 1u);
+  else
+    vt::sha256_peak_kernel<false><<<(unsigned)blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(sink, reps, 1u);
   return vt_check_launch("sha256_peak_kernel");
 }
 

@@ -14,7 +14,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libvtrain_b200.so")
+import os
+
+# VTRAIN_B200_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = Path(os.environ.get("VTRAIN_B200_LIB") or Path(__file__).resolve().with_name("libvtrain_b200.so"))
 
 VT_OK, VT_EINVAL, VT_ECUDA = 0, -1, -2
 ERR_NONFINITE = 1

@@ -20,6 +20,13 @@
 
 #include "vt_common.cuh"
 
+#ifndef VT_L2_PREFETCH  // round-and-log producer: L2 prefetch of each ticket's tiles when drawn
+#define VT_L2_PREFETCH 1
+#endif
+#ifndef VT_RP_L2_PREFETCH  // replay producer: the same (measured slower; off)
+#define VT_RP_L2_PREFETCH 0
+#endif
+
 namespace vt {
 
 constexpr int kSThreads = 256;
@@ -73,6 +80,13 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+
+// L2 prefetch of a ticket's tiles ahead of their TMA copies (no shared memory,
+// no barrier): the ring holds only kFStages tiles, so without it too few
+// bytes are in flight per SM to cover the loaded HBM latency.
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // Output stores relative to the tile: `o` points at the tile's first output
@@ -277,6 +291,8 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
                                          void* o, int lim, uint4* mslot, uint16_t* row, uint32_t sbase, int warp,
                                          int lane, uint32_t lt, uint32_t& err) {
   uint32_t wcnt = 0;
+  // staged entry of this lane's first element in slot 0: super-tile offset << 1
+  const uint32_t eb = (sbase + (uint32_t)(warp * kSWarpElems + lane * 2)) << 1;
 #pragma unroll
   for (int j = 0; j < kSSlots; ++j) {
     const int e0 = warp * kSWarpElems + j * 64 + lane * 2;
@@ -301,7 +317,10 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
       const uint32_t fb0 = (uint32_t)__float_as_int(f0), fb1 = (uint32_t)__float_as_int(f1);
       u0 = (int32_t)((fb0 << 31) ^ (lo0 << 2) ^ fb0) < 0;
       u1 = (int32_t)((fb1 << 31) ^ (lo1 << 2) ^ fb1) < 0;
-      if (outside_normal32(hi0 & 0x7fffffffu) | outside_normal32(hi1 & 0x7fffffffu)) {
+      // outside the FP32 normal range (subnormal results, overflow, inf / nan):
+      // the whole warp takes the exact routine -- a warp-uniform branch keeps
+      // the common path free of per-lane reconvergence and predicate spills
+      if (__any_sync(0xffffffffu, outside_normal32(hi0 & 0x7fffffffu) | outside_normal32(hi1 & 0x7fffffffu))) {
         uint32_t c0, c1;
         f0 = round_dir32(xv.x, thr32, g.thr_sub, c0, err);
         f1 = round_dir32(xv.y, thr32, g.thr_sub, c1, err);
@@ -327,7 +346,8 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
     // ballot-rank staging of the warp-tile's entries (first kRow only)
     const uint32_t r0 = wcnt + __popc(L0 & lt) + __popc(L1 & lt);
     const uint32_t r1 = r0 + (l0 ? 1u : 0u);
-    const uint32_t v0 = ((sbase + (uint32_t)e0) << 1) | (u0 ? 1u : 0u);
+    const uint32_t v0 = eb + (uint32_t)(j * 128) + (u0 ? 1u : 0u);
+    const uint32_t v1 = eb + (uint32_t)(j * 128 + 2) + (u1 ? 1u : 0u);
     if (KEYS) {  // also each entry's x (the adaptive selection then needs no gather of x)
       double* rk = reinterpret_cast<double*>(row);
       uint16_t* re = row + 4 * kRowK;
@@ -336,12 +356,12 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
         rk[r0] = xv.x;
       }
       if (l1 && r1 < (uint32_t)kRowK) {
-        re[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+        re[r1] = (uint16_t)v1;
         rk[r1] = xv.y;
       }
     } else {
       if (l0 && r0 < (uint32_t)kRow) row[r0] = (uint16_t)v0;
-      if (l1 && r1 < (uint32_t)kRow) row[r1] = (uint16_t)(v0 + 2u - (u0 ? 1u : 0u) + (u1 ? 1u : 0u));
+      if (l1 && r1 < (uint32_t)kRow) row[r1] = (uint16_t)v1;
     }
     wcnt += __popc(L0) + __popc(L1);
   }
@@ -490,7 +510,15 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
   if (warp == kProdWarp) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
+      // a ticket's whole tiles into L2 as soon as it is drawn
+      auto prefetch = [&](int64_t s) {
+        if (s < 0 || s >= a.num_super) return;
+        const int64_t t0 = st_first(a, s);
+        const int64_t t1 = min(t0 + (int64_t)st_ntiles(a, s), full_tiles);
+        if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
+      };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+      if (VT_L2_PREFETCH) prefetch(s);
       int64_t q = 0;  // ring sequence number
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
@@ -504,7 +532,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
           if (i == 0) S.ids[k & 3] = s;
           // draw the next ticket with this ordinal's last tile: late enough that
           // the grid runs dry together, early enough to hide the atomic
-          if (i == nt - 1 && s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+          if (i == nt - 1 && s >= 0) {
+            nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+            if (VT_L2_PREFETCH) prefetch(nxt);
+          }
           const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
             fence_proxy_async();
@@ -754,7 +785,14 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
         }
         return ti;
       };
+      // a ticket's whole tiles into L2 as soon as it is drawn (as rl_fused_kernel)
+      auto prefetch = [&](const TicketInfo& ti) {
+        if (!VT_L2_PREFETCH || ti.s < 0) return;
+        const int64_t t1 = min(ti.t0 + (int64_t)ti.nt, ti.full_tiles);
+        if (t1 > ti.t0) l2_prefetch(ti.x + ti.t0 * kSTile, (uint32_t)((t1 - ti.t0) * kSTile * sizeof(double)));
+      };
       TicketInfo cur = lookup(draw());
+      prefetch(cur);
       int64_t q = 0;  // ring sequence number
       for (int64_t k = 0;; ++k) {
         const int64_t s = cur.s;
@@ -779,7 +817,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
           }
           // the next ticket after this tile's copy is in flight: draw() waits
           // on its atomic and the tensor lookup, the TMA must not
-          if (i == nt - 1 && s >= 0) nxt = lookup(draw());
+          if (i == nt - 1 && s >= 0) {
+            nxt = lookup(draw());
+            prefetch(nxt);
+          }
         }
         if (s < 0) break;
         cur = nxt;
@@ -1106,7 +1147,18 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
   if (warp == kWarps) {  // producer: tickets and TMA
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
+      // a ticket's whole tiles into L2 as soon as it is drawn -- off: the
+      // replay's 4-stage ring already covers the latency, and the prefetch
+      // cost it 2-8% (2^24: 0.66 vs 0.75 of the copy peak; the round-and-log
+      // gains 8-10%, see rl_fused_kernel)
+      auto prefetch = [&](int64_t s) {
+        if (!VT_RP_L2_PREFETCH || s < 0 || s >= a.num_super) return;
+        const int64_t t0 = rp_first(a, s);
+        const int64_t t1 = min(t0 + (int64_t)rp_ntiles(a, s), full_tiles);
+        if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
+      };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+      prefetch(s);
       int64_t q = 0;
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
@@ -1119,7 +1171,10 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
         for (int i = 0; i < nt; ++i, ++q) {
           const int st = (int)(q % kRStages);
           mbar_wait(S.empty + st, (uint32_t)(((q / kRStages) & 1) ^ 1));
-          if (i == nt - 1 && s >= 0) nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+          if (i == nt - 1 && s >= 0) {
+            nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
+            prefetch(nxt);
+          }
           const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
             fence_proxy_async();

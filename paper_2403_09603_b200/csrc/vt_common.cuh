@@ -337,6 +337,9 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
               const int32_t* gate = nullptr, uint64_t* keys = nullptr);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
+int rp_stream_packed(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out,
+                     const uint8_t* payload, int64_t nbytes, int64_t pos, int64_t* counters, int32_t* err, void* ws,
+                     cudaStream_t st);
 
 // Batched trainer pass: up to kMaxBatch tensors in one launch of the fused
 // round-and-log.  The table travels by value as a __grid_constant__ kernel

@@ -984,9 +984,9 @@ struct RPArgs {
   const double* x;
   int64_t n;
   Grid g;
-  const uint64_t* log;
-  int64_t n_words;
-  int64_t log_base;
+  const uint64_t* log;  // sparse words; PACKED: the .vtrl payload (bytes)
+  int64_t n_words;      // sparse words; PACKED: payload bytes
+  int64_t log_base;     // global index of element 0; PACKED: its stream position in the payload
   void* out;
   int64_t num_tiles;
   int64_t num_super;  // tickets, as for the trainer: n4 chunks of kSuper tiles, then single tiles
@@ -1002,7 +1002,8 @@ constexpr int kRIds = 8;                   // ordinals in flight between the thr
 
 struct ReplaySmem {
   double ring[kRStages][kSTile];
-  uint8_t cmap[kSTile];             // code map of the current tile, all 1 between tiles
+  uint8_t cmap[kSTile];             // code map of the current tile, all 1 between tiles (sparse)
+  uint16_t lut[256];                // PACKED: a payload byte's five base-3 digits, 2 bits each; bit 15 = invalid
   int64_t ids[kRIds], curs[kRIds];  // ticket (producer) and first log word (search warp) of ordinal k
   uint64_t full[kRStages], empty[kRStages], tfull[kRIds], nfull[kRIds];
   uint32_t red[kWarps];
@@ -1067,7 +1068,7 @@ __device__ int64_t log_lower_bound(const RPArgs& a, int64_t key, int lane) {
 // One tile of the auditor pass.  Each thread reads the codes of its own
 // elements from the map and resets them to 1, so the map is all-ignore
 // again for the next tile without an extra barrier.
-template <int OUT, bool FAST, bool FULL>
+template <int OUT, bool FAST, bool FULL, bool RESET = true>
 __device__ __forceinline__ uint32_t rp_tile(const RPArgs& a, const double* src, uint8_t* cs, void* o, int lim,
                                             int warp, int lane, uint32_t& err) {
   uint32_t flips = 0;
@@ -1077,7 +1078,7 @@ __device__ __forceinline__ uint32_t rp_tile(const RPArgs& a, const double* src, 
     const double2 xv = *reinterpret_cast<const double2*>(src + e0);
     uint16_t* cp = reinterpret_cast<uint16_t*>(cs + e0);
     const uint32_t cc = *cp;
-    *cp = 0x0101;
+    if (RESET) *cp = 0x0101;
     const uint32_t c0 = cc & 0xffu, c1 = cc >> 8;
     uint32_t f0, f1;
     if (FAST) {
@@ -1116,6 +1117,49 @@ __device__ __forceinline__ int scatter_window(uint8_t* cs, uint64_t w, uint64_t 
   return cnt;
 }
 
+// PACKED (.vtrl payload, roundlog.py:67-82): the three payload bytes holding
+// the codes of this thread's 8 consecutive elements [e8, e8 + 8) of a tile,
+// loaded a tile ahead (they sit at stream positions pos .. pos + 7).
+struct PackedWin {
+  uint32_t b0, b1, b2;
+  int ph;   // digit of the first element inside b0
+  int nv;   // valid elements of the 8
+};
+
+__device__ __forceinline__ PackedWin packed_load(const RPArgs& a, int64_t tbase, int tid) {
+  PackedWin w{1u, 1u, 1u, 0, 0};
+  const int64_t e = tbase + (int64_t)tid * 8;
+  w.nv = (int)std::max<int64_t>(0, std::min<int64_t>(8, a.n - e));
+  if (w.nv == 0) return w;
+  const int64_t pos = a.log_base + e;
+  const int64_t bi = pos / 5;
+  w.ph = (int)(pos - 5 * bi);
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(a.log);
+  const int last = (w.ph + w.nv - 1) / 5;  // byte offset of the last valid digit
+  w.b0 = bi < a.n_words ? (uint32_t)__ldg(p + bi) : 255u;
+  if (last >= 1) w.b1 = bi + 1 < a.n_words ? (uint32_t)__ldg(p + bi + 1) : 255u;
+  if (last >= 2) w.b2 = bi + 2 < a.n_words ? (uint32_t)__ldg(p + bi + 2) : 255u;
+  return w;
+}
+
+// decode the window into the code map: 8 code bytes, one 8-byte store
+__device__ __forceinline__ void packed_decode(const PackedWin& w, const uint16_t* lut, uint8_t* cs, int tid,
+                                              uint32_t& err) {
+  if (w.nv == 0) {
+    *reinterpret_cast<uint2*>(cs + tid * 8) = make_uint2(0x01010101u, 0x01010101u);
+    return;
+  }
+  const uint32_t l0 = lut[w.b0 & 0xffu], l1 = lut[w.b1 & 0xffu], l2 = lut[w.b2 & 0xffu];
+  if ((l0 | l1 | l2) & 0x8000u) err |= VT_ERR_BAD_LOG_BYTE;  // a byte > 242 (corrupt log byte)
+  // 15 digits of 2 bits, starting at this thread's first element
+  uint32_t c = ((l0 & 0x3ffu) | ((l1 & 0x3ffu) << 10) | ((l2 & 0x3ffu) << 20)) >> (2 * w.ph);
+  if (w.nv < 8) c = (c & ((1u << (2 * w.nv)) - 1u)) | (0x5555u & ~((1u << (2 * w.nv)) - 1u));  // past n: code 1
+  auto spread = [](uint32_t x) {  // four 2-bit codes -> four bytes
+    return (x & 3u) | ((x & 0xcu) << 6) | ((x & 0x30u) << 12) | ((x & 0xc0u) << 18);
+  };
+  *reinterpret_cast<uint2*>(cs + tid * 8) = make_uint2(spread(c & 0xffu), spread((c >> 8) & 0xffu));
+}
+
 // Auditor kernel, warp-specialised like the trainer's: the producer warp
 // draws tickets (super-tiles of kSuper tiles) and keeps kRStages TMA copies in
 // flight; the search warp finds each ordinal's first log word
@@ -1123,7 +1167,7 @@ __device__ __forceinline__ int scatter_window(uint8_t* cs, uint64_t w, uint64_t 
 // the compute warps scatter each tile's log slice into the code map and
 // replay the tile, prefetching the next tile's window of log words while the
 // current one computes (across ordinals too, through nfull).
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool PACKED = false>
 __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   ReplaySmem& S = *reinterpret_cast<ReplaySmem*>(smraw);
@@ -1131,6 +1175,15 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
   const int64_t full_tiles = a.n / kSTile;
   if (tid == 0) TL(0);
   if (tid < kSThreads) reinterpret_cast<uint2*>(S.cmap)[tid] = make_uint2(0x01010101u, 0x01010101u);
+  if (PACKED && tid < 256) {
+    uint32_t t = (uint32_t)tid, v = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      v |= (t % 3u) << (2 * k);
+      t /= 3u;
+    }
+    S.lut[tid] = (uint16_t)(v | (tid > 242 ? 0x8000u : 0u));
+  }
   if (tid == 0) {
     for (int st = 0; st < kRStages; ++st) {
       mbar_init(S.full + st, 1);
@@ -1193,7 +1246,7 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
       const int m = (int)(k % kRIds);
       mbar_wait(S.tfull + m, (uint32_t)((k / kRIds) & 1));
       const int64_t s = S.ids[m];
-      const int64_t cur = (s >= 0) ? log_lower_bound(a, a.log_base + rp_first(a, s) * kSTile, lane) : 0;
+      const int64_t cur = (!PACKED && s >= 0) ? log_lower_bound(a, a.log_base + rp_first(a, s) * kSTile, lane) : 0;
       if (lane == 0) {
         S.curs[m] = cur;
         mbar_arrive(S.nfull + m);
@@ -1204,6 +1257,7 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
     uint32_t err = 0, flips = 0;
     int64_t q = 0;
     uint64_t pw = 0, pp = 0;  // prefetched window for the next tile (word at cur + tid, its predecessor)
+    PackedWin pwin{1u, 1u, 1u, 0, 0};  // PACKED: the next tile's payload bytes
     bool pref = false;
     int64_t cur = 0;
     for (int64_t k = 0;; ++k) {
@@ -1212,6 +1266,43 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
       if (s < 0) break;
       const int nt = rp_ntiles(a, s);
       const int64_t t0 = rp_first(a, s);
+      if (PACKED) {
+#pragma unroll 1
+        for (int i = 0; i < nt; ++i, ++q) {
+          const int64_t t = t0 + i;
+          const int64_t tbase = t * kSTile;
+          // this tile's payload window (loaded a tile ahead, except the first)
+          if (!pref) pwin = packed_load(a, tbase, tid);
+          const PackedWin cw = pwin;
+          // the next tile of this ticket, or of the next ticket once it is known
+          int64_t nbase = -1;
+          if (i + 1 < nt) {
+            nbase = tbase + kSTile;
+          } else {
+            mbar_wait(S.nfull + ((k + 1) % kRIds), (uint32_t)(((k + 1) / kRIds) & 1));
+            const int64_t s2 = S.ids[(k + 1) % kRIds];
+            if (s2 >= 0) nbase = rp_first(a, s2) * kSTile;
+          }
+          pref = nbase >= 0;
+          if (pref) pwin = packed_load(a, nbase, tid);
+          packed_decode(cw, S.lut, S.cmap, tid, err);
+          const int st = (int)(q % kRStages);
+          const double* src = S.ring[st];
+          mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1));
+          if (t >= full_tiles) {  // partial last tile: plain loads into the (unused) ring slot
+            double* dst = S.ring[st];
+            for (int e = tid; e < kSTile; e += kSThreads) dst[e] = (tbase + e < a.n) ? a.x[tbase + e] : 0.0;
+          }
+          compute_sync();  // code map decoded, x tile resident
+          void* o = tile_out<OUT>(a.out, tbase);
+          flips += (t < full_tiles)
+                       ? rp_tile<OUT, FAST, true, false>(a, src, S.cmap, o, kSTile, warp, lane, err)
+                       : rp_tile<OUT, FAST, false, false>(a, src, S.cmap, o, (int)(a.n - tbase), warp, lane, err);
+          compute_sync();  // ring slot and code map consumed
+          if (tid == 0) mbar_arrive(S.empty + st);
+        }
+        continue;
+      }
       if (!pref) {
         cur = S.curs[k % kRIds];
         const int64_t i = cur + tid;
@@ -1400,11 +1491,11 @@ int rl_stream_batch(const RLBatch& b, bool fast, int out_kind, cudaStream_t st, 
   return keys ? rl_stream_batch_t<true>(b, fast, out_kind, st) : rl_stream_batch_t<false>(b, fast, out_kind, st);
 }
 
-template <int OUT, bool FAST>
+template <int OUT, bool FAST, bool PACKED = false>
 static int launch_rp(RPArgs a, cudaStream_t st) {
   const size_t smem = sizeof(ReplaySmem);
   static_assert(sizeof(ReplaySmem) <= 74 * 1024, "three replay CTAs per SM");
-  auto k = rp_fused_kernel<OUT, FAST>;
+  auto k = rp_fused_kernel<OUT, FAST, PACKED>;
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1419,6 +1510,21 @@ static int launch_rp(RPArgs a, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>(a.num_super, resident);
   k<<<grid, kRThreads, smem, st>>>(a);
   return vt_check_launch("rp_fused_kernel");
+}
+
+int rp_stream_packed(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out,
+                     const uint8_t* payload, int64_t nbytes, int64_t pos, int64_t* counters, int32_t* err, void* ws,
+                     cudaStream_t st) {
+  RPArgs a{x, n, g, reinterpret_cast<const uint64_t*>(payload), nbytes, pos, out, stream_tiles(n), 0, 0,
+           static_cast<FusedHeader*>(ws), counters, err};
+  if (fast) {
+    return out_kind == VT_OUT_F32 ? launch_rp<VT_OUT_F32, true, true>(a, st)
+         : out_kind == VT_OUT_F64 ? launch_rp<VT_OUT_F64, true, true>(a, st)
+                                  : launch_rp<VT_OUT_NONE, true, true>(a, st);
+  }
+  return out_kind == VT_OUT_F32 ? launch_rp<VT_OUT_F32, false, true>(a, st)
+       : out_kind == VT_OUT_F64 ? launch_rp<VT_OUT_F64, false, true>(a, st)
+                                : launch_rp<VT_OUT_NONE, false, true>(a, st);
 }
 
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,

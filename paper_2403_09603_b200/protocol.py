@@ -91,8 +91,10 @@ class GpuAuditorChannel:
         np.copyto(st.hview(0, n, np.float64), a.reshape(-1))
         st.hview(fo, 32, np.int64)[:] = 0
         st.h2d(fo + 256)
+        ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "replay_packed")
         _lib.call("vt_replay", st.dptr(0), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload), self.reader.payload_nbytes,
-                  pos, _lib.OUT_F64, st.dptr(oy), st.dptr(fo + 16), st.dptr(fo), None, 0, D.stream_ptr())
+                  pos, _lib.OUT_F64, st.dptr(oy), st.dptr(fo + 16), st.dptr(fo), D.ptr(ws), ws.numel(),
+                  D.stream_ptr())
         st.d2h_wait(fo, oy + 8 * n)
         fl = st.hview(fo, 6, np.int64)
         err = int(fl[0]) & 0xFFFFFFFF
@@ -112,9 +114,10 @@ class GpuAuditorChannel:
         if isinstance(self.reader, LogReader):
             payload, pos = self.reader.take_device(n)
             if n:
+                ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "replay_packed")
                 _lib.call("vt_replay", D.ptr(t), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload),
                           self.reader.payload_nbytes, pos, _lib.OUT_F64, D.ptr(y), f.cnt_ptr, f.err_ptr,
-                          None, 0, D.stream_ptr())
+                          D.ptr(ws), ws.numel(), D.stream_ptr())
         else:
             codes = np.ascontiguousarray(self.reader.read_array(n), dtype=np.uint8)
             c = torch.from_numpy(codes).to(t.device)

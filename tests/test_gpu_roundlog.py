@@ -157,3 +157,65 @@ def test_unpack_and_histogram_device(rl, oracle):
     assert packed.cpu().numpy().tobytes() == oracle.pack_groups(digits)
     for pos, n in [(0, 17), (3, 1000), (7, 5 * 40_000 - 7)]:
         assert np.array_equal(rl.unpack_device(packed, pos, n).cpu().numpy(), digits[pos:pos + n])
+
+
+def _packed_payload(codes_all):
+    """Reference .vtrl payload bytes for a code stream (roundlog.py:67-70, pad with 1)."""
+    c = np.asarray(codes_all, dtype=np.uint8)
+    pad = (-c.size) % 5
+    g = np.concatenate([c, np.ones(pad, np.uint8)]).reshape(-1, 5).astype(np.uint16)
+    return (g * np.array([1, 3, 9, 27, 81], np.uint16)).sum(1).astype(np.uint8)
+
+
+@pytest.mark.parametrize("b_r,out64", [(32, False), (32, True), (26, True)])
+def test_fused_packed_replay_matches_oracle_and_tile_path(oracle, b_r, out64):
+    """vt_replay with the .vtrl payload through the persistent TMA replay
+    (rp_fused_kernel<PACKED>, a workspace given) == the per-tile
+    replay_kernel<PACKED> (no workspace) == oracle rev_array, over ragged
+    sizes and every stream phase; a corrupt byte and a short payload raise
+    the error bit."""
+    import torch
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, workloads
+    rng = np.random.default_rng(17)
+    for n in (1, 4, 5, 2047, 2048, 2049, 8192 * 3 + 7, (1 << 18) + 3, (1 << 20) + 13):
+        for pos in (0, 1, 3, 4, 12_345_679):
+            x = workloads.config0_x(n, n % 97) * (1.0 if b_r == 32 else 3.0)
+            codes = rng.integers(0, 3, size=n).astype(np.uint8)
+            stream_pos = pos  # the tensor's first entry in the .vtrl stream
+            lead = stream_pos % 5  # earlier entries sharing its first byte (code 1 here)
+            payload = np.concatenate([np.zeros(stream_pos // 5, np.uint8),
+                                      _packed_payload(np.concatenate([np.ones(lead, np.uint8), codes]))])
+            want = oracle.rev_array(x, b_r, codes)
+            want = want if out64 else want.astype(np.float32)
+            corr_want = int(np.count_nonzero(oracle.rev_array(x, b_r, codes) != oracle.rnd_array(x, b_r)))
+            xd = torch.from_numpy(x).cuda()
+            pd = torch.from_numpy(payload).cuda()
+            res = []
+            for use_ws in (True, False):
+                y = torch.empty(n, dtype=torch.float64 if out64 else torch.float32, device="cuda")
+                f = D.Flags()
+                ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "t_packed") if use_ws else None
+                _lib.call("vt_replay", D.ptr(xd), n, b_r, _lib.LOG_PACKED, D.ptr(pd), payload.size, stream_pos,
+                          _lib.OUT_F64 if out64 else _lib.OUT_F32, D.ptr(y), f.cnt_ptr, f.err_ptr,
+                          D.ptr(ws) if use_ws else None, ws.numel() if use_ws else 0, D.stream_ptr())
+                err, cnt = f.read()
+                assert err == 0, (n, pos, use_ws, err)
+                assert cnt[0] == corr_want, (n, pos, use_ws)
+                res.append(bits(y.cpu().numpy()))
+            assert np.array_equal(res[0], bits(want)), (n, pos)
+            assert np.array_equal(res[1], res[0])
+    # a corrupt byte inside the tensor's range, and a payload cut short
+    n = 300_001  # above the fused path's size threshold
+    x = torch.from_numpy(workloads.config0_x(n, 5)).cuda()
+    payload = _packed_payload(np.ones(n, np.uint8))
+    for bad, length in ((payload.copy(), payload.size), (payload, payload.size - 3)):
+        if length == payload.size:
+            bad[54_321] = 250
+        pd = torch.from_numpy(bad).cuda()
+        y = torch.empty(n, dtype=torch.float32, device="cuda")
+        f = D.Flags()
+        ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "t_packed")
+        _lib.call("vt_replay", D.ptr(x), n, 32, _lib.LOG_PACKED, D.ptr(pd), length, 0, _lib.OUT_F32, D.ptr(y),
+                  f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(), D.stream_ptr())
+        assert f.read()[0] & _lib.ERR_BAD_LOG_BYTE

@@ -1068,10 +1068,14 @@ def _pair_job(job):
     return hi - lo, int(np.count_nonzero(codes != 1)), corr
 
 
-def cpu_pair(total: int, procs: int, chunk: int = 1 << 22, seed: int = 100) -> dict:
+def cpu_pair(total: int, procs: int, chunk: int | None = None, seed: int = 100) -> dict:
     """configs[1] pair over ``total`` elements: GB/s of the step's algorithmic
-    bytes (both channels, the GPU formula) over the same-run wall clock."""
+    bytes (both channels, the GPU formula) over the same-run wall clock.
+    Chunks of 2^22 elements, smaller when needed so every
+    process has at least two."""
     from paper_2403_09603_b200 import workloads
+    if chunk is None:
+        chunk = max(1 << 16, min(1 << 22, total // (2 * max(procs, 1))))
     xt, xa = workloads.config1_pair(total, seed)
     _CPU.update(xt=xt, xa=xa, tau=workloads.TAU_CONFIG0)
     jobs = [(lo, min(total, lo + chunk)) for lo in range(0, total, chunk)]
@@ -1082,7 +1086,8 @@ def cpu_pair(total: int, procs: int, chunk: int = 1 << 22, seed: int = 100) -> d
             _CPU.pop(k, None)
     n = sum(r[0] for r in res)
     f = sum(r[1] for r in res) / n
-    return {"gbs": n * (8 + 4 + 8 * f) * 2 / wall / 1e9, "n": n, "wall_s": wall, "f": f, "procs": procs}
+    return {"gbs": n * (8 + 4 + 8 * f) * 2 / wall / 1e9, "n": n, "wall_s": wall, "f": f, "procs": procs,
+            "chunk": chunk}
 
 
 def _budget_job(job):
@@ -1170,8 +1175,9 @@ def cpu_baseline(args) -> dict:
     r1 = cpu_pair(1 << 22, 1)
     return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": cores, "kind": F.kind,
             "value_1core": round(r1["gbs"], 4),
-            "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair in 2^22 chunks over {cores} processes "
-                      f"(P=1: 2^22 elements in process); trainer channel: direction_array + _pack_block + rnd_array; "
+            "sample": f"2^{args.cpu_log2n} elements of the configs[1] pair in chunks of {r['chunk']} over {cores} "
+                      f"processes (P=1: 2^22 elements in process); trainer channel: direction_array + _pack_block + "
+                      f"rnd_array; "
                       f"auditor: rev_array + rnd_array count; same-run wall clock {r['wall_s']:.2f}s / "
                       f"{r1['wall_s']:.2f}s; {F.what}",
             "cpu_model": _cpu_model()}
@@ -1240,7 +1246,8 @@ def run_reference(args) -> None:
                    "n_per_gpu": 1 << args.log2n, "parallelism": f"{cores} host processes",
                    "sample": f"each step times a bounded sample of 2^{args.cpu_log2n} elements of that pair"},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": F.kind,
-                         "sample": f"2^{args.cpu_log2n} elements per step in 2^22 chunks, wall clock; {F.what}",
+                         "sample": f"2^{args.cpu_log2n} elements per step in chunks of {vals[-1]['chunk']} over {cores} "
+                                   f"processes, wall clock; {F.what}",
                          "cpu_model": _cpu_model()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,

@@ -510,15 +510,14 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
   if (warp == kProdWarp) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-      // a ticket's whole tiles into L2 as soon as it is drawn
-      auto prefetch = [&](int64_t s) {
+      // a ticket's whole tiles (from its tile `from` on) into L2 as soon as it is drawn
+      auto prefetch = [&](int64_t s, int from) {
         if (s < 0 || s >= a.num_super) return;
-        const int64_t t0 = st_first(a, s);
-        const int64_t t1 = min(t0 + (int64_t)st_ntiles(a, s), full_tiles);
+        const int64_t t0 = st_first(a, s) + from;
+        const int64_t t1 = min(st_first(a, s) + (int64_t)st_ntiles(a, s), full_tiles);
         if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
       };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
-      if (VT_L2_PREFETCH) prefetch(s);
       int64_t q = 0;  // ring sequence number
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
@@ -534,7 +533,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
           // the grid runs dry together, early enough to hide the atomic
           if (i == nt - 1 && s >= 0) {
             nxt = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
-            if (VT_L2_PREFETCH) prefetch(nxt);
+            if (VT_L2_PREFETCH) prefetch(nxt, 0);
           }
           const int64_t t = t0 + i;
           if (s >= 0 && t < full_tiles) {
@@ -543,6 +542,8 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
           } else {
             mbar_arrive(S.full + st);
           }
+          // the first ticket: its tiles beyond the ring, once the ring's copies are issued
+          if (VT_L2_PREFETCH && k == 0 && i == kFStages - 1) prefetch(s, kFStages);
         }
         if (s < 0) break;
         s = nxt;

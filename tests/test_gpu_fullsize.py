@@ -17,7 +17,8 @@ oracle on the same bits, at the size the bench times it:
 * configs[4]: the 1.5e9-parameter FP32 checkpoint's chunked Merkle tree,
   every node of every level against hashlib (merkle.py:24-25, 55-72);
 * the size sweep's 2^32 + 12,345 point: the first and the last 2^28
-  elements (indices past 2^32) of the log and output against the oracle.
+  elements (indices past 2^32) of the log and output against the oracle;
+* the north-star 2^30 pair, every element.
 
 The oracle runs over all host cores (``oracle/vt_parallel.py``: chunked,
 fork-shared inputs, comparisons in the workers); the checks are bit-exact.
@@ -198,3 +199,35 @@ def test_max_size_ends_vs_oracle():
                                   base=base + lo)
         P.assert_clean(r, f"[{lo}, {hi})")
     assert 0.09 * n < log.count < 0.11 * n and corr > 0
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(900)
+def test_north_star_2e30_pair_every_element_vs_oracle():
+    """The north-star size: a 2^30-element FP64 trainer tensor (the size
+    sweep's distribution) and its auditor copy with +-1 FP64 ulp on ~5% of
+    the elements -- every log word, every trainer and auditor FP32 output and
+    the correction count against the oracle, element for element."""
+    import torch
+    import vt_parallel as P
+
+    from paper_2403_09603_b200 import ops, workloads
+    n = 1 << 30
+    tau = workloads.TAU_CONFIG0
+    xt = workloads.config0_x_torch_bernoulli(n, seed=30)
+    yt, log = ops.round_and_log(xt, 32, tau, log_out=torch.empty(n // 8, dtype=torch.int64, device="cuda"))
+    xt_h = _np(xt)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(31)
+    m = torch.rand(n, device="cuda", generator=g) < 0.05
+    up = torch.rand(n, device="cuda", generator=g) < 0.5
+    tgt = torch.where(up, torch.full((1,), float("inf"), dtype=torch.float64, device="cuda"),
+                      torch.full((1,), float("-inf"), dtype=torch.float64, device="cuda"))
+    xa = torch.where(m, torch.nextafter(xt, tgt), xt)
+    del m, up, tgt, xt
+    torch.cuda.empty_cache()
+    ya, corr = ops.replay(xa, 32, log)
+    r = P.check_round_and_log(xt_h, 32, tau, _np(log.words), _np(yt), _np(xa), _np(ya))
+    P.assert_clean(r, "2^30")
+    assert r["corrections"] == corr > 0
+    assert torch.equal(yt.view(torch.int32), ya.view(torch.int32))

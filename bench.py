@@ -744,8 +744,10 @@ def budget_search() -> dict:
     """The standalone budget search (protocol.search_tau_budget ->
     vt_tau_budget: one read of x + the cooperative selection / bisection) at
     2^26 and 2^30 N(0,1) elements, 0.5% budget; algorithmic bytes = 8 per
-    element (one read of x).  The sharded form's exact 5-pass select
-    (dist.kth_largest_distance_sharded, one rank) is timed beside it."""
+    element (one read of x).  The sharded form (dist.search_tau_budget_sharded
+    on one process: candidate pass, exchange buffer, digit keys, host
+    selection -- host wall time incl. its syncs) and one pass of its exact
+    5-pass fallback are timed beside it."""
     import torch
 
     from paper_2403_09603_b200 import _device as D
@@ -771,8 +773,17 @@ def budget_search() -> dict:
         tau = float(res[0].item())
         assert tau == protocol.search_tau_budget(x, 32, B)
         ms5 = _time(lambda: vdist.ShardedKth(x, 32).local_hist(0), reps=5)  # one of the 5 exact passes
+        # the sharded form on one process: candidates + exchange buffer + digit keys + host selection
+        t_sh = []
+        for _ in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tau_sh = vdist.search_tau_budget_sharded(x, 32, B)
+            t_sh.append(time.perf_counter() - t0)
+        assert tau_sh == tau
         out[f"2^{lg}"] = {"ms": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1), "frac": round(8 * n / ms / 1e6 / peak, 4),
                           "tau_over_2^-24": round(tau / 2.0 ** -24, 6),
+                          "sharded_candidate_path_ms_wall": round(1e3 * min(t_sh[1:]), 3),
                           "sharded_exact_select_pass_ms": round(ms5, 4),
                           "sharded_exact_select_5_passes_ms_est": round(5 * ms5, 4)}
         del x, ws

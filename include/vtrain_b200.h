@@ -32,6 +32,7 @@
  *   vt_tau_kth_begin/hist/select: the same, one pass at a time (sharded tensors)
  *   vt_tau_budget_key    SURVEY.md Appendix A.4)
  *   vt_tau_budget     <- the same budget search incl. the bisection, one read of x
+ *   vt_tau_shard_*    <- the same over a tensor sharded across ranks
  *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
@@ -186,6 +187,26 @@ int vt_tau_budget_key(const double *x, int64_t n, int b_r, int64_t budget, doubl
 size_t vt_tau_budget_workspace(int64_t n);
 int vt_tau_budget(const double *x, int64_t n, int b_r, int64_t budget, int iters, double *tau_out,
                   uint64_t *key_out, int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * The budget search over ONE tensor sharded across ranks,
+ * candidate path: vt_tau_shard_plan gives the global plan (candidate
+ * threshold L as FP64 bits, digit shift) -- a function of the global n and
+ * budget only; vt_tau_shard_candidates reads this rank's shard once and fills
+ * xbuf (int64[2051]: 2048 top-digit counts of the candidate keys, keys above
+ * tau_hi, candidates, overflow flag) for the caller to sum over the ranks;
+ * vt_tau_shard_digit_keys writes this rank's keys in the selected digit for
+ * the caller to gather; the exact order statistic of the gathered keys and
+ * the bisection are the caller's (dist.search_tau_budget_sharded).  One
+ * workspace (vt_tau_shard_workspace(n), zero-filled once) per rank and
+ * stream, used by the two calls of one search.
+ */
+size_t vt_tau_shard_workspace(int64_t n);
+int vt_tau_shard_plan(int64_t n_global, int b_r, int64_t budget, uint64_t *L_key, int *s0);
+int vt_tau_shard_candidates(const double *x, int64_t n, int b_r, int64_t n_global, int64_t budget,
+                            int64_t *xbuf, int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+int vt_tau_shard_digit_keys(int64_t n, int b_r, int64_t n_global, int64_t budget, int64_t digit,
+                            uint64_t *keys_out, int64_t keys_cap, int64_t *count, void *ws, size_t ws_bytes,
+                            vt_stream_t stream);
 /*
  * Per-tensor adaptive round-and-log with no host round trip: budget select
  * (vt_tau_budget_key), the 30-step search_tau-skeleton bisection on the

@@ -62,6 +62,10 @@ EXPORTS: dict[str, tuple] = {
     "vt_tau_budget_key": (_i32, [_p, _i64, _i32, _i64, _dbl, _dbl, _p, _p, _p, _p, _sz, _p]),
     "vt_tau_budget_workspace": (_sz, [_i64]),
     "vt_tau_budget": (_i32, [_p, _i64, _i32, _i64, _i32, _p, _p, _p, _p, _sz, _p]),
+    "vt_tau_shard_workspace": (_sz, [_i64]),
+    "vt_tau_shard_plan": (_i32, [_i64, _i32, _i64, _p, _p]),
+    "vt_tau_shard_candidates": (_i32, [_p, _i64, _i32, _i64, _i64, _p, _p, _p, _sz, _p]),
+    "vt_tau_shard_digit_keys": (_i32, [_i64, _i32, _i64, _i64, _i64, _p, _i64, _p, _p, _sz, _p]),
     "vt_round_log_adaptive_workspace": (_sz, [_i64]),
     "vt_round_log_adaptive": (_i32, [_p, _i64, _i32, _i64, _i32, _i32, _p, _p, _i64, _i64, _p, _p, _p, _p, _p,
                                      _p, _sz, _p]),

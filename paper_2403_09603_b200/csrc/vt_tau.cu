@@ -1843,6 +1843,147 @@ extern "C" int vt_tau_budget(const double* x, int64_t n, int b_r, int64_t budget
 
 
 // ---------------------------------------------------------------------------
+// One tensor sharded over ranks: the budget search through the
+// candidate path, with the two exchanges as collectives between the steps.
+//   1. every rank: one read of its shard for the candidates above the GLOBAL
+//      plan's L (the plan depends only on the global n and budget, so every
+//      rank uses the same L), their keys, and a histogram of their top digit
+//      plus the count above tau_hi, the candidate count and an overflow flag
+//      (vt_tau_shard_candidates) -> summed over the ranks (all-reduce);
+//   2. every rank: the same digit from the summed histogram, then its keys in
+//      that digit (vt_tau_shard_digit_keys) -> gathered from every rank;
+//   3. the exact order statistic among the gathered keys and the FP64
+//      bisection (host).  One read of x per rank instead of the 5-pass exact
+//      select, which remains the fallback (too few candidates / overflow).
+// Exchange buffer (int64): [0, 2048) digit counts, [2048] keys > tau_hi,
+// [2049] candidates, [2050] 1 if this rank's candidates overflowed.
+// ---------------------------------------------------------------------------
+namespace vt {
+constexpr int kShardX = kAdBins + 3;
+
+__global__ void __launch_bounds__(kAdThreads) shard_hist_kernel(uint64_t* __restrict__ ck, const AdaptHdr* h,
+                                                                int64_t cap, Grid g0, uint64_t L_key,
+                                                                uint64_t hi_key, int s0,
+                                                                unsigned long long* __restrict__ xbuf,
+                                                                int32_t* errp) {
+  __shared__ uint32_t sh[kAdBins];
+  __shared__ unsigned long long s_above;
+  const int64_t Mraw = h->ccount;
+  const int64_t M = Mraw < cap ? Mraw : cap;
+  for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0u;
+  if (threadIdx.x == 0) s_above = 0ull;
+  __syncthreads();
+  uint32_t err = 0;
+  unsigned long long above = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < M; i += (int64_t)gridDim.x * kAdThreads) {
+    const uint64_t key = dist_key(__longlong_as_double((long long)ck[i]), g0, err);
+    ck[i] = key;  // the keys, in place of the x values, for the digit step
+    if (key > hi_key) ++above;
+    else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
+  }
+  for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, above);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAdBins; i += kAdThreads)
+    if (sh[i]) atomicAdd(xbuf + i, (unsigned long long)sh[i]);
+  if (threadIdx.x == 0) {
+    if (s_above) atomicAdd(xbuf + kAdBins, s_above);
+    if (blockIdx.x == 0) {
+      xbuf[kAdBins + 1] = (unsigned long long)Mraw;
+      xbuf[kAdBins + 2] = Mraw > cap ? 1ull : 0ull;
+    }
+  }
+  report_err(errp, err);
+}
+
+__global__ void __launch_bounds__(kAdThreads) shard_digit_kernel(const uint64_t* __restrict__ ck, AdaptHdr* h,
+                                                                 int64_t cap, uint64_t L_key, uint64_t hi_key,
+                                                                 int s0, uint64_t digit,
+                                                                 uint64_t* __restrict__ out, int64_t out_cap,
+                                                                 unsigned long long* count) {
+  const int64_t Mraw = h->ccount;
+  const int64_t M = Mraw < cap ? Mraw : cap;
+  const uint64_t lo1 = L_key + 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint64_t key = i < M ? ck[i] : 0ull;
+    const bool in = i < M && key <= hi_key && key >= lo1 && ((key - lo1) >> s0) == digit;
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if (lane == leader) pos = atomicAdd(count, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      const unsigned long long p = pos + __popc(m & lanemask_lt());
+      if (in && (int64_t)p < out_cap) out[p] = key;
+    }
+  }
+}
+
+__global__ void shard_reset_kernel(AdaptHdr* h) { h->ccount = 0; }
+}  // namespace vt
+
+extern "C" size_t vt_tau_shard_workspace(int64_t n) { return adapt_layout_rl(n > 0 ? n : 1, 0).total; }
+
+extern "C" int vt_tau_shard_candidates(const double* x, int64_t n, int b_r, int64_t n_global, int64_t budget,
+                                       int64_t* xbuf, int32_t* err, void* ws, size_t ws_bytes, vt_stream_t stream) {
+  if (n < 0 || n_global < n || n_global <= 0 || b_r < 10 || b_r > 32 || budget < 0 || !xbuf || !err || !ws ||
+      ws_bytes < vt_tau_shard_workspace(n) || reinterpret_cast<uintptr_t>(ws) % 256 ||
+      (n && (!x || (reinterpret_cast<uintptr_t>(x) & 31)))) {
+    vt_set_error("vt_tau_shard_candidates: bad argument (0 <= n <= n_global, 32-byte aligned x, workspace)");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const AdaptLayout lay = adapt_layout_rl(n > 0 ? n : 1, 0);
+  const AdPtrs A = adapt_ptrs(static_cast<uint8_t*>(ws), lay);
+  const AdPlan P = adapt_plan(n_global, b_r, budget);  // the GLOBAL plan: the same L on every rank
+  cudaMemsetAsync(xbuf, 0, sizeof(int64_t) * kShardX, s);
+  shard_reset_kernel<<<1, 1, 0, s>>>(A.h);
+  int rc = vt_check_launch("shard_reset_kernel");
+  if (rc) return rc;
+  if (n > 0 && (rc = adapt_key_pass(x, n, b_r, P, A.ck, lay.cap, A.h, err, s))) return rc;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lay.cap + 4095) / 4096, 148 * 4));
+  shard_hist_kernel<<<grid, kAdThreads, 0, s>>>(A.ck, A.h, lay.cap, P.g0, P.L_key, P.hi_key, P.s0,
+                                                reinterpret_cast<unsigned long long*>(xbuf), err);
+  return vt_check_launch("shard_hist_kernel");
+}
+
+extern "C" int vt_tau_shard_plan(int64_t n_global, int b_r, int64_t budget, uint64_t* L_key, int* s0) {
+  if (n_global <= 0 || b_r < 10 || b_r > 32 || budget < 0 || !L_key || !s0) {
+    vt_set_error("vt_tau_shard_plan: bad argument");
+    return VT_EINVAL;
+  }
+  const AdPlan P = adapt_plan(n_global, b_r, budget);
+  *L_key = P.L_key;
+  *s0 = P.s0;
+  return VT_OK;
+}
+
+extern "C" int vt_tau_shard_digit_keys(int64_t n, int b_r, int64_t n_global, int64_t budget, int64_t digit,
+                                       uint64_t* keys_out, int64_t keys_cap, int64_t* count, void* ws,
+                                       size_t ws_bytes, vt_stream_t stream) {
+  if (n < 0 || n_global <= 0 || b_r < 10 || b_r > 32 || budget < 0 || digit < 0 || digit >= kAdBins || !count ||
+      (keys_cap > 0 && !keys_out) || !ws || ws_bytes < vt_tau_shard_workspace(n)) {
+    vt_set_error("vt_tau_shard_digit_keys: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const AdaptLayout lay = adapt_layout_rl(n > 0 ? n : 1, 0);
+  const AdPtrs A = adapt_ptrs(static_cast<uint8_t*>(ws), lay);
+  const AdPlan P = adapt_plan(n_global, b_r, budget);
+  cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lay.cap + 4095) / 4096, 148 * 4));
+  shard_digit_kernel<<<grid, kAdThreads, 0, s>>>(A.ck, A.h, lay.cap, P.L_key, P.hi_key, P.s0, (uint64_t)digit,
+                                                 keys_out, keys_cap, reinterpret_cast<unsigned long long*>(count));
+  int rc = vt_check_launch("shard_digit_kernel");
+  if (rc) return rc;
+  shard_reset_kernel<<<1, 1, 0, s>>>(A.h);  // the workspace's candidate count starts at 0 for the next call
+  return vt_check_launch("shard_reset_kernel");
+}
+
+
+// ---------------------------------------------------------------------------
 // Batched adaptive round-and-log: many independent tensors (configs[2]: the
 // 161 ResNet-50 intermediates), each with its own budget, tau and log, in a
 // fixed number of launches instead of ~12 per tensor:

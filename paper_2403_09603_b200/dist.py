@@ -11,9 +11,12 @@ path shards naturally:
 * replay: each rank consumes its own slice; corrections are all-reduced.
 * adaptive threshold: independent tensors go to ranks whole, LPT-balanced
   (``lpt_assign``; no collective beyond gathering the taus).  One tensor
-  sharded across ranks: the exact radix select runs pass by pass with the
-  pass histogram summed over the ranks (``ncclAllReduce``, 64 KiB) before
-  every rank makes the same selection (``search_tau_budget_sharded``).
+  sharded across ranks (``search_tau_budget_sharded``): one read of each
+  shard for the candidates above the global plan's threshold, an all-reduce
+  of their digit histogram (16 KiB), an all-gather of the keys in the
+  selected digit, the exact order statistic and the FP64 bisection; the
+  exact radix select pass by pass (histograms summed over the ranks) as
+  the fallback.
 * Merkle: leaves are grouped in blocks of 2^K; each rank hashes a
   contiguous run of blocks and builds levels 0..K locally (fewer when the
   whole tree fits one block), all ranks all-gather the block roots and build
@@ -192,13 +195,101 @@ def kth_largest_distance_sharded(x_local: torch.Tensor, b_r: int, rank: int, gro
     return sk.value()
 
 
-def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iters: int = 30, group=None) -> float:
-    """protocol.search_tau_budget over a tensor sharded across ranks: the same
-    FP64 bisection on the exact global (budget+1)-th largest p (every rank
-    gets the same tau)."""
+SHARD_BINS = 2048  # top-digit bins of the candidate keys (kAdBins)
+SHARD_XWORDS = SHARD_BINS + 3  # + keys above tau_hi, candidates, overflow flag
+
+
+class ShardedBudget:
+    """One rank's side of the budget search over a tensor sharded across ranks,
+    through the candidate path (vt_tau_shard_*): the caller sums
+    ``candidates()`` over the ranks, every rank ``decide``s identically, the
+    caller gathers ``digit_keys`` from every rank, and ``finish`` selects the
+    exact order statistic.  The plan (candidate threshold L, digit shift)
+    depends only on the GLOBAL n and budget, so it is the same on every rank."""
+
+    def __init__(self, x_local: torch.Tensor, b_r: int, n_global: int, budget: int, tag: str = "tau_shard"):
+        import ctypes as C
+
+        from . import _device as D
+        from . import _lib
+        self.D, self.lib = D, _lib
+        self.t = D.aligned_f64(x_local.reshape(-1)) if x_local.numel() else x_local.reshape(-1).to(torch.float64)
+        self.n = int(self.t.numel())
+        self.b_r, self.n_global, self.budget = int(b_r), int(n_global), int(budget)
+        dev = self.t.device if self.t.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        self.ws = D.workspace(int(_lib.lib().vt_tau_shard_workspace(self.n)), tag)
+        self.flags = D.Flags()
+        self.dev = dev
+        L, s0 = C.c_uint64(0), C.c_int(0)
+        _lib.call("vt_tau_shard_plan", self.n_global, self.b_r, self.budget, C.byref(L), C.byref(s0))
+        self.L_key, self.s0 = int(L.value), int(s0.value)
+        self.digit_count = 0
+
+    def candidates(self) -> torch.Tensor:
+        """int64[SHARD_XWORDS]: this rank's digit histogram, keys above tau_hi,
+        candidate count, overflow flag -- to be summed over the ranks."""
+        xb = torch.empty(SHARD_XWORDS, dtype=torch.int64, device=self.dev)
+        self.lib.call("vt_tau_shard_candidates", self.D.ptr(self.t) if self.n else None, self.n, self.b_r,
+                      self.n_global, self.budget, self.D.ptr(xb), self.flags.err_ptr, self.D.ptr(self.ws),
+                      self.ws.numel(), self.D.stream_ptr())
+        return xb
+
+    def decide(self, xsum) -> tuple[str, object, int]:
+        """From the summed exchange buffer: ("value", v, -) when the keys above
+        tau_hi or the candidates settle v, ("digit", d, rank_in_digit) when the
+        digit's keys must be gathered (``self.digit_count`` = their number over
+        all ranks), ("exact", None, -) for the exact multi-pass fallback
+        (overflow, or fewer candidates than budget + 1 above a threshold
+        L > tau_lo)."""
+        from .fpround import tau_bounds
+        self.D.raise_fpround(self.flags.read()[0])
+        xs = np.asarray(xsum, dtype=np.int64)
+        hist, above_hi, m, overflow = xs[:SHARD_BINS], int(xs[SHARD_BINS]), int(xs[SHARD_BINS + 1]), \
+            int(xs[SHARD_BINS + 2])
+        lower, upper = tau_bounds(self.b_r)
+        B = self.budget
+        if self.n_global <= B:
+            return "value", lower, 0
+        if overflow:
+            return "exact", None, 0
+        if above_hi > B:
+            return "value", float("inf"), 0
+        if m < B + 1:
+            lo_key = int(np.array([lower], dtype=np.float64).view(np.uint64)[0])
+            return ("value", lower, 0) if self.L_key <= lo_key else ("exact", None, 0)
+        rank = B - above_hi  # 0-based from the top among the keys in (L, hi]
+        above = 0
+        for d in range(SHARD_BINS - 1, -1, -1):
+            h = int(hist[d])
+            if above + h > rank:
+                self.digit_count = h
+                return "digit", d, rank - above
+            above += h
+        return "exact", None, 0  # unreachable when the counts add up
+
+    def digit_keys(self, digit: int) -> torch.Tensor:
+        """This rank's candidate keys in ``digit`` (int64 bit patterns of p);
+        at most the digit's count over all ranks (``decide``)."""
+        out = torch.empty(max(1, int(self.digit_count)), dtype=torch.int64, device=self.dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.lib.call("vt_tau_shard_digit_keys", self.n, self.b_r, self.n_global, self.budget, int(digit),
+                      self.D.ptr(out), out.numel(), self.D.ptr(cnt), self.D.ptr(self.ws), self.ws.numel(),
+                      self.D.stream_ptr())
+        c = int(cnt.item())
+        if c > out.numel():
+            raise RuntimeError("vt_tau_shard_digit_keys: digit holds more keys than the buffer")
+        return out[:c]
+
+    @staticmethod
+    def finish(all_keys, rank_in_digit: int) -> float:
+        """The rank-th largest of the gathered keys (exact), as the FP64 p."""
+        k = np.sort(np.asarray(all_keys, dtype=np.int64).view(np.uint64))[::-1]
+        return float(k[rank_in_digit:rank_in_digit + 1].view(np.float64)[0])
+
+
+def _bisect_tau(v: float, b_r: int, iters: int) -> float:
     from .fpround import tau_bounds
     lower, upper = tau_bounds(b_r)
-    v = kth_largest_distance_sharded(x_local, b_r, int(budget), group)
     for _ in range(iters):
         tau = (lower + upper) / 2.0
         if v <= tau:
@@ -206,6 +297,42 @@ def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iter
         else:
             lower = tau
     return upper
+
+
+def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iters: int = 30, group=None) -> float:
+    """protocol.search_tau_budget over a tensor sharded across ranks: the same
+    FP64 bisection on the exact global (budget+1)-th largest p, every rank
+    getting the same tau.  Candidate path: one read of each shard, an
+    all-reduce of a 2051-word exchange buffer and an all-gather of the keys
+    in the selected digit (``ShardedBudget``); the exact 5-pass radix select
+    (``kth_largest_distance_sharded``) when the candidates cannot decide."""
+    world = _world(group)
+    n = torch.tensor([x_local.numel()], dtype=torch.int64, device=x_local.device)
+    if world > 1:
+        dist.all_reduce(n, group=group)
+    n_global = int(n.item())
+    if n_global == 0 or n_global <= budget:
+        from .fpround import tau_bounds
+        return _bisect_tau(tau_bounds(b_r)[0], b_r, iters)
+    sb = ShardedBudget(x_local, b_r, n_global, int(budget))
+    xb = sb.candidates()
+    if world > 1:
+        dist.all_reduce(xb, group=group)
+    kind, val, rank = sb.decide(xb.cpu().numpy())
+    if kind == "value":
+        return _bisect_tau(val, b_r, iters)
+    if kind == "exact":
+        return _bisect_tau(kth_largest_distance_sharded(x_local, b_r, int(budget), group), b_r, iters)
+    keys = sb.digit_keys(val)
+    if world > 1:
+        cnt = all_gather_counts(keys.numel(), group, device=x_local.device)
+        width = max(1, int(cnt.max()))
+        pad = torch.zeros(width, dtype=torch.int64, device=x_local.device)
+        pad[: keys.numel()] = keys
+        allk = torch.empty(world * width, dtype=torch.int64, device=x_local.device)
+        _all_gather_flat(allk, pad, group)
+        keys = torch.cat([allk[r * width: r * width + int(cnt[r])] for r in range(world)])
+    return _bisect_tau(ShardedBudget.finish(keys.cpu().numpy(), rank), b_r, iters)
 
 
 # ---------------------------------------------------------------------------

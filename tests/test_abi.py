@@ -81,6 +81,9 @@ BAD_CALLS = [
     ("vt_tau_kth_key", (None, -1, 32, 0, None, None, None, 0, None)),
     ("vt_tau_budget_key", (None, 10, 32, -1, 0.1, 0.2, None, None, None, None, 0, None)),
     ("vt_tau_budget", (None, 10, 32, -1, 30, None, None, None, None, 0, None)),
+    ("vt_tau_shard_plan", (0, 32, 10, None, None)),
+    ("vt_tau_shard_candidates", (None, 10, 32, 5, 1, None, None, None, 0, None)),
+    ("vt_tau_shard_digit_keys", (10, 32, 10, 1, 5000, None, 0, None, None, 0, None)),
     ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
                                None)),
     ("vt_round_log_adaptive_batch", (None, 0, 32, 30, 1, None, 0, None)),

@@ -218,3 +218,50 @@ def test_sharded_budget_search_virtual_ranks(oracle):
         assert upper == oracle.search_tau_budget(x, 32, B)
     # world of one: the sharded entry point equals the single-device search
     assert vd.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, 1_250) == oracle.search_tau_budget(x, 32, 1_250)
+
+
+def test_sharded_candidate_budget_search_virtual_ranks(oracle):
+    """The candidate path over a tensor cut into uneven shards (virtual ranks
+    on one GPU; the all-reduce is a sum of the exchange buffers, the
+    all-gather a concatenation): tau equals the oracle's budget search for
+    ordinary budgets, zero, a budget of 40% (candidate overflow -> the exact
+    multi-pass fallback), a tensor of ties, values near the grid (v <= tau_lo)
+    and an empty shard."""
+    import torch
+    from paper_2403_09603_b200 import dist as vd
+    rng = np.random.default_rng(21)
+    cases = [rng.normal(0.0, 3.0, 400_003), np.full(300_000, 1.0 + 0.4 * 2.0 ** -23),
+             1.0 + rng.uniform(0, 0.2, size=200_000) * 2.0 ** -23,
+             (rng.integers(1 << 23, 1 << 24, size=150_000) + 0.5) * 2.0 ** -23]
+    cases[1][::3] = 1.0 + 0.45 * 2.0 ** -23
+    for ci, x in enumerate(cases):
+        n = x.size
+        cuts = [0, n // 7, n // 7, n // 2 + 3, n]  # the second shard is empty
+        shards = [torch.from_numpy(x[a:b].copy()).cuda() for a, b in zip(cuts, cuts[1:])]
+        for B in (0, 1, int(0.005 * n), int(0.4 * n)):
+            sbs = [vd.ShardedBudget(s, 32, n, B, tag=f"sb{r}") for r, s in enumerate(shards)]
+            xsum = sum(sb.candidates() for sb in sbs)
+            decisions = [sb.decide(xsum.cpu().numpy()) for sb in sbs]
+            assert all(d[:2] == decisions[0][:2] for d in decisions)
+            kind, val, rank = decisions[0]
+            if kind == "value":
+                v = val
+            elif kind == "digit":
+                keys = torch.cat([sb.digit_keys(val) for sb in sbs])
+                assert keys.numel() == sbs[0].digit_count
+                v = vd.ShardedBudget.finish(keys.cpu().numpy(), rank)
+            else:
+                v = protocol_kth(x, B)
+            want = oracle.search_tau_budget(x, 32, B)
+            assert vd._bisect_tau(v, 32, 30) == want, (ci, B, kind)
+            if kind == "digit":  # the exact order statistic itself
+                assert v == oracle.kth_largest(oracle.normalized_distance(x, 32), B), (ci, B)
+    # the entry point on one process equals the single-device search
+    x = cases[0]
+    for B in (0, 2_000, int(0.4 * x.size)):
+        assert vd.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, B) == oracle.search_tau_budget(x, 32, B)
+
+
+def protocol_kth(x, B):
+    from paper_2403_09603_b200 import protocol
+    return protocol.kth_largest_distance(x, 32, B)

@@ -221,6 +221,18 @@ def run_ours(args) -> None:
     stream = torch.cuda.Stream(dev)  # every operator runs (and is captured) on this stream
     stream.wait_stream(torch.cuda.current_stream(dev))
 
+    # the exchange step at N ranks: the per-rank log counts, fused into the
+    # round-and-log kernel over peer memory (symmetric memory over NVLink:
+    # the kernel's last CTA stores its count into every rank's buffer, a wait
+    # kernel collects them) -- or an NCCL all-gather if that cannot be set up
+    xchg, xchg_kind = None, None
+    if ddp:
+        try:
+            xchg = vdist.CountExchange(device=dev)
+            xchg_kind = "peer-memory stores fused into rl_fused_kernel + counts_wait_kernel (symmetric memory)"
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] symmetric-memory exchange unavailable, using NCCL all-gather: {e!r}", file=sys.stderr)
+            xchg_kind = "NCCL all-gather of the counts"
     with torch.cuda.stream(stream):
         # the auditor receives the log with its length (as a file carries it);
         # take it from one untimed trainer pass
@@ -229,12 +241,26 @@ def run_ours(args) -> None:
     count = log0.count
     log_words = words[:count]
     state = {}
+    if xchg is not None:  # once, untimed: the fused exchange equals the NCCL all-gather
+        with torch.cuda.stream(stream):
+            pe = xchg.round_and_log(xt, 32, tau, base, out=y_t, log_out=words)
+            got = xchg.wait().clone()
+            pe.finish()
+        xchg.check()
+        want = vdist.all_gather_counts(count, device=dev)
+        if not torch.equal(got, want):
+            raise RuntimeError(f"peer-memory count exchange {got.tolist()} != NCCL all-gather {want.tolist()}")
 
     def trainer():
-        state["p"] = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
+        if xchg is not None:
+            state["p"] = xchg.round_and_log(xt, 32, tau, base, out=y_t, log_out=words)
+        else:
+            state["p"] = ops.round_and_log(xt, 32, tau, out=y_t, log_out=words, global_base=base, check=False)
 
     def exchange():
-        if ddp:  # the exchange step: all-gather of per-rank log counts (device-resident)
+        if xchg is not None:
+            xchg.wait()
+        elif ddp:  # the exchange step: all-gather of per-rank log counts (device-resident)
             vdist._all_gather_flat(counts, state["p"].flags.buf[2:3])
 
     def auditor():
@@ -250,6 +276,8 @@ def run_ours(args) -> None:
             step()
     torch.cuda.synchronize()
     # verify once (outside the timed region): auditor output == trainer output, no errors
+    if xchg is not None:
+        xchg.check()
     err_t, cnt_t = state["p"].flags.read()
     err_a, cnt_a = state["fa"].read()
     assert err_t == 0 and err_a == 0 and cnt_t[0] == count, (err_t, err_a, cnt_t, count)
@@ -301,6 +329,8 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
     if ddp:
         dist.barrier()
+    if xchg is not None:
+        xchg.check()
     ms_total = t0.elapsed_time(t1)
     rl_ms = statistics.mean(starts[i].elapsed_time(mids[i]) for i in range(args.steps))
     rp_ms = statistics.mean(mids[i].elapsed_time(ends[i]) for i in range(args.steps))
@@ -366,8 +396,9 @@ def run_ours(args) -> None:
                    "n_per_gpu": n, "logged_fraction": round(f, 6), "parallelism": f"dp{world} (contiguous shards)",
                    "l2": "no flush: every step streams 2 x 512 MiB of FP64 (>= 4x the 126 MB L2)",
                    "auditor_equals_trainer_bitwise": ok_equal,
-                   "launch": ("cuda graphs (trainer + count all-gather, auditor)" if ddp else
-                              "cuda graphs (one per operator)") if graphs else "eager"},
+                   "launch": ("cuda graphs (trainer + count exchange, auditor)" if ddp else
+                              "cuda graphs (one per operator)") if graphs else "eager",
+                   "exchange": xchg_kind},
         "roofline": {"bound": "hbm",
                      "kernel": "round-and-log op: rl_fused_kernel (single pass: TMA-pipelined rnd + direction + "
                                "ballot staging, in-kernel decoupled look-back, final log words)",

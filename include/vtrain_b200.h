@@ -33,6 +33,8 @@
  *   vt_tau_budget_key    SURVEY.md Appendix A.4)
  *   vt_tau_budget     <- the same budget search incl. the bisection, one read of x
  *   vt_tau_shard_*    <- the same over a tensor sharded across ranks
+ *   vt_round_log_exchange / vt_counts_wait <- vt_round_log + the count all-gather of
+ *                        a sharded round-and-log, fused over peer memory
  *   vt_min_f64        <- the all(p >= tau) predicate of search_tau  protocol.py:502
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
@@ -64,6 +66,7 @@ typedef void *vt_stream_t; /* a cudaStream_t; NULL = legacy default stream */
 #define VT_ERR_BAD_CODE 8       /* code not in {0,1,2}: "invalid direction code" */
 #define VT_ERR_BAD_LOG_BYTE 16  /* packed byte > 242: "corrupt log byte" */
 #define VT_ERR_BAD_SPARSE 32    /* sparse log not strictly ascending / out of range */
+#define VT_ERR_EXCHANGE 64      /* vt_counts_wait: a peer's count did not arrive within 10 s */
 
 /* output kinds for the rounded tensor */
 #define VT_OUT_NONE 0
@@ -187,6 +190,27 @@ int vt_tau_budget_key(const double *x, int64_t n, int b_r, int64_t budget, doubl
 size_t vt_tau_budget_workspace(int64_t n);
 int vt_tau_budget(const double *x, int64_t n, int b_r, int64_t budget, int iters, double *tau_out,
                   uint64_t *key_out, int32_t *err, void *ws, size_t ws_bytes, vt_stream_t stream);
+/*
+ * Round-and-log with the multi-GPU exchange step fused in (the
+ * per-rank log counts all-gathered so each rank knows its offset in the
+ * global log).  Same arguments and results as vt_round_log on the sparse path
+ * (codes / packed not allowed), plus `xpeers`: a DEVICE array of `world`
+ * pointers to every rank's exchange buffer of vt_exchange_words(world)
+ * uint64 words (symmetric memory mapped over NVLink, zero-filled once on
+ * every rank before first use).  The kernel's last CTA stores this call's
+ * entry count into every rank's buffer (st.release.sys), tagged with this
+ * rank's exchange sequence number; vt_counts_wait (same stream, later) spins
+ * until every rank's count for that sequence number is in this rank's buffer
+ * and writes them to counts_out[world] (device), or raises VT_ERR_EXCHANGE
+ * in *err after 10 s.  Replaces the ncclAllGather of counts.
+ */
+size_t vt_exchange_words(int world);
+int vt_round_log_exchange(const double *x, int64_t n, int b_r, double tau, int out_kind, void *out,
+                          uint64_t *sparse, int64_t sparse_cap, int64_t global_base,
+                          int64_t *counters, int32_t *err, void *ws, size_t ws_bytes,
+                          uint64_t *const *xpeers, int world, int rank, vt_stream_t stream);
+int vt_counts_wait(uint64_t *const *xpeers, int world, int rank, int64_t *counts_out, int32_t *err,
+                   vt_stream_t stream);
 /*
  * The budget search over ONE tensor sharded across ranks,
  * candidate path: vt_tau_shard_plan gives the global plan (candidate

@@ -26,6 +26,7 @@ ERR_RANGE_NEIGHBOR = 4
 ERR_BAD_CODE = 8
 ERR_BAD_LOG_BYTE = 16
 ERR_BAD_SPARSE = 32
+ERR_EXCHANGE = 64
 OUT_NONE, OUT_F32, OUT_F64 = 0, 1, 2
 LOG_SPARSE, LOG_CODES, LOG_PACKED = 0, 1, 2
 
@@ -62,6 +63,10 @@ EXPORTS: dict[str, tuple] = {
     "vt_tau_budget_key": (_i32, [_p, _i64, _i32, _i64, _dbl, _dbl, _p, _p, _p, _p, _sz, _p]),
     "vt_tau_budget_workspace": (_sz, [_i64]),
     "vt_tau_budget": (_i32, [_p, _i64, _i32, _i64, _i32, _p, _p, _p, _p, _sz, _p]),
+    "vt_exchange_words": (_sz, [_i32]),
+    "vt_round_log_exchange": (_i32, [_p, _i64, _i32, _dbl, _i32, _p, _p, _i64, _i64, _p, _p, _p, _sz, _p, _i32, _i32,
+                                     _p]),
+    "vt_counts_wait": (_i32, [_p, _i32, _i32, _p, _p, _p]),
     "vt_tau_shard_workspace": (_sz, [_i64]),
     "vt_tau_shard_plan": (_i32, [_i64, _i32, _i64, _p, _p]),
     "vt_tau_shard_candidates": (_i32, [_p, _i64, _i32, _i64, _i64, _p, _p, _p, _sz, _p]),

@@ -316,6 +316,17 @@ __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// system scope: peer GPUs' memory over NVLink (symmetric-memory exchange)
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -331,10 +342,19 @@ size_t rl_stream_workspace(int64_t n);
 size_t rp_stream_workspace(int64_t n);
 // dthr: nullable device thresholds overriding g.thr / g.thr_sub / thr32;
 // gate: nullable device flag, the kernel does nothing while *gate == 0
+// The per-rank count exchange over peer memory (vt_round_log_exchange):
+// xpeers = device array of `world` pointers to every rank's exchange buffer
+// (symmetric memory, vt_exchange_words(world) uint64 words each).
+struct XPeers {
+  uint64_t* const* peers;
+  int world, rank;
+};
+
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr,
-              const int32_t* gate = nullptr, uint64_t* keys = nullptr);
+              const int32_t* gate = nullptr, uint64_t* keys = nullptr, XPeers xp = XPeers{nullptr, 0, 0});
+int counts_wait(XPeers xp, int64_t* counts_out, int32_t* err, cudaStream_t st);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 int rp_stream_packed(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out,

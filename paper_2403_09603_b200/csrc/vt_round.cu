@@ -631,6 +631,37 @@ extern "C" int vt_round_log(const double* x, int64_t n, int b_r, double tau, int
   return vt_check_launch("round_log_kernel");
 }
 
+extern "C" size_t vt_exchange_words(int world) { return world > 0 ? (size_t)(1 + 2 * world) : 0; }
+
+extern "C" int vt_round_log_exchange(const double* x, int64_t n, int b_r, double tau, int out_kind, void* out,
+                                     uint64_t* sparse, int64_t sparse_cap, int64_t global_base, int64_t* counters,
+                                     int32_t* err, void* ws, size_t ws_bytes, uint64_t* const* xpeers, int world,
+                                     int rank, vt_stream_t stream) {
+  if (n <= 0 || !valid_b(b_r) || out_kind < 0 || out_kind > 2 || !counters || !err || !sparse || !ws ||
+      ws_bytes < vt_round_log_workspace(n) || !xpeers || world <= 0 || rank < 0 || rank >= world) {
+    vt_set_error("vt_round_log_exchange: bad argument (n > 0, sparse log, workspace, 0 <= rank < world)");
+    return VT_EINVAL;
+  }
+  if (!aligned(x, 32) || (out_kind == VT_OUT_F32 && !aligned(out, 16)) || (out_kind == VT_OUT_F64 && !aligned(out, 32))) {
+    vt_set_error("vt_round_log_exchange: misaligned buffer");
+    return VT_EINVAL;
+  }
+  const Grid g = make_grid(b_r, tau);
+  const int thr32 = (int)std::min<int64_t>(std::max<int64_t>(g.thr, 0), INT32_MAX);
+  return rl_stream(x, n, g, thr32, b_r == 32, out_kind, out, sparse, sparse_cap, global_base, nullptr, nullptr,
+                   counters, err, ws, static_cast<cudaStream_t>(stream), nullptr, nullptr, nullptr,
+                   XPeers{xpeers, world, rank});
+}
+
+extern "C" int vt_counts_wait(uint64_t* const* xpeers, int world, int rank, int64_t* counts_out, int32_t* err,
+                              vt_stream_t stream) {
+  if (!xpeers || world <= 0 || rank < 0 || rank >= world || !counts_out || !err) {
+    vt_set_error("vt_counts_wait: bad argument");
+    return VT_EINVAL;
+  }
+  return counts_wait(XPeers{xpeers, world, rank}, counts_out, err, static_cast<cudaStream_t>(stream));
+}
+
 namespace {
 template <int OUT, int L, bool F>
 void launch_rp(const ReplayArgs& a, int64_t tiles, cudaStream_t st) {

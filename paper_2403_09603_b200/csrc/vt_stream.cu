@@ -144,6 +144,10 @@ __device__ __forceinline__ void* tile_out(void* out, int64_t tbase) {
 // ---------------------------------------------------------------------------
 
 constexpr int kEpochShift = 44;
+// exchange words: sequence number (24 bits) << 40 | entry count (40 bits)
+constexpr int kXSeqShift = 40;
+constexpr uint64_t kXSeqMask = (1ull << 24) - 1;
+constexpr uint64_t kXCountMask = (1ull << 40) - 1;
 constexpr uint64_t kEpochMask = (1ull << 20) - 1;
 constexpr uint64_t kLBAgg = 1ull << 42;
 constexpr uint64_t kLBInc = 2ull << 42;
@@ -221,8 +225,10 @@ struct FusedHeader {
   uint32_t ticket;  // next super-tile to hand out
   uint32_t done;    // CTAs finished
   uint32_t hwm;     // most status words any call has written
-  uint32_t pad[12];
+  uint64_t total;   // this call's log entries (written with the last super-tile's look-back)
+  uint32_t pad[10];
 };
+static_assert(sizeof(FusedHeader) == 64, "the look-back words start at byte 64");
 
 struct FusedSmem {
   double ring[kFStages][kSTile];
@@ -261,6 +267,7 @@ struct RLFArgs {
   const DevThr* dthr;
   const int32_t* gate;  // nullable: the kernel returns at once when *gate == 0
   uint64_t* keys;       // KEYS launches only
+  XPeers xp;            // nullable peers: the last CTA publishes the call's entry count to every rank
 };
 
 // Ticket s -> its first tile and tile count: n4 super-tiles of kSuper tiles,
@@ -573,6 +580,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
         if (s == a.num_super - 1) {
           atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)agg));
           if (a.cursor_out) *a.cursor_out = cur + excl + (int64_t)agg;
+          a.hdr->total = (uint64_t)(excl + (int64_t)agg);
         }
         S.sbase[slot] = cur + excl;
       }
@@ -688,12 +696,58 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     __syncthreads();
   }
   if (tid == 0) {
+    if (a.xp.peers) {
+      // the exchange step fused into the kernel: the call's entry count goes
+      // to every rank's exchange buffer over peer memory (NVLink), tagged
+      // with this rank's exchange sequence number; slots alternate by parity
+      // so a rank one exchange ahead cannot overwrite a slot still awaited
+      __threadfence();
+      const uint64_t total = *(volatile uint64_t*)&a.hdr->total;
+      uint64_t* mine = a.xp.peers[a.xp.rank];
+      const uint64_t seq = mine[0] + 1ull;
+      mine[0] = seq;
+      const uint64_t word = ((seq & kXSeqMask) << kXSeqShift) | (total & kXCountMask);
+      const int par = (int)(seq & 1ull);
+      for (int p = 0; p < a.xp.world; ++p)
+        st_release_sys_u64(a.xp.peers[p] + 1 + par * a.xp.world + a.xp.rank, word);
+    }
     a.hdr->ticket = 0u;
     a.hdr->done = 0u;
     a.hdr->hwm = hwm;
     a.hdr->epoch = S.epoch == (uint32_t)kEpochMask ? 0u : S.epoch;
     __threadfence();
   }
+}
+
+// The other half of the exchange: wait until every rank's count for this
+// rank's current sequence number has arrived (bounded spin: after
+// timeout_ns the error bit VT_ERR_EXCHANGE is raised instead of hanging).
+__global__ void counts_wait_kernel(const XPeers xp, int64_t* counts_out, int32_t* err, uint64_t timeout_ns) {
+  const uint64_t* mine = xp.peers[xp.rank];
+  const uint64_t seq = *(volatile const uint64_t*)mine;
+  const int par = (int)(seq & 1ull);
+  for (int q = threadIdx.x; q < xp.world; q += blockDim.x) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint64_t w;
+    while (true) {
+      w = ld_acquire_sys_u64(mine + 1 + par * xp.world + q);
+      if ((w >> kXSeqShift) == (seq & kXSeqMask)) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicOr(err, VT_ERR_EXCHANGE);
+        w = 0;
+        break;
+      }
+      __nanosleep(100);
+    }
+    counts_out[q] = (int64_t)(w & kXCountMask);
+  }
+}
+
+int counts_wait(XPeers xp, int64_t* counts_out, int32_t* err, cudaStream_t st) {
+  counts_wait_kernel<<<1, 32, 0, st>>>(xp, counts_out, err, 10ull * 1000 * 1000 * 1000);
+  return vt_check_launch("counts_wait_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -713,7 +767,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
 
 // the fields rlf_write_rows / st_first / st_ntiles read, for tensor j
 __device__ __forceinline__ RLFArgs seg_view(const RLBatch& b, int j) {
-  RLFArgs v;
+  RLFArgs v{};
   const RLSeg& sg = b.seg[j];
   v.x = sg.x;
   v.n = sg.n;
@@ -1433,11 +1487,11 @@ static int launch_rlf(RLFArgs a, cudaStream_t st) {
 int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, int out_kind, void* out,
               uint64_t* sparse, int64_t cap, int64_t global_base, const int64_t* cursor_in, int64_t* cursor_out,
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr,
-              const int32_t* gate, uint64_t* keys) {
+              const int32_t* gate, uint64_t* keys, XPeers xp) {
   uint8_t* w = static_cast<uint8_t*>(ws);
   RLFArgs f{x, n, g, thr32, out, stream_tiles(n), 0, 0, reinterpret_cast<FusedHeader*>(w),
             reinterpret_cast<uint64_t*>(w + 64), sparse, cap, global_base, cursor_in, cursor_out, counters, err,
-            dthr, gate, keys};
+            dthr, gate, keys, xp};
   if (keys) {  // the adaptive candidate pass (b_r = 32 or not)
     if (fast)
       return out_kind == VT_OUT_F32 ? launch_rlf<VT_OUT_F32, true, true>(f, st)

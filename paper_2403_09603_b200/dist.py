@@ -8,6 +8,10 @@ path shards naturally:
   the only exchange is an all-gather of the per-rank entry counts, whose
   exclusive prefix places each rank's slice in the global log (concatenation
   in rank order is the reference order).  The log itself stays sharded.
+  The exchange is fused into the round-and-log kernel over peer memory
+  (``CountExchange``: the last CTA stores the count into every rank's
+  symmetric-memory buffer, a wait kernel collects them), or an NCCL
+  all-gather.
 * replay: each rank consumes its own slice; corrections are all-reduced.
 * adaptive threshold: independent tensors go to ranks whole, LPT-balanced
   (``lpt_assign``; no collective beyond gathering the taus).  One tensor
@@ -98,13 +102,92 @@ class ShardedLog:
     counts: torch.Tensor   # per-rank counts
 
 
+class CountExchange:
+    """The count exchange of a sharded round-and-log over peer memory: a
+    symmetric-memory buffer per rank (``torch.distributed._symmetric_memory``,
+    mapped into every peer over NVLink; a plain device buffer in a single
+    process) and the two kernels that use it.  ``round_and_log`` runs the
+    fused round-and-log whose last CTA stores the call's entry count into
+    every rank's buffer (``vt_round_log_exchange``); ``wait`` launches the
+    kernel that waits for every rank's count (``vt_counts_wait``).  No NCCL
+    call, no host round trip: both are plain kernels on the current stream,
+    so a whole step can be graph-captured."""
+
+    def __init__(self, group=None, device=None):
+        from . import _device as D
+        from . import _lib
+        self.D, self.lib = D, _lib
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        words = int(_lib.lib().vt_exchange_words(self.world))
+        if dist.is_initialized():
+            import torch.distributed._symmetric_memory as symm
+            self.buf = symm.empty(words, dtype=torch.int64, device=dev)
+            self.buf.zero_()
+            name = (group or dist.group.WORLD).group_name
+            self.handle = symm.rendezvous(self.buf, name)
+            self.peers = int(self.handle.buffer_ptrs_dev)
+            torch.cuda.synchronize(dev)
+            dist.barrier(group)  # every buffer is zero before any rank publishes
+        else:
+            self.buf = torch.zeros(words, dtype=torch.int64, device=dev)
+            self._ptrs = torch.tensor([self.buf.data_ptr()], dtype=torch.int64, device=dev)
+            self.peers = int(self._ptrs.data_ptr())
+        self.counts = torch.zeros(self.world, dtype=torch.int64, device=dev)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)
+
+    def round_and_log(self, x_local: torch.Tensor, b_r: int, tau: float, global_base: int, *, out=None,
+                      log_out=None, out_dtype=torch.float32, workspace=None):
+        """ops.round_and_log(check=False) with the count published to every rank."""
+        from . import ops
+        from .fpround import _check_b
+        _check_b(b_r)
+        t = self.D.aligned_f64(x_local.reshape(-1))
+        n = t.numel()
+        if n == 0:
+            raise ValueError("CountExchange.round_and_log: empty shard")
+        y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
+        self.D.check_out(y, n, out_dtype, t.device, "out")
+        words = log_out if log_out is not None else torch.empty(ops.default_log_capacity(n), dtype=torch.int64,
+                                                                device=t.device)
+        need = int(self.lib.lib().vt_round_log_workspace(n))
+        ws = workspace if workspace is not None else self.D.workspace(need, "round_log")
+        f = self.D.Flags()
+        self.lib.call("vt_round_log_exchange", self.D.ptr(t), n, b_r, float(tau), ops._out_kind(out_dtype),
+                      self.D.ptr(y), self.D.ptr(words), words.numel(), int(global_base), f.cnt_ptr, f.err_ptr,
+                      self.D.ptr(ws), ws.numel(), self.peers, self.world, self.rank, self.D.stream_ptr())
+        return ops.PendingRound(y, words, f)
+
+    def wait(self) -> torch.Tensor:
+        """Enqueue the wait for every rank's count of the latest exchange;
+        returns the device int64[world] they land in (valid in stream order)."""
+        self.lib.call("vt_counts_wait", self.peers, self.world, self.rank, self.D.ptr(self.counts),
+                      self.flags.data_ptr(), self.D.stream_ptr())
+        return self.counts
+
+    def check(self) -> None:
+        if int(self.flags[0].item()) & self.lib.ERR_EXCHANGE:
+            raise RuntimeError("count exchange: a peer's count did not arrive (10 s)")
+
+
 def round_and_log_sharded(x_local: torch.Tensor, b_r: int, tau: float, global_base: int,
-                          group=None, **kw):
+                          group=None, exchange: CountExchange | None = None, **kw):
+    """Sharded round-and-log: this rank's log with global indices plus every
+    rank's entry count -- through the peer-memory exchange fused into the
+    kernel when ``exchange`` is given, else an NCCL all-gather."""
     from . import ops
-    y, log = ops.round_and_log(x_local, b_r, tau, global_base=global_base, **kw)
-    counts = all_gather_counts(log.count, group, device=x_local.device)
-    offs = exclusive_offsets(counts)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if exchange is not None:
+        p = exchange.round_and_log(x_local, b_r, tau, global_base, **kw)
+        counts = exchange.wait()
+        y, log = p.finish()
+        exchange.check()
+        counts = counts.clone()
+    else:
+        y, log = ops.round_and_log(x_local, b_r, tau, global_base=global_base, **kw)
+        counts = all_gather_counts(log.count, group, device=x_local.device)
+    offs = exclusive_offsets(counts)
     return y, ShardedLog(log, int(offs[rank]), int(counts.sum()), counts)
 
 

@@ -70,3 +70,62 @@ def test_merkle_sharded_nccl(nccl_group):
     lv, top = vdist.merkle_sharded(b, n_leaves, group=nccl_group, k=8)
     ref = merkle.merkle_chunked(w)
     assert bytes(top[-1][0].cpu().numpy()) == ref.root
+
+
+def test_count_exchange_over_symmetric_memory(nccl_group):
+    """The count exchange fused into the round-and-log kernel (last CTA ->
+    every rank's symmetric-memory buffer; wait kernel) equals the NCCL
+    all-gather, over repeated calls of varying size (the sequence number and
+    slot parity advance), graph-captured as well."""
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    from paper_2403_09603_b200 import ops, workloads
+    ex = vdist.CountExchange(nccl_group)
+    for i, n in enumerate((5_000, (1 << 20) + 3, 70_001, 1 << 22, 640)):
+        x = workloads.config0_x_torch(n, 50 + i)
+        y, slog = vdist.round_and_log_sharded(x, 32, workloads.TAU_CONFIG0, 7 * n, group=nccl_group, exchange=ex)
+        y1, log1 = ops.round_and_log(x, 32, workloads.TAU_CONFIG0, global_base=7 * n)
+        assert slog.counts.tolist() == [log1.count] and slog.total == log1.count, i
+        assert torch.equal(slog.local.words, log1.words) and torch.equal(y.view(torch.int32), y1.view(torch.int32))
+    assert int(ex.buf[0].item()) == 5  # five exchanges, five sequence numbers
+    # graph-captured: the fused kernel + the wait kernel replayed
+    n = 1 << 21
+    x = workloads.config0_x_torch(n, 60)
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    words = torch.empty(n // 4, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    state = {}
+
+    def step():
+        state["p"] = ex.round_and_log(x, 32, workloads.TAU_CONFIG0, 0, out=y, log_out=words)
+        state["c"] = ex.wait()
+
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    _, log1 = ops.round_and_log(x, 32, workloads.TAU_CONFIG0)
+    assert state["c"].tolist() == [log1.count]
+    ex.check()
+    assert int(ex.buf[0].item()) == 5 + 1 + 3  # warm-up call, then 3 replays (capture runs nothing)
+
+
+def test_count_exchange_single_process():
+    """Without a process group the exchange is the one-rank case (its own buffer)."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is active in this session")
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    from paper_2403_09603_b200 import ops, workloads
+    ex = vdist.CountExchange()
+    x = workloads.config0_x_torch(300_000, 70)
+    y, slog = vdist.round_and_log_sharded(x, 32, workloads.TAU_CONFIG0, 0, exchange=ex)
+    assert slog.counts.tolist() == [ops.round_and_log(x, 32, workloads.TAU_CONFIG0)[1].count]
+    assert torch.equal(y.view(torch.int32), ops.round_and_log(x, 32, workloads.TAU_CONFIG0)[0].view(torch.int32))

@@ -61,3 +61,44 @@ def test_reference_run_through_gpu_channels(traces, name, tmp_path):
         assert np.array_equal(bits(y.astype(np.float32)), bits(a_out[i])), i
         assert corr == m["corrections"][i] and directed == 0
     assert r.remaining == 0
+
+
+@pytest.mark.parametrize("b_r", [32, 26, 10])
+def test_staged_channels_shapes_and_grids(oracle, b_r, tmp_path):
+    """The staged host-array path of the GPU channels (one H2D, one D2H per
+    call) over odd shapes -- 0-d, empty, non-contiguous, 3-D, sizes around the
+    5-code packing phase -- at several grids: outputs and counts equal the
+    oracle's channel arithmetic (protocol.py:198-216), the .vtrl file the
+    reference writer's bytes, and a corrupt payload byte raises."""
+    from paper_2403_09603_b200 import protocol, roundlog
+    rng = np.random.default_rng(b_r)
+    base = rng.normal(0, 3, size=(40, 30))
+    tensors = [np.float64(1.0 + 0.6 * 2.0 ** -23), np.zeros(0), base[:, ::3], rng.normal(0, 1e-3, (2, 3, 7)),
+               rng.normal(0, 1, 4), rng.normal(0, 1, 5), rng.normal(0, 1, 6), rng.normal(0, 50, 10_007)]
+    tau = 2.0 ** -25
+    path = tmp_path / "s.vtrl"
+    w = roundlog.LogWriter(path, b_r)
+    tc = protocol.GpuTrainerChannel(w, b_r)
+    all_codes = []
+    for t in tensors:
+        y, directed, corr = tc.process(t, tau)
+        codes = oracle.direction_array(t, b_r, tau)
+        all_codes.append(np.asarray(codes).reshape(-1))
+        want = oracle.rnd_array(t, b_r)
+        assert y.shape == np.shape(want) and np.array_equal(bits(y), bits(want))
+        assert directed == int(np.count_nonzero(codes != 1)) and corr == 0
+    w.close()
+    assert path.read_bytes() == oracle.vtrl_bytes(all_codes, b_r)
+    ac = protocol.GpuAuditorChannel(roundlog.LogReader(path), b_r)
+    for t, codes in zip(tensors, all_codes):
+        noisy = np.nextafter(t, np.where(rng.random(np.shape(t)) < 0.5, np.inf, -np.inf))
+        y, directed, corr = ac.process(noisy, tau)
+        want = oracle.rev_array(noisy, b_r, codes.reshape(np.shape(noisy)) if np.shape(noisy) else codes)
+        assert np.array_equal(bits(y), bits(want))
+        assert corr == int(np.count_nonzero(want != oracle.rnd_array(noisy, b_r)))
+    assert ac.reader.remaining == 0
+    raw = bytearray(path.read_bytes())
+    raw[roundlog.HEADER_LEN + 3] = 251
+    path.write_bytes(bytes(raw))
+    with pytest.raises(roundlog.LogFormatError, match="corrupt log byte"):
+        roundlog.LogReader(path)

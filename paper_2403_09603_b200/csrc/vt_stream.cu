@@ -17,6 +17,7 @@
 // through cp.async.bulk (TMA bulk copies, L2 evict-first) into a shared-memory
 // ring guarded by mbarriers, so HBM streams continuously while the SM computes.
 #include <algorithm>
+#include <cstdlib>
 
 #include "vt_common.cuh"
 
@@ -1475,6 +1476,7 @@ static int launch_rlf(RLFArgs a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kFThreads, smem);
+    if (const char* e = getenv("VT_RL_CTAS_PER_SM")) per = std::max(1, std::min(per, atoi(e)));  // A/B only
     resident = std::max(1, per * sms);
   }
   a.n4 = a.num_tiles / kSuper;

@@ -1201,7 +1201,12 @@ __global__ void __launch_bounds__(kAdThreads) adapt_keys32_kernel(const double* 
   };
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 31) == 0;
   const int64_t nfull = vec ? (n / kIter) * kIter : 0;
-  for (int64_t base = (int64_t)blockIdx.x * kIter; base < n; base += (int64_t)gridDim.x * kIter) {
+  // back to front: the in-place rounding pass that follows streams x front to
+  // back, so the part of x this pass read last is the part it reads first,
+  // while it is still in L2
+  const int64_t nit = (n + kIter - 1) / kIter;
+  for (int64_t it = nit - 1 - (int64_t)blockIdx.x; it >= 0; it -= (int64_t)gridDim.x) {
+    const int64_t base = it * kIter;
     D4 xv[kSteps];
     if (base < nfull) {
 #pragma unroll

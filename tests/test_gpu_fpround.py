@@ -316,3 +316,45 @@ def test_large_properties():
     y2, corr = ops.replay(x, 32, log)
     assert corr == 0 and torch.equal(y.view(torch.int32), y2.view(torch.int32))
     assert torch.equal(y.view(torch.int32), x.float().view(torch.int32))  # b_r=32 is RNE to FP32
+
+
+@pytest.mark.parametrize("b_r", list(range(10, 33)))
+def test_every_grid_random_bit_patterns(oracle, fp, b_r):
+    """Every b_r in [10, 32] (fpround.py:44-46): random FP64 BIT PATTERNS over
+    the whole finite range below grid_max (FP64 subnormals, FP32-subnormal
+    results, ties of the dropped bits, values at tau from the grid), through
+    rnd / direction at three taus / grid neighbours / rev and the fused sparse
+    round-and-log + replay, against the oracle bit for bit."""
+    import torch
+
+    from paper_2403_09603_b200 import ops
+    rng = np.random.default_rng(7000 + b_r)
+    n = 40_000
+    raw = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) | (rng.integers(0, 2, size=n, dtype=np.uint64) << 63)
+    x = raw.view(np.float64)
+    x = x[np.isfinite(x) & (np.abs(x) <= oracle.grid_max(b_r))]
+    # exact ties and near-ties of the dropped bits on the normal FP32 range
+    drop = 52 - (b_r - 9)
+    base = rng.normal(size=2000)
+    tb = (base.view(np.uint64) & ~np.uint64((1 << drop) - 1)) | np.uint64(1 << (drop - 1))
+    ties = np.concatenate([tb.view(np.float64), np.nextafter(tb.view(np.float64), np.inf),
+                           np.nextafter(tb.view(np.float64), -np.inf)])
+    x = np.concatenate([x, ties, -ties, np.ldexp(rng.normal(size=500), -140), [0.0, -0.0]])
+    lo, hi = oracle.tau_bounds(b_r)
+    for tau in (0.0, lo, 0.5 * (lo + hi), hi):
+        assert np.array_equal(fp.direction_array(x, b_r, tau), oracle.direction_array(x, b_r, tau)), tau
+    assert np.array_equal(bits(fp.rnd_array(x, b_r)), bits(oracle.rnd_array(x, b_r)))
+    glo, ghi = fp.grid_neighbors_array(x, b_r)
+    wlo, whi = oracle.grid_neighbors_array(x, b_r)
+    assert np.array_equal(bits(glo), bits(wlo)) and np.array_equal(bits(ghi), bits(whi))
+    codes = rng.integers(0, 3, size=x.size).astype(np.uint8)
+    assert np.array_equal(bits(fp.rev_array(x, b_r, codes)), bits(oracle.rev_array(x, b_r, codes)))
+    # the fused sparse path, FP64 out (every grid value is exact in FP32 too)
+    tau = 0.5 * (lo + hi)
+    xd = torch.from_numpy(x).cuda()
+    y, log = ops.round_and_log(xd, b_r, tau, out_dtype=torch.float64, global_base=3)
+    want = oracle.direction_array(x, b_r, tau)
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64), oracle.sparse_from_codes(want, base=3))
+    assert np.array_equal(bits(y.cpu().numpy()), bits(oracle.rnd_array(x, b_r)))
+    ya, corr = ops.replay(xd, b_r, log, out_dtype=torch.float64, global_base=3)
+    assert np.array_equal(bits(ya.cpu().numpy()), bits(oracle.rev_array(x, b_r, want))) and corr == 0

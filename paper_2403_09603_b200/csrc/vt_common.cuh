@@ -355,6 +355,7 @@ int rl_stream(const double* x, int64_t n, const Grid& g, int thr32, bool fast, i
               int64_t* counters, int32_t* err, void* ws, cudaStream_t st, const DevThr* dthr = nullptr,
               const int32_t* gate = nullptr, uint64_t* keys = nullptr, XPeers xp = XPeers{nullptr, 0, 0});
 int counts_wait(XPeers xp, int64_t* counts_out, int32_t* err, cudaStream_t st);
+int exchange_publish_empty(XPeers xp, cudaStream_t st);
 int rp_stream(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out, const uint64_t* log,
               int64_t n_words, int64_t log_base, int64_t* counters, int32_t* err, void* ws, cudaStream_t st);
 int rp_stream_packed(const double* x, int64_t n, const Grid& g, bool fast, int out_kind, void* out,

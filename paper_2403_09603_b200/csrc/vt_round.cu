@@ -637,9 +637,15 @@ extern "C" int vt_round_log_exchange(const double* x, int64_t n, int b_r, double
                                      uint64_t* sparse, int64_t sparse_cap, int64_t global_base, int64_t* counters,
                                      int32_t* err, void* ws, size_t ws_bytes, uint64_t* const* xpeers, int world,
                                      int rank, vt_stream_t stream) {
-  if (n <= 0 || !valid_b(b_r) || out_kind < 0 || out_kind > 2 || !counters || !err || !sparse || !ws ||
-      ws_bytes < vt_round_log_workspace(n) || !xpeers || world <= 0 || rank < 0 || rank >= world) {
-    vt_set_error("vt_round_log_exchange: bad argument (n > 0, sparse log, workspace, 0 <= rank < world)");
+  if (n < 0 || !valid_b(b_r) || out_kind < 0 || out_kind > 2 || !counters || !err || !xpeers || world <= 0 ||
+      rank < 0 || rank >= world) {
+    vt_set_error("vt_round_log_exchange: bad argument (n >= 0, 0 <= rank < world)");
+    return VT_EINVAL;
+  }
+  if (n == 0)  // an empty shard still takes part: it publishes a count of 0
+    return exchange_publish_empty(XPeers{xpeers, world, rank}, static_cast<cudaStream_t>(stream));
+  if (!sparse || !ws || ws_bytes < vt_round_log_workspace(n)) {
+    vt_set_error("vt_round_log_exchange: bad argument (sparse log, workspace)");
     return VT_EINVAL;
   }
   if (!aligned(x, 32) || (out_kind == VT_OUT_F32 && !aligned(out, 16)) || (out_kind == VT_OUT_F64 && !aligned(out, 32))) {

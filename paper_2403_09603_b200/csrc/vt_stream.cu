@@ -149,6 +149,22 @@ constexpr int kEpochShift = 44;
 constexpr int kXSeqShift = 40;
 constexpr uint64_t kXSeqMask = (1ull << 24) - 1;
 constexpr uint64_t kXCountMask = (1ull << 40) - 1;
+
+// The last CTA of an exchanging round-and-log (or an empty shard's one
+// thread): this call's entry count into slot [parity][rank] of every rank's
+// exchange buffer, tagged with this rank's next sequence number.
+__device__ __forceinline__ void exchange_publish(const XPeers& xp, uint64_t total) {
+  uint64_t* mine = xp.peers[xp.rank];
+  const uint64_t seq = mine[0] + 1ull;
+  mine[0] = seq;
+  const uint64_t word = ((seq & kXSeqMask) << kXSeqShift) | (total & kXCountMask);
+  const int par = (int)(seq & 1ull);
+  for (int p = 0; p < xp.world; ++p) st_release_sys_u64(xp.peers[p] + 1 + par * xp.world + xp.rank, word);
+}
+
+__global__ void exchange_publish_kernel(const XPeers xp, uint64_t total) { exchange_publish(xp, total); }
+
+
 constexpr uint64_t kEpochMask = (1ull << 20) - 1;
 constexpr uint64_t kLBAgg = 1ull << 42;
 constexpr uint64_t kLBInc = 2ull << 42;
@@ -703,14 +719,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       // with this rank's exchange sequence number; slots alternate by parity
       // so a rank one exchange ahead cannot overwrite a slot still awaited
       __threadfence();
-      const uint64_t total = *(volatile uint64_t*)&a.hdr->total;
-      uint64_t* mine = a.xp.peers[a.xp.rank];
-      const uint64_t seq = mine[0] + 1ull;
-      mine[0] = seq;
-      const uint64_t word = ((seq & kXSeqMask) << kXSeqShift) | (total & kXCountMask);
-      const int par = (int)(seq & 1ull);
-      for (int p = 0; p < a.xp.world; ++p)
-        st_release_sys_u64(a.xp.peers[p] + 1 + par * a.xp.world + a.xp.rank, word);
+      exchange_publish(a.xp, *(volatile uint64_t*)&a.hdr->total);
     }
     a.hdr->ticket = 0u;
     a.hdr->done = 0u;
@@ -718,6 +727,11 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     a.hdr->epoch = S.epoch == (uint32_t)kEpochMask ? 0u : S.epoch;
     __threadfence();
   }
+}
+
+int exchange_publish_empty(XPeers xp, cudaStream_t st) {
+  exchange_publish_kernel<<<1, 1, 0, st>>>(xp, 0ull);
+  return vt_check_launch("exchange_publish_kernel");
 }
 
 // The other half of the exchange: wait until every rank's count for this

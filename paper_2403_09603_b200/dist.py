@@ -143,18 +143,17 @@ class CountExchange:
         from . import ops
         from .fpround import _check_b
         _check_b(b_r)
-        t = self.D.aligned_f64(x_local.reshape(-1))
-        n = t.numel()
-        if n == 0:
-            raise ValueError("CountExchange.round_and_log: empty shard")
+        t = self.D.aligned_f64(x_local.reshape(-1)) if x_local.numel() else x_local.reshape(-1)
+        n = t.numel()  # an empty shard still publishes (a count of 0)
         y = out if out is not None else torch.empty(n, dtype=out_dtype, device=t.device)
         self.D.check_out(y, n, out_dtype, t.device, "out")
         words = log_out if log_out is not None else torch.empty(ops.default_log_capacity(n), dtype=torch.int64,
                                                                 device=t.device)
-        need = int(self.lib.lib().vt_round_log_workspace(n))
+        need = int(self.lib.lib().vt_round_log_workspace(max(n, 1)))
         ws = workspace if workspace is not None else self.D.workspace(need, "round_log")
         f = self.D.Flags()
-        self.lib.call("vt_round_log_exchange", self.D.ptr(t), n, b_r, float(tau), ops._out_kind(out_dtype),
+        self.lib.call("vt_round_log_exchange", self.D.ptr(t) if n else None, n, b_r, float(tau),
+                      ops._out_kind(out_dtype),
                       self.D.ptr(y), self.D.ptr(words), words.numel(), int(global_base), f.cnt_ptr, f.err_ptr,
                       self.D.ptr(ws), ws.numel(), self.peers, self.world, self.rank, self.D.stream_ptr())
         return ops.PendingRound(y, words, f)

@@ -83,6 +83,7 @@ BAD_CALLS = [
     ("vt_tau_budget", (None, 10, 32, -1, 30, None, None, None, None, 0, None)),
     ("vt_tau_shard_plan", (0, 32, 10, None, None)),
     ("vt_round_log_exchange", (None, 10, 32, 0.0, 1, None, None, 0, 0, None, None, None, 0, None, 1, 0, None)),
+    ("vt_round_log_exchange", (None, 10, 32, 0.0, 1, None, None, 0, 0, None, None, None, 0, None, 1, 1, None)),
     ("vt_counts_wait", (None, 1, 0, None, None, None)),
     ("vt_tau_shard_candidates", (None, 10, 32, 5, 1, None, None, None, 0, None)),
     ("vt_tau_shard_digit_keys", (10, 32, 10, 1, 5000, None, 0, None, None, 0, None)),

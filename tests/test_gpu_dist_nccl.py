@@ -88,6 +88,11 @@ def test_count_exchange_over_symmetric_memory(nccl_group):
         assert slog.counts.tolist() == [log1.count] and slog.total == log1.count, i
         assert torch.equal(slog.local.words, log1.words) and torch.equal(y.view(torch.int32), y1.view(torch.int32))
     assert int(ex.buf[0].item()) == 5  # five exchanges, five sequence numbers
+    # an empty shard still takes part: it publishes a count of 0
+    p = ex.round_and_log(torch.empty(0, dtype=torch.float64, device="cuda"), 32, workloads.TAU_CONFIG0, 0)
+    assert ex.wait().tolist() == [0] and p.finish()[1].count == 0
+    ex.check()
+    assert int(ex.buf[0].item()) == 6
     # graph-captured: the fused kernel + the wait kernel replayed
     n = 1 << 21
     x = workloads.config0_x_torch(n, 60)
@@ -113,5 +118,5 @@ def test_count_exchange_over_symmetric_memory(nccl_group):
     _, log1 = ops.round_and_log(x, 32, workloads.TAU_CONFIG0)
     assert state["c"].tolist() == [log1.count]
     ex.check()
-    assert int(ex.buf[0].item()) == 5 + 1 + 3  # warm-up call, then 3 replays (capture runs nothing)
+    assert int(ex.buf[0].item()) == 6 + 1 + 3  # warm-up call, then 3 replays (capture runs nothing)
 

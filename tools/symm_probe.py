@@ -1,3 +1,5 @@
+"""Development aid: does torch symmetric memory (the count exchange's buffer,
+dist.CountExchange) rendezvous on this box?  Prints the handle's fields."""
 import os, torch, torch.distributed as dist
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29533")
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))

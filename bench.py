@@ -202,13 +202,23 @@ def run_ours(args) -> None:
     from paper_2403_09603_b200 import dist as vdist
 
     world, rank, local = dist_env()
+    # --dist-backend gloo (tests only): every rank on GPU 0 with host-side
+    # collectives, to exercise the multi-rank code paths on a one-GPU box --
+    # its numbers are not measurements (ranks share one GPU)
+    gloo = args.dist_backend == "gloo"
+    if gloo:
+        local = local % torch.cuda.device_count()
+        args.no_graph = True  # host-side collectives cannot be captured
     torch.cuda.set_device(local)
     # under a launcher (WORLD_SIZE set, even 1) the NCCL path runs: process
     # group, count all-gather captured in the step's graph, max over ranks
     ddp = "WORLD_SIZE" in os.environ
     if ddp:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     n = 1 << args.log2n
     tau = workloads.TAU_CONFIG0
@@ -226,7 +236,9 @@ def run_ours(args) -> None:
     # the kernel's last CTA stores its count into every rank's buffer, a wait
     # kernel collects them) -- or an NCCL all-gather if that cannot be set up
     xchg, xchg_kind = None, None
-    if ddp:
+    if gloo:
+        xchg_kind = "gloo all-gather (multi-rank code-path check on one GPU)"
+    elif ddp:
         try:
             xchg = vdist.CountExchange(device=dev)
             xchg_kind = "peer-memory stores fused into rl_fused_kernel + counts_wait_kernel (symmetric memory)"
@@ -1317,6 +1329,8 @@ def main():
                     help="skip the configs[2]/[3]/[4] extras, the size sweep and the strong-scaling legs at N=1")
     ap.add_argument("--harness-check", action="store_true",
                     help="CPU self-test of the multi-rank launcher (gloo, no kernels; tests only)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: every rank on GPU 0, host collectives -- a code-path check, not a measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     maybe_spawn(args)

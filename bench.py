@@ -685,7 +685,7 @@ def config2() -> dict:
                     "ordered filter; CUDA graph. Per-tensor calls (8 streams, one graph) kept for comparison"}
 
 
-def config3_gpt2(steps: int = 3) -> dict:
+def config3_gpt2(steps: int = 6) -> dict:
     """configs[3]: one GPT-2-small FP64 training step (batch 8 x 1024 tokens,
     random init, SGD) with every leaf-module output and input gradient passed
     through the adaptive round-and-log (hooks.RoundAndLogHooks), against the

@@ -27,6 +27,12 @@
 #ifndef VT_RP_L2_PREFETCH  // replay producer: the same (measured slower; off)
 #define VT_RP_L2_PREFETCH 0
 #endif
+#ifndef VT_START_WAVES  // round-and-log: at start, also prefetch tickets s + w * grid, w = 1..VT_START_WAVES
+#define VT_START_WAVES 0
+#endif
+#ifndef VT_RP_START_WAVES  // replay: the same at start
+#define VT_RP_START_WAVES 0
+#endif
 
 namespace vt {
 
@@ -392,44 +398,60 @@ __device__ __forceinline__ uint32_t rlf_tile(const Grid& g, uint32_t c8, uint32_
   return wcnt;
 }
 
-// Look-back by one warp over up to 128 predecessors per round trip (the
-// super-tile's own aggregate was published by its compute warps).  Valid
-// aggregates before the first unpublished word are kept, so every retry
+// Look-back window: words per lane per round trip (window = 32 x this).
+// One word per lane measured best (pair step, graph-timed, round-and-log /
+// copy peak): 2^26 0.918 vs 0.870 for 4 words per lane, 2^28 1.022 vs
+// 0.978, 2^24 0.63 vs 0.59; 8 and 16 words: 0.81 at 2^26.  Most look-backs
+// find an inclusive prefix within the first few predecessors, and the wider
+// window's loads (and re-loads while a predecessor is unpublished) only
+// lengthen each round trip of the log warp, whose placement gates the row
+// writes.  The poll interval (0-512 ns) does not matter.
+#ifndef VT_LB_WORDS
+#define VT_LB_WORDS 1
+#endif
+#ifndef VT_LB_SLEEP  // ns between look-back polls of an unpublished word
+#define VT_LB_SLEEP 32
+#endif
+
+// Look-back by one warp over up to 32 * VT_LB_WORDS predecessors per round
+// trip (the super-tile's own aggregate was published by its compute warps).
+// Valid aggregates before the first unpublished word are kept, so every retry
 // starts at the first word still missing.  Returns the exclusive prefix of
 // super-tile s (same value in every lane) and publishes its inclusive prefix.
-__device__ __forceinline__ int64_t lookback128(uint64_t* status, int64_t s, uint64_t agg, uint32_t epoch,
+__device__ __forceinline__ int64_t lookback(uint64_t* status, int64_t s, uint64_t agg, uint32_t epoch,
                                                int lane) {
+  constexpr int M = VT_LB_WORDS, WIN = 32 * M;
   if (s == 0) return 0;
   int64_t excl = 0, pred = s - 1;
   while (true) {
-    uint64_t w[4];
+    uint64_t w[M];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < M; ++m) {
       const int64_t idx = pred - (m * 32 + lane);
       w[m] = (idx >= 0) ? ld_relaxed_u64(status + idx) : lb_word(epoch, kLBInc, 0);
     }
-    int p_inc = 128, p_inv = 128;  // first INC / first unpublished window position
+    int p_inc = WIN, p_inv = WIN;  // first INC / first unpublished window position
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < M; ++m) {
       const bool valid = ((w[m] >> kEpochShift) & kEpochMask) == epoch;
       const uint64_t flag = valid ? ((w[m] >> 42) & 3ull) : 0ull;
       const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
       const uint32_t inv = __ballot_sync(0xffffffffu, flag == 0);
-      if (p_inc == 128 && inc) p_inc = m * 32 + __ffs(inc) - 1;
-      if (p_inv == 128 && inv) p_inv = m * 32 + __ffs(inv) - 1;
+      if (p_inc == WIN && inc) p_inc = m * 32 + __ffs(inc) - 1;
+      if (p_inv == WIN && inv) p_inv = m * 32 + __ffs(inv) - 1;
     }
     const bool done = p_inc < p_inv;
     const int upto = done ? p_inc + 1 : p_inv;  // positions [0, upto) are summed
     uint64_t v = 0;
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < M; ++m)
       if (m * 32 + lane < upto) v += w[m] & kLBVal;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     excl += (int64_t)v;
     if (done) break;
     pred -= upto;
-    if (upto < 128) __nanosleep(32);
+    if (upto < WIN) __nanosleep(VT_LB_SLEEP);
   }
   if (lane == 0) st_relaxed_u64(status + s, lb_word(epoch, kLBInc, (uint64_t)excl + agg));
   return excl;
@@ -567,7 +589,10 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
             mbar_arrive(S.full + st);
           }
           // the first ticket: its tiles beyond the ring, once the ring's copies are issued
-          if (VT_L2_PREFETCH && k == 0 && i == kFStages - 1) prefetch(s, kFStages);
+          if (VT_L2_PREFETCH && k == 0 && i == kFStages - 1) {
+            prefetch(s, kFStages);
+            for (int w = 1; w <= VT_START_WAVES; ++w) prefetch(s + (int64_t)w * gridDim.x, 0);
+          }
         }
         if (s < 0) break;
         s = nxt;
@@ -592,7 +617,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
       }
       const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
       if (lane < kRows) S.rpos[slot][lane] = inc - c;
-      const int64_t excl = lookback128(a.status, s, agg, epoch, lane);
+      const int64_t excl = lookback(a.status, s, agg, epoch, lane);
       if (lane == 0) {
         if (s == a.num_super - 1) {
           atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(excl + (int64_t)agg));
@@ -917,7 +942,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       }
       const uint64_t agg = __shfl_sync(0xffffffffu, inc, 31);
       if (lane < kRows) S.rpos[slot][lane] = inc - c;
-      const int64_t excl = lookback128(status + sg.tick0, ls, agg, epoch, lane);
+      const int64_t excl = lookback(status + sg.tick0, ls, agg, epoch, lane);
       if (lane == 0) {
         if (ls == v.num_super - 1) {
           if (sg.counters)
@@ -1282,6 +1307,13 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
       };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
       prefetch(s);
+      for (int w = 1; w <= VT_RP_START_WAVES; ++w) {
+        const int64_t s2 = s + (int64_t)w * gridDim.x;
+        if (s2 < a.num_super) {
+          const int64_t t0 = rp_first(a, s2), t1 = min(t0 + (int64_t)rp_ntiles(a, s2), full_tiles);
+          if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
+        }
+      }
       int64_t q = 0;
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;

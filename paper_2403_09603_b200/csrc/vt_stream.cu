@@ -27,12 +27,7 @@
 #ifndef VT_RP_L2_PREFETCH  // replay producer: the same (measured slower; off)
 #define VT_RP_L2_PREFETCH 0
 #endif
-#ifndef VT_START_WAVES  // round-and-log: at start, also prefetch tickets s + w * grid, w = 1..VT_START_WAVES
-#define VT_START_WAVES 0
-#endif
-#ifndef VT_RP_START_WAVES  // replay: the same at start
-#define VT_RP_START_WAVES 0
-#endif
+
 
 namespace vt {
 
@@ -216,9 +211,21 @@ extern "C" int vt_debug_timeline(uint64_t* host) {
 }
 #define TL(i) tl_mark(i)
 #define TLV(i, v) tl_put(i, v)
+__device__ __forceinline__ uint64_t tl_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TWAIT(acc, stmt)            \
+  do {                              \
+    const uint64_t t_ = tl_now();   \
+    stmt;                           \
+    acc += tl_now() - t_;           \
+  } while (0)
 #else
 #define TL(i)
 #define TLV(i, v)
+#define TWAIT(acc, stmt) stmt
 #endif
 
 // A ticket ("super-tile") is kSuper tiles: the unit of the dynamic schedule
@@ -589,10 +596,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
             mbar_arrive(S.full + st);
           }
           // the first ticket: its tiles beyond the ring, once the ring's copies are issued
-          if (VT_L2_PREFETCH && k == 0 && i == kFStages - 1) {
-            prefetch(s, kFStages);
-            for (int w = 1; w <= VT_START_WAVES; ++w) prefetch(s + (int64_t)w * gridDim.x, 0);
-          }
+          if (VT_L2_PREFETCH && k == 0 && i == kFStages - 1) prefetch(s, kFStages);
         }
         if (s < 0) break;
         s = nxt;
@@ -1144,11 +1148,15 @@ __device__ int64_t warp_lower_bound(const uint64_t* w, int64_t lo, int64_t hi, i
 // binomial around the interpolated position, with sd <= sqrt(nw) / 2, so 32
 // probes spaced sqrt(nw) / 8 (+-4 sd) usually bracket the answer; otherwise
 // (skewed logs) the bracket is one side of the probes.  Then the 32-ary search.
+// Measured and not kept: two-round forms (128 probes then the bracket, or 32
+// probes then the whole bracket in one round of up to 12 loads per lane):
+// the first search of each CTA still waits behind the TMA burst, and the
+// extra scattered probes cost 1-8% at 2^26.
 __device__ int64_t log_lower_bound(const RPArgs& a, int64_t key, int lane) {
   const int64_t nw = a.n_words;
   if (nw == 0) return 0;
-  const int64_t d = std::max<int64_t>(64, (int64_t)(sqrt((double)nw) * 0.125));
   const int64_t g = (int64_t)((double)(key - a.log_base) / (double)a.n * (double)nw);
+  const int64_t d = std::max<int64_t>(64, (int64_t)(sqrt((double)nw) * 0.125));
   const int64_t p = g + (int64_t)(lane - 16) * d;
   const bool lt = (p < 0) || (p < nw && (int64_t)(__ldg(a.log + p) >> 1) < key);
   const int c = __popc(__ballot_sync(0xffffffffu, lt));
@@ -1307,18 +1315,15 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
       };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
       prefetch(s);
-      for (int w = 1; w <= VT_RP_START_WAVES; ++w) {
-        const int64_t s2 = s + (int64_t)w * gridDim.x;
-        if (s2 < a.num_super) {
-          const int64_t t0 = rp_first(a, s2), t1 = min(t0 + (int64_t)rp_ntiles(a, s2), full_tiles);
-          if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
-        }
-      }
       int64_t q = 0;
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
         S.ids[k % kRIds] = s;
         mbar_arrive(S.tfull + (k % kRIds));
+        // the first ticket's log search (2-3 dependent loads) runs before this
+        // CTA's TMA burst instead of queueing behind it: 2^22 0.37 vs 0.33 of
+        // the copy peak, no change from 2^24 up
+        if (k == 0) mbar_wait(S.nfull, 0u);
         const int nt = (s >= 0) ? rp_ntiles(a, s) : 1;
         const int64_t t0 = (s >= 0) ? rp_first(a, s) : 0;
         int64_t nxt = -1;
@@ -1358,12 +1363,14 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
   } else {  // compute warps
     uint32_t err = 0, flips = 0;
     int64_t q = 0;
+    uint64_t tw_top = 0, tw_next = 0, tw_full = 0;  // timeline builds: ns waited (thread 0)
+    (void)tw_top, (void)tw_next, (void)tw_full;
     uint64_t pw = 0, pp = 0;  // prefetched window for the next tile (word at cur + tid, its predecessor)
     PackedWin pwin{1u, 1u, 1u, 0, 0};  // PACKED: the next tile's payload bytes
     bool pref = false;
     int64_t cur = 0;
     for (int64_t k = 0;; ++k) {
-      mbar_wait(S.nfull + (k % kRIds), (uint32_t)((k / kRIds) & 1));
+      TWAIT(tw_top, mbar_wait(S.nfull + (k % kRIds), (uint32_t)((k / kRIds) & 1)));
       const int64_t s = S.ids[k % kRIds];
       if (s < 0) break;
       const int nt = rp_ntiles(a, s);
@@ -1437,7 +1444,7 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
         pref = true;
         int64_t ncur = cur;
         if (i == nt - 1) {  // next ordinal: its first word comes from the producer's search
-          mbar_wait(S.nfull + ((k + 1) % kRIds), (uint32_t)(((k + 1) / kRIds) & 1));
+          TWAIT(tw_next, mbar_wait(S.nfull + ((k + 1) % kRIds), (uint32_t)(((k + 1) / kRIds) & 1)));
           if (S.ids[(k + 1) % kRIds] >= 0) ncur = S.curs[(k + 1) % kRIds];
           if (s == a.num_super - 1 && tid == 0) a.counters[2] = cur;
         }
@@ -1452,7 +1459,7 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
         const int st = (int)(q % kRStages);
         const double* src = S.ring[st];
         if (t < full_tiles) {
-          mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1));
+          TWAIT(tw_full, mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1)));
         } else {  // partial last tile: plain loads into the (unused) ring slot
           mbar_wait(S.full + st, (uint32_t)((q / kRStages) & 1));
           double* dst = S.ring[st];
@@ -1469,6 +1476,12 @@ __global__ void __launch_bounds__(kRThreads, 3) rp_fused_kernel(const RPArgs a) 
       }
     }
     report_err(a.err, err);
+    if (tid == 0) {
+      TLV(10, tw_top);
+      TLV(11, tw_next);
+      TLV(12, tw_full);
+      TLV(13, (uint64_t)q);
+    }
     uint32_t v = flips;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

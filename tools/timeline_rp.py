@@ -39,3 +39,8 @@ t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
 for name, i in (("CTA start", 0), ("first data", 1), ("CTA end", 3)):
     print(f"{name:10s} min/med/max us:", np.percentile(rel[:, i], [0, 5, 50, 95, 100]).round(2))
+tw = t[:, 10:14].astype(np.float64)
+print("compute thread 0 waits (us, min/5%/med/95%/max over CTAs):")
+for name, col in (("ticket top (search result)", 0), ("next ticket (search result)", 1), ("TMA data (full)", 2)):
+    print(f"  {name:28s}", np.percentile(tw[:, col] / 1000.0, [0, 5, 50, 95, 100]).round(2))
+print("tiles per CTA min/med/max", tw[:, 3].min(), np.median(tw[:, 3]), tw[:, 3].max())

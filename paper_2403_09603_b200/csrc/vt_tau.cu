@@ -1461,6 +1461,50 @@ __device__ void tail_exact(const TailArgs& a, const TailSel& t, uint32_t* sh) {
   }
 }
 
+// 3'. the same selection over the whole grid when the digit holds few keys
+// (the common case): one warp per key counts, across its lanes, how many of
+// the m keys are larger / equal; the warp holding the (rank)-th largest
+// writes it and runs the bisection (equal keys write the same values).  One
+// CTA doing the m^2 / 256 comparisons alone took 22 us for m = 516 (2^26
+// N(0,1)); the last CTA out resets the tensor's state.
+__device__ void tail_exact_grid(const TailArgs& a, const TailSel& t, uint32_t* sh, int64_t blk, int64_t nblk) {
+  AdaptHdr* h = a.h;
+  const int64_t m = (int64_t)h->cand2;
+  if (t.past_hi || m > kSmallSel) {
+    if (blk == 0) tail_exact(a, t, sh);
+    return;
+  }
+  const uint64_t lo1 = a.L_key + 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = nblk * (kAdThreads / 32);
+  for (int64_t i = (blk * kAdThreads + threadIdx.x) >> 5; i < m; i += warps) {
+    const uint64_t ki = a.c2[i];
+    uint32_t gt = 0, eq = 0;
+#pragma unroll 4
+    for (int64_t j = lane; j < m; j += 32) {
+      const uint64_t kj = a.c2[j];
+      gt += kj > ki ? 1u : 0u;
+      eq += kj == ki ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gt += __shfl_xor_sync(0xffffffffu, gt, o);
+      eq += __shfl_xor_sync(0xffffffffu, eq, o);
+    }
+    if (lane == 0 && (int64_t)gt <= t.rank && t.rank < (int64_t)(gt + eq)) {
+      *a.key = lo1 + ki;
+      bisect_to(lo1 + ki, a.lower, a.upper, a.iters, a.dthr, a.tau_out);
+    }
+  }
+  if (last_cta(&h->arrived, (uint32_t)nblk) && threadIdx.x == 0) {  // every CTA has read cand2
+    h->arrived = 0;
+    h->above = 0;
+    h->cand2 = 0;
+    h->above_lo = 0;
+    h->fallback = 0;
+  }
+}
+
 // 4a. per-CTA count of the candidates with key > tau in its contiguous range
 __device__ void tail_filter_count(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk,
                                   unsigned long long* s_acc) {
@@ -1510,6 +1554,28 @@ __device__ void tail_filter_write(const TailArgs& a, int64_t M, int64_t blk, int
     if (a.cursor_out) *a.cursor_out = pos;
   }
 }
+
+#ifndef VT_TAIL_GRID_EXACT
+#define VT_TAIL_GRID_EXACT 1
+#endif
+#ifdef VT_TIMELINE  // development builds only: per-CTA phase stamps of adapt_tail_kernel
+__device__ uint64_t g_tl_tail[1024][8];
+__device__ __forceinline__ void tail_mark(int i) {
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl_tail[blockIdx.x][i] = t;
+  }
+}
+extern "C" int vt_debug_timeline_tail(uint64_t* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_tl_tail, sizeof(g_tl_tail));
+}
+#define TTL(i) tail_mark(i)
+__device__ __forceinline__ void g_tl_tail_cand2(uint64_t v) { g_tl_tail[1023][0] = v; }
+#else
+#define TTL(i)
+#define g_tl_tail_cand2(v)
+#endif
 
 __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a) {
   __shared__ __align__(16) uint32_t sh[kBudBins];
@@ -1561,14 +1627,25 @@ __global__ void __launch_bounds__(kAdThreads) adapt_tail_kernel(const TailArgs a
     return;
   }
   uint32_t err = 0;
+  TTL(0);
   tail_hist(a, M, blk, nblk, sh, &s_acc, err);
+  TTL(1);
   grid.sync();
+  TTL(2);
   if (blk == 0 && tid == 0) h->ccount = 0;  // read by every CTA at entry; the next in-place key pass appends from 0
   const TailSel t = tail_digit(a, M, blk, nblk, sh);
+  TTL(3);
   grid.sync();
+  TTL(4);
   // every CTA clears its share of the histogram (all read it before the sync)
   for (int64_t i = blk * kAdThreads + tid; i < kAdBins; i += nblk * kAdThreads) a.ahist[i] = 0u;
+  if (blk == 0 && tid == 0) g_tl_tail_cand2(a.h->cand2);
+#if VT_TAIL_GRID_EXACT
+  tail_exact_grid(a, t, sh, blk, nblk);
+#else
   if (blk == 0) tail_exact(a, t, sh);
+#endif
+  TTL(5);
   report_err(a.err, err);
   if (!gather) return;
   grid.sync();

@@ -78,7 +78,9 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
     on ONE stream may share a workspace because the stream serialises them.
     Zero-filled once at allocation (the epoch scheme needs a zero start).
     A grown-out-of buffer is retired, not freed: a CUDA graph captured with
-    the old pointer (or queued work) may still use it."""
+    the old pointer (or queued work) may still use it.  Growth is by at
+    least 1.5x, so a run of ever larger calls retires O(log) buffers whose
+    total stays below twice the live one."""
     key = (torch.cuda.current_device(), stream_ptr(), tag)
     with _WS_LOCK:
         ws = _WS.get(key)
@@ -90,7 +92,8 @@ def workspace(nbytes: int, tag: str) -> torch.Tensor:
                 warnings.warn(f"paper_2403_09603_b200: workspace '{tag}' first allocated inside a CUDA graph capture; "
                               "its zero-fill becomes part of the graph.  Warm up on the capture stream "
                               "(torch.cuda.graph(g, stream=s)) or pass workspace=.", stacklevel=3)
-            ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+            grow = ws.numel() * 3 // 2 if ws is not None else 0
+            ws = torch.zeros(max(nbytes, 1 << 20, grow), dtype=torch.uint8, device="cuda")
             _WS[key] = ws
         return ws
 

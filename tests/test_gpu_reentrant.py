@@ -86,6 +86,22 @@ def test_workspaces_are_per_stream():
     assert big.numel() >= 8 << 20 and any(r.data_ptr() == a.data_ptr() for r in D._RETIRED)
 
 
+def test_workspace_growth_is_geometric():
+    """A run of ever larger calls retires O(log) buffers, not one per call."""
+    import torch
+
+    from paper_2403_09603_b200 import _device as D
+    s = torch.cuda.Stream()
+    before = len(D._RETIRED)
+    with torch.cuda.stream(s):
+        for k in range(1, 201):
+            ws = D.workspace(k * (1 << 20) + 7, "t_ws_geo")
+            assert ws.numel() >= k * (1 << 20) + 7
+    retired = D._RETIRED[before:]
+    assert len(retired) <= 16, len(retired)
+    assert sum(r.numel() for r in retired) <= 2 * ws.numel()
+
+
 def test_out_buffers_are_validated():
     import torch
 

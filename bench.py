@@ -982,11 +982,20 @@ def strong_scaling(args, world: int, rank: int, dev) -> dict:
         torch.empty(0, device=dev)
     wb = w.view(torch.uint8)
     res = {}
+    dx = None  # N > 1 over NCCL: the block roots travel over peer memory (DigestExchange)
+    if dist.is_initialized() and args.dist_backend == "nccl":
+        try:
+            n_blocks = (n_leaves + (1 << vdist.BLOCK_LEAVES_LOG2) - 1) >> vdist.BLOCK_LEAVES_LOG2
+            dx = vdist.DigestExchange(n_blocks, device=dev)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] symmetric-memory block-root exchange unavailable, using NCCL: {e!r}", file=sys.stderr)
 
     def mk():
-        res["lv"], res["top"] = vdist.merkle_sharded(wb, n_leaves)
+        res["lv"], res["top"] = vdist.merkle_sharded(wb, n_leaves, exchange=dx, check=False)
 
     ms_m = timed(mk, 3)
+    if dx is not None:
+        dx.check()
     root = bytes(res["top"][-1][0].cpu().numpy())
     del w, wb, res
     torch.cuda.empty_cache()
@@ -997,7 +1006,9 @@ def strong_scaling(args, world: int, rank: int, dev) -> dict:
         del wall
         torch.cuda.empty_cache()
     out["merkle_1.5B"] = {"ms": round(ms_m, 3), "hashed_gbs": round(nparam * 4 / ms_m / 1e6, 1),
-                          "root": root.hex()[:16], "root_equals_single_gpu": same}
+                          "root": root.hex()[:16], "root_equals_single_gpu": same,
+                          "block_roots": ("peer memory (vt_merkle_level_exchange + vt_digests_wait)" if dx is not None
+                                          else "all-gather" if world > 1 else "local")}
     # --- configs[2], LPT over ranks
     xs = workloads.config2_tensors_torch(device=dev)
     sizes = [t.numel() for t in xs]

@@ -39,6 +39,9 @@
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
  *   vt_merkle_build   <- merkle.build over chunked leaves    merkle.py:55-72
+ *   vt_merkle_level_exchange / vt_digests_publish / vt_digests_wait
+ *                     <- the block-root all-gather of a sharded merkle.build,
+ *                        fused over peer memory
  *   vt_serialize_f32  <- the FP32 serialization + finiteness check of
  *                        merkle.hash_weights                 merkle.py:155-166
  */
@@ -211,6 +214,28 @@ int vt_round_log_exchange(const double *x, int64_t n, int b_r, double tau, int o
                           uint64_t *const *xpeers, int world, int rank, vt_stream_t stream);
 int vt_counts_wait(uint64_t *const *xpeers, int world, int rank, int64_t *counts_out, int32_t *err,
                    vt_stream_t stream);
+/*
+ * The block-root exchange of the sharded Merkle tree, fused
+ * over peer memory like the count exchange.  xpeers: device array of
+ * `world` pointers to every rank's buffer of vt_digest_exchange_words(world,
+ * n_total) uint64 words (zero-filled once on every rank).  Rank `rank` owns
+ * the block roots [dst, dst + n) of the n_total roots of all ranks:
+ * vt_merkle_level_exchange hashes its last local level (as vt_merkle_level)
+ * and stores every output digest into every rank's buffer; when the roots
+ * need no hashing (one node, depth 0, or an empty rank) vt_digests_publish
+ * stores them instead.  Either way the kernel's last CTA publishes the
+ * rank's arrival (st.release.sys).  vt_digests_wait (same stream, later)
+ * waits for every rank's arrival of that exchange and copies the n_total
+ * roots, in block order, to out (32 bytes each), or raises VT_ERR_EXCHANGE
+ * in *err after 10 s.  Replaces the ncclAllGather of the block roots.
+ */
+size_t vt_digest_exchange_words(int world, int64_t n_total);
+int vt_merkle_level_exchange(const uint8_t *in, int64_t n_in, uint8_t *out, uint64_t *const *xpeers,
+                             int world, int rank, int64_t dst, int64_t n_total, vt_stream_t stream);
+int vt_digests_publish(const uint8_t *digests, int64_t n, uint64_t *const *xpeers, int world, int rank,
+                       int64_t dst, int64_t n_total, vt_stream_t stream);
+int vt_digests_wait(uint64_t *const *xpeers, int world, int rank, int64_t n_total, uint8_t *out,
+                    int32_t *err, vt_stream_t stream);
 /*
  * The budget search over ONE tensor sharded across ranks,
  * candidate path: vt_tau_shard_plan gives the global plan (candidate

@@ -67,6 +67,10 @@ EXPORTS: dict[str, tuple] = {
     "vt_round_log_exchange": (_i32, [_p, _i64, _i32, _dbl, _i32, _p, _p, _i64, _i64, _p, _p, _p, _sz, _p, _i32, _i32,
                                      _p]),
     "vt_counts_wait": (_i32, [_p, _i32, _i32, _p, _p, _p]),
+    "vt_digest_exchange_words": (_sz, [_i32, _i64]),
+    "vt_merkle_level_exchange": (_i32, [_p, _i64, _p, _p, _i32, _i32, _i64, _i64, _p]),
+    "vt_digests_publish": (_i32, [_p, _i64, _p, _i32, _i32, _i64, _i64, _p]),
+    "vt_digests_wait": (_i32, [_p, _i32, _i32, _i64, _p, _p, _p]),
     "vt_tau_shard_workspace": (_sz, [_i64]),
     "vt_tau_shard_plan": (_i32, [_i64, _i32, _i64, _p, _p]),
     "vt_tau_shard_candidates": (_i32, [_p, _i64, _i32, _i64, _i64, _p, _p, _p, _sz, _p]),

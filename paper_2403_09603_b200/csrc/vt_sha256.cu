@@ -309,6 +309,197 @@ extern "C" int vt_merkle_level(const uint8_t* in, int64_t n_in, uint8_t* out, vt
   return vt_check_launch("merkle_level_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Block-root exchange of the sharded Merkle tree over peer
+// memory: the level kernel that produces a rank's block roots also stores
+// every root into EVERY rank's exchange buffer (symmetric memory mapped over
+// NVLink) at its global block index, and its last CTA publishes the rank's
+// arrival with st.release.sys; a one-CTA wait kernel then gathers all roots.
+// Replaces the ncclAllGather of the block roots.
+//
+// Buffer (uint64 words): [0] this rank's exchange sequence number, [1] CTA
+// done counter (local), [2 + par * world + r] rank r's arrival tag for
+// parity par, then the digests [par][n_total][4 words].  Digest areas and
+// tags alternate by the parity of the sequence number: a rank can only run
+// one exchange ahead of a peer after that peer has published, i.e. after its
+// wait kernel (and every reader of its roots, stream-ordered before its next
+// publish) is done -- the argument of the count exchange (vt_stream.cu).
+// ---------------------------------------------------------------------------
+struct DXPeers {
+  uint64_t* const* peers;
+  int world, rank;
+  int64_t dst;      // this rank's first block index
+  int64_t n_total;  // block roots over all ranks
+};
+
+__device__ __forceinline__ uint64_t* dx_digest(const DXPeers& xp, int p, int par, int64_t j) {
+  return xp.peers[p] + 2 + 2 * xp.world + ((int64_t)par * xp.n_total + j) * 4;
+}
+
+__device__ __forceinline__ void dx_store(const DXPeers& xp, int par, int64_t j, const uint32_t* h) {
+  // the digest's 32 bytes, big-endian words as in store_digest
+  uint4 d0, d1;
+  d0.x = bswap(h[0]); d0.y = bswap(h[1]); d0.z = bswap(h[2]); d0.w = bswap(h[3]);
+  d1.x = bswap(h[4]); d1.y = bswap(h[5]); d1.z = bswap(h[6]); d1.w = bswap(h[7]);
+  for (int p = 0; p < xp.world; ++p) {
+    uint4* q = reinterpret_cast<uint4*>(dx_digest(xp, p, par, xp.dst + j));
+    q[0] = d0;
+    q[1] = d1;
+  }
+}
+
+// every thread of the grid calls this once, after its stores
+__device__ __forceinline__ void dx_finish(const DXPeers& xp, int par) {
+  __shared__ unsigned s_last;
+  __threadfence_system();
+  __syncthreads();
+  uint64_t* mine = xp.peers[xp.rank];
+  if (threadIdx.x == 0)
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(mine + 1), 1ull) == (unsigned long long)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence_system();
+  const uint64_t seq = mine[0] + 1ull;
+  mine[0] = seq;
+  mine[1] = 0ull;
+  for (int p = 0; p < xp.world; ++p) st_release_sys_u64(xp.peers[p] + 2 + par * xp.world + xp.rank, seq);
+}
+
+template <bool FMA>
+__global__ void __launch_bounds__(128) merkle_level_xchg_kernel(const NodeArgs a, const DXPeers xp) {
+  const int par = (int)((xp.peers[xp.rank][0] + 1ull) & 1ull);  // this exchange's parity
+  const uint32_t one = a.one;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_out = (a.n_in + 1) >> 1;
+  if (i < n_out) {
+    uint32_t s[8];
+    if (2 * i + 1 >= a.n_in) {  // unpaired: promoted unchanged (merkle.py:66-67)
+      const uint4* src = reinterpret_cast<const uint4*>(a.in + 64 * i);
+      uint4* dst = reinterpret_cast<uint4*>(a.out + 32 * i);
+      const uint4 v0 = src[0], v1 = src[1];
+      dst[0] = v0;
+      dst[1] = v1;
+      s[0] = bswap(v0.x); s[1] = bswap(v0.y); s[2] = bswap(v0.z); s[3] = bswap(v0.w);
+      s[4] = bswap(v1.x); s[5] = bswap(v1.y); s[6] = bswap(v1.z); s[7] = bswap(v1.w);
+    } else {
+      const uint4* src = reinterpret_cast<const uint4*>(a.in + 64 * i);
+      uint32_t w[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = src[q];
+        w[4 * q + 0] = bswap(v.x);
+        w[4 * q + 1] = bswap(v.y);
+        w[4 * q + 2] = bswap(v.z);
+        w[4 * q + 3] = bswap(v.w);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] = kIV[k];
+      compress<FMA>(s, w, one);
+      compress_wk<FMA>(s, a.pad, one);
+      store_digest(a.out + 32 * i, s);
+    }
+    dx_store(xp, par, i, s);
+  }
+  dx_finish(xp, par);
+}
+
+// roots that need no hashing at this rank (one node, depth 0, or none)
+__global__ void __launch_bounds__(128) digests_publish_kernel(const uint8_t* in, int64_t n, const DXPeers xp) {
+  const int par = (int)((xp.peers[xp.rank][0] + 1ull) & 1ull);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(in + 32 * i);
+    const uint4 v0 = src[0], v1 = src[1];
+    const uint32_t s[8] = {bswap(v0.x), bswap(v0.y), bswap(v0.z), bswap(v0.w),
+                           bswap(v1.x), bswap(v1.y), bswap(v1.z), bswap(v1.w)};
+    dx_store(xp, par, i, s);
+  }
+  dx_finish(xp, par);
+}
+
+__global__ void __launch_bounds__(256) digests_wait_kernel(const DXPeers xp, uint8_t* out, int32_t* err,
+                                                           uint64_t timeout_ns) {
+  __shared__ int s_ok;
+  const uint64_t* mine = xp.peers[xp.rank];
+  const uint64_t seq = *(volatile const uint64_t*)mine;
+  const int par = (int)(seq & 1ull);
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < xp.world; q += blockDim.x) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys_u64(mine + 2 + par * xp.world + q) != seq) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicOr(err, VT_ERR_EXCHANGE);
+        s_ok = 0;
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const uint4* src = reinterpret_cast<const uint4*>(mine + 2 + 2 * xp.world + (int64_t)par * xp.n_total * 4);
+  uint4* dst = reinterpret_cast<uint4*>(out);
+  for (int64_t i = threadIdx.x; i < 2 * xp.n_total; i += blockDim.x) dst[i] = __ldcg(src + i);
+}
+
+extern "C" size_t vt_digest_exchange_words(int world, int64_t n_total) {
+  return (world > 0 && n_total >= 0) ? (size_t)(2 + 2 * world + 8 * n_total) : 0;
+}
+
+static bool dx_ok(uint64_t* const* xpeers, int world, int rank, int64_t dst, int64_t n, int64_t n_total) {
+  return xpeers && world > 0 && rank >= 0 && rank < world && dst >= 0 && n >= 0 && n_total >= 0 &&
+         dst + n <= n_total;
+}
+
+extern "C" int vt_merkle_level_exchange(const uint8_t* in, int64_t n_in, uint8_t* out, uint64_t* const* xpeers,
+                                        int world, int rank, int64_t dst, int64_t n_total, vt_stream_t stream) {
+  const int64_t n_out = (n_in + 1) / 2;
+  if (n_in <= 0 || !in || !out || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      !dx_ok(xpeers, world, rank, dst, n_out, n_total)) {
+    vt_set_error("vt_merkle_level_exchange: bad argument");
+    return VT_EINVAL;
+  }
+  NodeArgs a;
+  a.in = in;
+  a.n_in = n_in;
+  a.out = out;
+  a.pad = make_pad(64);
+  a.one = 1u;
+  const DXPeers xp{xpeers, world, rank, dst, n_total};
+  const unsigned grid = (unsigned)((n_out + 127) / 128);
+  if (sha_fma_adds())
+    merkle_level_xchg_kernel<true><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a, xp);
+  else
+    merkle_level_xchg_kernel<false><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a, xp);
+  return vt_check_launch("merkle_level_xchg_kernel");
+}
+
+extern "C" int vt_digests_publish(const uint8_t* digests, int64_t n, uint64_t* const* xpeers, int world, int rank,
+                                  int64_t dst, int64_t n_total, vt_stream_t stream) {
+  if ((n > 0 && (!digests || (reinterpret_cast<uintptr_t>(digests) & 15))) ||
+      !dx_ok(xpeers, world, rank, dst, n, n_total)) {
+    vt_set_error("vt_digests_publish: bad argument");
+    return VT_EINVAL;
+  }
+  const DXPeers xp{xpeers, world, rank, dst, n_total};
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 148));
+  digests_publish_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(digests, n, xp);
+  return vt_check_launch("digests_publish_kernel");
+}
+
+extern "C" int vt_digests_wait(uint64_t* const* xpeers, int world, int rank, int64_t n_total, uint8_t* out,
+                               int32_t* err, vt_stream_t stream) {
+  if (!dx_ok(xpeers, world, rank, 0, 0, n_total) || !err || (n_total > 0 && (!out || (reinterpret_cast<uintptr_t>(out) & 15)))) {
+    vt_set_error("vt_digests_wait: bad argument");
+    return VT_EINVAL;
+  }
+  const DXPeers xp{xpeers, world, rank, 0, n_total};
+  digests_wait_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(xp, out, err, 10ull * 1000 * 1000 * 1000);
+  return vt_check_launch("digests_wait_kernel");
+}
+
 extern "C" int64_t vt_merkle_node_count(int64_t n_leaves) {
   if (n_leaves <= 0) return 0;
   int64_t total = n_leaves, m = n_leaves;

@@ -481,7 +481,8 @@ def assemble_levels(per_rank_local: list[list], top: list) -> list:
 
 
 def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes: int = 4096,
-                   k: int = BLOCK_LEAVES_LOG2, group=None, hash_leaves=None, hash_level=None):
+                   k: int = BLOCK_LEAVES_LOG2, group=None, hash_leaves=None, hash_level=None,
+                   exchange: DigestExchange | None = None, check: bool = True):
     """Per-rank lower levels (0..depth) + all-gathered block roots + top levels.
 
     Returns (local_levels, top_levels).  Every rank returns depth + 1 local
@@ -490,6 +491,11 @@ def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes:
     full tree is the rank-order concatenation of every rank's local level L
     (ranks own whole blocks); top_levels[0] are the block roots (= global
     level depth) and the levels above it follow (``assemble_levels``).
+    With ``exchange`` (a ``DigestExchange`` for this tree's block count) the
+    block roots travel over peer memory from the kernel that hashes them,
+    instead of an NCCL all-gather; ``check`` reads the exchange's error
+    word (a host sync) -- pass False in a timed loop and call
+    ``exchange.check()`` after it.
     """
     if hash_leaves is None or hash_level is None:
         from . import merkle as mk
@@ -498,15 +504,38 @@ def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes:
     world = _world(group)
     depth = local_depth(n_leaves_total, k)
     leaves = hash_leaves(w_local_bytes) if w_local_bytes.numel() else None
+    # each rank contributes its block roots; ranks own whole blocks, so the
+    # number of roots per rank is known from the plan
+    n_blocks = [(hi - lo + (1 << k) - 1) >> k
+                for lo, hi in (leaf_block_range(n_leaves_total, r, world, k) for r in range(world))]
+    if exchange is not None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if exchange.n_total != sum(n_blocks):
+            raise ValueError(f"DigestExchange sized for {exchange.n_total} block roots, the tree has {sum(n_blocks)}")
+        dst = sum(n_blocks[:rank])
+        if leaves is None or leaves.shape[0] == 0:
+            lv = [torch.zeros((0, 32), dtype=torch.uint8, device=w_local_bytes.device) for _ in range(depth + 1)]
+            exchange.publish(lv[-1], dst)
+        else:  # local_levels, with the level that yields the block roots publishing them
+            lv, cur, published = [leaves], leaves, False
+            for L in range(depth):
+                if cur.shape[0] > 1:
+                    if L == depth - 1:
+                        cur, published = exchange.publish_level(cur, dst), True
+                    else:
+                        cur = hash_level(cur)
+                lv.append(cur)
+            if not published:
+                exchange.publish(lv[-1], dst)
+        roots = exchange.wait()
+        if check:
+            exchange.check()
+        return lv, combine_top(roots.clone(), hash_level)
     if leaves is None or leaves.shape[0] == 0:
         dev = w_local_bytes.device
         lv = [torch.zeros((0, 32), dtype=torch.uint8, device=dev) for _ in range(depth + 1)]
     else:
         lv = local_levels(leaves, depth, hash_level)
-    # each rank contributes its block roots; ranks own whole blocks, so the
-    # number of roots per rank is known from the plan
-    n_blocks = [(hi - lo + (1 << k) - 1) >> k
-                for lo, hi in (leaf_block_range(n_leaves_total, r, world, k) for r in range(world))]
     mine = lv[-1]
     width = max(n_blocks)
     pad = torch.zeros((width, 32), dtype=torch.uint8, device=mine.device)
@@ -515,6 +544,68 @@ def merkle_sharded(w_local_bytes: torch.Tensor, n_leaves_total: int, leaf_bytes:
     _all_gather_flat(gathered, pad, group)
     roots = torch.cat([gathered[r * width: r * width + n_blocks[r]] for r in range(world)])
     return lv, combine_top(roots, hash_level)
+
+
+class DigestExchange:
+    """The block-root exchange of ``merkle_sharded`` over peer memory, like
+    ``CountExchange``: a symmetric-memory buffer per rank (a plain device
+    buffer in a single process) sized for ``n_total`` block roots.  The level
+    kernel that produces this rank's block roots also stores each of them
+    into every rank's buffer at its global block index
+    (``vt_merkle_level_exchange``; ``vt_digests_publish`` when the roots need
+    no hashing), and ``wait`` gathers all of them in block order
+    (``vt_digests_wait``).  No NCCL call, no host round trip."""
+
+    def __init__(self, n_total: int, group=None, device=None):
+        from . import _device as D
+        from . import _lib
+        self.D, self.lib = D, _lib
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n_total = int(n_total)
+        words = int(_lib.lib().vt_digest_exchange_words(self.world, self.n_total))
+        if dist.is_initialized():
+            import torch.distributed._symmetric_memory as symm
+            self.buf = symm.empty(words, dtype=torch.int64, device=dev)
+            self.buf.zero_()
+            name = (group or dist.group.WORLD).group_name
+            self.handle = symm.rendezvous(self.buf, name)
+            self.peers = int(self.handle.buffer_ptrs_dev)
+            torch.cuda.synchronize(dev)
+            dist.barrier(group)  # every buffer is zero before any rank publishes
+        else:
+            self.buf = torch.zeros(words, dtype=torch.int64, device=dev)
+            self._ptrs = torch.tensor([self.buf.data_ptr()], dtype=torch.int64, device=dev)
+            self.peers = int(self._ptrs.data_ptr())
+        self.roots = torch.empty((self.n_total, 32), dtype=torch.uint8, device=dev)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)
+
+    def publish_level(self, cur: torch.Tensor, dst: int) -> torch.Tensor:
+        """One Merkle level over ``cur`` ([m, 32] digests) whose outputs are
+        this rank's block roots [dst, dst + (m+1)//2): hashed and published."""
+        m = int(cur.shape[0])
+        out = torch.empty(((m + 1) // 2, 32), dtype=torch.uint8, device=cur.device)
+        self.lib.call("vt_merkle_level_exchange", self.D.ptr(cur.contiguous()), m, self.D.ptr(out), self.peers,
+                      self.world, self.rank, int(dst), self.n_total, self.D.stream_ptr())
+        return out
+
+    def publish(self, roots: torch.Tensor, dst: int) -> None:
+        """Publish block roots that need no hashing (possibly none)."""
+        n = int(roots.shape[0])
+        self.lib.call("vt_digests_publish", self.D.ptr(roots.contiguous()) if n else None, n, self.peers,
+                      self.world, self.rank, int(dst), self.n_total, self.D.stream_ptr())
+
+    def wait(self) -> torch.Tensor:
+        """Every rank's block roots of the latest exchange, [n_total, 32], in
+        block order (valid in stream order)."""
+        self.lib.call("vt_digests_wait", self.peers, self.world, self.rank, self.n_total,
+                      self.D.ptr(self.roots) if self.n_total else None, self.flags.data_ptr(), self.D.stream_ptr())
+        return self.roots
+
+    def check(self) -> None:
+        if int(self.flags[0].item()) & self.lib.ERR_EXCHANGE:
+            raise RuntimeError("block-root exchange: a peer's roots did not arrive (10 s)")
 
 
 def _device_level(cur: torch.Tensor) -> torch.Tensor:

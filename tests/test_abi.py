@@ -85,6 +85,11 @@ BAD_CALLS = [
     ("vt_round_log_exchange", (None, 10, 32, 0.0, 1, None, None, 0, 0, None, None, None, 0, None, 1, 0, None)),
     ("vt_round_log_exchange", (None, 10, 32, 0.0, 1, None, None, 0, 0, None, None, None, 0, None, 1, 1, None)),
     ("vt_counts_wait", (None, 1, 0, None, None, None)),
+    ("vt_merkle_level_exchange", (None, 2, None, None, 1, 0, 0, 1, None)),
+    ("vt_merkle_level_exchange", (1 << 40, 4, 1 << 40, 1 << 40, 2, 0, 1, 2, None)),  # roots past n_total
+    ("vt_digests_publish", (None, 1, 1 << 40, 1, 0, 0, 1, None)),
+    ("vt_digests_publish", (1 << 40, 1, 1 << 40, 2, 2, 0, 1, None)),  # rank >= world
+    ("vt_digests_wait", (1 << 40, 2, 0, 3, None, 1 << 40, None)),  # no out buffer for 3 roots
     ("vt_tau_shard_candidates", (None, 10, 32, 5, 1, None, None, None, 0, None)),
     ("vt_tau_shard_digit_keys", (10, 32, 10, 1, 5000, None, 0, None, None, 0, None)),
     ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
@@ -114,7 +119,8 @@ def test_entry_points_reject_bad_arguments(name, args):
 
 def test_every_compute_entry_point_is_covered():
     host_only = {"vt_version", "vt_last_error", "vt_tile_elems", "vt_merkle_node_count", "vt_tau_kth_hist_offset",
-                 "vt_tau_kth_hist_bins", "vt_int_mix_ops_per_thread_rep", "vt_exchange_words"}
+                 "vt_tau_kth_hist_bins", "vt_int_mix_ops_per_thread_rep", "vt_exchange_words",
+                 "vt_digest_exchange_words"}
     covered = {c[0] for c in BAD_CALLS}
     assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}
 

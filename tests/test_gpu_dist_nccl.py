@@ -120,3 +120,25 @@ def test_count_exchange_over_symmetric_memory(nccl_group):
     ex.check()
     assert int(ex.buf[0].item()) == 6 + 1 + 3  # warm-up call, then 3 replays (capture runs nothing)
 
+
+
+def test_digest_exchange_over_symmetric_memory(nccl_group):
+    """merkle_sharded with the block roots over peer memory (the level kernel
+    publishes them) equals the NCCL all-gather path and merkle_chunked."""
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    from paper_2403_09603_b200 import merkle
+    g = torch.Generator(device="cuda")
+    g.manual_seed(19)
+    w = torch.randn(5 * (1 << 20) + 4321, dtype=torch.float32, device="cuda", generator=g)
+    b = w.view(torch.uint8)
+    n_leaves = (b.numel() + 4095) // 4096
+    n_blocks = (n_leaves + (1 << 8) - 1) >> 8
+    ex = vdist.DigestExchange(n_blocks, nccl_group)
+    for _ in range(3):
+        lv, top = vdist.merkle_sharded(b, n_leaves, group=nccl_group, k=8, exchange=ex)
+    lv2, top2 = vdist.merkle_sharded(b, n_leaves, group=nccl_group, k=8)
+    assert all(torch.equal(a, c) for a, c in zip(top, top2))
+    assert bytes(top[-1][0].cpu().numpy()) == merkle.merkle_chunked(w).root
+    ex.check()
+    assert int(ex.buf[0].item()) == 3

@@ -1,4 +1,5 @@
-"""The peer-memory count exchange with several ranks on ONE GPU, without
+"""The peer-memory exchanges (round-and-log counts, Merkle block roots)
+with several ranks on ONE GPU, without
 kernels that wait on one another: W virtual ranks, each with its own
 exchange buffer (plain device memory standing in for the symmetric-memory
 mapping), drive vt_round_log_exchange / vt_counts_wait on one stream in an
@@ -120,3 +121,118 @@ def test_virtual_ranks_one_exchange_ahead():
     assert all(got0[r].tolist() == want0 for r in range(W)), (got0, want0)
     assert all(got1[r].tolist() == want1 for r in range(W)), (got1, want1)
     assert all(int(f[0].item()) == 0 for f in vr.flags)
+
+
+# ---------------------------------------------------------------------------
+# the Merkle block-root exchange (vt_merkle_level_exchange / vt_digests_publish
+# / vt_digests_wait), W virtual ranks on one GPU in the same publish-then-wait
+# order
+# ---------------------------------------------------------------------------
+
+def _virtual_merkle(w_bytes, n_leaves: int, world: int, k: int, rounds: int = 1):
+    """Every virtual rank hashes its whole 2^k-leaf blocks; the level that
+    yields its block roots publishes them; then every rank waits and builds
+    the top levels.  Returns (per-rank local levels, per-rank roots, root)."""
+    import torch
+
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib, merkle
+    from paper_2403_09603_b200 import dist as vdist
+    depth = vdist.local_depth(n_leaves, k)
+    ranges = [vdist.leaf_block_range(n_leaves, r, world, k) for r in range(world)]
+    n_blocks = [(hi - lo + (1 << k) - 1) >> k for lo, hi in ranges]
+    n_total = sum(n_blocks)
+    words = int(_lib.lib().vt_digest_exchange_words(world, n_total))
+    bufs = [torch.zeros(words, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    out = None
+    for _ in range(rounds):
+        local = []
+        for r, (lo, hi) in enumerate(ranges):
+            dst = sum(n_blocks[:r])
+            b = w_bytes[lo * 4096: min(hi * 4096, w_bytes.numel())]
+            if hi <= lo:
+                lv = [torch.zeros((0, 32), dtype=torch.uint8, device="cuda") for _ in range(depth + 1)]
+                _lib.call("vt_digests_publish", None, 0, ptrs.data_ptr(), world, r, dst, n_total, D.stream_ptr())
+                local.append(lv)
+                continue
+            cur = merkle.sha256_leaves(b, 4096)
+            lv, published = [cur], False
+            for L in range(depth):
+                if cur.shape[0] > 1:
+                    nxt = torch.empty(((cur.shape[0] + 1) // 2, 32), dtype=torch.uint8, device="cuda")
+                    if L == depth - 1:
+                        _lib.call("vt_merkle_level_exchange", D.ptr(cur), cur.shape[0], D.ptr(nxt), ptrs.data_ptr(),
+                                  world, r, dst, n_total, D.stream_ptr())
+                        published = True
+                    else:
+                        _lib.call("vt_merkle_level", D.ptr(cur), cur.shape[0], D.ptr(nxt), D.stream_ptr())
+                    cur = nxt
+                lv.append(cur)
+            if not published:
+                _lib.call("vt_digests_publish", D.ptr(lv[-1]), lv[-1].shape[0], ptrs.data_ptr(), world, r, dst,
+                          n_total, D.stream_ptr())
+            local.append(lv)
+        roots = []
+        for r in range(world):
+            got = torch.empty((n_total, 32), dtype=torch.uint8, device="cuda")
+            _lib.call("vt_digests_wait", ptrs.data_ptr(), world, r, n_total, D.ptr(got), flags[r].data_ptr(),
+                      D.stream_ptr())
+            roots.append(got)
+        top = vdist.combine_top(roots[0], vdist._device_level)
+        out = (local, roots, bytes(top[-1][0].cpu().numpy()))
+    torch.cuda.synchronize()
+    assert all(int(f[0].item()) == 0 for f in flags)
+    return out
+
+
+@pytest.mark.parametrize("n_params,k", [(3 * (1 << 20) + 12345, 4), ((1 << 18) + 7, 2), (9 * 1024, 4),
+                                        (1024, 4), (5 * 1024, 12)])
+def test_virtual_ranks_merkle_block_roots(n_params, k):
+    """Every rank gathers the same block roots = level `depth` of the full
+    tree, and the top levels give merkle_chunked's root; uneven, empty and
+    single-block ranks included (k small so four ranks get blocks)."""
+    import torch
+
+    from paper_2403_09603_b200 import merkle
+    from paper_2403_09603_b200 import dist as vdist
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n_params)
+    w = torch.randn(n_params, dtype=torch.float32, device="cuda", generator=g)
+    n_leaves = (n_params * 4 + 4095) // 4096
+    local, roots, root = _virtual_merkle(w.view(torch.uint8), n_leaves, W, k, rounds=3)
+    ref = merkle.merkle_chunked(w)
+    assert root == ref.root
+    full = ref.levels_device
+    depth = vdist.local_depth(n_leaves, k)
+    for r in range(W):
+        assert torch.equal(roots[r], full[depth])
+    levels = vdist.assemble_levels(local, vdist.combine_top(roots[0], vdist._device_level))
+    assert len(levels) == len(full) and all(torch.equal(a, b) for a, b in zip(levels, full))
+
+
+def test_digest_exchange_single_process():
+    """Without a process group DigestExchange is the one-rank case, and
+    merkle_sharded through it equals merkle_chunked level for level."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is active in this session")
+    import torch
+
+    from paper_2403_09603_b200 import merkle
+    from paper_2403_09603_b200 import dist as vdist
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    for n_params in (3 * (1 << 20) + 999, 1000):
+        w = torch.randn(n_params, dtype=torch.float32, device="cuda", generator=g)
+        n_leaves = (n_params * 4 + 4095) // 4096
+        n_blocks = (n_leaves + (1 << vdist.BLOCK_LEAVES_LOG2) - 1) >> vdist.BLOCK_LEAVES_LOG2
+        ex = vdist.DigestExchange(n_blocks)
+        for _ in range(3):  # repeated exchanges: the parity alternates
+            lv, top = vdist.merkle_sharded(w.view(torch.uint8), n_leaves, exchange=ex)
+        ref = merkle.merkle_chunked(w)
+        levels = vdist.assemble_levels([lv], top)
+        assert len(levels) == len(ref.levels_device)
+        assert all(torch.equal(a, b) for a, b in zip(levels, ref.levels_device))
+        assert int(ex.buf[0].item()) == 3

@@ -6,11 +6,15 @@
  * copy (vt_replay: protocol._AuditorChannel.process, :212-216) of one FP64
  * tensor, then host checks: the FP32 outputs equal (float)x, the auditor
  * lands on the trainer's grid, the log is strictly ascending with global
- * indices, and its length matches the count the library reports.
+ * indices, and its length matches the count the library reports.  Then the
+ * checkpoint commitment of the trainer's FP32 output: vt_merkle_build (SHA-256
+ * of 4 KiB chunks + merkle.build's levels, merkle.py:24-25,55-72) prints the
+ * root; with a second argument the FP32 bytes are written to that file so a
+ * caller can recompute the root independently (tests/test_abi_c.py, hashlib).
  *
  *   cc -O2 -I include -I /usr/local/cuda/include examples/abi_roundtrip.c \
  *      -L paper_2403_09603_b200 -lvtrain_b200 -L /usr/local/cuda/lib64 -lcudart \
- *      -Wl,-rpath,paper_2403_09603_b200 -o abi_roundtrip && ./abi_roundtrip [n]
+ *      -Wl,-rpath,paper_2403_09603_b200 -o abi_roundtrip && ./abi_roundtrip [n [y.bin]]
  */
 #include <math.h>
 #include <stdint.h>
@@ -122,5 +126,22 @@ int main(int argc, char** argv) {
   printf("n=%lld logged=%lld (%.2f%%) corrections=%lld replay_err=%d bad_y=%lld bad_auditor=%lld bad_log=%lld\n",
          (long long)n, (long long)count, 100.0 * (double)count / (double)n, (long long)hf[10], (int)(int32_t)hf[8],
          (long long)bad_y, (long long)bad_a, (long long)bad_log);
+  /* Merkle commitment of the FP32 output (little-endian bytes, 4 KiB leaves) */
+  const int64_t nbytes = n * 4, leaf = 4096, leaves = (nbytes + leaf - 1) / leaf;
+  const int64_t nodes = vt_merkle_node_count(leaves);
+  uint8_t* dnodes;
+  uint8_t root[32];
+  CK(cudaMalloc((void**)&dnodes, (size_t)nodes * 32));
+  VT(vt_merkle_build((const uint8_t*)dy, nbytes, leaf, dnodes, nodes, st));
+  CK(cudaMemcpyAsync(root, dnodes + (nodes - 1) * 32, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  printf("merkle leaves=%lld nodes=%lld root=", (long long)leaves, (long long)nodes);
+  for (int k = 0; k < 32; ++k) printf("%02x", root[k]);
+  printf("\n");
+  if (argc > 2) {
+    FILE* f = fopen(argv[2], "wb");
+    if (!f || fwrite(hy, 4, (size_t)n, f) != (size_t)n) return 5;
+    fclose(f);
+  }
   return (bad_y || bad_a || bad_log || (int32_t)hf[8]) ? 1 : 0;
 }

@@ -28,9 +28,16 @@ def test_c_example_compiles_and_links(tmp_path):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n", [1, 4099, (1 << 22) + 12345])
-def test_c_example_runs(tmp_path, n):
+def test_c_example_runs(tmp_path, n, oracle):
     exe = tmp_path / "abi_roundtrip"
     _build(exe)
-    r = subprocess.run([str(exe), str(n)], capture_output=True, text=True, timeout=120)
+    ybin = tmp_path / "y.bin"
+    r = subprocess.run([str(exe), str(n), str(ybin)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "bad_y=0 bad_auditor=0 bad_log=0" in r.stdout and "replay_err=0" in r.stdout
+    # the Merkle root the C caller got from vt_merkle_build == the oracle's
+    # (hashlib SHA-256 of 4 KiB chunks, merkle.build's promotion rule)
+    data = ybin.read_bytes()
+    assert len(data) == 4 * n
+    want = oracle.merkle_levels(oracle.chunk_leaves(data, 4096))[-1][0]
+    assert f"root={want.hex()}" in r.stdout, r.stdout

@@ -417,7 +417,10 @@ struct RLBatch {
 };
 
 // tiles (of 2048 elements) per round-and-log ticket / look-back word
-constexpr int kRLSuper = 4;
+#ifndef VT_RL_SUPER  // A/B: tiles per round-and-log ticket
+#define VT_RL_SUPER 4
+#endif
+constexpr int kRLSuper = VT_RL_SUPER;
 __host__ __device__ inline int64_t rl_batch_tickets(int64_t n) {
   const int64_t tiles = (n + 2047) / 2048;
   return tiles / kRLSuper + tiles % kRLSuper;

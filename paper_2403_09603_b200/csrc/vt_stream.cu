@@ -235,8 +235,14 @@ __device__ __forceinline__ uint64_t tl_now() {
 // 2^26 78% vs 81%, 2^28 85% vs 90% -- twice the look-backs and ordinal
 // overheads, and the tail spread (CTA speeds differ ~1.6x) barely moved.
 constexpr int kSuper = kRLSuper;                 // tiles per super-tile / status word
-constexpr int kMaskSlots = 3;                    // super-tiles of masks in flight
-constexpr int kFStages = 3;                      // TMA ring depth of the fused kernel
+#ifndef VT_MASK_SLOTS  // A/B
+#define VT_MASK_SLOTS 3
+#endif
+#ifndef VT_RL_STAGES  // A/B
+#define VT_RL_STAGES 3
+#endif
+constexpr int kMaskSlots = VT_MASK_SLOTS;        // super-tiles of masks in flight
+constexpr int kFStages = VT_RL_STAGES;           // TMA ring depth of the fused kernel
 constexpr int kRow = 64;                         // staged entries per warp-tile (else from masks)
 // KEYS launches reuse a row's 128 bytes as kRowK {key, entry} pairs: 8-byte
 // keys first, then the 16-bit entries

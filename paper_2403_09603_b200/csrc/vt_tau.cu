@@ -1461,6 +1461,12 @@ __device__ void tail_exact(const TailArgs& a, const TailSel& t, uint32_t* sh) {
   }
 }
 
+#ifndef VT_TAIL_GRID_EXACT
+#define VT_TAIL_GRID_EXACT 1
+#endif
+#ifndef VT_GRID_SEL_MIN  // digit keys up to this many: block 0 alone (select_by_count), no grid-wide hand-off
+#define VT_GRID_SEL_MIN 192
+#endif
 // 3'. the same selection over the whole grid when the digit holds few keys
 // (the common case): one warp per key counts, across its lanes, how many of
 // the m keys are larger / equal; the warp holding the (rank)-th largest
@@ -1470,7 +1476,7 @@ __device__ void tail_exact(const TailArgs& a, const TailSel& t, uint32_t* sh) {
 __device__ void tail_exact_grid(const TailArgs& a, const TailSel& t, uint32_t* sh, int64_t blk, int64_t nblk) {
   AdaptHdr* h = a.h;
   const int64_t m = (int64_t)h->cand2;
-  if (t.past_hi || m > kSmallSel) {
+  if (t.past_hi || m > kSmallSel || m <= VT_GRID_SEL_MIN) {  // few keys: one CTA counts them faster
     if (blk == 0) tail_exact(a, t, sh);
     return;
   }
@@ -1555,9 +1561,6 @@ __device__ void tail_filter_write(const TailArgs& a, int64_t M, int64_t blk, int
   }
 }
 
-#ifndef VT_TAIL_GRID_EXACT
-#define VT_TAIL_GRID_EXACT 1
-#endif
 #ifdef VT_TIMELINE  // development builds only: per-CTA phase stamps of adapt_tail_kernel
 __device__ uint64_t g_tl_tail[1024][8];
 __device__ __forceinline__ void tail_mark(int i) {

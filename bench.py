@@ -687,9 +687,11 @@ def config2() -> dict:
 
 def config3_gpt2(steps: int = 6) -> dict:
     """configs[3]: one GPT-2-small FP64 training step (batch 8 x 1024 tokens,
-    random init, SGD) with every leaf-module output and input gradient passed
-    through the adaptive round-and-log (hooks.RoundAndLogHooks), against the
-    same step without the hooks."""
+    random init, SGD) with every leaf-module output and input gradient, and
+    the loss gradient, passed through the adaptive round-and-log
+    (hooks.RoundAndLogHooks, protocol.py:264-285) and the updated parameters
+    rounded onto the grid (hooks.round_parameters, protocol.py:286-293),
+    against the same step without any of it."""
     import torch
 
     from paper_2403_09603_b200 import hooks, workloads
@@ -700,16 +702,22 @@ def config3_gpt2(steps: int = 6) -> dict:
     idx = torch.randint(0, 50257, (8, 1024), device="cuda", generator=g)
     tgt = torch.randint(0, 50257, (8, 1024), device="cuda", generator=g)
 
+    cur = {"hk": None}
+
     def step():
         opt.zero_grad(set_to_none=True)
         logits = model(idx)
+        if cur["hk"] is not None:
+            cur["hk"].loss_grad(logits)
         loss = torch.nn.functional.cross_entropy(logits.view(-1, logits.shape[-1]), tgt.view(-1))
         loss.backward()
         opt.step()
+        if cur["hk"] is not None:
+            hooks.round_parameters(model)
         return loss
 
     ms_plain = _time(step, reps=steps, warm=1)
-    hk = hooks.RoundAndLogHooks(model)
+    hk = cur["hk"] = hooks.RoundAndLogHooks(model)
     step()
     info = hk.collect()
 
@@ -722,7 +730,7 @@ def config3_gpt2(steps: int = 6) -> dict:
     logs = hk.collect(keep_logs=True)["logs"]
     hk.remove()
     # the auditor's step: the same hook points replay a trainer step's logs in place
-    ha = hooks.ReplayHooks(model, logs)
+    ha = cur["hk"] = hooks.ReplayHooks(model, logs)
 
     def step_audited():
         step()
@@ -734,7 +742,8 @@ def config3_gpt2(steps: int = 6) -> dict:
             "step_ms_plain": round(ms_plain, 2), "step_ms_round_and_log": round(ms_hooked, 2),
             "trainer_overhead": round(ms_hooked / ms_plain, 4), "step_ms_replay": round(ms_audited, 2),
             "auditor_overhead": round(ms_audited / ms_plain, 4), "hooked_tensors": info["tensors"],
-            "hooked_fwd": info["fwd"], "hooked_bwd": info["bwd"], "hooked_elements": info["elements"],
+            "hooked_fwd": info["fwd"], "hooked_bwd": info["bwd"], "hooked_loss_grad": info["loss"],
+            "parameters_rounded": True, "hooked_elements": info["elements"],
             "logged_entries": info["logged"], "budget": "0.5% per tensor",
             "paper_trainer_overhead": "1.2-1.4x (PAPER.md:402, A40 / Titan XP / 2080 Ti)"}
 

@@ -106,6 +106,17 @@ class RoundAndLogHooks:
             return tuple(self._round(g, name, "bwd") if isinstance(g, torch.Tensor) else g for g in grad_input)
         return hook
 
+    def loss_grad(self, output: torch.Tensor, name: str = "loss") -> torch.Tensor:
+        """Route the loss gradient (d loss / d ``output``, the model's output)
+        through the round-and-log as well -- protocol.py:277-280, where the
+        reference passes the loss gradient through the channel before the
+        backward stages.  Call on the output before ``backward()``; the
+        gradient is rounded and logged when autograd reaches it (recorded
+        with kind "loss")."""
+        if self.enabled and isinstance(output, torch.Tensor) and output.requires_grad:
+            output.register_hook(lambda g: self._round(g, name, "loss"))
+        return output
+
     def collect(self, keep_logs: bool = False) -> dict:
         """Synchronise once: per-tensor taus and log sizes of the step (one
         copy of the step's result slots), then clear the slots for the next
@@ -129,6 +140,7 @@ class RoundAndLogHooks:
         out = {"tensors": m, "elements": sum(r.numel for r in records),
                "logged": sum(counts), "fwd": sum(1 for r in records if r.kind == "fwd"),
                "bwd": sum(1 for r in records if r.kind == "bwd"),
+               "loss": sum(1 for r in records if r.kind == "loss"),
                "tau_min": min(taus) if taus else None, "tau_max": max(taus) if taus else None,
                "taus": taus, "counts": counts,
                "calls": [(r.name, r.kind, r.numel, r.budget) for r in records]}
@@ -201,6 +213,13 @@ class ReplayHooks:
             return tuple(self._replay(g, name, "bwd") if isinstance(g, torch.Tensor) else g for g in grad_input)
         return hook
 
+    def loss_grad(self, output: torch.Tensor, name: str = "loss") -> torch.Tensor:
+        """The auditor's side of ``RoundAndLogHooks.loss_grad``: the loss
+        gradient is replayed against the trainer's log at the same point."""
+        if self.enabled and isinstance(output, torch.Tensor) and output.requires_grad:
+            output.register_hook(lambda g: self._replay(g, name, "loss"))
+        return output
+
     def collect(self) -> dict:
         """Synchronise once: per-tensor corrections (elements where the log
         overrode plain rounding), errors raised as the reference does."""
@@ -220,6 +239,29 @@ class ReplayHooks:
         for h in self._handles:
             h.remove()
         self._handles.clear()
+
+
+@torch.no_grad()
+def round_parameters(model: torch.nn.Module, b_r: int = 32) -> None:
+    """Every FP64 parameter onto the b_r grid in place after the update, no
+    log (protocol.py:286-293: ``stage.W = rnd_array(new_W, b_r)`` -- the
+    stored parameters live on the grid).  One elementwise rounding launch per
+    parameter; errors (non-finite / out of range) raise like rnd_array."""
+    flags = D.Flags()
+    launched = False
+    for p in model.parameters():
+        if not (p.is_cuda and p.dtype == torch.float64 and p.numel()):
+            continue
+        d = p.detach()
+        inplace = d.is_contiguous() and d.data_ptr() % 32 == 0
+        flat = d.view(-1) if inplace else d.reshape(-1).clone()
+        _lib.call("vt_round_log", D.ptr(flat), flat.numel(), b_r, 0.0, _lib.OUT_F64, D.ptr(flat), None, 0, 0,
+                  None, None, None, None, 0, None, flags.cnt_ptr, flags.err_ptr, None, 0, D.stream_ptr())
+        if not inplace:
+            d.copy_(flat.view(d.shape))
+        launched = True
+    if launched:
+        D.raise_fpround(flags.read()[0])
 
 
 def _lib_call_replay(flat: torch.Tensor, b_r: int, words: torch.Tensor, f) -> None:

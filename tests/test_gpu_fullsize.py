@@ -11,7 +11,7 @@ oracle on the same bits, at the size the bench times it:
   the oracle's budget search (the search_tau skeleton of
   protocol.py:494-506), and the full log + output of 30 tensors including
   the 5 largest;
-* configs[3]: 9 full-size hooked tensors of the GPT-2-small FP64 step
+* configs[3]: 10 full-size hooked tensors of the GPT-2-small FP64 step (the loss gradient among them)
   (forward outputs incl. the 411,705,344-element logits, and input
   gradients): tau, log and the in-place rounded values;
 * configs[4]: the 1.5e9-parameter FP32 checkpoint's chunked Merkle tree,
@@ -88,9 +88,10 @@ def test_config2_all_161_tensors_vs_oracle():
     torch.cuda.empty_cache()
 
 
-# the hooked GPT-2 tensors compared in full: (module, "fwd" output | "bwd" input gradient)
+# the hooked GPT-2 tensors compared in full: (module, "fwd" output | "bwd" input gradient | "loss" gradient)
 GPT2_PICKS = [("wte", "fwd"), ("h.0.c_attn", "fwd"), ("h.5.c_fc", "fwd"), ("h.11.gelu", "fwd"), ("lm_head", "fwd"),
-              ("lm_head", "bwd"), ("h.11.c_fc_proj", "bwd"), ("h.6.c_attn", "bwd"), ("h.0.ln_1", "bwd")]
+              ("loss", "loss"), ("lm_head", "bwd"), ("h.11.c_fc_proj", "bwd"), ("h.6.c_attn", "bwd"),
+              ("h.0.ln_1", "bwd")]
 
 
 @pytest.mark.timeout(900)
@@ -121,7 +122,7 @@ def test_config3_gpt2_full_size_hooked_tensors_vs_oracle():
     tgt = torch.randint(0, 50257, (8, 1024), device="cuda", generator=g)
     hk = Capture(model)
     hk._want, hk._cap = set(GPT2_PICKS), {}
-    logits = model(idx)
+    logits = hk.loss_grad(model(idx))  # the loss gradient (d loss / d logits) through the channel too
     loss = torch.nn.functional.cross_entropy(logits.view(-1, logits.shape[-1]), tgt.view(-1))
     del logits
     loss.backward()

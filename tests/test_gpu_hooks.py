@@ -117,7 +117,7 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
         hk = hk_factory(m)
         hs = [mod.register_forward_hook(lambda mod, i, o: seen.append(o.detach().clone()))
               for mod in m.modules() if not any(True for _ in mod.children())]
-        logits = m(idx)
+        logits = hk.loss_grad(m(idx))  # the loss gradient goes through the channel too (protocol.py:277-280)
         loss = torch.nn.functional.cross_entropy(logits.view(-1, 97), idx.view(-1))
         loss.backward()
         for h in hs:
@@ -127,7 +127,7 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
     hk_t, seen_t, loss_t, grads_t = run(model, lambda m: hooks.RoundAndLogHooks(m))
     info = hk_t.collect(keep_logs=True)
     hk_t.remove()
-    assert len(info["logs"]) == info["tensors"] and info["logged"] > 0
+    assert len(info["logs"]) == info["tensors"] and info["logged"] > 0 and info["loss"] == 1
 
     g = torch.Generator(device="cuda")
     g.manual_seed(11)
@@ -173,3 +173,44 @@ def test_replay_hooks_out_of_step():
     with pytest.raises(RuntimeError, match="out of step"):
         ha.collect()
     ha.remove()
+
+
+def test_loss_gradient_and_parameters_on_the_grid(oracle):
+    """hooks.loss_grad: the gradient reaching the model output is rounded and
+    logged with its own budget tau (protocol.py:277-280); round_parameters:
+    every parameter lands on the grid after the update (protocol.py:286-293)."""
+    import torch
+    from paper_2403_09603_b200 import hooks, workloads
+    torch.manual_seed(6)
+    model = workloads.gpt2_small_fp64(vocab=97, d=64, layers=2, heads=4, ctx=32)
+    idx = torch.randint(0, 97, (2, 32), device="cuda")
+    hk = hooks.RoundAndLogHooks(model)
+    seen, raw = [], []
+    out = model(idx)
+    out.register_hook(lambda g_: raw.append(g_.detach().clone()))  # tensor hooks run in order: the raw gradient
+    logits = hk.loss_grad(out)
+    logits.register_hook(lambda g_: seen.append(g_.detach().clone()))  # after the rounding hook
+    torch.nn.functional.cross_entropy(logits.view(-1, 97), idx.view(-1)).backward()
+    info = hk.collect(keep_logs=True)
+    hk.remove()
+    assert info["loss"] == 1 and len(seen) == 1 and len(raw) == 1
+    k = [c[1] for c in info["calls"]].index("loss")
+    g = seen[0].cpu().numpy().reshape(-1)
+    assert np.array_equal(g.view(np.uint64), oracle.rnd_array(g, 32).view(np.uint64))
+    # the loss gradient's log is the oracle's at the oracle's budget tau
+    r = raw[0].cpu().numpy().reshape(-1)
+    B = int(0.005 * r.size)
+    tau = oracle.search_tau_budget(r, 32, B)
+    assert info["taus"][k] == tau
+    codes = oracle.direction_array(r, 32, tau)
+    want = np.flatnonzero(codes != 1)
+    words = info["logs"][k][2].cpu().numpy()
+    assert np.array_equal(words >> 1, want) and np.array_equal(words & 1, (codes[want] == 2).astype(np.int64))
+    # parameters after an SGD update
+    with torch.no_grad():
+        for p in model.parameters():
+            p.add_(p.grad, alpha=-1e-3)
+    hooks.round_parameters(model)
+    for p in model.parameters():
+        a = p.detach().cpu().numpy().reshape(-1)
+        assert np.array_equal(a.view(np.uint64), oracle.rnd_array(a, 32).view(np.uint64))

@@ -1287,7 +1287,8 @@ def cpu_legs() -> dict:
         "P_all": c3, "P_1": c3_1, "unit": "G elements/s",
         "sample": "16 hooked-tensor shapes of the GPT-2-small step (12 x 8x1024x768, 4 x 8x1024x3072), budget "
                   "search + trainer channel each; P=1: one 8x1024x768 tensor",
-        "step_s_extrapolated_P_all": round(2.55e9 / (c3["g_elements_per_s"] * 1e9), 2)}
+        # 2.96e9 hooked elements per step: 88 outputs, 86 input gradients, the loss gradient
+        "step_s_extrapolated_P_all": round(2.96e9 / (c3["g_elements_per_s"] * 1e9), 2)}
     m_all = cpu_merkle(1 << 18, cores)
     m_1 = cpu_merkle(1 << 15, 1)
     out["configs[4]_merkle"] = {"P_all": m_all, "P_1": m_1, "unit": "GB/s hashed",

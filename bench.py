@@ -850,7 +850,8 @@ def f2_trend() -> dict:
     from baseline/_ref) on the shipped ``trend`` config, trainer then auditor,
     with the reference's NumPy channels and with the GPU channels in the seam;
     wall time of each run and of the channel calls inside it (a timing proxy
-    around process()).  Roots / .vtrl / corrections must agree."""
+    around process()), after an untimed warm-up of both arms on the `tiny`
+    config.  Roots / .vtrl / corrections must agree."""
     ref = REPO / "baseline" / "_ref"
     if not (ref / "vtrain" / "protocol.py").exists():
         return {"skipped": "reference not installed (tools/install_reference.sh)"}
@@ -878,6 +879,16 @@ def f2_trend() -> dict:
     cfg = cli.load_config(ref / "vtrain_configs" / "trend.json")
     out = {}
     with tempfile.TemporaryDirectory() as td:
+        # warm-up, untimed: the shipped `tiny` config through both arms (first
+        # kernel launches, staging buffers, NumPy paths), as every timed leg here
+        warm = cli.load_config(ref / "vtrain_configs" / "tiny.json")
+        for W, R, T, A in ((rrl.LogWriter, rrl.LogReader, pr._TrainerChannel, pr._AuditorChannel),
+                           (roundlog.LogWriter, roundlog.LogReader, gp.GpuTrainerChannel, gp.GpuAuditorChannel)):
+            wl = Path(td) / "warm.vtrl"
+            w = W(wl, warm.b_r)
+            pr._run(warm, pr.get_profile(warm.trainer_profile), T(w, warm.b_r), False)
+            w.close()
+            pr._run(warm, pr.get_profile("pairwise"), A(R(wl), warm.b_r), False)
         for side, W, R, T, A in (("reference_numpy", rrl.LogWriter, rrl.LogReader, pr._TrainerChannel,
                                   pr._AuditorChannel),
                                  ("gpu", roundlog.LogWriter, roundlog.LogReader, gp.GpuTrainerChannel,

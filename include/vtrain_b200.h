@@ -83,6 +83,8 @@ typedef void *vt_stream_t; /* a cudaStream_t; NULL = legacy default stream */
 
 const char *vt_version(void);
 const char *vt_last_error(void);
+/* host wait for `stream` (cudaStreamSynchronize); VT_ECUDA on a CUDA error */
+int vt_stream_synchronize(vt_stream_t stream);
 int vt_tile_elems(void); /* elements per CTA tile (shard boundaries align to it) */
 
 /* ---- fused round-and-log (trainer) ------------------------------------ */

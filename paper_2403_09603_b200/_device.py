@@ -29,8 +29,22 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr(device=None) -> int:
+    """The current CUDA stream of ``device`` (default: the current device) as
+    a raw cudaStream_t.  The direct C accessor skips torch.cuda.current_stream's
+    Python device-index handling (~7 us per call, which the reference-API
+    channels on small tensors pay on every call)."""
+    if _RAW_STREAM is not None and device is None:
+        return int(_RAW_STREAM(torch.cuda.current_device()))
     return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+def sync_stream(stream: int | None = None) -> None:
+    """Wait for the current (or the given raw) stream on the host."""
+    _lib.call("vt_stream_synchronize", stream_ptr() if stream is None else stream)
 
 
 def ptr(t: torch.Tensor | None) -> int | None:
@@ -180,7 +194,7 @@ class HostStage:
 
     def d2h_wait(self, lo: int, hi: int) -> None:
         self.host[lo:hi].copy_(self.dev[lo:hi], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        sync_stream()
 
     def hview(self, off: int, n: int, dtype) -> np.ndarray:
         return self.host_np[off:off + n * np.dtype(dtype).itemsize].view(dtype)

@@ -24,3 +24,12 @@ int vt_check_launch(const char* what) {
 extern "C" const char* vt_version(void) { return "vtrain_b200 0.1.0 sm_100a"; }
 
 extern "C" const char* vt_last_error(void) { return g_err; }
+
+// Host wait for a stream (the reference-API channels' one wait per call,
+// without a round trip through torch's stream objects).
+extern "C" int vt_stream_synchronize(vt_stream_t stream) {
+  const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) return VT_OK;
+  std::snprintf(g_err, sizeof(g_err), "vt_stream_synchronize: %s", cudaGetErrorString(e));
+  return VT_ECUDA;
+}

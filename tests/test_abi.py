@@ -120,7 +120,7 @@ def test_entry_points_reject_bad_arguments(name, args):
 def test_every_compute_entry_point_is_covered():
     host_only = {"vt_version", "vt_last_error", "vt_tile_elems", "vt_merkle_node_count", "vt_tau_kth_hist_offset",
                  "vt_tau_kth_hist_bins", "vt_int_mix_ops_per_thread_rep", "vt_exchange_words",
-                 "vt_digest_exchange_words"}
+                 "vt_digest_exchange_words", "vt_stream_synchronize"}
     covered = {c[0] for c in BAD_CALLS}
     assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}
 

@@ -833,9 +833,19 @@ def budget_search() -> dict:
             tau_sh = vdist.search_tau_budget_sharded(x, 32, B)
             t_sh.append(time.perf_counter() - t0)
         assert tau_sh == tau
+        # the same with both exchanges over peer memory and the decision on the device
+        ex = vdist.BudgetExchange()
+        t_x = []
+        for _ in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tau_x = vdist.search_tau_budget_sharded(x, 32, B, exchange=ex, n_global=n)
+            t_x.append(time.perf_counter() - t0)
+        assert tau_x == tau
         out[f"2^{lg}"] = {"ms": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1), "frac": round(8 * n / ms / 1e6 / peak, 4),
                           "tau_over_2^-24": round(tau / 2.0 ** -24, 6),
                           "sharded_candidate_path_ms_wall": round(1e3 * min(t_sh[1:]), 3),
+                          "sharded_peer_exchange_path_ms_wall": round(1e3 * min(t_x[1:]), 3),
                           "sharded_exact_select_pass_ms": round(ms5, 4),
                           "sharded_exact_select_5_passes_ms_est": round(5 * ms5, 4)}
         del x, ws

@@ -39,6 +39,8 @@
  *   vt_sha256_leaves  <- merkle._sha256 over 4 KiB chunks    merkle.py:24-25
  *   vt_merkle_level   <- one level of merkle.build           merkle.py:55-72
  *   vt_merkle_build   <- merkle.build over chunked leaves    merkle.py:55-72
+ *   vt_tau_shard_search_x <- search_tau_budget over a sharded tensor, both
+ *                        exchanges over peer memory
  *   vt_merkle_level_exchange / vt_digests_publish / vt_digests_wait
  *                     <- the block-root all-gather of a sharded merkle.build,
  *                        fused over peer memory
@@ -238,6 +240,26 @@ int vt_digests_publish(const uint8_t *digests, int64_t n, uint64_t *const *xpeer
                        int64_t dst, int64_t n_total, vt_stream_t stream);
 int vt_digests_wait(uint64_t *const *xpeers, int world, int rank, int64_t n_total, uint8_t *out,
                     int32_t *err, vt_stream_t stream);
+/*
+ * The same sharded budget search with both exchanges over peer memory and
+ * the decision, the digit-key gather, the exact order statistic and the FP64
+ * bisection on the device: one call enqueues the whole search (phases = 7)
+ * and the host reads *status (0: tau_out holds tau; 1: the candidates could
+ * not decide -- run the exact multi-pass path) and *tau_out once.  xpeers:
+ * device array of every rank's buffer of vt_tau_shard_exchange_words(world,
+ * keys_cap) uint64 words (zero-filled once), own = this rank's; keys_cap
+ * bounds one rank's keys in the selected digit (more: *status = 1).  ws:
+ * vt_tau_shard_search_x_workspace(n) bytes, 256-byte aligned.  phases picks
+ * A (1: candidates + histogram to every rank), B (2: decision + this rank's
+ * digit keys to every rank), C (4: gather + selection + bisection); every
+ * wait is bounded (VT_ERR_EXCHANGE in *err after 10 s).
+ */
+size_t vt_tau_shard_exchange_words(int world, int64_t keys_cap);
+size_t vt_tau_shard_search_x_workspace(int64_t n);
+int vt_tau_shard_search_x(const double *x, int64_t n, int b_r, int64_t n_global, int64_t budget, int iters,
+                          uint64_t *const *xpeers, uint64_t *own, int world, int rank, int64_t keys_cap,
+                          double *tau_out, int32_t *status, int32_t *err, void *ws, size_t ws_bytes,
+                          int phases, vt_stream_t stream);
 /*
  * The budget search over ONE tensor sharded across ranks,
  * candidate path: vt_tau_shard_plan gives the global plan (candidate

@@ -65,6 +65,10 @@ EXPORTS: dict[str, tuple] = {
     "vt_tau_budget": (_i32, [_p, _i64, _i32, _i64, _i32, _p, _p, _p, _p, _sz, _p]),
     "vt_exchange_words": (_sz, [_i32]),
     "vt_stream_synchronize": (_i32, [_p]),
+    "vt_tau_shard_exchange_words": (_sz, [_i32, _i64]),
+    "vt_tau_shard_search_x_workspace": (_sz, [_i64]),
+    "vt_tau_shard_search_x": (_i32, [_p, _i64, _i32, _i64, _i64, _i32, _p, _p, _i32, _i32, _i64, _p, _p, _p, _p,
+                                     _sz, _i32, _p]),
     "vt_round_log_exchange": (_i32, [_p, _i64, _i32, _dbl, _i32, _p, _p, _i64, _i64, _p, _p, _p, _sz, _p, _i32, _i32,
                                      _p]),
     "vt_counts_wait": (_i32, [_p, _i32, _i32, _p, _p, _p]),

@@ -2069,6 +2069,328 @@ extern "C" int vt_tau_shard_digit_keys(int64_t n, int b_r, int64_t n_global, int
 
 
 // ---------------------------------------------------------------------------
+// The same search with both exchanges over peer memory and no host step in
+// the common path (vt_tau_shard_search_x): the rank's summed-histogram
+// decision, its digit keys and the exact selection + bisection all run on
+// the device, so one call enqueues the whole search and the host reads
+// (status, tau) once.  Exchange buffer per rank (uint64 words, symmetric
+// memory; zero-filled once):
+//   [0] sequence number, [1] key counter, [2] CTA done counter,
+//   [3 + par*W + r] rank r's phase-A (histogram) tag, [3 + 2W + par*W + r]
+//   its phase-B (keys) tag, then the histogram buffers [par][r][kShardX],
+//   the key counts [par][r], the keys [par][r][keys_cap] and a local
+//   decision block {mode, digit, rank in digit, value bits}.
+// Parities alternate per call as in the count exchange (vt_stream.cu).
+// ---------------------------------------------------------------------------
+namespace vt {
+struct SXLayout {
+  int world;
+  int64_t kcap, hist, counts, keys, dec, total;
+};
+__host__ __device__ inline SXLayout sx_layout(int world, int64_t kcap) {
+  SXLayout l;
+  l.world = world;
+  l.kcap = kcap;
+  l.hist = 3 + 4 * (int64_t)world;
+  l.counts = l.hist + 2 * (int64_t)world * kShardX;
+  l.keys = l.counts + 2 * (int64_t)world;
+  l.dec = l.keys + 2 * (int64_t)world * kcap;
+  l.total = l.dec + 8;
+  return l;
+}
+struct SXArgs {
+  uint64_t* const* peers;
+  uint64_t* own;
+  int world, rank;
+  SXLayout L;
+  int64_t budget, n_global;
+  uint64_t L_key, hi_key, lo_key;
+  int s0, iters;
+  double lower, upper;
+};
+enum { kSXValue = 0, kSXDigit = 1, kSXExact = 2 };
+
+// 1 CTA: this rank's histogram buffer to every rank (phase A)
+__global__ void __launch_bounds__(256) sx_publish_hist_kernel(const SXArgs a, const unsigned long long* xbuf) {
+  const uint64_t seq = a.own[0] + 1ull;
+  const int par = (int)(seq & 1ull);
+  for (int p = 0; p < a.world; ++p) {
+    uint64_t* dst = a.peers[p] + a.L.hist + ((int64_t)par * a.world + a.rank) * kShardX;
+    for (int i = threadIdx.x; i < kShardX; i += blockDim.x) dst[i] = xbuf[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.own[0] = seq;
+    for (int p = 0; p < a.world; ++p) st_release_sys_u64(a.peers[p] + 3 + par * a.world + a.rank, seq);
+  }
+}
+
+__device__ bool sx_wait(const SXArgs& a, int64_t tag0, uint64_t seq, int par, int32_t* err) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < a.world; q += blockDim.x) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys_u64(a.own + tag0 + par * a.world + q) != seq) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10ull * 1000 * 1000 * 1000) {
+        atomicOr(err, VT_ERR_EXCHANGE);
+        s_ok = 0;
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// 1 CTA: sum every rank's histogram buffer, decide as ShardedBudget.decide
+__global__ void __launch_bounds__(256) sx_decide_kernel(const SXArgs a, int32_t* err) {
+  __shared__ unsigned long long sum[kShardX];
+  const uint64_t seq = a.own[0];
+  const int par = (int)(seq & 1ull);
+  uint64_t* dec = a.own + a.L.dec;
+  if (!sx_wait(a, 3, seq, par, err)) {
+    if (threadIdx.x == 0) {
+      dec[0] = kSXExact;
+      a.own[1] = 0ull;
+      a.own[2] = 0ull;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < kShardX; i += blockDim.x) {
+    unsigned long long v = 0;
+    for (int r = 0; r < a.world; ++r) v += __ldcg(a.own + a.L.hist + ((int64_t)par * a.world + r) * kShardX + i);
+    sum[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  a.own[1] = 0ull;  // the digit-key pass counts from 0
+  a.own[2] = 0ull;
+  const int64_t B = a.budget;
+  const int64_t above_hi = (int64_t)sum[kAdBins], m = (int64_t)sum[kAdBins + 1];
+  const bool overflow = sum[kAdBins + 2] != 0ull;
+  uint64_t mode = kSXExact, digit = 0, rank = 0, val = 0;
+  if (a.n_global <= B) {
+    mode = kSXValue;
+    val = a.lo_key;
+  } else if (overflow) {
+    mode = kSXExact;
+  } else if (above_hi > B) {
+    mode = kSXValue;
+    val = 0x7ff0000000000000ull;  // v > tau_hi: the bisection ends at upper
+  } else if (m < B + 1) {
+    if (a.L_key <= a.lo_key) {
+      mode = kSXValue;
+      val = a.lo_key;
+    }
+  } else {
+    const int64_t rk = B - above_hi;  // 0-based from the top among the keys in (L, hi]
+    int64_t above = 0;
+    for (int d = kAdBins - 1; d >= 0; --d) {
+      const int64_t h = (int64_t)sum[d];
+      if (above + h > rk) {
+        mode = kSXDigit;
+        digit = (uint64_t)d;
+        rank = (uint64_t)(rk - above);
+        break;
+      }
+      above += h;
+    }
+  }
+  dec[0] = mode;
+  dec[1] = digit;
+  dec[2] = rank;
+  dec[3] = val;
+}
+
+// grid: this rank's keys in the decided digit into every rank's key area (phase B)
+__global__ void __launch_bounds__(kAdThreads) sx_digit_keys_kernel(const SXArgs a, const uint64_t* __restrict__ ck,
+                                                                   const AdaptHdr* h, int64_t cap) {
+  __shared__ unsigned s_last;
+  const uint64_t seq = a.own[0];
+  const int par = (int)(seq & 1ull);
+  const uint64_t* dec = a.own + a.L.dec;
+  const int lane = threadIdx.x & 31;
+  if (dec[0] == kSXDigit) {
+    const uint64_t digit = dec[1], lo1 = a.L_key + 1;
+    const int64_t Mraw = h->ccount;
+    const int64_t M = Mraw < cap ? Mraw : cap;
+    for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
+      const int64_t i = i0 + threadIdx.x;
+      const uint64_t key = i < M ? ck[i] : 0ull;
+      const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(a.own + 1), (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        const int64_t q = (int64_t)(pos + __popc(m & lanemask_lt()));
+        if (in && q < a.L.kcap)
+          for (int p = 0; p < a.world; ++p)
+            a.peers[p][a.L.keys + ((int64_t)par * a.world + a.rank) * a.L.kcap + q] = key;
+      }
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_last = atomicAdd(reinterpret_cast<unsigned long long*>(a.own + 2), 1ull) == (unsigned long long)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence_system();
+  const uint64_t cnt = dec[0] == kSXDigit ? *(volatile uint64_t*)(a.own + 1) : 0ull;
+  for (int p = 0; p < a.world; ++p) a.peers[p][a.L.counts + (int64_t)par * a.world + a.rank] = cnt;
+  __threadfence_system();
+  for (int p = 0; p < a.world; ++p) st_release_sys_u64(a.peers[p] + 3 + 2 * a.world + par * a.world + a.rank, seq);
+}
+
+// 1 CTA: gather every rank's digit keys, the exact order statistic, the bisection
+__global__ void __launch_bounds__(kAdThreads) sx_finish_kernel(const SXArgs a, AdaptHdr* h, double* tau_out,
+                                                               int32_t* status, int32_t* err) {
+  __shared__ __align__(16) uint32_t sh[kBudBins];
+  __shared__ int64_t s_tot;
+  __shared__ int s_bad;
+  const uint64_t seq = a.own[0];
+  const int par = (int)(seq & 1ull);
+  const uint64_t* dec = a.own + a.L.dec;
+  const uint64_t mode = dec[0];
+  const bool ok = sx_wait(a, 3 + 2 * (int64_t)a.world, seq, par, err);
+  if (threadIdx.x == 0) {
+    h->ccount = 0;  // the shard workspace's candidate count starts at 0 for the next call
+    int64_t tot = 0;
+    int bad = !ok || mode == kSXExact;
+    if (ok && mode == kSXDigit)
+      for (int r = 0; r < a.world; ++r) {
+        const int64_t c = (int64_t)__ldcg(a.own + a.L.counts + (int64_t)par * a.world + r);
+        if (c > a.L.kcap) bad = 1;
+        tot += c;
+      }
+    s_tot = tot;
+    s_bad = bad;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) *status = 1;  // the exact multi-pass path decides (host)
+    return;
+  }
+  uint64_t key;
+  if (mode == kSXValue) {
+    key = dec[3];
+  } else {
+    // the rank-th largest among the gathered digit offsets o = key - L - 1 (the
+    // digit's bits included), digit by digit over the low s0 bits
+    const uint64_t lo1 = a.L_key + 1;
+    const int64_t m = s_tot;
+    int64_t rank = (int64_t)dec[2];
+    uint64_t low = 0, lmask = 0;
+    const uint64_t* base = a.own + a.L.keys + (int64_t)par * a.world * a.L.kcap;
+    for (int top = a.s0; top > 0;) {
+      const int bits = top < kAdBits ? top : kAdBits;
+      top -= bits;
+      for (int i = threadIdx.x; i < kAdBins; i += kAdThreads) sh[i] = 0;
+      __syncthreads();
+      for (int r = 0; r < a.world; ++r) {
+        const int64_t c = (int64_t)__ldcg(a.own + a.L.counts + (int64_t)par * a.world + r);
+        for (int64_t i = threadIdx.x; i < c; i += kAdThreads) {
+          const uint64_t o = __ldcg(base + (int64_t)r * a.L.kcap + i) - lo1;
+          if ((o & lmask) == low) atomicAdd(&sh[(uint32_t)(o >> top) & ((1u << bits) - 1u)], 1u);
+        }
+      }
+      __syncthreads();
+      int b2;
+      int64_t ab2;
+      select_digit(sh, 1 << bits, rank, b2, ab2);
+      low |= (uint64_t)b2 << top;
+      lmask |= ((1ull << bits) - 1ull) << top;
+      rank -= ab2;
+      __syncthreads();
+    }
+    (void)m;
+    key = lo1 + ((dec[1] << a.s0) | low);
+  }
+  if (threadIdx.x == 0) {
+    DevThr d;
+    bisect_to(key, a.lower, a.upper, a.iters, &d, tau_out);
+    *status = 0;
+  }
+}
+}  // namespace vt
+
+extern "C" size_t vt_tau_shard_exchange_words(int world, int64_t keys_cap) {
+  return (world > 0 && keys_cap > 0) ? (size_t)vt::sx_layout(world, keys_cap).total : 0;
+}
+
+extern "C" int vt_tau_shard_search_x(const double* x, int64_t n, int b_r, int64_t n_global, int64_t budget,
+                                     int iters, uint64_t* const* xpeers, uint64_t* own, int world, int rank,
+                                     int64_t keys_cap, double* tau_out, int32_t* status, int32_t* err, void* ws,
+                                     size_t ws_bytes, int phases, vt_stream_t stream) {
+  using namespace vt;
+  if (phases <= 0 || phases > 7 ||
+      n < 0 || n_global < n || n_global <= 0 || b_r < 10 || b_r > 32 || budget < 0 || iters < 0 || !xpeers ||
+      !own || world <= 0 || rank < 0 || rank >= world || keys_cap <= 0 || !tau_out || !status || !err || !ws ||
+      ws_bytes < vt_tau_shard_workspace(n) + sizeof(int64_t) * kShardX ||
+      reinterpret_cast<uintptr_t>(ws) % 256 || (n && (!x || (reinterpret_cast<uintptr_t>(x) & 31)))) {
+    vt_set_error("vt_tau_shard_search_x: bad argument");
+    return VT_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const AdaptLayout lay = adapt_layout_rl(n > 0 ? n : 1, 0);
+  const AdPtrs A = adapt_ptrs(static_cast<uint8_t*>(ws), lay);
+  const AdPlan P = adapt_plan(n_global, b_r, budget);
+  // this rank's histogram buffer: after the shard workspace
+  unsigned long long* xbuf =
+      reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + vt_tau_shard_workspace(n));
+  SXArgs a;
+  a.peers = xpeers;
+  a.own = own;
+  a.world = world;
+  a.rank = rank;
+  a.L = sx_layout(world, keys_cap);
+  a.budget = budget;
+  a.n_global = n_global;
+  a.L_key = P.L_key;
+  a.hi_key = P.hi_key;
+  a.lo_key = P.lo_key;
+  a.s0 = P.s0;
+  a.iters = iters;
+  a.lower = P.lo;
+  a.upper = P.hi;
+  int rc;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lay.cap + 4095) / 4096, 148 * 4));
+  if (phases & 1) {  // A: candidates, their digit histogram, to every rank
+    cudaMemsetAsync(xbuf, 0, sizeof(int64_t) * kShardX, s);
+    shard_reset_kernel<<<1, 1, 0, s>>>(A.h);
+    if ((rc = vt_check_launch("shard_reset_kernel"))) return rc;
+    if (n > 0 && (rc = adapt_key_pass(x, n, b_r, P, A.ck, lay.cap, A.h, err, s))) return rc;
+    shard_hist_kernel<<<grid, kAdThreads, 0, s>>>(A.ck, A.h, lay.cap, P.g0, P.L_key, P.hi_key, P.s0, xbuf, err);
+    if ((rc = vt_check_launch("shard_hist_kernel"))) return rc;
+    sx_publish_hist_kernel<<<1, 256, 0, s>>>(a, xbuf);
+    if ((rc = vt_check_launch("sx_publish_hist_kernel"))) return rc;
+  }
+  if (phases & 2) {  // B: the decision from every rank's histogram, this rank's digit keys to every rank
+    sx_decide_kernel<<<1, 256, 0, s>>>(a, err);
+    if ((rc = vt_check_launch("sx_decide_kernel"))) return rc;
+    sx_digit_keys_kernel<<<grid, kAdThreads, 0, s>>>(a, A.ck, A.h, lay.cap);
+    if ((rc = vt_check_launch("sx_digit_keys_kernel"))) return rc;
+  }
+  if (phases & 4) {  // C: every rank's digit keys, the exact order statistic, the bisection
+    sx_finish_kernel<<<1, kAdThreads, 0, s>>>(a, A.h, tau_out, status, err);
+    if ((rc = vt_check_launch("sx_finish_kernel"))) return rc;
+  }
+  return VT_OK;
+}
+
+extern "C" size_t vt_tau_shard_search_x_workspace(int64_t n) {
+  return vt_tau_shard_workspace(n) + sizeof(int64_t) * vt::kShardX;
+}
+
+
+// ---------------------------------------------------------------------------
 // Batched adaptive round-and-log: many independent tensors (configs[2]: the
 // 161 ResNet-50 intermediates), each with its own budget, tau and log, in a
 // fixed number of launches instead of ~12 per tensor:

@@ -369,6 +369,63 @@ class ShardedBudget:
         return float(k[rank_in_digit:rank_in_digit + 1].view(np.float64)[0])
 
 
+class BudgetExchange:
+    """The sharded budget search's two exchanges over peer memory
+    (``vt_tau_shard_search_x``): a symmetric-memory buffer per rank (a plain
+    device buffer in a single process) holding every rank's digit histogram
+    and digit keys; the decision, the gather, the exact order statistic and
+    the bisection run on the device, so a search is one enqueue and one host
+    read.  ``keys_cap`` bounds one rank's keys in the selected digit."""
+
+    def __init__(self, group=None, device=None, keys_cap: int = 1 << 16):
+        from . import _device as D
+        from . import _lib
+        self.D, self.lib = D, _lib
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.keys_cap = int(keys_cap)
+        words = int(_lib.lib().vt_tau_shard_exchange_words(self.world, self.keys_cap))
+        if dist.is_initialized():
+            import torch.distributed._symmetric_memory as symm
+            self.buf = symm.empty(words, dtype=torch.int64, device=dev)
+            self.buf.zero_()
+            name = (group or dist.group.WORLD).group_name
+            self.handle = symm.rendezvous(self.buf, name)
+            self.peers = int(self.handle.buffer_ptrs_dev)
+            torch.cuda.synchronize(dev)
+            dist.barrier(group)  # every buffer is zero before any rank publishes
+        else:
+            self.buf = torch.zeros(words, dtype=torch.int64, device=dev)
+            self._ptrs = torch.tensor([self.buf.data_ptr()], dtype=torch.int64, device=dev)
+            self.peers = int(self._ptrs.data_ptr())
+        self.out = torch.zeros(3, dtype=torch.int64, device=dev)  # [tau bits, status, error bits]
+
+    def search(self, x_local: torch.Tensor, b_r: int, n_global: int, budget: int, iters: int = 30,
+               phases: int = 7) -> None:
+        """Enqueue the search (all phases by default); ``result`` reads it."""
+        D = self.D
+        t = D.aligned_f64(x_local.reshape(-1)) if x_local.numel() else x_local.reshape(-1).to(torch.float64)
+        n = int(t.numel())
+        ws = D.workspace(int(self.lib.lib().vt_tau_shard_search_x_workspace(n)), "tau_shard_x")
+        if phases & 1:
+            self.out.zero_()
+        o = self.out.data_ptr()
+        self.lib.call("vt_tau_shard_search_x", D.ptr(t) if n else None, n, int(b_r), int(n_global), int(budget),
+                      int(iters), self.peers, self.buf.data_ptr(), self.world, self.rank, self.keys_cap, o, o + 8,
+                      o + 16, D.ptr(ws), ws.numel(), int(phases), D.stream_ptr())
+
+    def result(self) -> tuple[int, float]:
+        """(status, tau): status 0 = tau decided on the device, 1 = the exact
+        multi-pass path must decide.  One host read."""
+        v = self.out.cpu()
+        err = int(v[2].item()) & 0xFFFFFFFF
+        if err & self.lib.ERR_EXCHANGE:
+            raise RuntimeError("budget exchange: a peer's data did not arrive (10 s)")
+        self.D.raise_fpround(err)
+        return int(v[1].item()), float(v[0:1].view(torch.float64).item())
+
+
 def _bisect_tau(v: float, b_r: int, iters: int) -> float:
     from .fpround import tau_bounds
     lower, upper = tau_bounds(b_r)
@@ -381,21 +438,32 @@ def _bisect_tau(v: float, b_r: int, iters: int) -> float:
     return upper
 
 
-def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iters: int = 30, group=None) -> float:
+def search_tau_budget_sharded(x_local: torch.Tensor, b_r: int, budget: int, iters: int = 30, group=None,
+                              exchange: BudgetExchange | None = None, n_global: int | None = None) -> float:
     """protocol.search_tau_budget over a tensor sharded across ranks: the same
     FP64 bisection on the exact global (budget+1)-th largest p, every rank
     getting the same tau.  Candidate path: one read of each shard, an
     all-reduce of a 2051-word exchange buffer and an all-gather of the keys
     in the selected digit (``ShardedBudget``); the exact 5-pass radix select
-    (``kth_largest_distance_sharded``) when the candidates cannot decide."""
+    (``kth_largest_distance_sharded``) when the candidates cannot decide.
+    With ``exchange`` the two exchanges run over peer memory and every step
+    after the shard read on the device (one enqueue, one host read); pass
+    ``n_global`` to skip the all-reduce of the shard sizes."""
     world = _world(group)
-    n = torch.tensor([x_local.numel()], dtype=torch.int64, device=x_local.device)
-    if world > 1:
-        dist.all_reduce(n, group=group)
-    n_global = int(n.item())
+    if n_global is None:
+        n = torch.tensor([x_local.numel()], dtype=torch.int64, device=x_local.device)
+        if world > 1:
+            dist.all_reduce(n, group=group)
+        n_global = int(n.item())
     if n_global == 0 or n_global <= budget:
         from .fpround import tau_bounds
         return _bisect_tau(tau_bounds(b_r)[0], b_r, iters)
+    if exchange is not None:
+        exchange.search(x_local, b_r, n_global, int(budget), iters)
+        status, tau = exchange.result()
+        if status == 0:
+            return tau
+        return _bisect_tau(kth_largest_distance_sharded(x_local, b_r, int(budget), group), b_r, iters)
     sb = ShardedBudget(x_local, b_r, n_global, int(budget))
     xb = sb.candidates()
     if world > 1:

@@ -90,6 +90,10 @@ BAD_CALLS = [
     ("vt_digests_publish", (None, 1, 1 << 40, 1, 0, 0, 1, None)),
     ("vt_digests_publish", (1 << 40, 1, 1 << 40, 2, 2, 0, 1, None)),  # rank >= world
     ("vt_digests_wait", (1 << 40, 2, 0, 3, None, 1 << 40, None)),  # no out buffer for 3 roots
+    ("vt_tau_shard_search_x", (None, 10, 32, 10, 1, 30, 1 << 40, 1 << 40, 1, 0, 16, 1 << 40, 1 << 40, 1 << 40,
+                               None, 0, 7, None)),  # no workspace
+    ("vt_tau_shard_search_x", (None, 0, 32, 10, 1, 30, 1 << 40, 1 << 40, 1, 0, 16, 1 << 40, 1 << 40, 1 << 40,
+                               1 << 40, 1 << 40, 8, None)),  # phases out of range
     ("vt_tau_shard_candidates", (None, 10, 32, 5, 1, None, None, None, 0, None)),
     ("vt_tau_shard_digit_keys", (10, 32, 10, 1, 5000, None, 0, None, None, 0, None)),
     ("vt_round_log_adaptive", (None, 0, 32, 10, 30, 1, None, None, 0, 0, None, None, None, None, None, None, 0,
@@ -120,7 +124,8 @@ def test_entry_points_reject_bad_arguments(name, args):
 def test_every_compute_entry_point_is_covered():
     host_only = {"vt_version", "vt_last_error", "vt_tile_elems", "vt_merkle_node_count", "vt_tau_kth_hist_offset",
                  "vt_tau_kth_hist_bins", "vt_int_mix_ops_per_thread_rep", "vt_exchange_words",
-                 "vt_digest_exchange_words", "vt_stream_synchronize"}
+                 "vt_digest_exchange_words", "vt_stream_synchronize",
+                 "vt_tau_shard_exchange_words"}
     covered = {c[0] for c in BAD_CALLS}
     assert declared() - host_only - covered == {n for n in declared() if n.endswith("_workspace")}
 

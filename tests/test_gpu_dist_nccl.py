@@ -142,3 +142,20 @@ def test_digest_exchange_over_symmetric_memory(nccl_group):
     assert bytes(top[-1][0].cpu().numpy()) == merkle.merkle_chunked(w).root
     ex.check()
     assert int(ex.buf[0].item()) == 3
+
+
+def test_budget_exchange_over_symmetric_memory(nccl_group, oracle):
+    """The sharded budget search with both exchanges over peer memory and
+    the decision on the device equals the oracle (and the NCCL path)."""
+    import torch
+    from paper_2403_09603_b200 import dist as vdist
+    ex = vdist.BudgetExchange(nccl_group)
+    rng = np.random.default_rng(21)
+    for k in range(3):
+        x = rng.normal(0.0, 3.0, 400_003 + 11 * k)
+        B = int(0.005 * x.size)
+        xt = torch.from_numpy(x).cuda()
+        tau = vdist.search_tau_budget_sharded(xt, 32, B, group=nccl_group, exchange=ex)
+        assert tau == oracle.search_tau_budget(x, 32, B) == vdist.search_tau_budget_sharded(xt, 32, B,
+                                                                                              group=nccl_group)
+    assert int(ex.buf[0].item()) == 3

@@ -236,3 +236,111 @@ def test_digest_exchange_single_process():
         assert len(levels) == len(ref.levels_device)
         assert all(torch.equal(a, b) for a, b in zip(levels, ref.levels_device))
         assert int(ex.buf[0].item()) == 3
+
+
+# ---------------------------------------------------------------------------
+# the sharded budget search with both exchanges over peer memory
+# (vt_tau_shard_search_x): phase A for every virtual rank, then B, then C
+# ---------------------------------------------------------------------------
+
+def _virtual_budget(shards, b_r: int, budget: int, keys_cap: int = 1 << 16, iters: int = 30):
+    import torch
+
+    from paper_2403_09603_b200 import _device as D
+    from paper_2403_09603_b200 import _lib
+    world = len(shards)
+    n_global = sum(int(s.numel()) for s in shards)
+    words = int(_lib.lib().vt_tau_shard_exchange_words(world, keys_cap))
+    bufs = [torch.zeros(words, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    outs = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(world)]
+    wss = [torch.zeros(int(_lib.lib().vt_tau_shard_search_x_workspace(int(s.numel()))) + 256, dtype=torch.uint8,
+                       device="cuda") for s in shards]
+    wss = [w[(-w.data_ptr()) % 256:] for w in wss]  # 256-byte aligned views
+    for phase in (1, 2, 4):
+        for r, s in enumerate(shards):
+            o = outs[r].data_ptr()
+            _lib.call("vt_tau_shard_search_x", D.ptr(s) if s.numel() else None, int(s.numel()), b_r, n_global,
+                      budget, iters, ptrs.data_ptr(), bufs[r].data_ptr(), world, r, keys_cap, o, o + 8, o + 16,
+                      D.ptr(wss[r]), wss[r].numel(), phase, D.stream_ptr())
+    torch.cuda.synchronize()
+    res = []
+    for o in outs:
+        v = o.cpu()
+        assert int(v[2]) & 0xFFFFFFFF == 0
+        res.append((int(v[1]), float(v[0:1].view(torch.float64).item())))
+    return res
+
+
+@pytest.mark.parametrize("case", ["normal", "uneven_empty", "budget0", "wide", "tiny_budget_digit"])
+def test_virtual_ranks_sharded_budget_search(case, oracle):
+    """Every virtual rank gets the oracle's budget tau of the whole tensor,
+    decided on the device (status 0), for uneven and empty shards and the
+    decision's edge cases."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng({"normal": 1, "uneven_empty": 2, "budget0": 3, "wide": 4,
+                                 "tiny_budget_digit": 5}[case])
+    if case == "uneven_empty":
+        sizes = [300_001, 0, 77_777, 5]
+    elif case == "wide":
+        sizes = [200_000] * 4
+    else:
+        sizes = [250_000, 250_003, 249_999, 1]
+    x = rng.normal(0.0, 3.0, sum(sizes))
+    if case == "wide":
+        x *= np.exp2(rng.integers(-60, 60, x.size))
+    budget = {"budget0": 0, "tiny_budget_digit": 3}.get(case, int(0.005 * x.size))
+    shards, lo = [], 0
+    for n in sizes:
+        shards.append(torch.from_numpy(x[lo:lo + n].copy()).cuda())
+        lo += n
+    res = _virtual_budget(shards, 32, budget)
+    want = oracle.search_tau_budget(x, 32, budget)
+    for status, tau in res:
+        assert status == 0 and tau == want, (res, want)
+
+
+def test_virtual_ranks_sharded_budget_fallback_flag(oracle):
+    """More digit keys on a rank than keys_cap: status 1 on every rank (the
+    host then runs the exact multi-pass path), never a wrong tau."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(9)
+    x = rng.normal(0.0, 1.0, 800_000)
+    # half the elements share one value just below an FP32 rounding midpoint:
+    # the (B+1)-th largest distance is theirs, so its digit holds ~100 K keys per rank
+    x[rng.random(x.size) < 0.5] = 1.0 + 2.0 ** -24 * (1.0 - 2.0 ** -12)
+    shards = [torch.from_numpy(p.copy()).cuda() for p in np.array_split(x, 4)]
+    B = int(0.005 * x.size)
+    res = _virtual_budget(shards, 32, B, keys_cap=1024)
+    assert all(status == 1 for status, _ in res), res
+    # (with a larger keys_cap the candidates themselves overflow the shard
+    # workspace here -- also status 1).  Through search_tau_budget_sharded the
+    # host then runs the exact multi-pass path: the oracle's tau.
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        from paper_2403_09603_b200 import dist as vdist
+        ex = vdist.BudgetExchange(keys_cap=1024)
+        tau = vdist.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, B, exchange=ex)
+        assert tau == oracle.search_tau_budget(x, 32, B)
+
+
+def test_budget_exchange_single_process(oracle):
+    """BudgetExchange without a process group (the one-rank case) equals the
+    oracle, repeated (the parity alternates), through search_tau_budget_sharded."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is active in this session")
+    import numpy as np
+    import torch
+
+    from paper_2403_09603_b200 import dist as vdist
+    ex = vdist.BudgetExchange()
+    rng = np.random.default_rng(12)
+    for k in range(3):
+        x = rng.normal(0.0, 2.0, 300_003 + k)
+        B = int(0.005 * x.size)
+        tau = vdist.search_tau_budget_sharded(torch.from_numpy(x).cuda(), 32, B, exchange=ex)
+        assert tau == oracle.search_tau_budget(x, 32, B)
+    assert int(ex.buf[0].item()) == 3

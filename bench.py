@@ -932,8 +932,11 @@ def strong_scaling(args, world: int, rank: int, dev) -> dict:
       * the 2^32 size-sweep point: round-and-log + count all-gather + replay
         over contiguous shards (dist.shard_range; global indices);
       * configs[4]: the 1.5e9-parameter Merkle tree, whole 2^12-leaf blocks
-        per rank + block-root all-gather + top levels (dist.merkle_sharded);
-        its root is checked equal to the single-GPU root;
+        per rank + block-root exchange (peer memory at N > 1 on NCCL) + top
+        levels (dist.merkle_sharded); its root is checked equal to the
+        single-GPU root;
+      * the budget search of one 2^30-element N(0,1) tensor sharded over the
+        ranks (dist.search_tau_budget_sharded with a BudgetExchange);
       * configs[2]: the 161 ResNet-50 tensors LPT-assigned to ranks, each rank
         one batched adaptive call; taus checked against the single-GPU batch."""
     import numpy as np
@@ -1039,6 +1042,31 @@ def strong_scaling(args, world: int, rank: int, dev) -> dict:
                           "root": root.hex()[:16], "root_equals_single_gpu": same,
                           "block_roots": ("peer memory (vt_merkle_level_exchange + vt_digests_wait)" if dx is not None
                                           else "all-gather" if world > 1 else "local")}
+    # --- one 2^30-element tensor's budget search, sharded (SURVEY §8e tau search)
+    total_b = 1 << 30
+    lo_b, hi_b = vdist.shard_range(total_b, rank, world)
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(30 + rank)
+    xb_ = torch.randn(hi_b - lo_b, dtype=torch.float64, device=dev, generator=gx)
+    Bb = int(0.005 * total_b)
+    bx = None
+    if args.dist_backend == "nccl" or not dist.is_initialized():
+        try:
+            bx = vdist.BudgetExchange(device=dev)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] symmetric-memory budget exchange unavailable, using NCCL: {e!r}", file=sys.stderr)
+    rb = {}
+
+    def bs():
+        rb["tau"] = vdist.search_tau_budget_sharded(xb_, 32, Bb, exchange=bx, n_global=total_b)
+
+    ms_b = timed(bs, 3)  # wall-inclusive: each search ends in one host read of (status, tau)
+    out["budget_search_2^30_sharded"] = {"ms": round(ms_b, 3), "gbs": round(8 * total_b / ms_b / 1e6, 1),
+                                         "tau_over_2^-24": round(rb["tau"] / 2.0 ** -24, 6),
+                                         "exchange": "peer memory (vt_tau_shard_search_x)" if bx is not None
+                                         else "NCCL + host decision"}
+    del xb_
+    torch.cuda.empty_cache()
     # --- configs[2], LPT over ranks
     xs = workloads.config2_tensors_torch(device=dev)
     sizes = [t.numel() for t in xs]

@@ -111,7 +111,9 @@ class CountExchange:
     every rank's buffer (``vt_round_log_exchange``); ``wait`` launches the
     kernel that waits for every rank's count (``vt_counts_wait``).  No NCCL
     call, no host round trip: both are plain kernels on the current stream,
-    so a whole step can be graph-captured."""
+    so a whole step can be graph-captured.  Construction is collective (a
+    symmetric-memory rendezvous): every rank of the group constructs its
+    exchanges in the same order."""
 
     def __init__(self, group=None, device=None):
         from . import _device as D
@@ -375,7 +377,8 @@ class BudgetExchange:
     device buffer in a single process) holding every rank's digit histogram
     and digit keys; the decision, the gather, the exact order statistic and
     the bisection run on the device, so a search is one enqueue and one host
-    read.  ``keys_cap`` bounds one rank's keys in the selected digit."""
+    read.  ``keys_cap`` bounds one rank's keys in the selected digit.
+    Construction is collective, like ``CountExchange``'s."""
 
     def __init__(self, group=None, device=None, keys_cap: int = 1 << 16):
         from . import _device as D
@@ -622,7 +625,8 @@ class DigestExchange:
     into every rank's buffer at its global block index
     (``vt_merkle_level_exchange``; ``vt_digests_publish`` when the roots need
     no hashing), and ``wait`` gathers all of them in block order
-    (``vt_digests_wait``).  No NCCL call, no host round trip."""
+    (``vt_digests_wait``).  No NCCL call, no host round trip.  Construction
+    is collective, like ``CountExchange``'s."""
 
     def __init__(self, n_total: int, group=None, device=None):
         from . import _device as D

@@ -1400,18 +1400,27 @@ __device__ TailSel tail_digit(const TailArgs& a, int64_t M, int64_t blk, int64_t
   t.rank = a.budget - above_hi - above_bin;
   const uint64_t digit = (uint64_t)t.bin, lo1 = a.L_key + 1;
   const int64_t stride = nblk * kAdThreads;
-  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += stride) {  // warp-uniform bounds: a ballot follows
-    const int64_t i = i0 + tid;
-    const uint64_t key = i < M ? a.ck[i] : 0ull;
-    const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      unsigned long long pos = 0;
-      if (lane == leader)
-        pos = atomicAdd(reinterpret_cast<unsigned long long*>(&a.h->cand2), (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (in) a.c2[pos + __popc(m & lanemask_lt())] = key - lo1;
+  constexpr int kDU = 8;  // keys in flight per thread (each round of the loop is one memory latency)
+  for (int64_t i0 = blk * kAdThreads; i0 < M; i0 += kDU * stride) {  // warp-uniform bounds: ballots follow
+    uint64_t key[kDU];
+#pragma unroll
+    for (int u = 0; u < kDU; ++u) {
+      const int64_t i = i0 + u * stride + tid;
+      key[u] = i < M ? a.ck[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kDU; ++u) {
+      const int64_t i = i0 + u * stride + tid;
+      const bool in = i < M && key[u] <= a.hi_key && key[u] >= lo1 && ((key[u] - lo1) >> a.s0) == digit;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader)
+          pos = atomicAdd(reinterpret_cast<unsigned long long*>(&a.h->cand2), (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (in) a.c2[pos + __popc(m & lanemask_lt())] = key[u] - lo1;
+      }
     }
   }
   return t;

@@ -1533,6 +1533,10 @@ __device__ void tail_filter_count(const TailArgs& a, int64_t M, int64_t blk, int
 }
 
 // 4b. the log words of that range at the prefix of the earlier CTAs' counts
+#ifndef VT_FILTER_RUNS  // A/B: 8 contiguous candidates per thread per round (else one per thread)
+#define VT_FILTER_RUNS 1
+#endif
+
 __device__ void tail_filter_write(const TailArgs& a, int64_t M, int64_t blk, int64_t nblk,
                                   unsigned long long* s_acc, uint32_t* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1544,25 +1548,66 @@ __device__ void tail_filter_write(const TailArgs& a, int64_t M, int64_t blk, int
   pre = block_sum(pre, s_acc);
   const int64_t cur = a.cursor_in ? *a.cursor_in : 0;
   int64_t pos = cur + (int64_t)pre;
-  for (int64_t c0 = r0; c0 < r1; c0 += kAdThreads) {
-    const int64_t i = c0 + tid;
-    const bool keep = i < r1 && a.ck[i] > tau_key;
-    const uint32_t m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_warp[warp] = __popc(m);
-    __syncthreads();
-    uint32_t wpre = 0, tot = 0;
+  if (VT_FILTER_RUNS) {
+    // each thread a run of 8 consecutive candidates per round (all loads of a
+    // round in flight at once), one CTA-wide exclusive scan of the run counts
+    constexpr int kRun = 8;
+    for (int64_t c0 = r0; c0 < r1; c0 += (int64_t)kRun * kAdThreads) {
+      const int64_t i0 = c0 + (int64_t)tid * kRun;
+      uint64_t k[kRun];
 #pragma unroll
-    for (int w = 0; w < kAdThreads / 32; ++w) {
-      wpre += w < warp ? s_warp[w] : 0u;
-      tot += s_warp[w];
+      for (int u = 0; u < kRun; ++u) k[u] = (i0 + u < r1) ? a.ck[i0 + u] : 0ull;
+      uint32_t keep = 0;
+#pragma unroll
+      for (int u = 0; u < kRun; ++u) keep |= (i0 + u < r1 && k[u] > tau_key) ? (1u << u) : 0u;
+      const uint32_t cnt = __popc(keep);
+      uint32_t inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) s_warp[warp] = inc;
+      __syncthreads();
+      uint32_t wpre = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kAdThreads / 32; ++w) {
+        wpre += w < warp ? s_warp[w] : 0u;
+        tot += s_warp[w];
+      }
+      int64_t p = pos + wpre + (inc - cnt);
+#pragma unroll
+      for (int u = 0; u < kRun; ++u) {
+        if (keep & (1u << u)) {
+          const uint64_t w = a.cw[i0 + u];
+          if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+          ++p;
+        }
+      }
+      pos += tot;
+      __syncthreads();
     }
-    if (keep) {
-      const int64_t p = pos + wpre + __popc(m & lanemask_lt());
-      const uint64_t w = a.cw[i];
-      if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+  } else {
+    for (int64_t c0 = r0; c0 < r1; c0 += kAdThreads) {
+      const int64_t i = c0 + tid;
+      const bool keep = i < r1 && a.ck[i] > tau_key;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s_warp[warp] = __popc(m);
+      __syncthreads();
+      uint32_t wpre = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kAdThreads / 32; ++w) {
+        wpre += w < warp ? s_warp[w] : 0u;
+        tot += s_warp[w];
+      }
+      if (keep) {
+        const int64_t p = pos + wpre + __popc(m & lanemask_lt());
+        const uint64_t w = a.cw[i];
+        if (p < a.sparse_cap) a.sparse[p] = ((uint64_t)(a.global_base + (int64_t)(w >> 1)) << 1) | (w & 1ull);
+      }
+      pos += tot;
+      __syncthreads();
     }
-    pos += tot;
-    __syncthreads();
   }
   if (blk == nblk - 1 && tid == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(a.counters), (unsigned long long)(pos - cur));

@@ -2014,11 +2014,21 @@ __global__ void __launch_bounds__(kAdThreads) shard_hist_kernel(uint64_t* __rest
   __syncthreads();
   uint32_t err = 0;
   unsigned long long above = 0;
-  for (int64_t i = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i < M; i += (int64_t)gridDim.x * kAdThreads) {
-    const uint64_t key = dist_key(__longlong_as_double((long long)ck[i]), g0, err);
-    ck[i] = key;  // the keys, in place of the x values, for the digit step
-    if (key > hi_key) ++above;
-    else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
+  constexpr int kU = 8;  // loads in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * kAdThreads;
+  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads + threadIdx.x; i0 < M; i0 += kU * stride) {
+    uint64_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = (i0 + u * stride < M) ? ck[i0 + u * stride] : 0ull;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= M) break;
+      const uint64_t key = dist_key(__longlong_as_double((long long)v[u]), g0, err);
+      ck[i] = key;  // the keys, in place of the x values, for the digit step
+      if (key > hi_key) ++above;
+      else if (key > L_key) atomicAdd(&sh[(uint32_t)((key - L_key - 1) >> s0)], 1u);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
   if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, above);
@@ -2044,18 +2054,29 @@ __global__ void __launch_bounds__(kAdThreads) shard_digit_kernel(const uint64_t*
   const int64_t M = Mraw < cap ? Mraw : cap;
   const uint64_t lo1 = L_key + 1;
   const int lane = threadIdx.x & 31;
-  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    const uint64_t key = i < M ? ck[i] : 0ull;
-    const bool in = i < M && key <= hi_key && key >= lo1 && ((key - lo1) >> s0) == digit;
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      unsigned long long pos = 0;
-      if (lane == leader) pos = atomicAdd(count, (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      const unsigned long long p = pos + __popc(m & lanemask_lt());
-      if (in && (int64_t)p < out_cap) out[p] = key;
+  constexpr int kU = 8;  // loads in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * kAdThreads;
+  for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += kU * stride) {  // warp-uniform bounds
+    uint64_t kv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride + threadIdx.x;
+      kv[u] = i < M ? ck[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride + threadIdx.x;
+      const uint64_t key = kv[u];
+      const bool in = i < M && key <= hi_key && key >= lo1 && ((key - lo1) >> s0) == digit;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (lane == leader) pos = atomicAdd(count, (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        const unsigned long long p = pos + __popc(m & lanemask_lt());
+        if (in && (int64_t)p < out_cap) out[p] = key;
+      }
     }
   }
 }
@@ -2273,20 +2294,32 @@ __global__ void __launch_bounds__(kAdThreads) sx_digit_keys_kernel(const SXArgs 
     const uint64_t digit = dec[1], lo1 = a.L_key + 1;
     const int64_t Mraw = h->ccount;
     const int64_t M = Mraw < cap ? Mraw : cap;
-    for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += (int64_t)gridDim.x * kAdThreads) {
-      const int64_t i = i0 + threadIdx.x;
-      const uint64_t key = i < M ? ck[i] : 0ull;
-      const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
-      const uint32_t m = __ballot_sync(0xffffffffu, in);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        unsigned long long pos = 0;
-        if (lane == leader) pos = atomicAdd(reinterpret_cast<unsigned long long*>(a.own + 1), (unsigned long long)__popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        const int64_t q = (int64_t)(pos + __popc(m & lanemask_lt()));
-        if (in && q < a.L.kcap)
-          for (int p = 0; p < a.world; ++p)
-            a.peers[p][a.L.keys + ((int64_t)par * a.world + a.rank) * a.L.kcap + q] = key;
+    constexpr int kU = 8;  // loads in flight per thread
+    const int64_t stride = (int64_t)gridDim.x * kAdThreads;
+    for (int64_t i0 = (int64_t)blockIdx.x * kAdThreads; i0 < M; i0 += kU * stride) {  // warp-uniform bounds
+      uint64_t kv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + u * stride + threadIdx.x;
+        kv[u] = i < M ? ck[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + u * stride + threadIdx.x;
+        const uint64_t key = kv[u];
+        const bool in = i < M && key <= a.hi_key && key >= lo1 && ((key - lo1) >> a.s0) == digit;
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long pos = 0;
+          if (lane == leader)
+            pos = atomicAdd(reinterpret_cast<unsigned long long*>(a.own + 1), (unsigned long long)__popc(m));
+          pos = __shfl_sync(0xffffffffu, pos, leader);
+          const int64_t q = (int64_t)(pos + __popc(m & lanemask_lt()));
+          if (in && q < a.L.kcap)
+            for (int p = 0; p < a.world; ++p)
+              a.peers[p][a.L.keys + ((int64_t)par * a.world + a.rank) * a.L.kcap + q] = key;
+        }
       }
     }
   }

@@ -2552,7 +2552,10 @@ __global__ void __launch_bounds__(kAdThreads) adapt_select_batch_kernel(const __
                     (int64_t)blockIdx.x - sg.blk0, ad_nblk(b, j));
 }
 
-__global__ void __launch_bounds__(kAdThreads) adapt_filter_batch_kernel(const __grid_constant__ AdBatch b) {
+#ifndef VT_FILTER_MINB  // resident CTAs per SM the batch filter is compiled for (64 registers; 1: 68 registers, 3 CTAs/SM, configs[2] 2.15-2.17 vs 2.14 ms)
+#define VT_FILTER_MINB 4
+#endif
+__global__ void __launch_bounds__(kAdThreads, VT_FILTER_MINB) adapt_filter_batch_kernel(const __grid_constant__ AdBatch b) {
   const int j = ad_find(b, blockIdx.x);
   const AdSeg& sg = b.seg[j];
   const AdPtrs p = adapt_ptrs(sg.ws, adapt_layout_rl(sg.n, 0));

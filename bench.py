@@ -137,6 +137,13 @@ def maybe_spawn(args) -> None:
     this does nothing."""
     if "WORLD_SIZE" in os.environ or args.gpus <= 1:
         return
+    if args.dist_backend == "nccl" and not args.harness_check:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:  # NCCL puts one rank on one GPU; say so instead of a communicator error
+            print(f"[bench] --gpus {args.gpus} needs {args.gpus} visible GPUs, this node has {have} "
+                  f"(--dist-backend gloo runs the N-rank code path on one GPU)", file=sys.stderr)
+            sys.exit(2)
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",

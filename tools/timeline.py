@@ -70,3 +70,9 @@ print("ordinals per CTA min/med/max", nord.min(), np.median(nord), nord.max())
 # per-SM: mean sentinel by sm parity/half
 for name, m in (("sm<74", sm < 74), ("sm>=74", sm >= 74), ("even", sm % 2 == 0), ("odd", sm % 2 == 1)):
     print(name, "sentinel med", np.median(sent[m]).round(2), "ordinals med", np.median(nord[m]))
+# ordinals per CTA by launch wave (CTA id // 148: the first, second, third CTA
+# placed on each SM), and when each wave's CTAs end
+for w in range(3):
+    m = (np.arange(G) // 148) == w
+    print(f"CTA ids {148 * w}-{148 * w + 147}: ordinals min/med/max", nord[m].min(), np.median(nord[m]), nord[m].max(),
+          " sentinel med", np.median(sent[m]).round(2))

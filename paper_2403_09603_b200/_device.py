@@ -163,7 +163,15 @@ class HostStage:
     Layout (host and device alike, 256-byte aligned regions):
         [ x: in_bytes | flags: 256 | out regions ... ]
     H2D covers [0, flags_end); D2H covers [flags_off, end).  One stage per
-    channel object; calls on it are sequential (the channel is)."""
+    channel object; calls on it are sequential (the channel is).
+
+    Zero-copy form for small calls (``ZERO_COPY_MAX`` elements and below):
+    the kernel reads x from and writes its outputs to the pinned host buffer
+    directly (pinned memory is device-addressable under UVA, ``hptr``); only
+    the flag words, which the kernel accumulates with atomics, live on the
+    device -- zeroed before the call and read back with one 64-byte copy."""
+
+    ZERO_COPY_MAX = (1 << 18) - 1  # below the TMA-pipelined kernels' size threshold
 
     def __init__(self):
         self.cap = 0
@@ -191,6 +199,13 @@ class HostStage:
 
     def h2d(self, end: int) -> None:
         self.dev[:end].copy_(self.host[:end], non_blocking=True)
+
+    def hptr(self, off: int) -> int:
+        """Device-usable address of the pinned host buffer at ``off`` (UVA)."""
+        return self.host.data_ptr() + off
+
+    def zero_dev(self, off: int, nbytes: int) -> None:
+        self.dev[off:off + nbytes].zero_()
 
     def d2h_wait(self, lo: int, hi: int) -> None:
         self.host[lo:hi].copy_(self.dev[lo:hi], non_blocking=True)

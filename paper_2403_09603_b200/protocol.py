@@ -76,7 +76,8 @@ class GpuAuditorChannel:
     def _process_host(self, values, tau: float):
         """NumPy input with a device-resident .vtrl payload: one H2D copy of
         [x | zeroed flags], the fused packed replay, one D2H copy of
-        [flags | y], one host wait."""
+        [flags | y], one host wait; small arrays zero-copy (the kernel reads
+        x from and writes y to the pinned buffer, only the flags come back)."""
         a = np.asarray(values, dtype=np.float64)
         shape = a.shape if a.shape else (1,)
         n = a.size
@@ -89,13 +90,20 @@ class GpuAuditorChannel:
         fo, (oy,), end = st.layout(8 * n, [8 * n])
         st.ensure(end)
         np.copyto(st.hview(0, n, np.float64), a.reshape(-1))
-        st.hview(fo, 32, np.int64)[:] = 0
-        st.h2d(fo + 256)
         ws = D.workspace(int(_lib.lib().vt_replay_workspace(n)), "replay_packed")
-        _lib.call("vt_replay", st.dptr(0), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload), self.reader.payload_nbytes,
-                  pos, _lib.OUT_F64, st.dptr(oy), st.dptr(fo + 16), st.dptr(fo), D.ptr(ws), ws.numel(),
-                  D.stream_ptr())
-        st.d2h_wait(fo, oy + 8 * n)
+        if n <= st.ZERO_COPY_MAX:  # zero-copy: x and y in the pinned buffer, flags on the device
+            st.zero_dev(fo, 64)
+            _lib.call("vt_replay", st.hptr(0), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload),
+                      self.reader.payload_nbytes, pos, _lib.OUT_F64, st.hptr(oy), st.dptr(fo + 16), st.dptr(fo),
+                      D.ptr(ws), ws.numel(), D.stream_ptr())
+            st.d2h_wait(fo, fo + 64)
+        else:
+            st.hview(fo, 32, np.int64)[:] = 0
+            st.h2d(fo + 256)
+            _lib.call("vt_replay", st.dptr(0), n, self.b_r, _lib.LOG_PACKED, D.ptr(payload),
+                      self.reader.payload_nbytes, pos, _lib.OUT_F64, st.dptr(oy), st.dptr(fo + 16), st.dptr(fo),
+                      D.ptr(ws), ws.numel(), D.stream_ptr())
+            st.d2h_wait(fo, oy + 8 * n)
         fl = st.hview(fo, 6, np.int64)
         err = int(fl[0]) & 0xFFFFFFFF
         if err & _lib.ERR_BAD_LOG_BYTE:

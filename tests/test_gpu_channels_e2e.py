@@ -65,8 +65,8 @@ def test_reference_run_through_gpu_channels(traces, name, tmp_path):
 
 @pytest.mark.parametrize("b_r", [32, 26, 10])
 def test_staged_channels_shapes_and_grids(oracle, b_r, tmp_path):
-    """The staged host-array path of the GPU channels (one H2D, one D2H per
-    call) over odd shapes -- 0-d, empty, non-contiguous, 3-D, sizes around the
+    """The host-array paths of the GPU channels (zero-copy for small arrays,
+    one H2D + one D2H for large ones) over odd shapes -- 0-d, empty, non-contiguous, 3-D, sizes around the
     5-code packing phase -- at several grids: outputs and counts equal the
     oracle's channel arithmetic (protocol.py:198-216), the .vtrl file the
     reference writer's bytes, and a corrupt payload byte raises."""
@@ -74,7 +74,8 @@ def test_staged_channels_shapes_and_grids(oracle, b_r, tmp_path):
     rng = np.random.default_rng(b_r)
     base = rng.normal(0, 3, size=(40, 30))
     tensors = [np.float64(1.0 + 0.6 * 2.0 ** -23), np.zeros(0), base[:, ::3], rng.normal(0, 1e-3, (2, 3, 7)),
-               rng.normal(0, 1, 4), rng.normal(0, 1, 5), rng.normal(0, 1, 6), rng.normal(0, 50, 10_007)]
+               rng.normal(0, 1, 4), rng.normal(0, 1, 5), rng.normal(0, 1, 6), rng.normal(0, 50, 10_007),
+               rng.normal(0, 2, 300_001)]  # the last above HostStage.ZERO_COPY_MAX: the staged-copy path
     tau = 2.0 ** -25
     path = tmp_path / "s.vtrl"
     w = roundlog.LogWriter(path, b_r)

@@ -95,7 +95,8 @@ def test_hooks_error_then_clean_step():
     hk.remove()
 
 
-def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
+@pytest.mark.parametrize("b_r", [32, 26])
+def test_auditor_replay_hooks_reproduce_the_trainer(oracle, b_r):
     """Trainer: RoundAndLogHooks on a small FP64 GPT-2 step, logs kept.
     Auditor: the same step on a copy of the model whose every hooked tensor
     is perturbed (a stand-in for other hardware: 5% of the elements moved by
@@ -109,6 +110,9 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
     from paper_2403_09603_b200 import hooks, workloads
     torch.manual_seed(4)
     model = workloads.gpt2_small_fp64(vocab=97, d=64, layers=2, heads=4, ctx=32)
+    with torch.no_grad():  # full 53-bit FP64 parameters: an FP32-derived init puts 1/64 of the embedding
+        for prm in model.parameters():  # rows exactly on b_r = 26 midpoints, which no budget tau logs
+            prm.add_(torch.randn_like(prm) * 1e-9)
     model_a = copy.deepcopy(model)
     idx = torch.randint(0, 97, (4, 32), device="cuda")
 
@@ -124,7 +128,7 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
             h.remove()
         return hk, seen, loss.detach().clone(), [p.grad.clone() for p in m.parameters()]
 
-    hk_t, seen_t, loss_t, grads_t = run(model, lambda m: hooks.RoundAndLogHooks(m))
+    hk_t, seen_t, loss_t, grads_t = run(model, lambda m: hooks.RoundAndLogHooks(m, b_r=b_r))
     info = hk_t.collect(keep_logs=True)
     hk_t.remove()
     assert len(info["logs"]) == info["tensors"] and info["logged"] > 0 and info["loss"] == 1
@@ -136,10 +140,12 @@ def test_auditor_replay_hooks_reproduce_the_trainer(oracle):
         sel = torch.rand(flat.numel(), device="cuda", generator=g) < 0.05
         # below the budget tau's margin to the midpoint ((1 - tau / 2^-24) ~ 0.005 of the half-ulp):
         # an auditor deviation the trainer's log covers
-        rel = (torch.rand(flat.numel(), device="cuda", dtype=torch.float64, generator=g) * 2 - 1) * 2.0 ** -34
+        rel = (torch.rand(flat.numel(), device="cuda", dtype=torch.float64, generator=g) * 2 - 1) * \
+            2.0 ** -(b_r + 2)  # the same fraction of a grid step (2^-(b_r - 9) relative) on every grid
         flat.add_(torch.where(sel, flat * rel, torch.zeros_like(flat)))
 
-    hk_a, seen_a, loss_a, grads_a = run(model_a, lambda m: hooks.ReplayHooks(m, info["logs"], perturb=perturb))
+    hk_a, seen_a, loss_a, grads_a = run(model_a, lambda m: hooks.ReplayHooks(m, info["logs"], b_r=b_r,
+                                                                              perturb=perturb))
     res = hk_a.collect()
     hk_a.remove()
     assert res["tensors"] == info["tensors"]

@@ -26,8 +26,12 @@ fork-shared inputs, comparisons in the workers); the checks are bit-exact.
 
 from __future__ import annotations
 
+import json
+
 import numpy as np
 import pytest
+
+from conftest import REPO
 
 pytestmark = pytest.mark.gpu
 
@@ -128,6 +132,9 @@ def test_config3_gpt2_full_size_hooked_tensors_vs_oracle():
     loss.backward()
     info = hk.collect(keep_logs=True)
     hk.remove()
+    # the pinned tensor list: same modules, kinds, sizes and budgets, in call order
+    pinned = json.loads((REPO / "tests" / "golden" / "gpt2_hooked_tensors.json").read_text())
+    assert [list(c) for c in info["calls"]] == pinned["calls"] and info["elements"] == pinned["elements"]
     del model, loss
     torch.cuda.empty_cache()
     assert {(v[0], v[1]) for v in hk._cap.values()} == set(GPT2_PICKS)

@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
         if (t1 > t0) l2_prefetch(a.x + t0 * kSTile, (uint32_t)((t1 - t0) * kSTile * sizeof(double)));
       };
       int64_t s = (int64_t)atomicAdd(&a.hdr->ticket, 1u);
-      int64_t q = 0;  // ring sequence number
+      uint32_t q = 0;  // ring sequence number (32-bit: q % 3 and q / 3 are one multiply-high)
       for (int64_t k = 0;; ++k) {
         if (s >= a.num_super) s = -1;
         int64_t nxt = -1;
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_fused_kernel(const RLFArgs a)
     const uint32_t w8 = (thr32 >= (1 << 28)) ? 0u : ((0x20000000u - 2u * (uint32_t)thr32 - 1u) << 3);
     const uint32_t epoch = S.epoch;
     int64_t hist[kMaskSlots];  // super-tile of ordinal kk at hist[kk % kMaskSlots]
-    int64_t q = 0;             // ring sequence number
+    uint32_t q = 0;            // ring sequence number (32-bit, as the producer's)
     for (int64_t k = 0;; ++k) {
       // this warp's rows of ordinal k - kMaskSlots leave slot k % kMaskSlots before it is reused
       if (warp == 0 && lane == 0 && k < 14) TL(4 + 4 * (int)k);
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
       };
       TicketInfo cur = lookup(draw());
       prefetch(cur);
-      int64_t q = 0;  // ring sequence number
+      uint32_t q = 0;  // ring sequence number (32-bit)
       for (int64_t k = 0;; ++k) {
         const int64_t s = cur.s;
         const int nt = cur.nt, j = cur.j;
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(kFThreads, 3) rl_batch_kernel(const __grid_con
     const uint32_t epoch = S.epoch;
     int64_t hist[kMaskSlots];  // ticket of ordinal kk at hist[kk % kMaskSlots]
     int histj[kMaskSlots];     // and its tensor
-    int64_t q = 0;
+    uint32_t q = 0;  // ring sequence number (32-bit)
     auto write_rows = [&](int64_t kk, int64_t s, int j) {
       rlf_write_rows<KEYS>(seg_view(b, j), S, kk, s - b.seg[j].tick0, warp, lane, lt);
     };

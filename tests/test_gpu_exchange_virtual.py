@@ -72,16 +72,17 @@ def test_virtual_ranks_exchange_counts_in_lockstep():
     for rnd in range(5):
         xs = _shards(rnd)
         want = []
+        base0 = (1 << 33) + 17 if rnd == 4 else 0  # global indices past 32 bits in the last round
         for r, x in enumerate(xs):
             xx = x if x is not None else torch.empty(0, dtype=torch.float64, device="cuda")
-            vr.publish(r, xx, tau, 1_000 * r)
-            want.append(ops.round_and_log(xx, 32, tau, global_base=1_000 * r)[1].count if xx.numel() else 0)
+            vr.publish(r, xx, tau, base0 + 1_000 * r)
+            want.append(ops.round_and_log(xx, 32, tau, global_base=base0 + 1_000 * r)[1].count if xx.numel() else 0)
         for r in range(W):
             assert vr.wait(r).tolist() == want, (rnd, r)
         for r, x in enumerate(xs):
             y, log = vr.pending[r].finish()
             if x is not None:
-                y1, log1 = ops.round_and_log(x, 32, tau, global_base=1_000 * r)
+                y1, log1 = ops.round_and_log(x, 32, tau, global_base=base0 + 1_000 * r)
                 assert torch.equal(y.view(torch.int32), y1.view(torch.int32))
                 assert torch.equal(log.words, log1.words)
         torch.cuda.synchronize()

@@ -273,7 +273,7 @@ def _virtual_budget(shards, b_r: int, budget: int, keys_cap: int = 1 << 16, iter
     return res
 
 
-@pytest.mark.parametrize("case", ["normal", "uneven_empty", "budget0", "wide", "tiny_budget_digit"])
+@pytest.mark.parametrize("case", ["normal", "uneven_empty", "budget0", "wide", "tiny_budget_digit", "b_r26"])
 def test_virtual_ranks_sharded_budget_search(case, oracle):
     """Every virtual rank gets the oracle's budget tau of the whole tensor,
     decided on the device (status 0), for uneven and empty shards and the
@@ -281,7 +281,8 @@ def test_virtual_ranks_sharded_budget_search(case, oracle):
     import numpy as np
     import torch
     rng = np.random.default_rng({"normal": 1, "uneven_empty": 2, "budget0": 3, "wide": 4,
-                                 "tiny_budget_digit": 5}[case])
+                                 "tiny_budget_digit": 5, "b_r26": 6}[case])
+    b_r = 26 if case == "b_r26" else 32
     if case == "uneven_empty":
         sizes = [300_001, 0, 77_777, 5]
     elif case == "wide":
@@ -296,8 +297,8 @@ def test_virtual_ranks_sharded_budget_search(case, oracle):
     for n in sizes:
         shards.append(torch.from_numpy(x[lo:lo + n].copy()).cuda())
         lo += n
-    res = _virtual_budget(shards, 32, budget)
-    want = oracle.search_tau_budget(x, 32, budget)
+    res = _virtual_budget(shards, b_r, budget)
+    want = oracle.search_tau_budget(x, b_r, budget)
     for status, tau in res:
         assert status == 0 and tau == want, (res, want)
 

@@ -86,13 +86,17 @@ def _out_kind(out_dtype) -> int:
 def round_and_log(x: torch.Tensor, b_r: int, tau: float, *, out_dtype=torch.float32,
                   global_base: int = 0, out: torch.Tensor | None = None,
                   log_out: torch.Tensor | None = None, codes_out: torch.Tensor | None = None,
-                  check: bool = True, workspace: torch.Tensor | None = None):
+                  check: bool = True, workspace: torch.Tensor | None = None,
+                  flags_out: torch.Tensor | None = None):
     """Fused rnd + direction + stream compaction (one kernel launch).
 
     Reentrant across streams and host threads: the call's scratch state lives
     in a workspace keyed by the current stream (or the caller's
     ``workspace``, a zero-initialised uint8 CUDA tensor of at least
-    ``vt_round_log_workspace(n)`` bytes used by one stream at a time)."""
+    ``vt_round_log_workspace(n)`` bytes used by one stream at a time).
+    ``flags_out`` (a zeroed int64[6] CUDA tensor: error bits, -, entry count,
+    ...) replaces the per-call flag allocation, e.g. a row of a per-step
+    arena, as ``round_and_log_adaptive``'s."""
     _check_b(b_r)
     D.require_cuda()
     shape = tuple(x.shape) if x.dim() else (1,)
@@ -108,7 +112,8 @@ def round_and_log(x: torch.Tensor, b_r: int, tau: float, *, out_dtype=torch.floa
     need = int(_lib.lib().vt_round_log_workspace(n))
     ws = workspace if workspace is not None else D.workspace(need, "round_log")
     D.check_out(ws, need, torch.uint8, t.device, "workspace")
-    f = D.Flags()
+    D.check_out(flags_out, 6, torch.int64, t.device, "flags_out")
+    f = D.Flags(buf=flags_out)
     if n:
         _lib.call("vt_round_log", D.ptr(t), n, b_r, float(tau), kind, D.ptr(y),
                   D.ptr(words), words.numel(), int(global_base), None, None, D.ptr(codes_out),
@@ -120,17 +125,21 @@ def round_and_log(x: torch.Tensor, b_r: int, tau: float, *, out_dtype=torch.floa
     if log_out is None and err == 0 and cnt[0] > words.numel():
         # more entries than the default capacity: once more with the exact size
         words = torch.empty(cnt[0], dtype=torch.int64, device=t.device)
+        if flags_out is not None:
+            flags_out.zero_()
         return round_and_log(x, b_r, tau, out_dtype=out_dtype, global_base=global_base, out=out,
-                             log_out=words, codes_out=codes_out, check=True, workspace=workspace)
+                             log_out=words, codes_out=codes_out, check=True, workspace=workspace,
+                             flags_out=flags_out)
     return pending.finish(err, cnt)
 
 
 def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtype=torch.float32,
            global_base: int = 0, out: torch.Tensor | None = None, strict: bool = True,
-           check: bool = True, workspace: torch.Tensor | None = None):
+           check: bool = True, workspace: torch.Tensor | None = None, flags_out: torch.Tensor | None = None):
     """Fused rev with a sparse log; returns (y, corrections).  Reentrant
     across streams (workspace keyed by the current stream, or the caller's
-    zeroed ``workspace`` of ``vt_replay_workspace(n)`` bytes)."""
+    zeroed ``workspace`` of ``vt_replay_workspace(n)`` bytes); ``flags_out``
+    as for ``round_and_log``."""
     _check_b(b_r)
     D.require_cuda()
     words = log.words if isinstance(log, SparseLog) else log
@@ -146,7 +155,8 @@ def replay(x: torch.Tensor, b_r: int, log: SparseLog | torch.Tensor, *, out_dtyp
     need = int(_lib.lib().vt_replay_workspace(n))
     ws = workspace if workspace is not None else D.workspace(need, "replay")
     D.check_out(ws, need, torch.uint8, t.device, "workspace")
-    f = D.Flags()
+    D.check_out(flags_out, 6, torch.int64, t.device, "flags_out")
+    f = D.Flags(buf=flags_out)
     if n:
         _lib.call("vt_replay", D.ptr(t), n, b_r, _lib.LOG_SPARSE, D.ptr(words), words.numel(),
                   int(global_base), kind, D.ptr(y), f.cnt_ptr, f.err_ptr, D.ptr(ws), ws.numel(),

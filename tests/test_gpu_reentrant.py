@@ -149,3 +149,51 @@ def test_default_log_capacity_grows_when_needed(oracle):
     assert np.array_equal(log.words.cpu().numpy().view(np.uint64), want)
     with pytest.raises(ops.LogOverflow):
         ops.round_and_log(x, 32, 0.0, check=False).finish()
+
+
+def test_flags_out_arena_for_round_and_log_and_replay(oracle):
+    """flags_out: caller-owned zeroed flag rows instead of a per-call
+    allocation -- same outputs, counts and corrections; a graph of both
+    operators on arena rows allocates nothing per replay."""
+    import numpy as np
+    import torch
+
+    from paper_2403_09603_b200 import ops, workloads
+    n = (1 << 20) + 33
+    xt, xa = workloads.config1_pair(n, 5)
+    tau = workloads.TAU_CONFIG0
+    t, a = torch.from_numpy(xt).cuda(), torch.from_numpy(xa).cuda()
+    arena = torch.zeros((2, 6), dtype=torch.int64, device="cuda")
+    y, log = ops.round_and_log(t, 32, tau, flags_out=arena[0])
+    ya, corr = ops.replay(a, 32, log, flags_out=arena[1])
+    y1, log1 = ops.round_and_log(t, 32, tau)
+    ya1, corr1 = ops.replay(a, 32, log1)
+    assert torch.equal(log.words, log1.words) and torch.equal(y.view(torch.int32), y1.view(torch.int32))
+    assert torch.equal(ya.view(torch.int32), ya1.view(torch.int32)) and corr == corr1
+    assert int(arena[0, 2]) == log.count and int(arena[1, 2]) == corr
+    codes = oracle.direction_array(xt, 32, tau)
+    assert np.array_equal(log.words.cpu().numpy().view(np.uint64), oracle.sparse_from_codes(codes))
+    # graph-captured on arena rows (zeroed inside the graph, no allocation per replay)
+    yo = torch.empty(n, dtype=torch.float32, device="cuda")
+    yao = torch.empty(n, dtype=torch.float32, device="cuda")
+    words = torch.empty(n // 4, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+
+    def step():
+        arena.zero_()
+        p = ops.round_and_log(t, 32, tau, out=yo, log_out=words, check=False, flags_out=arena[0])
+        ops.replay(a, 32, words[:log.count], out=yao, check=False, flags_out=arena[1])
+        return p
+
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(arena[0, 2]) == log.count and int(arena[1, 2]) == corr
+    assert torch.equal(yao.view(torch.int32), ya1.view(torch.int32))
